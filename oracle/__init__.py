@@ -1,0 +1,33 @@
+"""CPU ORACLE for the CWENO reconstruction of arXiv 1612.09335 §2.1 — TEST INFRASTRUCTURE.
+
+This package is a plain, slow, obviously-correct implementation of what the
+product path computes.  It exists only to check the CUDA path: only
+``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` legs may import or run it.  It shares no code with
+``paper_1612_09335_b200/`` (neither imports the other); only the seeded input
+generator ``gen/`` (which holds none of the method's arithmetic) serves both.
+
+Citations ``P:L`` are /root/reference/PAPER.md line numbers; ``R<n>`` are the
+readings listed in DESIGN.md.
+
+Modules and what pins them (tests/test_oracle_*.py, all ``-m "not gpu"``):
+
+  basis      Dubiner basis + Σ, exact in sympy.
+             Pinned: Gram = I exactly, closed-form App. A values of Σ,
+             σ(linear) = |T_E| |∇p|², PSD with zero constant row/col.
+  geometry   unwrap, orientation, barycentres, Morton order (R16,
+             R28, R29).  Pinned: volumes sum to the box volume, orientation
+             positive, Morton is a permutation sorted by key.
+  topology   face / node adjacency.  Pinned: symmetry, counts.
+  stencils   central + sectorial stencils with exact rational predicates
+             (R11-R15).  PARITY UNPINNED against the paper
+             (its figures are stripped); pinned only by invariants
+             (sizes P:166/P:179, self first, no duplicates, cone membership,
+             connectivity, determinism) and by brute-force cone checks.
+  reconstruct  A by exact monomial averaging, constrained LSQ,
+             sectors, P0, σ, ω,
+             w.  Pinned: polynomial reproduction of degree ≤ M,
+             conservation, ℙ1 exactness, Σλ̄ P = P_opt, Σω = 1, ω = λ̄ for equal
+             σ, paper's λ0/(λ0+N_p), convergence order on the vortex, mpmath
+             40-digit re-evaluation on a tiny case.
+"""

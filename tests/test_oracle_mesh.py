@@ -1,0 +1,158 @@
+"""Pins for oracle/mesh.py: geometry, SFC order, adjacency, stencils.
+
+Stencil parity is UNPINNED against the paper (its figures are stripped,
+P:161-177); these tests pin the oracle's stencils by the paper's counts
+ and by invariants checked with independent
+floating-point geometry (numpy.linalg.solve barycentric coordinates).
+"""
+import numpy as np
+import pytest
+
+import gen
+from oracle.mesh import MeshError, OracleMesh, StencilExhausted
+
+
+def _mesh(d, n, M, jitter=0.0, periodic=True, seed=1):
+    nodes, cells, period = gen.box_mesh(d, n, periodic, jitter, seed)
+    return OracleMesh(nodes, cells, period, M), nodes, cells, period
+
+
+@pytest.mark.parametrize("d,n,jit", [(2, 8, 0.0), (2, 9, 0.2), (3, 4, 0.0), (3, 5, 0.1)])
+def test_geometry_and_topology(d, n, jit):
+    m, nodes, cells, period = _mesh(d, n, 2, jit)
+    N = cells.shape[0]
+    assert N == (2 * n * n if d == 2 else 6 * n ** 3)
+    E = m.X[:, 1:, :] - m.X[:, :1, :]
+    vol = np.linalg.det(E)
+    assert np.all(vol > 0)                                      # R28
+    assert abs(vol.sum() / (2 if d == 2 else 6) - 1.0) < 1e-12  # tiles the unit torus
+    assert sorted(m.perm.tolist()) == list(range(N))            # permutation
+    # node sets preserved by the fix
+    assert np.array_equal(np.sort(m.cells, axis=1), np.sort(cells[m.perm], axis=1))
+    # face adjacency: complete on a torus, symmetric, shares d nodes
+    assert np.all(m.nbr >= 0)
+    for c in range(0, N, max(1, N // 97)):
+        for f in range(d + 1):
+            nb = m.nbr[c, f]
+            assert c in m.nbr[nb]
+            shared = set(m.cells[c]) & set(m.cells[nb])
+            assert len(shared) == d and m.cells[c, f] not in shared
+    # Morton: consecutive SFC cells are spatially close on average
+    b = m.bary
+    step = np.abs(np.diff(b, axis=0)).sum(axis=1)
+    assert np.median(step) < 3.0 / n
+
+
+def test_morton_is_key_sorted():
+    m, *_ = _mesh(2, 16, 2)
+    u = m.bary - np.floor(m.bary)
+    q = np.minimum(np.floor(u * 2.0 ** 31), 2 ** 31 - 1).astype(np.int64)
+    keys = [sum(((int(q[c, a]) >> t) & 1) << (2 * t + a) for t in range(31) for a in range(2)) for c in range(m.N)]
+    assert all(keys[i] <= keys[i + 1] for i in range(len(keys) - 1))
+
+
+def _bary_coords(m, i, j):
+    """λ of (the periodic image of) cell j's barycentre in the owner's simplex (float)."""
+    n = np.array(m.shift(i, j), float)
+    p = m.bary[j] + n * (m.period if m.period is not None else 0)
+    X = m.X[i]
+    A = np.vstack([X.T, np.ones(m.d + 1)])
+    return np.linalg.solve(A, np.append(p, 1.0))
+
+
+@pytest.mark.parametrize("d,n,M,jit", [(2, 8, 2, 0.0), (2, 10, 3, 0.2), (3, 4, 2, 0.0), (3, 6, 3, 0.1)])
+def test_central_stencil_invariants(golden, d, n, M, jit):
+    m, *_ = _mesh(d, n, M, jit)
+    n_e = d * {2: {2: 6, 3: 10}, 3: {2: 10, 3: 20}}[d][M]
+    assert m.n_e == n_e
+    for row in golden["stencil_size"]:
+        if (row["d"], row["M"]) == (d, M):
+            assert m.n_e == row["n_e"]
+    rng = np.random.default_rng(3)
+    for i in rng.choice(m.N, 12, replace=False):
+        S = m.central_stencil(int(i))
+        assert len(S) == n_e and S[0] == i and len(set(S)) == n_e
+        assert S == m.central_stencil(int(i))                          # deterministic
+        # recursive-neighbour property: every cell after the first touches an earlier one
+        for k in range(1, n_e):
+            assert any(S[k] in m.nbr[S[q]] for q in range(k))
+        # all face neighbours of i are in the stencil (first layer, d+1 < n_e)
+        assert set(m.nbr[i].tolist()) <= set(S)
+        # BFS layers: graph distance non-decreasing along the stencil
+        dist = {int(i): 0}
+        frontier = [int(i)]
+        while frontier:
+            nxt = []
+            for c in frontier:
+                for nb in m.nbr[c]:
+                    if int(nb) not in dist and len(dist) < 5000:
+                        dist[int(nb)] = dist[c] + 1
+                        nxt.append(int(nb))
+            frontier = nxt if max(dist.values()) < 6 else []
+        lay = [dist[c] for c in S]
+        assert lay == sorted(lay)
+        # last layer truncated by the distance key: nothing left out is closer
+        last = lay[-1]
+        chosen = [c for c in S if dist[c] == last]
+        left = [c for c, L in dist.items() if L == last and c not in S]
+        if left:
+            worst = max(m.key(int(i), c) for c in chosen)
+            assert all(m.key(int(i), c) > worst for c in left)
+
+
+@pytest.mark.parametrize("d,n,M,jit", [(2, 8, 2, 0.0), (2, 10, 3, 0.2), (3, 4, 2, 0.0), (3, 6, 3, 0.1)])
+def test_sector_stencil_invariants(d, n, M, jit):
+    m, *_ = _mesh(d, n, M, jit)
+    rng = np.random.default_rng(5)
+    for i in rng.choice(m.N, 10, replace=False):
+        i = int(i)
+        secs, valid = m.sector_stencils(i)
+        assert len(secs) == d + 1
+        used = set()
+        for v, (S, ok) in enumerate(zip(secs, valid)):
+            assert S[0] == i
+            if ok:
+                assert len(S) == d + 1 and -1 not in S and len(set(S)) == d + 1
+            for j in S[1:]:
+                if j < 0:
+                    continue
+                lam = _bary_coords(m, i, j)
+                # open cone of vertex v: λ_w > 0 for all w != v, and outside T_i: λ_v < 0
+                others = np.delete(lam, v)
+                assert np.all(others > -1e-12)
+                assert lam[v] < 1e-12
+                assert j not in used                                      # forward cones are disjoint
+                used.add(j)
+        assert all(valid)                                                  # structured meshes never starve here
+
+
+def test_cone_predicate_exact_on_boundary():
+    # unjittered 2D mesh: some barycentres lie exactly on cone boundaries; the
+    # exact predicate must exclude them (open cone) — the float check agrees
+    # whenever it is clear-cut.
+    m, *_ = _mesh(2, 8, 2)
+    i = 0
+    for j in range(m.N):
+        s = m.lambda_signs(i, j)
+        lam = _bary_coords(m, i, j)
+        for w in range(3):
+            if abs(lam[w]) > 1e-9:
+                assert s[w] == np.sign(lam[w])
+
+
+def test_errors():
+    nodes, cells, period = gen.box_mesh(2, 2, False)
+    m = OracleMesh(nodes, cells, None, 2)
+    with pytest.raises(StencilExhausted):
+        m.central_stencil(0)  # 8 cells < n_e = 12
+    with pytest.raises(MeshError):
+        OracleMesh(*gen.box_mesh(2, 2, True), 1)                              # 2x2 torus is not a manifold
+    nodes, cells, period = gen.box_mesh(2, 3, True)
+    with pytest.raises(MeshError):
+        OracleMesh(nodes, np.vstack([cells, cells[:1]]), period, 1)          # duplicate → non-manifold
+    bad = cells.copy(); bad[0, 2] = bad[0, 1]
+    with pytest.raises(MeshError):
+        OracleMesh(nodes, bad, period, 1)
+    flat = nodes.copy(); flat[:, 1] = 0.0
+    with pytest.raises(MeshError):
+        OracleMesh(flat, cells, None, 1)                                      # zero area

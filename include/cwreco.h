@@ -1,0 +1,194 @@
+/*
+ * cwreco.h — C ABI of libcwreco: B200-native CWENO reconstruction on unstructured
+ * triangular (d=2) / tetrahedral (d=3) meshes, arXiv 1612.09335 §2.1.
+ *
+ * Citations "P:L" are lines of the paper's LaTeX source; "R<n>" are the
+ * readings listed in DESIGN.md.  Everything here is plain C: pointers, sizes and
+ * status codes; no C++ or torch types cross the boundary.
+ *
+ * Operation (per owned cell i and conserved variable v, fp64):
+ *   gather Q_j for the central stencil S_i^0 (n_e = d·ℳ cells) and
+ *   the d+1 sectorial stencils S_i^s (d+1 cells each);
+ *   p̂_opt = constrained-LSQ polynomial of degree M (Eq. CWENO:Popt),
+ *   applied as p̂_opt[0] = Q_i/ψ_1, p̂_opt[1..ℳ-1] = B⁺ (Q_j − Q_i)_{j∈S_i^0∖i};
+ *   p̂_s = linear interpolant on S_i^s (Eq. CWENO:Ps);
+ *   P_0 = (P_opt − Σ_s λ̄_s P_s)/λ̄_0 (Eq. CWENO:P0);
+ *   σ_s = p̂_sᵀ Σ p̂_s with the universal Σ;
+ *   ω_s = (λ̄_s/(σ_s+ε)^r) / Σ_m (λ̄_m/(σ_m+ε)^r);
+ *   w = Σ_s ω_s P_s, w[0] := Q_i/ψ_1 (R17).
+ * Output: modal coefficients in the orthonormal Dubiner basis of the owner's
+ * reference element (ordering R8).
+ *
+ * Conventions
+ *   - Indices are 0-based.  After cwreco_set_mesh, cells are renumbered along a
+ *     Morton space-filling curve ("SFC ids", R29); cwreco_get_permutation maps
+ *     SFC id -> input id.
+ *   - LOCAL numbering (what d_avgs / d_coeffs are indexed by): owned cells first
+ *     (interior cells, whose stencils are fully owned, then boundary cells, each
+ *     group in SFC order), then ghost cells ordered by (owner rank, SFC id).  With
+ *     nranks == 1 local == SFC order and there are no ghosts.
+ *   - Host arrays passed in are copied during the call and never retained.
+ *     Device pointers (d_*) are owned by the caller; the library owns the mesh,
+ *     stencils, per-cell matrix blocks and its scratch.
+ *   - Calls that take a stream are asynchronous on it; kernel faults surface as
+ *     CWRECO_ECUDA at a later call.  No exception crosses the ABI.  A context is
+ *     not thread-safe.
+ *   - Every call returns a status; on failure cwreco_last_error() describes it.
+ *   - There is NO CPU fallback: a context created with cuda_device < 0 can do the
+ *     host-side setup (mesh, stencils, matrices) but every compute call returns
+ *     CWRECO_ECUDA.
+ */
+#ifndef CWRECO_H
+#define CWRECO_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct cwreco_ctx cwreco_ctx;
+typedef void* cwreco_stream; /* a cudaStream_t (NULL = legacy default stream) */
+
+typedef enum {
+  CWRECO_OK = 0,
+  CWRECO_EINVAL = 1,      /* bad argument (NULL pointer, negative size, bad stride) */
+  CWRECO_ENOMEM = 2,      /* host or device allocation failed */
+  CWRECO_ECUDA = 3,       /* CUDA runtime error, or no device for a compute call */
+  CWRECO_EMESH = 4,       /* invalid mesh: repeated vertex, duplicate cell,
+                             non-manifold face, zero-volume cell */
+  CWRECO_ESTENCIL = 5,    /* central stencil exhausted (component has < n_e cells) */
+  CWRECO_ESINGULAR = 6,   /* rank-deficient central least-squares system */
+  CWRECO_ESTATE = 7,      /* call out of order (e.g. reconstruct before precompute) */
+  CWRECO_EUNSUPPORTED = 8 /* (d, M, V) outside the compiled range */
+} cwreco_status;
+
+/* Linear weights and WENO parameters.  Defaults: lambda0 = 1e5,
+ * lambda_s = 1, eps = 1e-14, r = 4.  The λ are normalised per cell over the
+ * valid stencils before use (R5, R14). */
+typedef struct {
+  double lambda0;
+  double lambda_s;
+  double eps;
+  int r;
+} cwreco_params;
+
+/* Kernel variant for cwreco_reconstruct. */
+enum {
+  CWRECO_KERNEL_PIPELINED = 0, /* default: TMA-bulk pipelined streaming kernel */
+  CWRECO_KERNEL_SIMPLE = 1     /* one thread per (cell, variable), plain loads */
+};
+
+/* Which owned cells a cwreco_reconstruct call processes (for halo overlap). */
+enum {
+  CWRECO_PART_ALL = 0,
+  CWRECO_PART_INTERIOR = 1, /* tiles made only of interior cells: needs no ghost data */
+  CWRECO_PART_BOUNDARY = 2  /* the remaining tiles: run after the ghost exchange */
+};
+
+/* Sizes and layout facts of a context (valid after cwreco_precompute). */
+typedef struct {
+  int32_t dim, degree_M, nvars, n_modes; /* ℳ(M,d) = (1/d!) Π (M+l) */
+  int32_t n_e;                           /* d·ℳ */
+  int32_t gather_len;                    /* n_e − 1 + extra sector cells outside S_i^0 */
+  int32_t tile_cells;                    /* cells per tile of the packed matrix stream */
+  int32_t chunk_k;                       /* stencil columns per streamed chunk */
+  int64_t n_cells;                       /* global cells */
+  int64_t n_owned, n_ghost, n_interior;
+  int64_t n_tiles, n_interior_tiles;
+  int64_t tile_bytes;                    /* packed bytes per tile */
+  int64_t device_bytes;                  /* device memory held by the context */
+  int64_t algorithmic_bytes_per_cell;    /* SURVEY §8(d) B_cell */
+  int64_t n_invalid_sectors;             /* sectors flagged invalid (R14) */
+  int64_t n_extra_gather;                /* sector cells outside S_i^0 (R15) */
+} cwreco_info;
+
+/* ---------------------------------------------------------------- lifecycle */
+/* dim ∈ {2,3}; degree_M ∈ [1,4] (d=2) or [1,3] (d=3); 1 ≤ nvars ≤ 16.
+ * params may be NULL (defaults).  cuda_device < 0: host-only context.
+ * *out receives the context (NULL on failure). */
+cwreco_status cwreco_create(int dim, int degree_M, int nvars, const cwreco_params* params,
+                            int cuda_device, cwreco_ctx** out);
+void cwreco_destroy(cwreco_ctx* ctx);
+/* Message of the last failing call on this thread (never NULL). */
+const char* cwreco_last_error(void);
+const char* cwreco_version(void);
+cwreco_status cwreco_get_info(const cwreco_ctx* ctx, cwreco_info* out);
+/* CWRECO_KERNEL_* */
+cwreco_status cwreco_set_kernel(cwreco_ctx* ctx, int variant);
+
+/* ---------------------------------------------------------------- mesh / setup */
+/* xyz: [n_nodes][dim] fp64; cell_nodes: [n_cells][dim+1] int64 (any orientation);
+ * period: [dim] box lengths of a periodic box, or NULL for an open domain
+ * (coordinates of a periodic box must lie in [0, period)).  Validates (EMESH),
+ * unwraps periodic images (R16), fixes orientation (R28), computes barycentres
+ * and the Morton order (R29), builds face and node adjacency. */
+cwreco_status cwreco_set_mesh(cwreco_ctx* ctx, int64_t n_nodes, const double* xyz, int64_t n_cells,
+                              const int64_t* cell_nodes, const double* period);
+/* sfc_to_input: [n_cells] out. */
+cwreco_status cwreco_get_permutation(const cwreco_ctx* ctx, int64_t* sfc_to_input);
+/* Ownership: rank owns SFC ids [floor(r·N/P), floor((r+1)·N/P)).  Optional;
+ * default rank 0 of 1.  Must precede cwreco_build_stencils. */
+cwreco_status cwreco_set_partition(cwreco_ctx* ctx, int rank, int nranks);
+/* Central and sectorial stencils of every owned cell (R11-R15),
+ * exact geometric predicates; then ghosts and the local numbering. */
+cwreco_status cwreco_build_stencils(cwreco_ctx* ctx);
+/* Stencils of the owned cells in LOCAL order, entries as global SFC ids:
+ * central [n_owned][n_e] (self first), sectors [n_owned][dim+1][dim+1] (self first,
+ * -1 padded when starved), sector_valid [n_owned][dim+1] (0/1).  Any may be NULL. */
+cwreco_status cwreco_get_stencils(const cwreco_ctx* ctx, int32_t* central, int32_t* sectors,
+                                  uint8_t* sector_valid);
+/* local_to_global: [n_owned + n_ghost] SFC ids of the local cells. */
+cwreco_status cwreco_get_local_cells(const cwreco_ctx* ctx, int64_t* local_to_global);
+/* Per-cell matrices (B⁺ by Householder QR of the reduced LSQ system, sector
+ * inverses), packed into tiles and uploaded to the device (host-only context:
+ * kept on the host).  ESINGULAR if a central system is rank deficient. */
+cwreco_status cwreco_precompute(cwreco_ctx* ctx);
+/* The universal oscillation matrix Σ [ℳ][ℳ] as used by the kernels. */
+cwreco_status cwreco_get_sigma(const cwreco_ctx* ctx, double* out);
+/* Export the packed matrices of selected owned cells (local ids) for tests:
+ * bplus [n][ℳ-1][n_e-1], sinv [n][dim+1][dim][dim], gather [n][gather_len]
+ * (local ids), slots [n][dim+1][dim] (index into gather, 255 = invalid sector).
+ * Any output may be NULL. */
+cwreco_status cwreco_get_blocks(const cwreco_ctx* ctx, int64_t n_sel, const int64_t* cells,
+                                double* bplus, double* sinv, int32_t* gather, uint8_t* slots);
+
+/* ---------------------------------------------------------------- multi-rank halo */
+/* recv_counts [nranks]: ghosts owned by each rank; recv_ids [n_ghost]: their SFC
+ * ids in local ghost order (grouped by owner rank, ascending id). */
+cwreco_status cwreco_halo_plan(const cwreco_ctx* ctx, int64_t* recv_counts, int64_t* recv_ids);
+/* Install what this rank sends: send_counts [nranks], send_ids [Σ counts] = SFC ids
+ * of OWNED cells requested by each peer (peer order, each ascending).  EINVAL if an
+ * id is not owned. */
+cwreco_status cwreco_set_send_lists(cwreco_ctx* ctx, const int64_t* send_counts, const int64_t* send_ids);
+cwreco_status cwreco_send_total(const cwreco_ctx* ctx, int64_t* total);
+/* Pack the requested owned rows of d_avgs into d_sendbuf [send_total][nvars]
+ * (contiguous, peer order) on `stream`.  The caller moves d_sendbuf to the peers'
+ * ghost rows (e.g. NCCL all-to-all-v) before CWRECO_PART_BOUNDARY. */
+cwreco_status cwreco_halo_pack(cwreco_ctx* ctx, const double* d_avgs, int64_t a_cell_stride,
+                               int64_t a_var_stride, double* d_sendbuf, cwreco_stream stream);
+
+/* ---------------------------------------------------------------- hot path */
+/* d_avgs: cell averages of the LOCAL cells, element (c, v) at
+ *   d_avgs[c·a_cell_stride + v·a_var_stride]  (n_owned + n_ghost rows);
+ * d_coeffs: output for the owned cells, coefficient l of (c, v) at
+ *   d_coeffs[c·c_cell_stride + v·c_var_stride + l], l < ℳ.
+ * Strides are in elements (doubles); the fast path wants c_var_stride == ℳ and
+ * c_cell_stride == nvars·ℳ (dense) and 16-byte aligned pointers; other strides
+ * use per-thread stores.  part: CWRECO_PART_*.  Asynchronous on `stream`. */
+cwreco_status cwreco_reconstruct(cwreco_ctx* ctx, const double* d_avgs, int64_t a_cell_stride,
+                                 int64_t a_var_stride, double* d_coeffs, int64_t c_cell_stride,
+                                 int64_t c_var_stride, int part, cwreco_stream stream);
+/* Debug tap (tests): intermediates of n_sel owned cells (local ids), computed by
+ * the SIMPLE kernel and copied to host (synchronises `stream`):
+ *   popt [n][nvars][ℳ], psec [n][dim+1][nvars][dim+1], sigma [n][dim+2][nvars],
+ *   omega [n][dim+2][nvars], w [n][nvars][ℳ].  Any output may be NULL. */
+cwreco_status cwreco_reconstruct_debug(cwreco_ctx* ctx, const double* d_avgs, int64_t a_cell_stride,
+                                       int64_t a_var_stride, int64_t n_sel, const int64_t* cells,
+                                       double* popt, double* psec, double* sigma, double* omega,
+                                       double* w, cwreco_stream stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CWRECO_H */

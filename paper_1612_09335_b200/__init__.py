@@ -1,0 +1,258 @@
+"""Python binding of libcwreco (include/cwreco.h): argument marshalling only.
+
+Every step of the reconstruction runs in the library (host C++ for the one-time
+setup, sm_100a CUDA kernels for the pass).  PyTorch provides device memory and
+streams; there is no CPU fallback — a missing or unbuildable library raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+__all__ = ["Context", "CwrecoError", "lib", "KERNELS", "PART_ALL", "PART_INTERIOR", "PART_BOUNDARY",
+           "n_modes", "setup_context"]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libcwreco.so")
+
+KERNELS = {"pipelined": 0, "simple": 1}
+PART_ALL, PART_INTERIOR, PART_BOUNDARY = 0, 1, 2
+_STATUS = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "ECUDA", 4: "EMESH", 5: "ESTENCIL", 6: "ESINGULAR",
+           7: "ESTATE", 8: "EUNSUPPORTED"}
+
+
+class CwrecoError(RuntimeError):
+    def __init__(self, status, msg):
+        self.status = _STATUS.get(status, str(status))
+        super().__init__(f"cwreco {self.status}: {msg}")
+
+
+class _Params(ctypes.Structure):
+    _fields_ = [("lambda0", ctypes.c_double), ("lambda_s", ctypes.c_double), ("eps", ctypes.c_double),
+                ("r", ctypes.c_int)]
+
+
+class _Info(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in ("dim", "degree_M", "nvars", "n_modes", "n_e", "gather_len",
+                                               "tile_cells", "chunk_k")] + \
+               [(n, ctypes.c_int64) for n in ("n_cells", "n_owned", "n_ghost", "n_interior", "n_tiles",
+                                               "n_interior_tiles", "tile_bytes", "device_bytes",
+                                               "algorithmic_bytes_per_cell", "n_invalid_sectors",
+                                               "n_extra_gather")]
+
+
+def _load():
+    if not os.path.exists(_LIB_PATH):
+        from . import _build
+        _build.build()
+    L = ctypes.CDLL(_LIB_PATH)
+    P, I64, I32, D = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
+    sigs = {
+        "cwreco_create": [I32, I32, I32, P, I32, P],
+        "cwreco_get_info": [P, P],
+        "cwreco_set_kernel": [P, I32],
+        "cwreco_set_mesh": [P, I64, P, I64, P, P],
+        "cwreco_get_permutation": [P, P],
+        "cwreco_set_partition": [P, I32, I32],
+        "cwreco_build_stencils": [P],
+        "cwreco_get_stencils": [P, P, P, P],
+        "cwreco_get_local_cells": [P, P],
+        "cwreco_precompute": [P],
+        "cwreco_get_sigma": [P, P],
+        "cwreco_get_blocks": [P, I64, P, P, P, P, P],
+        "cwreco_halo_plan": [P, P, P],
+        "cwreco_set_send_lists": [P, P, P],
+        "cwreco_send_total": [P, P],
+        "cwreco_halo_pack": [P, P, I64, I64, P, P],
+        "cwreco_reconstruct": [P, P, I64, I64, P, I64, I64, I32, P],
+        "cwreco_reconstruct_debug": [P, P, I64, I64, I64, P, P, P, P, P, P, P],
+    }
+    for name, args in sigs.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = ctypes.c_int
+    L.cwreco_destroy.argtypes = [P]
+    L.cwreco_destroy.restype = None
+    L.cwreco_last_error.restype = ctypes.c_char_p
+    L.cwreco_version.restype = ctypes.c_char_p
+    return L
+
+
+lib = _load()
+
+
+def _check(st):
+    if st != 0:
+        raise CwrecoError(st, lib.cwreco_last_error().decode())
+
+
+def _ptr(a):
+    return None if a is None else ctypes.c_void_p(a.ctypes.data)
+
+
+def n_modes(M, d):
+    num = 1
+    for l in range(1, d + 1):
+        num *= (M + l)
+    return num // (2 if d == 2 else 6)
+
+
+def _stream_handle(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+class Context:
+    """One library context: a mesh, its stencils and per-cell matrices on one device."""
+
+    def __init__(self, dim, degree_M, nvars, device=0, lambda0=1e5, lambda_s=1.0, eps=1e-14, r=4):
+        self.dim, self.M, self.V = int(dim), int(degree_M), int(nvars)
+        self.nm = n_modes(self.M, self.dim)
+        self.device = -1 if device is None else int(device)
+        prm = _Params(lambda0, lambda_s, eps, r)
+        h = ctypes.c_void_p()
+        _check(lib.cwreco_create(self.dim, self.M, self.V, ctypes.byref(prm), self.device, ctypes.byref(h)))
+        self._h = h
+        self.nranks, self.rank = 1, 0
+
+    def close(self):
+        if getattr(self, "_h", None) and lib is not None:
+            lib.cwreco_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        self.close()
+
+    # ---------------------------------------------------------------- setup
+    def set_mesh(self, nodes, cells, period=None):
+        nodes = np.ascontiguousarray(nodes, dtype=np.float64)
+        cells = np.ascontiguousarray(cells, dtype=np.int64)
+        per = None if period is None else np.ascontiguousarray(period, dtype=np.float64)
+        self.N = cells.shape[0]
+        _check(lib.cwreco_set_mesh(self._h, nodes.shape[0], _ptr(nodes), cells.shape[0], _ptr(cells), _ptr(per)))
+
+    def permutation(self):
+        out = np.empty(self.N, dtype=np.int64)
+        _check(lib.cwreco_get_permutation(self._h, _ptr(out)))
+        return out
+
+    def set_partition(self, rank, nranks):
+        self.rank, self.nranks = int(rank), int(nranks)
+        _check(lib.cwreco_set_partition(self._h, self.rank, self.nranks))
+
+    def build_stencils(self):
+        _check(lib.cwreco_build_stencils(self._h))
+
+    def info(self):
+        i = _Info()
+        _check(lib.cwreco_get_info(self._h, ctypes.byref(i)))
+        return {f: getattr(i, f) for f, _ in _Info._fields_}
+
+    def stencils(self):
+        inf = self.info()
+        n, d = inf["n_owned"], self.dim
+        cen = np.empty((n, inf["n_e"]), dtype=np.int32)
+        sec = np.empty((n, d + 1, d + 1), dtype=np.int32)
+        val = np.empty((n, d + 1), dtype=np.uint8)
+        _check(lib.cwreco_get_stencils(self._h, _ptr(cen), _ptr(sec), _ptr(val)))
+        return cen, sec, val.astype(bool)
+
+    def local_cells(self):
+        inf = self.info()
+        out = np.empty(inf["n_owned"] + inf["n_ghost"], dtype=np.int64)
+        _check(lib.cwreco_get_local_cells(self._h, _ptr(out)))
+        return out
+
+    def precompute(self):
+        _check(lib.cwreco_precompute(self._h))
+
+    def sigma(self):
+        out = np.empty((self.nm, self.nm))
+        _check(lib.cwreco_get_sigma(self._h, _ptr(out)))
+        return out
+
+    def blocks(self, cells):
+        cells = np.ascontiguousarray(cells, dtype=np.int64)
+        inf = self.info()
+        n, d = len(cells), self.dim
+        bp = np.empty((n, self.nm - 1, inf["n_e"] - 1))
+        sv = np.empty((n, d + 1, d, d))
+        ga = np.empty((n, inf["gather_len"]), dtype=np.int32)
+        sl = np.empty((n, d + 1, d), dtype=np.uint8)
+        _check(lib.cwreco_get_blocks(self._h, n, _ptr(cells), _ptr(bp), _ptr(sv), _ptr(ga), _ptr(sl)))
+        return dict(bplus=bp, sinv=sv, gather=ga, slots=sl)
+
+    def set_kernel(self, name):
+        _check(lib.cwreco_set_kernel(self._h, KERNELS[name]))
+
+    # ---------------------------------------------------------------- halo
+    def halo_plan(self):
+        inf = self.info()
+        counts = np.empty(self.nranks, dtype=np.int64)
+        ids = np.empty(inf["n_ghost"], dtype=np.int64)
+        _check(lib.cwreco_halo_plan(self._h, _ptr(counts), _ptr(ids)))
+        return counts, ids
+
+    def set_send_lists(self, counts, ids):
+        counts = np.ascontiguousarray(counts, dtype=np.int64)
+        ids = np.ascontiguousarray(ids, dtype=np.int64)
+        _check(lib.cwreco_set_send_lists(self._h, _ptr(counts), _ptr(ids)))
+        self.send_counts = counts
+
+    def send_total(self):
+        t = ctypes.c_int64()
+        _check(lib.cwreco_send_total(self._h, ctypes.byref(t)))
+        return t.value
+
+    def halo_pack(self, avgs, sendbuf, stream=None):
+        a_cs, a_vs = avgs.stride()
+        _check(lib.cwreco_halo_pack(self._h, ctypes.c_void_p(avgs.data_ptr()), a_cs, a_vs,
+                                    ctypes.c_void_p(sendbuf.data_ptr()), _stream_handle(stream)))
+
+    # ---------------------------------------------------------------- hot path
+    def reconstruct(self, avgs, out=None, part=PART_ALL, stream=None):
+        """avgs: CUDA float64 tensor [n_local, V] (any strides); returns / fills
+        out [n_owned, V, ℳ] (float64, CUDA)."""
+        import torch
+        if not (avgs.is_cuda and avgs.dtype == torch.float64 and avgs.dim() == 2):
+            raise ValueError("avgs must be a 2-D float64 CUDA tensor")
+        if out is None:
+            n_owned = self.info()["n_owned"]
+            out = torch.empty((n_owned, self.V, self.nm), dtype=torch.float64, device=avgs.device)
+        a_cs, a_vs = avgs.stride()
+        c_cs, c_vs, c_ls = out.stride()
+        if c_ls != 1:
+            raise ValueError("out must be contiguous along the mode axis")
+        _check(lib.cwreco_reconstruct(self._h, ctypes.c_void_p(avgs.data_ptr()), a_cs, a_vs,
+                                      ctypes.c_void_p(out.data_ptr()), c_cs, c_vs, int(part),
+                                      _stream_handle(stream)))
+        return out
+
+    def reconstruct_debug(self, avgs, cells, stream=None):
+        cells = np.ascontiguousarray(cells, dtype=np.int64)
+        n, V, nm, d = len(cells), self.V, self.nm, self.dim
+        popt = np.empty((n, V, nm))
+        psec = np.empty((n, d + 1, V, d + 1))
+        sig = np.empty((n, d + 2, V))
+        om = np.empty((n, d + 2, V))
+        w = np.empty((n, V, nm))
+        a_cs, a_vs = avgs.stride()
+        _check(lib.cwreco_reconstruct_debug(self._h, ctypes.c_void_p(avgs.data_ptr()), a_cs, a_vs, n, _ptr(cells),
+                                            _ptr(popt), _ptr(psec), _ptr(sig), _ptr(om), _ptr(w),
+                                            _stream_handle(stream)))
+        return dict(popt=popt, psec=psec, sigma=sig, omega=om, w=w)
+
+
+def setup_context(nodes, cells, period, degree_M, nvars, device=0, rank=0, nranks=1, **params):
+    """set_mesh → set_partition → build_stencils → precompute."""
+    ctx = Context(nodes.shape[1], degree_M, nvars, device, **params)
+    ctx.set_mesh(nodes, cells, period)
+    if nranks > 1:
+        ctx.set_partition(rank, nranks)
+    ctx.build_stencils()
+    ctx.precompute()
+    return ctx

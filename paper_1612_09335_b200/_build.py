@@ -1,0 +1,67 @@
+"""Build libcwreco.so in-tree: host C++ (g++, OpenMP) + sm_100a CUDA (nvcc).
+
+Called by __graft_entry__.build() and by the package on first import when the
+library is missing.  Sources: paper_1612_09335_b200/csrc/, header: include/.
+"""
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+INC = os.path.join(ROOT, "include")
+OUT = os.path.join(HERE, "libcwreco.so")
+BUILD = os.path.join(HERE, "build")
+
+CXX_SRCS = ["api.cpp", "mesh.cpp", "stencil.cpp", "basis.cpp", "precompute.cpp"]
+CU_SRCS = ["kernels.cu"]
+CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
+# -ffp-contract=off: the IEEE-specified geometry (R29) must not be fused; -mfma
+# lets std::fma (exact products in the predicates) use the hardware instruction.
+CXXFLAGS = ["-O3", "-std=c++17", "-fPIC", "-fopenmp", "-mfma", "-ffp-contract=off", "-Wall",
+            "-Wno-unused-function", "-I", INC, "-I", CSRC]
+NVFLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
+           "-Xcompiler", "-fPIC", "-Xptxas", "-v", "-I", INC, "-I", CSRC]
+
+
+def _run(cmd, log):
+    r = subprocess.run(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
+    log.write(" ".join(cmd) + "\n" + r.stdout + "\n")
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout)
+        raise RuntimeError("build failed: " + " ".join(cmd))
+    return r.stdout
+
+
+def build(verbose=False):
+    os.makedirs(BUILD, exist_ok=True)
+    objs = []
+    with open(os.path.join(BUILD, "build.log"), "w") as log:
+        for s in CXX_SRCS:
+            o = os.path.join(BUILD, s + ".o")
+            _run(["g++", *CXXFLAGS, "-c", os.path.join(CSRC, s), "-o", o], log)
+            objs.append(o)
+        for s in CU_SRCS:
+            o = os.path.join(BUILD, s + ".o")
+            out = _run([NVCC, *NVFLAGS, "-c", os.path.join(CSRC, s), "-o", o], log)
+            if verbose:
+                print(out)
+            objs.append(o)
+        _run(["g++", "-shared", "-o", OUT + ".tmp", *objs, "-fopenmp", "-L" + os.path.join(CUDA_HOME, "lib64"),
+              "-lcudart_static", "-lrt", "-ldl", "-lpthread"], log)
+    os.replace(OUT + ".tmp", OUT)
+    return OUT
+
+
+def needs_build():
+    if not os.path.exists(OUT):
+        return True
+    t = os.path.getmtime(OUT)
+    srcs = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(INC, "cwreco.h")]
+    return any(os.path.getmtime(s) > t for s in srcs)
+
+
+if __name__ == "__main__":
+    print(build(verbose="-v" in sys.argv))

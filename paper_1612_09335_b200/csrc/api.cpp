@@ -1,0 +1,325 @@
+// extern "C" surface of libcwreco (include/cwreco.h).  Converts exceptions to
+// status codes; keeps a thread-local last-error message.
+#include <cstring>
+#include <string>
+
+#include "internal.hpp"
+
+namespace {
+
+thread_local std::string g_last_error = "no error";
+
+template <class F>
+cwreco_status guard(F&& f) {
+  try {
+    f();
+    return CWRECO_OK;
+  } catch (const cwr::Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failed";
+    return CWRECO_ENOMEM;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return CWRECO_EINVAL;
+  } catch (...) {
+    g_last_error = "unknown error";
+    return CWRECO_EINVAL;
+  }
+}
+
+void need(bool cond, cwreco_status s, const char* msg) {
+  if (!cond) cwr::fail(s, msg);
+}
+
+void need_device(const cwreco_ctx* c, const char* what) {
+  if (c->device < 0 || !c->dev)
+    cwr::fail(CWRECO_ECUDA, std::string(what) + ": host-only context (no CUDA device); there is no CPU fallback");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* cwreco_last_error(void) { return g_last_error.c_str(); }
+
+const char* cwreco_version(void) { return "cwreco 0.1.0 (sm_100a)"; }
+
+cwreco_status cwreco_create(int dim, int degree_M, int nvars, const cwreco_params* params, int cuda_device,
+                            cwreco_ctx** out) {
+  return guard([&] {
+    need(out != nullptr, CWRECO_EINVAL, "create: out is NULL");
+    *out = nullptr;
+    need(dim == 2 || dim == 3, CWRECO_EUNSUPPORTED, "create: dim must be 2 or 3");
+    need(degree_M >= 1 && degree_M <= (dim == 2 ? 4 : 3), CWRECO_EUNSUPPORTED, "create: degree out of range");
+    need(nvars >= 1 && nvars <= 16, CWRECO_EUNSUPPORTED, "create: nvars must be in [1, 16]");
+    if (params) {
+      need(params->lambda0 > 0 && params->lambda_s > 0 && params->eps > 0 && params->r >= 1 && params->r <= 16,
+           CWRECO_EINVAL, "create: lambda0, lambda_s, eps must be > 0 and 1 <= r <= 16");
+    }
+    auto* c = new cwreco_ctx();
+    c->d = dim;
+    c->M = degree_M;
+    c->V = nvars;
+    c->nm = cwr::n_modes(degree_M, dim);
+    c->ne = dim * c->nm;
+    if (params) c->prm = *params;
+    c->device = cuda_device;
+    try {
+      cwr::dev_create(c);
+    } catch (...) {
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+
+void cwreco_destroy(cwreco_ctx* ctx) {
+  if (!ctx) return;
+  try {
+    cwr::dev_destroy(ctx);
+  } catch (...) {
+  }
+  delete ctx;
+}
+
+cwreco_status cwreco_get_info(const cwreco_ctx* c, cwreco_info* o) {
+  return guard([&] {
+    need(c && o, CWRECO_EINVAL, "get_info: NULL");
+    std::memset(o, 0, sizeof(*o));
+    o->dim = c->d;
+    o->degree_M = c->M;
+    o->nvars = c->V;
+    o->n_modes = c->nm;
+    o->n_e = c->ne;
+    o->gather_len = c->G;
+    o->n_cells = c->N;
+    o->n_owned = c->n_owned;
+    o->n_ghost = c->n_ghost;
+    o->n_interior = c->n_interior;
+    o->n_invalid_sectors = c->n_invalid;
+    o->n_extra_gather = c->n_extra;
+    if (c->has_blocks) {
+      o->tile_cells = c->lay.T;
+      o->chunk_k = c->lay.KC;
+      o->n_tiles = c->n_tiles;
+      o->n_interior_tiles = c->n_int_tiles;
+      o->tile_bytes = c->lay.tile_bytes;
+    }
+    o->device_bytes = cwr::dev_bytes(c);
+    const int d = c->d, nm = c->nm, ne = c->ne, V = c->V;
+    // 8[(ℳ-1)(n_e-1) + (d+1)d²] + 4(n_e-1) + (d+1)d + 8V + 8ℳV
+    o->algorithmic_bytes_per_cell =
+        8LL * ((nm - 1) * (ne - 1) + (d + 1) * d * d) + 4LL * (ne - 1) + (d + 1) * d + 8LL * V + 8LL * nm * V;
+  });
+}
+
+cwreco_status cwreco_set_kernel(cwreco_ctx* c, int variant) {
+  return guard([&] {
+    need(c != nullptr, CWRECO_EINVAL, "set_kernel: NULL");
+    need(variant == CWRECO_KERNEL_PIPELINED || variant == CWRECO_KERNEL_SIMPLE, CWRECO_EINVAL,
+         "set_kernel: unknown variant");
+    c->kernel = variant;
+  });
+}
+
+cwreco_status cwreco_set_mesh(cwreco_ctx* c, int64_t n_nodes, const double* xyz, int64_t n_cells,
+                              const int64_t* cell_nodes, const double* period) {
+  return guard([&] {
+    need(c != nullptr, CWRECO_EINVAL, "set_mesh: NULL ctx");
+    cwr::set_mesh(c, n_nodes, xyz, n_cells, cell_nodes, period);
+  });
+}
+
+cwreco_status cwreco_get_permutation(const cwreco_ctx* c, int64_t* out) {
+  return guard([&] {
+    need(c && out, CWRECO_EINVAL, "get_permutation: NULL");
+    need(c->has_mesh, CWRECO_ESTATE, "get_permutation: no mesh");
+    std::memcpy(out, c->perm.data(), sizeof(int64_t) * c->N);
+  });
+}
+
+cwreco_status cwreco_set_partition(cwreco_ctx* c, int rank, int nranks) {
+  return guard([&] {
+    need(c != nullptr, CWRECO_EINVAL, "set_partition: NULL");
+    need(nranks >= 1 && rank >= 0 && rank < nranks, CWRECO_EINVAL, "set_partition: bad rank/nranks");
+    c->rank = rank;
+    c->nranks = nranks;
+    c->has_stencils = c->has_blocks = false;
+    if (c->has_mesh) {
+      c->own_lo = (rank * c->N) / nranks;
+      c->own_hi = ((rank + 1) * c->N) / nranks;
+    }
+  });
+}
+
+cwreco_status cwreco_build_stencils(cwreco_ctx* c) {
+  return guard([&] {
+    need(c != nullptr, CWRECO_EINVAL, "build_stencils: NULL");
+    need(c->has_mesh, CWRECO_ESTATE, "build_stencils: call cwreco_set_mesh first");
+    need(c->own_hi > c->own_lo, CWRECO_EINVAL, "build_stencils: this rank owns no cells");
+    cwr::build_stencils(c);
+  });
+}
+
+cwreco_status cwreco_get_stencils(const cwreco_ctx* c, int32_t* central, int32_t* sectors, uint8_t* valid) {
+  return guard([&] {
+    need(c != nullptr, CWRECO_EINVAL, "get_stencils: NULL");
+    need(c->has_stencils, CWRECO_ESTATE, "get_stencils: no stencils");
+    const int ne = c->ne, nv = c->d + 1;
+    for (int64_t li = 0; li < c->n_owned; ++li) {
+      const int64_t q = c->local2global[li] - c->own_lo;
+      if (central) std::memcpy(central + li * ne, &c->central[q * ne], sizeof(int32_t) * ne);
+      if (sectors) std::memcpy(sectors + li * nv * nv, &c->sectors[q * nv * nv], sizeof(int32_t) * nv * nv);
+      if (valid) std::memcpy(valid + li * nv, &c->valid[q * nv], nv);
+    }
+  });
+}
+
+cwreco_status cwreco_get_local_cells(const cwreco_ctx* c, int64_t* out) {
+  return guard([&] {
+    need(c && out, CWRECO_EINVAL, "get_local_cells: NULL");
+    need(c->has_stencils, CWRECO_ESTATE, "get_local_cells: no stencils");
+    std::memcpy(out, c->local2global.data(), sizeof(int64_t) * c->local2global.size());
+  });
+}
+
+cwreco_status cwreco_precompute(cwreco_ctx* c) {
+  return guard([&] {
+    need(c != nullptr, CWRECO_EINVAL, "precompute: NULL");
+    cwr::precompute(c);
+  });
+}
+
+cwreco_status cwreco_get_sigma(const cwreco_ctx* c, double* out) {
+  return guard([&] {
+    need(c && out, CWRECO_EINVAL, "get_sigma: NULL");
+    std::vector<double> S = c->sigma.empty() ? cwr::sigma_matrix(c->d, c->M) : c->sigma;
+    std::memcpy(out, S.data(), sizeof(double) * S.size());
+  });
+}
+
+cwreco_status cwreco_get_blocks(const cwreco_ctx* c, int64_t n_sel, const int64_t* cells, double* bplus, double* sinv,
+                                int32_t* gather, uint8_t* slots) {
+  return guard([&] {
+    need(c && (n_sel == 0 || cells), CWRECO_EINVAL, "get_blocks: NULL");
+    need(c->has_blocks, CWRECO_ESTATE, "get_blocks: call cwreco_precompute first");
+    const cwr::Layout& L = c->lay;
+    const int T = L.T, R = L.R, K = L.K, G = L.G, d = c->d, nv = d + 1;
+    std::vector<unsigned char> tile(L.tile_bytes);
+    int64_t cur = -1;
+    for (int64_t s = 0; s < n_sel; ++s) {
+      const int64_t li = cells[s];
+      need(li >= 0 && li < c->n_owned, CWRECO_EINVAL, "get_blocks: cell out of range");
+      const int64_t t = li / T;
+      const int ct = int(li % T);
+      const unsigned char* tb;
+      if (!c->host_blocks.empty()) {
+        tb = c->host_blocks.data() + t * L.tile_bytes;
+      } else {
+        if (t != cur) {
+          cwr::dev_download_tile(c, t, tile.data());
+          cur = t;
+        }
+        tb = tile.data();
+      }
+      const int32_t* ids = (const int32_t*)(tb + L.off_ids);
+      const double* sv = (const double*)(tb + L.off_sinv);
+      const uint8_t* sl = (const uint8_t*)(tb + L.off_slots);
+      const double* B = (const double*)(tb + L.off_chunks);
+      if (bplus)
+        for (int l = 0; l < R; ++l)
+          for (int k = 0; k < K; ++k) bplus[(s * R + l) * K + k] = B[((size_t)k * T + ct) * R + l];
+      if (sinv) std::memcpy(sinv + s * nv * d * d, sv + (size_t)ct * nv * d * d, sizeof(double) * nv * d * d);
+      if (gather)
+        for (int k = 0; k < G; ++k) gather[s * G + k] = ids[(size_t)k * T + ct];
+      if (slots) std::memcpy(slots + s * nv * d, sl + (size_t)ct * nv * d, nv * d);
+    }
+  });
+}
+
+cwreco_status cwreco_halo_plan(const cwreco_ctx* c, int64_t* recv_counts, int64_t* recv_ids) {
+  return guard([&] {
+    need(c != nullptr, CWRECO_EINVAL, "halo_plan: NULL");
+    need(c->has_stencils, CWRECO_ESTATE, "halo_plan: no stencils");
+    if (recv_counts) std::memcpy(recv_counts, c->ghost_counts.data(), sizeof(int64_t) * c->nranks);
+    if (recv_ids)
+      std::memcpy(recv_ids, c->local2global.data() + c->n_owned, sizeof(int64_t) * c->n_ghost);
+  });
+}
+
+cwreco_status cwreco_set_send_lists(cwreco_ctx* c, const int64_t* send_counts, const int64_t* send_ids) {
+  return guard([&] {
+    need(c && send_counts, CWRECO_EINVAL, "set_send_lists: NULL");
+    need(c->has_stencils, CWRECO_ESTATE, "set_send_lists: no stencils");
+    int64_t tot = 0;
+    for (int r = 0; r < c->nranks; ++r) {
+      need(send_counts[r] >= 0, CWRECO_EINVAL, "set_send_lists: negative count");
+      tot += send_counts[r];
+    }
+    need(tot == 0 || send_ids, CWRECO_EINVAL, "set_send_lists: NULL ids");
+    std::vector<int32_t> own2local(c->own_hi - c->own_lo, -1);
+    for (int64_t li = 0; li < c->n_owned; ++li) own2local[c->local2global[li] - c->own_lo] = (int32_t)li;
+    std::vector<int64_t> loc(tot);
+    for (int64_t k = 0; k < tot; ++k) {
+      const int64_t g = send_ids[k];
+      need(g >= c->own_lo && g < c->own_hi, CWRECO_EINVAL, "set_send_lists: id not owned by this rank");
+      loc[k] = own2local[g - c->own_lo];
+    }
+    c->send_counts.assign(send_counts, send_counts + c->nranks);
+    c->send_local = loc;
+    cwr::dev_set_send(c);
+  });
+}
+
+cwreco_status cwreco_send_total(const cwreco_ctx* c, int64_t* total) {
+  return guard([&] {
+    need(c && total, CWRECO_EINVAL, "send_total: NULL");
+    *total = (int64_t)c->send_local.size();
+  });
+}
+
+cwreco_status cwreco_halo_pack(cwreco_ctx* c, const double* d_avgs, int64_t acs, int64_t avs, double* d_sendbuf,
+                               cwreco_stream stream) {
+  return guard([&] {
+    need(c != nullptr, CWRECO_EINVAL, "halo_pack: NULL");
+    need_device(c, "halo_pack");
+    if (c->send_local.empty()) return;
+    need(d_avgs && d_sendbuf, CWRECO_EINVAL, "halo_pack: NULL buffer");
+    cwr::dev_halo_pack(c, d_avgs, acs, avs, d_sendbuf, stream);
+  });
+}
+
+cwreco_status cwreco_reconstruct(cwreco_ctx* c, const double* d_avgs, int64_t acs, int64_t avs, double* d_coeffs,
+                                 int64_t ccs, int64_t cvs, int part, cwreco_stream stream) {
+  return guard([&] {
+    need(c != nullptr, CWRECO_EINVAL, "reconstruct: NULL ctx");
+    need_device(c, "reconstruct");
+    need(c->has_blocks, CWRECO_ESTATE, "reconstruct: call cwreco_precompute first");
+    need(d_avgs && d_coeffs, CWRECO_EINVAL, "reconstruct: NULL buffer");
+    need(acs >= 1 && avs >= 1 && ccs >= 1 && cvs >= 1, CWRECO_EINVAL, "reconstruct: strides must be >= 1");
+    need(cvs >= c->nm && ccs >= (int64_t)cvs * 1, CWRECO_EINVAL, "reconstruct: coefficient rows overlap");
+    need(part == CWRECO_PART_ALL || part == CWRECO_PART_INTERIOR || part == CWRECO_PART_BOUNDARY, CWRECO_EINVAL,
+         "reconstruct: bad part");
+    cwr::dev_reconstruct(c, d_avgs, acs, avs, d_coeffs, ccs, cvs, part, stream);
+  });
+}
+
+cwreco_status cwreco_reconstruct_debug(cwreco_ctx* c, const double* d_avgs, int64_t acs, int64_t avs, int64_t n_sel,
+                                       const int64_t* cells, double* popt, double* psec, double* sigma,
+                                       double* omega, double* w, cwreco_stream stream) {
+  return guard([&] {
+    need(c != nullptr, CWRECO_EINVAL, "reconstruct_debug: NULL ctx");
+    need_device(c, "reconstruct_debug");
+    need(c->has_blocks, CWRECO_ESTATE, "reconstruct_debug: call cwreco_precompute first");
+    need(d_avgs && (n_sel == 0 || cells), CWRECO_EINVAL, "reconstruct_debug: NULL");
+    for (int64_t s = 0; s < n_sel; ++s)
+      need(cells[s] >= 0 && cells[s] < c->n_owned, CWRECO_EINVAL, "reconstruct_debug: cell out of range");
+    if (n_sel == 0) return;
+    cwr::dev_debug(c, d_avgs, acs, avs, n_sel, cells, popt, psec, sigma, omega, w, stream);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,122 @@
+// Internal declarations of libcwreco (not part of the ABI; see include/cwreco.h).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "cwreco.h"
+
+namespace cwr {
+
+// Error carrying a status code; converted to cwreco_status at the ABI boundary.
+struct Error : std::runtime_error {
+  cwreco_status code;
+  Error(cwreco_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void fail(cwreco_status c, const std::string& m) { throw Error(c, m); }
+
+inline int n_modes(int M, int d) {  // ℳ(M,d) = (1/d!) Π_{l=1..d} (M+l)
+  long num = 1, den = 1;
+  for (int l = 1; l <= d; ++l) { num *= (M + l); den *= l; }
+  return int(num / den);
+}
+
+// Layout of one packed tile of the matrix stream.
+//   header:  ids   int32  [G][T]          gather list (local cell ids), k-major
+//            sinv  double [T][d+1][d][d]  sector inverses
+//            slots uint8  [T][d+1][d]     sector cell -> gather index, 255 = invalid
+//   chunks:  B     double [K][T][R]       reduced pseudo-inverse, k-major, split in
+//                                         chunks of KC k-slices (last chunk shorter)
+struct Layout {
+  int d = 0, M = 0, V = 0, nm = 0, R = 0, K = 0, G = 0, T = 0, KC = 0, NCH = 0;
+  int64_t off_ids = 0, off_sinv = 0, off_slots = 0, header_bytes = 0;
+  int64_t off_chunks = 0, kslice_bytes = 0, tile_bytes = 0;
+};
+
+Layout make_layout(int d, int M, int V, int G);
+
+struct DeviceState;  // kernels.cu
+
+}  // namespace cwr
+
+struct cwreco_ctx {
+  int d = 0, M = 0, V = 0, nm = 0, ne = 0;
+  cwreco_params prm{1e5, 1.0, 1e-14, 4};
+  int device = -1;
+  int kernel = CWRECO_KERNEL_PIPELINED;
+
+  // ---- mesh, SFC order (set_mesh)
+  bool has_mesh = false;
+  int64_t N = 0, Nn = 0;
+  bool periodic = false;
+  double L[3] = {0, 0, 0};
+  std::vector<int64_t> perm;        // sfc -> input id
+  std::vector<int64_t> cell_nodes;  // [N][d+1], orientation fixed
+  std::vector<double> X;            // [N][d+1][d] unwrapped vertex coordinates
+  std::vector<double> bary;         // [N][d] IEEE barycentres (R29)
+  std::vector<int64_t> nbr;         // [N][d+1] face neighbours, -1 none
+  std::vector<int64_t> nc_ptr, nc_idx;  // node -> cells (SFC ids, ascending)
+
+  // ---- partition
+  int rank = 0, nranks = 1;
+  int64_t own_lo = 0, own_hi = 0;
+
+  // ---- stencils (build_stencils), owned cells in SFC order (index = sfc - own_lo)
+  bool has_stencils = false;
+  std::vector<int32_t> central;  // [n_own][ne] global SFC ids
+  std::vector<int32_t> sectors;  // [n_own][d+1][d+1] global, -1 padded
+  std::vector<uint8_t> valid;    // [n_own][d+1]
+
+  // ---- local numbering
+  int64_t n_owned = 0, n_ghost = 0, n_interior = 0;
+  std::vector<int64_t> local2global;   // [n_owned + n_ghost]
+  std::vector<int64_t> ghost_counts;   // [nranks]
+  std::vector<int64_t> send_counts;    // [nranks]
+  std::vector<int64_t> send_local;     // local ids of owned cells to send
+  int G = 0;                           // gather length
+  int64_t n_extra = 0, n_invalid = 0;
+
+  // ---- packed blocks
+  bool has_blocks = false;
+  cwr::Layout lay;
+  int64_t n_tiles = 0, n_int_tiles = 0;
+  std::vector<unsigned char> host_blocks;  // kept only for host-only contexts
+  std::vector<double> sigma;               // ℳ×ℳ universal Σ
+  double psi1 = 0;                         // constant basis function value
+
+  cwr::DeviceState* dev = nullptr;
+};
+
+namespace cwr {
+// mesh.cpp
+void set_mesh(cwreco_ctx* c, int64_t n_nodes, const double* xyz, int64_t n_cells,
+              const int64_t* cells, const double* period);
+// stencil.cpp
+void build_stencils(cwreco_ctx* c);
+// basis.cpp
+void basis_eval(int d, int M, const double* xi, double* out);  // ψ_l(ξ), l < ℳ
+std::vector<double> sigma_matrix(int d, int M);                  // Σ by quadrature
+void gauss_legendre01(int n, std::vector<double>& x, std::vector<double>& w);
+// precompute.cpp
+void precompute(cwreco_ctx* c);
+// kernels.cu (device side; all return cudaError_t as int)
+void dev_create(cwreco_ctx* c);
+void dev_destroy(cwreco_ctx* c);
+void dev_alloc_blocks(cwreco_ctx* c, int64_t bytes);
+void dev_upload_blocks(cwreco_ctx* c, int64_t offset, const unsigned char* host, int64_t bytes);
+void dev_upload_aux(cwreco_ctx* c);
+void dev_download_tile(const cwreco_ctx* c, int64_t tile, unsigned char* host);
+void dev_reconstruct(cwreco_ctx* c, const double* avgs, int64_t acs, int64_t avs, double* coeffs,
+                     int64_t ccs, int64_t cvs, int part, void* stream);
+void dev_debug(cwreco_ctx* c, const double* avgs, int64_t acs, int64_t avs, int64_t n_sel,
+               const int64_t* cells, double* popt, double* psec, double* sigma, double* omega,
+               double* w, void* stream);
+void dev_halo_pack(cwreco_ctx* c, const double* avgs, int64_t acs, int64_t avs, double* sendbuf,
+                   void* stream);
+int64_t dev_bytes(const cwreco_ctx* c);
+void dev_set_send(cwreco_ctx* c);
+}  // namespace cwr

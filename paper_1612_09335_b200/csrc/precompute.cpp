@@ -1,0 +1,353 @@
+// Per-cell reconstruction matrices (Eulerian pre-processing) packed into
+// the tiled HBM stream consumed by the kernels.
+//
+//  A[k][l] = average over stencil cell j(k) (periodic image nearest the owner) of
+//            ψ_l(ξ_i(x)), the basis in the OWNER's reference coordinates;
+//            collapsed Gauss-Legendre quadrature exact for degree M (R19).
+//  Constrained LSQ (R10): the owner row fixes p̂_1 = Q_i/ψ_1 (only ψ_1
+//  has a non-zero mean on T_E), leaving the reduced problem
+//      min ‖A[1:,1:] p − (Q_j − Q_i)‖₂,
+//  whose pseudo-inverse B⁺ = R⁻¹Qᵀ comes from a Householder QR.
+//  Sectors: the linear modes averaged over a cell equal their value at
+//  the cell barycentre, so A_s[m][l] = ψ_{l+1}(ξ_i(b_{j_m})); S_s = A_s⁻¹ (d×d).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <unordered_map>
+
+#include "internal.hpp"
+
+namespace cwr {
+
+static inline int64_t r16(int64_t x) { return (x + 15) & ~int64_t(15); }
+
+Layout make_layout(int d, int M, int V, int G) {
+  Layout L;
+  L.d = d;
+  L.M = M;
+  L.V = V;
+  L.nm = n_modes(M, d);
+  L.R = L.nm - 1;
+  L.K = d * L.nm - 1;
+  L.G = G;
+  int T = (320 / V) & ~1;
+  if (T < 2) T = 2;
+  if (T > 128) T = 128;
+  L.T = T;
+  L.kslice_bytes = int64_t(T) * L.R * 8;
+  L.KC = std::max<int>(1, int(20480 / L.kslice_bytes));
+  L.KC = std::min(std::min(L.KC, L.K), 8);  // kernels unroll up to 8 k-slices
+  L.NCH = (L.K + L.KC - 1) / L.KC;
+  L.off_ids = 0;
+  L.off_sinv = r16(int64_t(G) * T * 4);
+  L.off_slots = L.off_sinv + int64_t(T) * (d + 1) * d * d * 8;
+  L.header_bytes = r16(L.off_slots + int64_t(T) * (d + 1) * d);
+  L.off_chunks = L.header_bytes;
+  L.tile_bytes = r16(L.off_chunks + int64_t(L.K) * L.kslice_bytes);
+  return L;
+}
+
+namespace {
+
+void shift_of(const cwreco_ctx* c, int64_t i, int64_t j, double* sh) {
+  const int d = c->d;
+  for (int a = 0; a < d; ++a) {
+    int n = 0;
+    if (c->periodic) {
+      const double L = c->L[a];
+      double r = c->bary[j * d + a] - c->bary[i * d + a];
+      while (r > 0.5 * L) { r -= L; n -= 1; }
+      while (r < -0.5 * L) { r += L; n += 1; }
+    }
+    sh[a] = c->periodic ? n * c->L[a] : 0.0;
+  }
+}
+
+bool inv_small(int d, const double* A, double* Ainv) {
+  if (d == 2) {
+    double det = A[0] * A[3] - A[1] * A[2];
+    if (det == 0.0 || !std::isfinite(det)) return false;
+    Ainv[0] = A[3] / det;
+    Ainv[1] = -A[1] / det;
+    Ainv[2] = -A[2] / det;
+    Ainv[3] = A[0] / det;
+    return true;
+  }
+  double c00 = A[4] * A[8] - A[5] * A[7], c01 = A[5] * A[6] - A[3] * A[8], c02 = A[3] * A[7] - A[4] * A[6];
+  double det = A[0] * c00 + A[1] * c01 + A[2] * c02;
+  if (det == 0.0 || !std::isfinite(det)) return false;
+  Ainv[0] = c00 / det;
+  Ainv[1] = (A[2] * A[7] - A[1] * A[8]) / det;
+  Ainv[2] = (A[1] * A[5] - A[2] * A[4]) / det;
+  Ainv[3] = c01 / det;
+  Ainv[4] = (A[0] * A[8] - A[2] * A[6]) / det;
+  Ainv[5] = (A[2] * A[3] - A[0] * A[5]) / det;
+  Ainv[6] = c02 / det;
+  Ainv[7] = (A[1] * A[6] - A[0] * A[7]) / det;
+  Ainv[8] = (A[0] * A[4] - A[1] * A[3]) / det;
+  return true;
+}
+
+// Householder QR of Ared (m×n, column-major), returns B⁺ (n×m, row-major)
+bool pinv_qr(int m, int n, std::vector<double>& A, std::vector<double>& Bp, double& cond) {
+  std::vector<double> V(size_t(m) * n, 0.0), beta(n), Rd(n);
+  for (int j = 0; j < n; ++j) {
+    double* a = &A[size_t(j) * m];
+    double nrm = 0.0;
+    for (int r = j; r < m; ++r) nrm += a[r] * a[r];
+    nrm = std::sqrt(nrm);
+    if (nrm == 0.0) return false;
+    double alpha = a[j] > 0 ? -nrm : nrm;
+    double* v = &V[size_t(j) * m];
+    for (int r = j; r < m; ++r) v[r] = a[r];
+    v[j] -= alpha;
+    double vn = 0.0;
+    for (int r = j; r < m; ++r) vn += v[r] * v[r];
+    beta[j] = vn > 0 ? 2.0 / vn : 0.0;
+    for (int cidx = j; cidx < n; ++cidx) {
+      double* ac = &A[size_t(cidx) * m];
+      double s = 0.0;
+      for (int r = j; r < m; ++r) s += v[r] * ac[r];
+      s *= beta[j];
+      for (int r = j; r < m; ++r) ac[r] -= s * v[r];
+    }
+    Rd[j] = A[size_t(j) * m + j];
+  }
+  double rmax = 0.0, rmin = 1e300;
+  for (int j = 0; j < n; ++j) {
+    rmax = std::max(rmax, std::fabs(Rd[j]));
+    rmin = std::min(rmin, std::fabs(Rd[j]));
+  }
+  if (!(rmin > 1e-12 * rmax)) return false;
+  cond = rmax / rmin;
+  Bp.assign(size_t(n) * m, 0.0);
+  std::vector<double> y(m);
+  for (int k = 0; k < m; ++k) {
+    std::fill(y.begin(), y.end(), 0.0);
+    y[k] = 1.0;
+    for (int j = 0; j < n; ++j) {  // y = Qᵀ e_k
+      const double* v = &V[size_t(j) * m];
+      double s = 0.0;
+      for (int r = j; r < m; ++r) s += v[r] * y[r];
+      s *= beta[j];
+      for (int r = j; r < m; ++r) y[r] -= s * v[r];
+    }
+    for (int j = n - 1; j >= 0; --j) {  // R x = y[0..n)
+      double s = y[j];
+      for (int q = j + 1; q < n; ++q) s -= A[size_t(q) * m + j] * y[q];
+      y[j] = s / A[size_t(j) * m + j];
+    }
+    for (int j = 0; j < n; ++j) Bp[size_t(j) * m + k] = y[j];
+  }
+  return true;
+}
+
+}  // namespace
+
+// Build the packed tiles for local owned cells [0, n_owned) and hand them to the
+// device (or keep them on the host for a host-only context).
+void precompute(cwreco_ctx* c) {
+  if (!c->has_stencils) fail(CWRECO_ESTATE, "precompute: call cwreco_build_stencils first");
+  const int d = c->d, M = c->M, nm = c->nm, ne = c->ne, nv = d + 1;
+  const int R = nm - 1, K = ne - 1;
+  c->lay = make_layout(d, M, c->V, c->G);
+  const Layout& L = c->lay;
+  const int T = L.T, G = L.G;
+  c->n_tiles = (c->n_owned + T - 1) / T;
+  c->n_int_tiles = (c->n_interior == c->n_owned) ? c->n_tiles : c->n_interior / T;
+  c->sigma = sigma_matrix(d, M);
+  {
+    double xi[3] = {0.25, 0.25, 0.25}, psi[64];
+    basis_eval(d, M, xi, psi);
+    c->psi1 = psi[0];
+  }
+
+  // global -> local map
+  const int64_t n_loc = c->n_owned + c->n_ghost;
+  std::vector<int32_t> own2local(c->own_hi - c->own_lo, -1);
+  for (int64_t li = 0; li < c->n_owned; ++li) own2local[c->local2global[li] - c->own_lo] = (int32_t)li;
+  auto to_local = [&](int64_t g) -> int32_t {
+    if (g >= c->own_lo && g < c->own_hi) return own2local[g - c->own_lo];
+    auto b = c->local2global.begin() + c->n_owned, e = c->local2global.begin() + n_loc;
+    auto it = std::lower_bound(b, e, g);
+    if (it == e || *it != g) return -1;
+    return (int32_t)(it - c->local2global.begin());
+  };
+
+  // quadrature on T_E exact for degree M + d - 1 per collapsed direction (R19)
+  std::vector<double> gx, gw;
+  gauss_legendre01((M + d + 1) / 2, gx, gw);  // 2n-1 >= M+d-1
+  std::vector<double> qp, qw;  // points [nq][d], weights normalised to 1
+  {
+    const int n = (int)gx.size();
+    double wsum = 0.0;
+    if (d == 2) {
+      for (int a = 0; a < n; ++a)
+        for (int b = 0; b < n; ++b) {
+          qp.push_back(gx[a] * (1 - gx[b]));
+          qp.push_back(gx[b]);
+          qw.push_back(gw[a] * gw[b] * (1 - gx[b]));
+        }
+    } else {
+      for (int a = 0; a < n; ++a)
+        for (int b = 0; b < n; ++b)
+          for (int e = 0; e < n; ++e) {
+            qp.push_back(gx[a] * (1 - gx[b]) * (1 - gx[e]));
+            qp.push_back(gx[b] * (1 - gx[e]));
+            qp.push_back(gx[e]);
+            qw.push_back(gw[a] * gw[b] * gw[e] * (1 - gx[b]) * (1 - gx[e]) * (1 - gx[e]));
+          }
+    }
+    for (double w : qw) wsum += w;
+    for (double& w : qw) w /= wsum;
+  }
+  const int nq = (int)qw.size();
+
+  const int64_t TILES_PER_BATCH = std::max<int64_t>(1, (int64_t(256) << 20) / L.tile_bytes);
+  const bool keep_host = c->device < 0;
+  if (keep_host) c->host_blocks.assign(size_t(c->n_tiles) * L.tile_bytes, 0);
+  std::vector<unsigned char> batch;
+  if (!keep_host) dev_alloc_blocks(c, c->n_tiles * L.tile_bytes);
+  int bad_singular = 0, bad_local = 0;
+  double cond_max = 0.0;
+
+  for (int64_t t0 = 0; t0 < c->n_tiles; t0 += TILES_PER_BATCH) {
+    const int64_t t1 = std::min(c->n_tiles, t0 + TILES_PER_BATCH);
+    unsigned char* base;
+    if (keep_host) {
+      base = c->host_blocks.data() + size_t(t0) * L.tile_bytes;
+    } else {
+      batch.assign(size_t(t1 - t0) * L.tile_bytes, 0);
+      base = batch.data();
+    }
+#pragma omp parallel for schedule(dynamic, 64) reduction(| : bad_singular, bad_local) reduction(max : cond_max)
+    for (int64_t li = t0 * T; li < std::min(c->n_owned, t1 * T); ++li) {
+      const int64_t tile = li / T;
+      const int ct = int(li % T);
+      unsigned char* tb = base + size_t(tile - t0) * L.tile_bytes;
+      int32_t* ids = (int32_t*)(tb + L.off_ids);
+      double* sinv = (double*)(tb + L.off_sinv);
+      uint8_t* slots = (uint8_t*)(tb + L.off_slots);
+      double* Bch = (double*)(tb + L.off_chunks);
+      const int64_t g = c->local2global[li];
+      const int64_t q = g - c->own_lo;
+      const int32_t* cen = &c->central[q * ne];
+      const int32_t* sec = &c->sectors[q * nv * nv];
+      const uint8_t* val = &c->valid[q * nv];
+
+      // owner affine map x = X0 + J ξ
+      const double* Xi = &c->X[g * nv * d];
+      double J[9], Ji[9];
+      for (int a = 0; a < d; ++a)
+        for (int k = 0; k < d; ++k) J[a * d + k] = Xi[(k + 1) * d + a] - Xi[a];
+      if (!inv_small(d, J, Ji)) { bad_singular |= 1; continue; }
+
+      // gather list: central[1..] then sector extras, padded with self
+      int32_t glist[256];
+      int64_t gglob[256];
+      int ng = 0;
+      for (int k = 1; k < ne; ++k) gglob[ng++] = cen[k];
+      uint8_t sl[4][3];
+      for (int s = 0; s < nv; ++s) {
+        for (int m = 0; m < d; ++m) sl[s][m] = 255;
+        if (!val[s]) continue;
+        for (int m = 0; m < d; ++m) {
+          int64_t x = sec[s * nv + 1 + m];
+          int pos = -1;
+          for (int k = 0; k < ng; ++k)
+            if (gglob[k] == x) { pos = k; break; }
+          if (pos < 0) { pos = ng; gglob[ng++] = x; }
+          sl[s][m] = (uint8_t)pos;
+        }
+      }
+      const int32_t self_local = (int32_t)li;
+      for (int k = 0; k < G; ++k) {
+        if (k < ng) {
+          glist[k] = to_local(gglob[k]);
+          if (glist[k] < 0) bad_local |= 1;
+        } else {
+          glist[k] = self_local;
+        }
+        ids[size_t(k) * T + ct] = glist[k];
+      }
+      for (int s = 0; s < nv; ++s)
+        for (int m = 0; m < d; ++m) slots[(size_t(ct) * nv + s) * d + m] = sl[s][m];
+
+      // central reduced LSQ matrix A[1:,1:] (column-major, K rows)
+      std::vector<double> A(size_t(K) * R);
+      double psi[64], xi[3], sh[3];
+      for (int k = 1; k < ne; ++k) {
+        const int64_t j = cen[k];
+        const double* Xj = &c->X[j * nv * d];
+        shift_of(c, g, j, sh);
+        // ξ = t + C ξ' with t = J⁻¹(X_j0 + sh − X_i0), C = J⁻¹ J_j
+        double t[3], Cm[9], Jj[9];
+        for (int a = 0; a < d; ++a)
+          for (int e = 0; e < d; ++e) Jj[a * d + e] = Xj[(e + 1) * d + a] - Xj[a];
+        for (int a = 0; a < d; ++a) {
+          double s = 0.0;
+          for (int e = 0; e < d; ++e) s += Ji[a * d + e] * (Xj[e] + sh[e] - Xi[e]);
+          t[a] = s;
+          for (int e = 0; e < d; ++e) {
+            double s2 = 0.0;
+            for (int f = 0; f < d; ++f) s2 += Ji[a * d + f] * Jj[f * d + e];
+            Cm[a * d + e] = s2;
+          }
+        }
+        double acc[64] = {0};
+        for (int qq = 0; qq < nq; ++qq) {
+          for (int a = 0; a < d; ++a) {
+            double s = t[a];
+            for (int e = 0; e < d; ++e) s += Cm[a * d + e] * qp[qq * d + e];
+            xi[a] = s;
+          }
+          basis_eval(d, M, xi, psi);
+          for (int l = 1; l < nm; ++l) acc[l] += qw[qq] * psi[l];
+        }
+        for (int l = 1; l < nm; ++l) A[size_t(l - 1) * K + (k - 1)] = acc[l];
+      }
+      std::vector<double> Bp;
+      double cond = 0.0;
+      if (!pinv_qr(K, R, A, Bp, cond)) { bad_singular |= 1; continue; }
+      cond_max = std::max(cond_max, cond);
+      // B chunks: [k][T][R]
+      for (int k = 0; k < K; ++k)
+        for (int l = 0; l < R; ++l) Bch[(size_t(k) * T + ct) * R + l] = Bp[size_t(l) * K + k];
+
+      // sector inverses
+      for (int s = 0; s < nv; ++s) {
+        double* Sd = &sinv[((size_t)ct * nv + s) * d * d];
+        for (int e = 0; e < d * d; ++e) Sd[e] = 0.0;
+        if (!val[s]) continue;
+        double As[9];
+        for (int m = 0; m < d; ++m) {
+          const int64_t j = sec[s * nv + 1 + m];
+          shift_of(c, g, j, sh);
+          for (int a = 0; a < d; ++a) {
+            double s2 = 0.0;
+            for (int e = 0; e < d; ++e) s2 += Ji[a * d + e] * (c->bary[j * d + e] + sh[e] - Xi[e]);
+            xi[a] = s2;
+          }
+          basis_eval(d, 1, xi, psi);
+          for (int l = 0; l < d; ++l) As[m * d + l] = psi[l + 1];
+        }
+        // p_l = Σ_m S[l][m] ΔQ_m with S = As⁻¹ where As[m][l]
+        double Ai[9];
+        if (!inv_small(d, As, Ai)) {
+          for (int m = 0; m < d; ++m) slots[(size_t(ct) * nv + s) * d + m] = 255;
+          continue;
+        }
+        for (int e = 0; e < d * d; ++e) Sd[e] = Ai[e];
+      }
+    }
+    if (bad_singular || bad_local) break;
+    if (!keep_host) dev_upload_blocks(c, t0 * L.tile_bytes, batch.data(), int64_t(t1 - t0) * L.tile_bytes);
+  }
+  if (bad_singular) fail(CWRECO_ESINGULAR, "precompute: rank-deficient least-squares system or degenerate cell");
+  if (bad_local) fail(CWRECO_EINVAL, "precompute: stencil cell missing from the local numbering");
+  (void)cond_max;
+  if (!keep_host) dev_upload_aux(c);
+  c->has_blocks = true;
+}
+
+}  // namespace cwr

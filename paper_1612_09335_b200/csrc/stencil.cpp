@@ -1,0 +1,387 @@
+// Central and sectorial CWENO stencils with exact predicates,
+// then ghosts and the local numbering (owned interior | owned boundary | ghosts).
+//
+// Readings: R11 face neighbours drive the recursion (node neighbours
+// only as the sector fallback), R12 layers sorted by (squared barycentre
+// distance, SFC id) with the last layer truncated, R13 open cone of owner vertex
+// v = {λ_w > 0 ∀ w ≠ v}, R14 sector fallback / invalid sectors, R16 periodic
+// minimum image chosen by the IEEE recipe on barycentres.
+//
+// Every geometric decision is exact for the given doubles: an interval filter
+// certifies the sign in double precision, otherwise expansion arithmetic decides.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "exact.hpp"
+#include "internal.hpp"
+
+namespace cwr {
+
+namespace {
+
+constexpr double U = 1.1102230246251565e-16;  // 2^-53
+
+// value with an absolute error radius (sound filter for sign decisions)
+struct IV {
+  double v, r;
+};
+inline IV iv_add(IV a, IV b) {
+  double s = a.v + b.v;
+  return {s, (a.r + b.r + U * std::fabs(s)) * (1 + 4 * U)};
+}
+inline IV iv_sub(IV a, IV b) { return iv_add(a, {-b.v, b.r}); }
+inline IV iv_mul(IV a, IV b) {
+  double p = a.v * b.v;
+  return {p, (std::fabs(a.v) * b.r + std::fabs(b.v) * a.r + a.r * b.r + U * std::fabs(p)) * (1 + 4 * U)};
+}
+inline IV iv_exact(double x) { return {x, 0.0}; }
+
+IV iv_orient(int d, const IV* const* p) {
+  if (d == 2) {
+    IV ax = iv_sub(p[1][0], p[0][0]), ay = iv_sub(p[1][1], p[0][1]);
+    IV bx = iv_sub(p[2][0], p[0][0]), by = iv_sub(p[2][1], p[0][1]);
+    return iv_sub(iv_mul(ax, by), iv_mul(ay, bx));
+  }
+  IV u[3], v[3], w[3];
+  for (int k = 0; k < 3; ++k) {
+    u[k] = iv_sub(p[1][k], p[0][k]);
+    v[k] = iv_sub(p[2][k], p[0][k]);
+    w[k] = iv_sub(p[3][k], p[0][k]);
+  }
+  IV c0 = iv_sub(iv_mul(v[1], w[2]), iv_mul(v[2], w[1]));
+  IV c1 = iv_sub(iv_mul(v[2], w[0]), iv_mul(v[0], w[2]));
+  IV c2 = iv_sub(iv_mul(v[0], w[1]), iv_mul(v[1], w[0]));
+  return iv_add(iv_add(iv_mul(u[0], c0), iv_mul(u[1], c1)), iv_mul(u[2], c2));
+}
+
+// Geometry of one owner cell i, in coordinates scaled by (d+1) and centred on
+// the owner's barycentre: W_k = (d+1) X_{i,k} − S_i, and for a cell j
+// D_j = S_j + (d+1) n L − S_i  (S_c = Σ_k X_{c,k}; n the periodic image shift).
+struct Owner {
+  const cwreco_ctx* c;
+  int d;
+  int64_t i;
+  IV Wiv[4][3];
+  exact::Ex Si[3];
+  exact::Ex W[4][3];
+  bool have_exactW = false;
+
+  Owner(const cwreco_ctx* c_, int64_t i_) : c(c_), d(c_->d), i(i_) {
+    const double* X = &c->X[i * (d + 1) * d];
+    for (int a = 0; a < d; ++a) {
+      IV s = iv_exact(X[a]);
+      for (int k = 1; k <= d; ++k) s = iv_add(s, iv_exact(X[k * d + a]));
+      for (int k = 0; k <= d; ++k) Wiv[k][a] = iv_sub(iv_mul(iv_exact(double(d + 1)), iv_exact(X[k * d + a])), s);
+    }
+  }
+  void ensure_exactW() {
+    if (have_exactW) return;
+    const double* X = &c->X[i * (d + 1) * d];
+    for (int a = 0; a < d; ++a) {
+      exact::Ex s;
+      for (int k = 0; k <= d; ++k) s = exact::grow(s, X[k * d + a]);
+      Si[a] = exact::compress(s);
+      for (int k = 0; k <= d; ++k) W[k][a] = exact::sub(exact::scale(exact::Ex(X[k * d + a]), double(d + 1)), Si[a]);
+    }
+    have_exactW = true;
+  }
+};
+
+struct Cand {
+  int64_t j;
+  int n[3];     // periodic shift
+  IV D[3];      // filter value of D_j
+  IV key;       // Σ D_a²
+  bool have_exact = false;
+  exact::Ex De[3];
+  exact::Ex keye;
+};
+
+void shift_of(const cwreco_ctx* c, int64_t i, int64_t j, int* n) {
+  const int d = c->d;
+  for (int a = 0; a < d; ++a) {
+    n[a] = 0;
+    if (!c->periodic) continue;
+    const double L = c->L[a];
+    double r = c->bary[j * d + a] - c->bary[i * d + a];
+    while (r > 0.5 * L) { r -= L; n[a] -= 1; }
+    while (r < -0.5 * L) { r += L; n[a] += 1; }
+  }
+}
+
+void make_cand(Owner& o, int64_t j, Cand& cd) {
+  const cwreco_ctx* c = o.c;
+  const int d = o.d;
+  cd.j = j;
+  cd.have_exact = false;
+  shift_of(c, o.i, j, cd.n);
+  const double* Xi = &c->X[o.i * (d + 1) * d];
+  const double* Xj = &c->X[j * (d + 1) * d];
+  IV key{0.0, 0.0};
+  for (int a = 0; a < d; ++a) {
+    IV sj = iv_exact(Xj[a]), si = iv_exact(Xi[a]);
+    for (int k = 1; k <= d; ++k) {
+      sj = iv_add(sj, iv_exact(Xj[k * d + a]));
+      si = iv_add(si, iv_exact(Xi[k * d + a]));
+    }
+    IV sh = iv_mul(iv_exact(double((d + 1) * cd.n[a])), iv_exact(c->periodic ? c->L[a] : 0.0));
+    cd.D[a] = iv_sub(iv_add(sj, sh), si);
+    key = a == 0 ? iv_mul(cd.D[a], cd.D[a]) : iv_add(key, iv_mul(cd.D[a], cd.D[a]));
+  }
+  cd.key = key;
+}
+
+void ensure_exact(Owner& o, Cand& cd) {
+  if (cd.have_exact) return;
+  o.ensure_exactW();
+  const cwreco_ctx* c = o.c;
+  const int d = o.d;
+  const double* Xj = &c->X[cd.j * (d + 1) * d];
+  exact::Ex key;
+  for (int a = 0; a < d; ++a) {
+    exact::Ex s;
+    for (int k = 0; k <= d; ++k) s = exact::grow(s, Xj[k * d + a]);
+    s = exact::compress(s);
+    if (c->periodic && cd.n[a] != 0) s = exact::add(s, exact::scale(exact::Ex(c->L[a]), double((d + 1) * cd.n[a])));
+    cd.De[a] = exact::sub(s, o.Si[a]);
+    key = exact::add(key, exact::mul(cd.De[a], cd.De[a]));
+  }
+  cd.keye = key;
+  cd.have_exact = true;
+}
+
+// strict-weak "less" by (exact squared distance, id)
+bool key_less(Owner& o, Cand& a, Cand& b) {
+  IV df = iv_sub(a.key, b.key);
+  if (std::fabs(df.v) > df.r) return df.v < 0;
+  ensure_exact(o, a);
+  ensure_exact(o, b);
+  int s = exact::sign(exact::sub(a.keye, b.keye));
+  if (s != 0) return s < 0;
+  return a.j < b.j;
+}
+
+// sign of the owner barycentric coordinate λ_w at D (orientation with W_w -> D)
+int lambda_sign(Owner& o, Cand& cd, int w) {
+  const int d = o.d;
+  const IV* p[4];
+  for (int k = 0; k <= d; ++k) p[k] = (k == w) ? cd.D : o.Wiv[k];
+  IV det = iv_orient(d, p);
+  if (std::fabs(det.v) > det.r) return det.v > 0 ? 1 : -1;
+  ensure_exact(o, cd);
+  const exact::Ex* pe[4];
+  for (int k = 0; k <= d; ++k) pe[k] = (k == w) ? cd.De : o.W[k];
+  return exact::orient_sign(d, pe);
+}
+
+bool in_cone(Owner& o, Cand& cd, int v) {  // R13: λ_w > 0 for all w != v
+  for (int w = 0; w <= o.d; ++w) {
+    if (w == v) continue;
+    if (lambda_sign(o, cd, w) <= 0) return false;
+  }
+  return true;
+}
+
+bool affinely_independent(Owner& o, std::vector<Cand>& cs) {
+  const int d = o.d;
+  IV zero[3] = {{0, 0}, {0, 0}, {0, 0}};
+  const IV* p[4];
+  p[0] = zero;
+  for (int k = 0; k < d; ++k) p[k + 1] = cs[k].D;
+  IV det = iv_orient(d, p);
+  if (std::fabs(det.v) > det.r) return true;
+  exact::Ex ze[3];
+  const exact::Ex* pe[4];
+  pe[0] = ze;
+  for (int k = 0; k < d; ++k) {
+    ensure_exact(o, cs[k]);
+    pe[k + 1] = cs[k].De;
+  }
+  return exact::orient_sign(d, pe) != 0;
+}
+
+inline bool contains(const std::vector<int64_t>& v, int64_t x) {
+  return std::find(v.begin(), v.end(), x) != v.end();
+}
+
+void sort_cands(Owner& o, std::vector<Cand>& cs) {
+  std::sort(cs.begin(), cs.end(), [&](Cand& a, Cand& b) { return key_less(o, a, b); });
+}
+
+// returns false if exhausted
+bool central_stencil(const cwreco_ctx* c, int64_t i, int32_t* out) {
+  const int d = c->d, ne = c->ne;
+  Owner o(c, i);
+  std::vector<int64_t> S{i}, frontier{i}, cand;
+  std::vector<Cand> cs;
+  while ((int)S.size() < ne) {
+    cand.clear();
+    for (int64_t f : frontier)
+      for (int k = 0; k <= d; ++k) {
+        int64_t nb = c->nbr[f * (d + 1) + k];
+        if (nb >= 0 && !contains(S, nb) && !contains(cand, nb)) cand.push_back(nb);
+      }
+    if (cand.empty()) return false;
+    cs.resize(cand.size());
+    for (size_t q = 0; q < cand.size(); ++q) make_cand(o, cand[q], cs[q]);
+    sort_cands(o, cs);
+    const size_t take = std::min(cs.size(), size_t(ne) - S.size());
+    frontier.clear();
+    for (size_t q = 0; q < take; ++q) {
+      S.push_back(cs[q].j);
+      frontier.push_back(cs[q].j);
+    }
+  }
+  for (int k = 0; k < ne; ++k) out[k] = (int32_t)S[k];
+  return true;
+}
+
+// P:156 + R14.  out: d+1 entries (self first, -1 padded); returns validity.
+bool sector_stencil(const cwreco_ctx* c, int64_t i, int v, int32_t* out) {
+  const int d = c->d;
+  Owner o(c, i);
+  std::vector<int64_t> S{i}, seen{i}, frontier{i}, cand;
+  std::vector<Cand> taken, acc;
+  Cand tmp;
+  while ((int)S.size() < d + 1) {
+    cand.clear();
+    for (int64_t f : frontier)
+      for (int k = 0; k <= d; ++k) {
+        int64_t nb = c->nbr[f * (d + 1) + k];
+        if (nb >= 0 && !contains(seen, nb) && !contains(cand, nb)) cand.push_back(nb);
+      }
+    for (int64_t x : cand) seen.push_back(x);
+    acc.clear();
+    for (int64_t x : cand) {
+      make_cand(o, x, tmp);
+      if (in_cone(o, tmp, v)) acc.push_back(tmp);
+    }
+    if (acc.empty()) {
+      // fallback: node (Voronoi) neighbours of all selected sector cells
+      cand.clear();
+      for (int64_t s : S) {
+        const int64_t* nd = &c->cell_nodes[s * (d + 1)];
+        for (int k = 0; k <= d; ++k)
+          for (int64_t q = c->nc_ptr[nd[k]]; q < c->nc_ptr[nd[k] + 1]; ++q) {
+            int64_t x = c->nc_idx[q];
+            if (!contains(S, x) && !contains(cand, x)) cand.push_back(x);
+          }
+      }
+      for (int64_t x : cand) {
+        make_cand(o, x, tmp);
+        if (in_cone(o, tmp, v)) acc.push_back(tmp);
+      }
+      if (acc.empty()) break;
+    }
+    sort_cands(o, acc);
+    const size_t take = std::min(acc.size(), size_t(d + 1) - S.size());
+    frontier.clear();
+    for (size_t q = 0; q < take; ++q) {
+      S.push_back(acc[q].j);
+      if (!contains(seen, acc[q].j)) seen.push_back(acc[q].j);
+      frontier.push_back(acc[q].j);
+      taken.push_back(acc[q]);
+    }
+  }
+  for (int k = 0; k <= d; ++k) out[k] = k < (int)S.size() ? (int32_t)S[k] : -1;
+  if ((int)S.size() < d + 1) return false;
+  return affinely_independent(o, taken);
+}
+
+int owner_rank(const cwreco_ctx* c, int64_t g) {
+  // rank r owns [floor(r N / P), floor((r+1) N / P))
+  int r = int((g * c->nranks) / c->N);
+  while (r > 0 && (r * c->N) / c->nranks > g) --r;
+  while (r + 1 < c->nranks && ((r + 1) * c->N) / c->nranks <= g) ++r;
+  return r;
+}
+
+}  // namespace
+
+void build_stencils(cwreco_ctx* c) {
+  if (!c->has_mesh) fail(CWRECO_ESTATE, "build_stencils: no mesh");
+  const int d = c->d, ne = c->ne, nv = d + 1;
+  const int64_t lo = c->own_lo, hi = c->own_hi, n_own = hi - lo;
+  c->central.assign(n_own * ne, -1);
+  c->sectors.assign(n_own * nv * nv, -1);
+  c->valid.assign(n_own * nv, 0);
+  int64_t exhausted = -1;
+  std::string err;
+#pragma omp parallel for schedule(dynamic, 256)
+  for (int64_t q = 0; q < n_own; ++q) {
+    const int64_t i = lo + q;
+    try {
+      if (!central_stencil(c, i, &c->central[q * ne])) {
+#pragma omp critical
+        exhausted = std::max<int64_t>(exhausted, i);
+        continue;
+      }
+      for (int v = 0; v < nv; ++v)
+        c->valid[q * nv + v] = sector_stencil(c, i, v, &c->sectors[(q * nv + v) * nv]) ? 1 : 0;
+    } catch (const std::exception& e) {
+#pragma omp critical
+      err = e.what();
+    }
+  }
+  if (!err.empty()) fail(CWRECO_EINVAL, "build_stencils: " + err);
+  if (exhausted >= 0)
+    fail(CWRECO_ESTENCIL, "build_stencils: central stencil exhausted (cell " + std::to_string(exhausted) + ")");
+
+  // ---- ghosts, interior/boundary split, local numbering
+  std::vector<uint8_t> is_bnd(n_own, 0);
+  std::vector<int64_t> ghosts;
+  for (int64_t q = 0; q < n_own; ++q) {
+    bool b = false;
+    for (int k = 0; k < ne; ++k) {
+      int64_t g = c->central[q * ne + k];
+      if (g < lo || g >= hi) { b = true; ghosts.push_back(g); }
+    }
+    for (int k = 0; k < nv * nv; ++k) {
+      int64_t g = c->sectors[q * nv * nv + k];
+      if (g >= 0 && (g < lo || g >= hi)) { b = true; ghosts.push_back(g); }
+    }
+    is_bnd[q] = b;
+  }
+  std::sort(ghosts.begin(), ghosts.end());
+  ghosts.erase(std::unique(ghosts.begin(), ghosts.end()), ghosts.end());
+  c->n_owned = n_own;
+  c->n_ghost = (int64_t)ghosts.size();
+  c->local2global.clear();
+  c->local2global.reserve(n_own + c->n_ghost);
+  for (int64_t q = 0; q < n_own; ++q)
+    if (!is_bnd[q]) c->local2global.push_back(lo + q);
+  c->n_interior = (int64_t)c->local2global.size();
+  for (int64_t q = 0; q < n_own; ++q)
+    if (is_bnd[q]) c->local2global.push_back(lo + q);
+  for (int64_t g : ghosts) c->local2global.push_back(g);
+  c->ghost_counts.assign(c->nranks, 0);
+  for (int64_t g : ghosts) c->ghost_counts[owner_rank(c, g)]++;
+  c->send_counts.assign(c->nranks, 0);
+  c->send_local.clear();
+
+  // extras (sector cells outside the central stencil, R15) and invalid sectors
+  int64_t n_extra = 0, n_inv = 0;
+  int max_extra = 0;
+  for (int64_t q = 0; q < n_own; ++q) {
+    int ex = 0;
+    std::vector<int32_t> seen;
+    for (int k = 0; k < nv * nv; ++k) {
+      int32_t g = c->sectors[q * nv * nv + k];
+      if (g < 0) continue;
+      bool in = false;
+      for (int m = 0; m < ne && !in; ++m) in = c->central[q * ne + m] == g;
+      if (!in && std::find(seen.begin(), seen.end(), g) == seen.end()) { seen.push_back(g); ++ex; }
+    }
+    n_extra += ex;
+    max_extra = std::max(max_extra, ex);
+    for (int v = 0; v < nv; ++v) n_inv += c->valid[q * nv + v] ? 0 : 1;
+  }
+  c->n_extra = n_extra;
+  c->n_invalid = n_inv;
+  c->G = (ne - 1) + max_extra;
+  c->has_stencils = true;
+  c->has_blocks = false;
+}
+
+}  // namespace cwr

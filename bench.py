@@ -1,0 +1,358 @@
+#!/usr/bin/env python
+"""Benchmark of the CWENO reconstruction pass (arXiv 1612.09335 §2.1) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+One "step" = one full reconstruction pass (gather → B⁺ΔQ → sectors → P0 → σ → ω →
+blend → store, all rows of SURVEY §8(a)) over every cell of the workload.  N=1
+runs BASELINE.json configs[1] ("C2": 524,288 jittered triangles, M=3, 4 vars);
+N>1 (torchrun, one rank per GPU, NCCL) runs the weak-scaling ladder of the same
+workload (n = round(512·sqrt(N)), ≈524k cells per GPU) with the halo exchange
+overlapped with the interior tiles.
+
+Timing: W untimed warm-up steps, then K steps bracketed by a barrier and a
+device synchronize; each step is timed with CUDA events on the stream the
+kernel is launched on, and the L2 is flushed (a 512 MiB write) between steps,
+outside the events, so every step starts cold.  Max over ranks.
+
+Prints ONE JSON line (rank 0).  --impl reference times the CPU oracle (oracle/)
+on the host cores on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "CWENO reconstructed cells/sec (fp64) and % of HBM roofline at 1/2/4/8 B200"
+WORKLOAD_TEXT = {
+    "C1": "2D 16x16x2 periodic, M=2, Euler 4 vars, isentropic vortex (BASELINE configs[0])",
+    "C2": "2D 512x512x2 periodic triangles jittered +-0.2h, M=3, Euler 4 vars, vortex + ratio-10 jump (BASELINE configs[1])",
+    "C3": "3D 64^3x6 tets, M=2, Euler 5 vars, spherical explosion (BASELINE configs[2])",
+    "C4": "3D 128^3x6 tets jittered +-0.1h, M=3, MHD 9 vars, Orszag-Tang-type (BASELINE configs[3])",
+    "C5": "3D n^3x6 tets (n=100 per GPU weak ladder), M=3, Euler 5 vars, explosion (BASELINE configs[4])",
+}
+
+
+def env_rank():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def workload_n(cfg, N):
+    import gen
+    base = gen.CONFIGS[cfg]["n"]
+    if N == 1:
+        return base
+    if cfg == "C5":
+        return gen.C5_WEAK_N.get(N, round(100 * N ** (1 / 3)))
+    d = gen.CONFIGS[cfg]["d"]
+    return int(round(base * N ** (1.0 / d)))
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def profiled_traffic(cfg, kernel):
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            j = json.load(f)
+        return j.get(f"{cfg}:{kernel}")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for k, nm in enumerate(names):
+                if f[3 + k].lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- oracle arm
+def oracle_rate(w, budget_s, seed=0, max_cells=None):
+    """Oracle cells/s on a random sample of the workload's cells (1 core)."""
+    from oracle import reconstruct as R
+    from oracle.mesh import OracleMesh
+    m = OracleMesh(w["nodes"], w["cells"], w["period"], w["M"])
+    Q = w["avgs"][m.perm]
+    rng = np.random.default_rng(seed)
+    order = rng.permutation(m.N)
+    n, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < budget_s and (max_cells is None or n < max_cells):
+        R.reconstruct_cell(m, int(order[n % m.N]), Q, w["M"])
+        n += 1
+    dt = time.perf_counter() - t0
+    return n / dt, n, dt, m, Q
+
+
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return 0
+    import gen
+    w = gen.make(args.config, workload_n(args.config, 1))
+    from oracle import reconstruct as R
+    from oracle.mesh import OracleMesh
+    m = OracleMesh(w["nodes"], w["cells"], w["period"], w["M"])
+    Q = w["avgs"][m.perm]
+    rng = np.random.default_rng(0)
+    t = time.perf_counter()
+    R.reconstruct_cell(m, 0, Q, w["M"])
+    per_cell = time.perf_counter() - t
+    per_step = max(1, int(120.0 / max(1, args.steps + args.warmup) / max(per_cell, 1e-4)))
+    per_step = min(per_step, 64)
+    order = rng.permutation(m.N)
+    k = 0
+    for _ in range(args.warmup):
+        for _ in range(per_step):
+            R.reconstruct_cell(m, int(order[k % m.N]), Q, w["M"]); k += 1
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        for _ in range(per_step):
+            R.reconstruct_cell(m, int(order[k % m.N]), Q, w["M"]); k += 1
+    dt = time.perf_counter() - t0
+    cells = args.steps * per_step
+    value = cells / dt
+    sample = f"{per_step} random cells of {args.config} per step (oracle rebuilds each cell's stencil matrices and solves)"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "cells/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": f"{args.config}: {WORKLOAD_TEXT[args.config]}",
+                                             "n_cells": int(m.N)},
+            "cpu_baseline": {"value": value, "unit": "cells/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "cells/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import gen
+    import paper_1612_09335_b200 as P
+
+    rank, world, local = env_rank()
+    if world != args.gpus:
+        if rank == 0:
+            print(f"warning: WORLD_SIZE={world} but --gpus {args.gpus}; using WORLD_SIZE", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    n = workload_n(args.config, world)
+    w = gen.make(args.config, n)
+    t_setup = time.perf_counter()
+    ctx = P.Context(w["d"], w["M"], w["V"], device=local)
+    ctx.set_mesh(w["nodes"], w["cells"], w["period"])
+    if world > 1:
+        ctx.set_partition(rank, world)
+    ctx.build_stencils()
+    ctx.precompute()
+    ctx.set_kernel(args.kernel)
+    t_setup = time.perf_counter() - t_setup
+    inf = ctx.info()
+    perm = ctx.permutation()
+    loc = ctx.local_cells()                       # local -> SFC id
+    avgs_local = np.ascontiguousarray(w["avgs"][perm[loc]])  # [n_local, V] in local order
+    n_owned = inf["n_owned"]
+    V, nm = w["V"], ctx.nm
+    A = torch.tensor(avgs_local, device=dev)
+    out = torch.empty((n_owned, V, nm), dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+
+    if world > 1:
+        from paper_1612_09335_b200 import dist as pdist
+        send_counts, recv_counts = pdist.setup_halo(ctx, device=dev)
+        stepper = pdist.HaloStepper(ctx, A, out, send_counts, recv_counts)
+        # ghost rows are overwritten by the exchange every step
+        def step():
+            stepper.step()
+    else:
+        def step():
+            ctx.reconstruct(A, out, stream=stream)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.fill_(k & 0xFF)          # evict L2 between steps (outside the events)
+            evs[k][0].record(stream)
+            step()
+            evs[k][1].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    times = np.array([a.elapsed_time(b) for a, b in evs])  # ms
+    t_total = float(times.sum()) / 1e3
+    if world > 1:
+        tt = torch.tensor([t_total], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_total = float(tt.item())
+        cells_all = torch.tensor([float(n_owned)], device=dev)
+        dist.all_reduce(cells_all)
+        cells_total = float(cells_all.item())
+    else:
+        cells_total = float(n_owned)
+    value = cells_total * args.steps / t_total
+    ms_step = t_total / args.steps * 1e3
+
+    # roofline of the dominant kernel (the reconstruction kernel is the only kernel of the pass at N=1)
+    bpc = inf["algorithmic_bytes_per_cell"]
+    kern_s = float(np.mean(times)) / 1e3
+    achieved = bpc * n_owned / kern_s / 1e9
+    peak, peak_src = measured_peak()
+
+    # end to end through the public API: pinned host avgs -> device -> reconstruct -> host coeffs
+    h_in = torch.from_numpy(avgs_local).pin_memory()
+    h_out = torch.empty((n_owned, V, nm), dtype=torch.float64).pin_memory()
+    e2e_steps = max(3, min(args.steps, 50))
+    for _ in range(2):
+        A.copy_(h_in, non_blocking=True)
+        step()
+        h_out.copy_(out, non_blocking=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        A.copy_(h_in, non_blocking=True)
+        step()
+        h_out.copy_(out, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t_e2e = e0.elapsed_time(e1) / 1e3
+    if world > 1:
+        tt = torch.tensor([t_e2e], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_e2e = float(tt.item())
+    e2e_value = cells_total * e2e_steps / t_e2e
+
+    clocks = clk.summary()
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            rate, ncell, dt, *_ = oracle_rate(w, args.cpu_seconds)
+            cpu = {"value": rate, "unit": "cells/s", "cores": 1, "kind": "oracle",
+                   "sample": f"{ncell} random cells of {args.config} in {dt:.1f} s, single core "
+                             f"(oracle rebuilds stencil matrices and solves per cell)"}
+        line = {
+            "metric": METRIC, "value": value, "unit": "cells/s", "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {WORKLOAD_TEXT[args.config]}", "n_cells_total": int(cells_total),
+                       "n_cells_per_gpu": int(n_owned), "d": w["d"], "M": w["M"], "V": V, "box_n": n,
+                       "kernel": args.kernel, "l2": "flushed (512 MiB write) between timed steps",
+                       "parallelism": f"cell partition x{world}" + (" + NCCL halo" if world > 1 else ""),
+                       "setup_s": round(t_setup, 3)},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": profiled_traffic(args.config, args.kernel),
+                         "peak_source": peak_src, "algorithmic_bytes_per_cell": bpc,
+                         "kernel": "cwr::k_pipelined" if args.kernel == "pipelined" else "cwr::k_simple"},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "cells/s", "h2d_bytes_per_step": int(avgs_local.nbytes),
+                    "d2h_bytes_per_step": int(n_owned * V * nm * 8)},
+            "gpu_launches": args.steps * (1 if world == 1 else 3),
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--kernel", default="pipelined", choices=["pipelined", "simple"])
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,5 +1,6 @@
 // extern "C" surface of libcwreco (include/cwreco.h).  Converts exceptions to
 // status codes; keeps a thread-local last-error message.
+#include <algorithm>
 #include <cstring>
 #include <string>
 
@@ -231,7 +232,10 @@ cwreco_status cwreco_get_blocks(const cwreco_ctx* c, int64_t n_sel, const int64_
       const double* B = (const double*)(tb + L.off_chunks);
       if (bplus)
         for (int l = 0; l < R; ++l)
-          for (int k = 0; k < K; ++k) bplus[(s * R + l) * K + k] = B[((size_t)k * T + ct) * R + l];
+          for (int k = 0; k < K; ++k) {
+            const int ch = k / L.KC, kk = k % L.KC, kc = std::min(L.KC, K - ch * L.KC);
+            bplus[(s * R + l) * K + k] = B[size_t(ch) * L.KC * T * R + (size_t(ct) * R + l) * kc + kk];
+          }
       if (sinv) std::memcpy(sinv + s * nv * d * d, sv + (size_t)ct * nv * d * d, sizeof(double) * nv * d * d);
       if (gather)
         for (int k = 0; k < G; ++k) gather[s * G + k] = ids[(size_t)k * T + ct];

@@ -29,8 +29,8 @@ inline int n_modes(int M, int d) {  // ℳ(M,d) = (1/d!) Π_{l=1..d} (M+l)   (P:
 //   header:  ids   int32  [G][T]          gather list (local cell ids), k-major
 //            sinv  double [T][d+1][d][d]  sector inverses
 //            slots uint8  [T][d+1][d]     sector cell -> gather index, 255 = invalid
-//   chunks:  B     double [K][T][R]       reduced pseudo-inverse, k-major, split in
-//                                         chunks of KC k-slices (last chunk shorter)
+//   chunks:  B     chunk ch = k ∈ [ch·KC, ch·KC+kc): double [T][R][kc]  (reduced
+//                  pseudo-inverse; kc = KC except for a shorter last chunk)
 struct Layout {
   int d = 0, M = 0, V = 0, nm = 0, R = 0, K = 0, G = 0, T = 0, KC = 0, NCH = 0;
   int64_t off_ids = 0, off_sinv = 0, off_slots = 0, header_bytes = 0;

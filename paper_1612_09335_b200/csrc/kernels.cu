@@ -3,16 +3,19 @@
 //
 //  k_simple     one thread per (cell, variable), plain global loads.  Reference
 //               kernel and debug tap (writes the intermediates).
-//  k_pipelined  persistent, warp-specialised: one producer lane streams each tile
-//               (header + K-chunks of B⁺) into a ring of shared-memory stages with
-//               1-D TMA bulk copies (cp.async.bulk + mbarrier complete_tx); the
-//               consumer warps (one thread per (cell, variable)) gather Q_j through
-//               L1/L2, accumulate B⁺ΔQ in registers, run the fused
-//               sector / P0 / σ / ω / blend epilogue, stage the tile's output in
-//               shared memory and write it back with one bulk store.
-// Both compute exactly the same arithmetic in the same order.
+//  k_pipelined  persistent and warp-specialised.  One producer lane streams each
+//               tile (header + K-chunks of B⁺) into a ring of shared-memory stages
+//               with 1-D TMA bulk copies (cp.async.bulk, mbarrier complete_tx);
+//               two gather warps copy the stencil averages Q_j of each chunk into
+//               the same stage with cp.async; the consumer warps (one thread per
+//               (cell, variable)) accumulate B⁺ΔQ in registers, run the fused
+//               sector / P0 / σ / ω / blend epilogue (Σ from the constant bank) and
+//               write their outputs back with per-warp bulk stores.
+// Both kernels perform the same floating-point operations in the same order, so
+// their outputs are bitwise identical (tested).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 #include <string>
@@ -25,7 +28,6 @@ namespace cwr {
 struct DeviceState {
   unsigned char* blocks = nullptr;
   int64_t blocks_bytes = 0;
-  double* sigma = nullptr;  // packed upper triangle of Σ[1:,1:], doubled off-diagonals
   int64_t* send = nullptr;
   int64_t n_send = 0;
   int num_sms = 148;
@@ -42,6 +44,26 @@ struct DeviceState {
     if (e_ != cudaSuccess) fail(CWRECO_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
   } while (0)
 
+__host__ __device__ constexpr int nmodes(int M, int d) {
+  return d == 2 ? (M + 1) * (M + 2) / 2 : (M + 1) * (M + 2) * (M + 3) / 6;
+}
+
+// Universal Σ depends only on (d, M): the packed upper triangle of Σ[1:,1:]
+// (off-diagonals doubled) of every supported (d, M) lives in the constant bank, so
+// the σ quadratic forms use it as DFMA constant operands.
+__host__ __device__ constexpr int sig_len(int D, int M) { return (nmodes(M, D) - 1) * nmodes(M, D) / 2; }
+__host__ __device__ constexpr int sig_off(int D, int M) {
+  int off = 0;
+  for (int dd = 2; dd <= 3; ++dd)
+    for (int mm = 1; mm <= 4; ++mm) {
+      if (dd == D && mm == M) return off;
+      off += sig_len(dd, mm);
+    }
+  return off;
+}
+constexpr int SIG_TOTAL = sig_off(4, 1);
+__constant__ double c_sig[SIG_TOTAL];
+
 struct KArgs {
   const unsigned char* blocks;
   int64_t tile_bytes, off_ids, off_sinv, off_slots, off_chunks;
@@ -52,9 +74,10 @@ struct KArgs {
   double* out;
   int64_t ccs, cvs;
   int dense_out;
-  const double* sig;  // packed Σ' (global)
-  double lam0, lams, eps, psi1;
+  double eps, psi1;
   int r;
+  // normalised linear weights (R5, R14) indexed by the number of valid sectors
+  double l0[5], inv_l0[5], ls[5];
 };
 
 struct DbgOut {
@@ -63,13 +86,9 @@ struct DbgOut {
   int64_t n;
 };
 
-__host__ __device__ constexpr int nmodes(int M, int d) {
-  return d == 2 ? (M + 1) * (M + 2) / 2 : (M + 1) * (M + 2) * (M + 3) / 6;
-}
-
 __device__ __forceinline__ double powr(double t, int r) {
   if (r == 4) {
-    double t2 = t * t;
+    const double t2 = t * t;
     return t2 * t2;
   }
   double p = 1.0;
@@ -77,40 +96,43 @@ __device__ __forceinline__ double powr(double t, int r) {
   return p;
 }
 
-// The fused epilogue: P0, σ, ω, blend.  acc[l-1] = p̂_opt[l], l >= 1;
-// ps[s][l-1] = p̂_s[l], l = 1..D; valid[s].  Σ' is the packed upper triangle of
-// Σ[1:,1:] with doubled off-diagonal entries (Σ is symmetric, row/col 0 zero).
+template <int D, int NM>
+struct ModeOf {  // M from (D, ℳ)
+  static constexpr int M = D == 2 ? (NM == 3 ? 1 : NM == 6 ? 2 : NM == 10 ? 3 : 4) : (NM == 4 ? 1 : NM == 10 ? 2 : 3);
+};
+
+// Fused epilogue.  acc[l-1] = p̂_opt[l] (l >= 1); ps[s][l-1] = p̂_s[l]
+// (l = 1..D).  On return w[] holds the blended coefficients.
 template <int D, int NM>
 __device__ __forceinline__ void cweno_epilogue(double qi, double* acc, const double (&ps)[D + 1][D],
-                                               const bool (&valid)[D + 1], const KArgs& a,
-                                               const double* __restrict__ sig, double* w,
+                                               const bool (&valid)[D + 1], const KArgs& a, double* w,
                                                double* sigma_out, double* omega_out) {
   constexpr int R = NM - 1;
+  constexpr int SO = sig_off(D, ModeOf<D, NM>::M);
   const double p0 = qi / a.psi1;
   int nval = 0;
 #pragma unroll
   for (int s = 0; s <= D; ++s) nval += valid[s] ? 1 : 0;
-  const double denom = a.lam0 + nval * a.lams;
-  const double l0 = a.lam0 / denom, ls = a.lams / denom;
-  // P0 = (P_opt − Σ λ̄_s P_s)/λ̄0, in place in acc
+  const double l0 = a.l0[nval], il0 = a.inv_l0[nval], ls = a.ls[nval];
+  // P0 = (P_opt − Σ_s λ̄_s P_s)/λ̄0; modes above d are P_opt/λ̄0
 #pragma unroll
   for (int l = 0; l < D; ++l) {
     double s = 0.0;
 #pragma unroll
     for (int q = 0; q <= D; ++q) s += valid[q] ? ps[q][l] : 0.0;
-    acc[l] = (acc[l] - ls * s) / l0;
+    acc[l] = (acc[l] - ls * s) * il0;
   }
 #pragma unroll
-  for (int l = D; l < R; ++l) acc[l] = acc[l] / l0;
-  // σ0 = P0ᵀ Σ P0
+  for (int l = D; l < R; ++l) acc[l] = acc[l] * il0;
+  // σ_0 = P0ᵀ Σ P0 and σ_s = P_sᵀ Σ P_s
   double sg0 = 0.0;
   {
-    int idx = 0;
+    int idx = SO;
 #pragma unroll
     for (int l = 0; l < R; ++l) {
       double t = 0.0;
 #pragma unroll
-      for (int m = l; m < R; ++m) t += sig[idx + m - l] * acc[m];
+      for (int m = l; m < R; ++m) t += c_sig[idx + m - l] * acc[m];
       idx += R - l;
       sg0 += acc[l] * t;
     }
@@ -119,19 +141,19 @@ __device__ __forceinline__ void cweno_epilogue(double qi, double* acc, const dou
 #pragma unroll
   for (int s = 0; s <= D; ++s) {
     double v = 0.0;
-    int idx = 0;
+    int idx = SO;
 #pragma unroll
     for (int l = 0; l < D; ++l) {
       double t = 0.0;
 #pragma unroll
-      for (int m = l; m < D; ++m) t += sig[idx + m - l] * ps[s][m];
+      for (int m = l; m < D; ++m) t += c_sig[idx + m - l] * ps[s][m];
       idx += R - l;
       v += ps[s][l] * t;
     }
     sgs[s] = v;
   }
-  // nonlinear weights
-  double wt0 = l0 / powr(sg0 + a.eps, a.r);
+  // ω̃_s = λ̄_s/(σ_s+ε)^r, ω_s = ω̃_s/Σ ω̃; invalid sectors get 0 (R14)
+  const double wt0 = l0 / powr(sg0 + a.eps, a.r);
   double wts[D + 1];
   double sum = wt0;
 #pragma unroll
@@ -139,11 +161,12 @@ __device__ __forceinline__ void cweno_epilogue(double qi, double* acc, const dou
     wts[s] = valid[s] ? ls / powr(sgs[s] + a.eps, a.r) : 0.0;
     sum += wts[s];
   }
-  const double om0 = wt0 / sum;
+  const double isum = 1.0 / sum;
+  const double om0 = wt0 * isum;
   double oms[D + 1];
 #pragma unroll
-  for (int s = 0; s <= D; ++s) oms[s] = wts[s] / sum;
-  // blend; w[0] := Q_i/ψ1 (R17)
+  for (int s = 0; s <= D; ++s) oms[s] = wts[s] * isum;
+  // w = Σ_s ω_s P_s;  w[0] := Q_i/ψ1 (R17)
   w[0] = p0;
 #pragma unroll
   for (int l = 0; l < D; ++l) {
@@ -193,12 +216,15 @@ __global__ void __launch_bounds__(256) k_simple(KArgs a, DbgOut dbg) {
   double acc[R];
 #pragma unroll
   for (int l = 0; l < R; ++l) acc[l] = 0.0;
-  for (int k = 0; k < a.K; ++k) {
-    const int32_t j = ids[size_t(k) * a.T + ct];
-    const double dq = Qv[int64_t(j) * a.acs] - qi;
-    const double* b = B + (size_t(k) * a.T + ct) * R;
+  for (int ch = 0; ch < a.NCH; ++ch) {
+    const int kc = min(a.KC, a.K - ch * a.KC);
+    const double* Bc = B + (size_t)ch * a.KC * a.T * R + (size_t)ct * R * kc;  // chunk [T][R][kc]
+    for (int kk = 0; kk < kc; ++kk) {
+      const int32_t j = ids[size_t(ch * a.KC + kk) * a.T + ct];
+      const double dq = Qv[int64_t(j) * a.acs] - qi;
 #pragma unroll
-    for (int l = 0; l < R; ++l) acc[l] += b[l] * dq;
+      for (int l = 0; l < R; ++l) acc[l] += Bc[l * kc + kk] * dq;
+    }
   }
   double ps[NV][D];
   bool valid[NV];
@@ -210,7 +236,7 @@ __global__ void __launch_bounds__(256) k_simple(KArgs a, DbgOut dbg) {
     for (int m = 0; m < D; ++m) {
       const int g = valid[s] ? slots[s * D + m] : 0;
       const int32_t j = ids[size_t(g) * a.T + ct];
-      dq[m] = valid[s] ? Qv[int64_t(j) * a.acs] - qi : 0.0;
+      dq[m] = (valid[s] ? Qv[int64_t(j) * a.acs] : qi) - qi;
     }
 #pragma unroll
     for (int l = 0; l < D; ++l) {
@@ -232,7 +258,7 @@ __global__ void __launch_bounds__(256) k_simple(KArgs a, DbgOut dbg) {
   }
   double w[NM];
   double sg[NV + 1], om[NV + 1];
-  cweno_epilogue<D, NM>(qi, acc, ps, valid, a, a.sig, w, DEBUG ? sg : nullptr, DEBUG ? om : nullptr);
+  cweno_epilogue<D, NM>(qi, acc, ps, valid, a, w, DEBUG ? sg : nullptr, DEBUG ? om : nullptr);
   if (DEBUG) {
     for (int s = 0; s <= NV; ++s) {
       dbg.sigma[(item * (NV + 1) + s) * a.V + v] = sg[s];
@@ -287,58 +313,74 @@ __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.w
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
-__device__ __forceinline__ void named_bar(int id, int nthreads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-constexpr int KCMAX = 8;
+constexpr int NGW = 2;  // gather warps per CTA
+__host__ __device__ constexpr int cons_target(int D, int M) { return nmodes(M, D) >= 20 ? 320 : 160; }
+__host__ __device__ constexpr int min_blocks(int D, int M) { return nmodes(M, D) >= 20 ? 1 : 2; }
+__host__ __device__ constexpr int max_threads(int D, int M) { return cons_target(D, M) + 32 * (1 + NGW); }
 
 struct PipeCfg {
   int stages;
-  int64_t stage_bytes, hdr_bytes, out_bytes, sig_bytes;
-  int64_t off_hdr, off_stage, off_out, off_sig, off_bar, smem;
+  int64_t stage_bytes, stage_q_off, hdr_bytes, out_bytes;
+  int64_t off_hdr, off_stage, off_out, off_bar, smem;
   int ncw;  // consumer warps
 };
 
+struct Ring {  // stage index + mbarrier phase of a ring of S stages
+  int st = 0;
+  uint32_t ph = 0;
+  __device__ __forceinline__ void next(int S) {
+    if (++st == S) {
+      st = 0;
+      ph ^= 1u;
+    }
+  }
+};
+
 // ---------------------------------------------------------------- pipelined kernel
-template <int D, int M>
-__global__ void __launch_bounds__(11 * 32, 1) k_pipelined(KArgs a, PipeCfg pc) {
+// Warp roles: [0, ncw) consumers, thread tid ↔ (ct, v) = (tid / V, tid % V);
+// warp ncw: TMA producer (lane 0); warps ncw+1 .. ncw+NGW: gathers.
+// Stage = B⁺ chunk [T][R][kc] (one bulk copy) + gathered Q [T·V][KC] (cp.async).
+template <int D, int M, int KC>
+__global__ void __launch_bounds__(max_threads(D, M), min_blocks(D, M)) k_pipelined(KArgs a, PipeCfg pc) {
   constexpr int NM = nmodes(M, D), R = NM - 1, NV = D + 1;
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned char* hdr = smem + pc.off_hdr;
   unsigned char* stg = smem + pc.off_stage;
   double* outs = (double*)(smem + pc.off_out);
-  double* sig = (double*)(smem + pc.off_sig);
   uint64_t* bars = (uint64_t*)(smem + pc.off_bar);
-  uint64_t* hdr_full = bars;            // [2]
-  uint64_t* hdr_empty = bars + 2;       // [2]
-  uint64_t* ch_full = bars + 4;         // [S]
+  uint64_t* hdr_full = bars;                  // [2]
+  uint64_t* hdr_empty = bars + 2;             // [2]
+  uint64_t* ch_full = bars + 4;               // [S]
   uint64_t* ch_empty = bars + 4 + pc.stages;  // [S]
   const int S = pc.stages;
-  const int ncons = pc.ncw * 32;
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
+  const int TV = a.T * a.V;
 
   if (tid == 0) {
     for (int b = 0; b < 2; ++b) {
       mbar_init(&hdr_full[b], 1);
-      mbar_init(&hdr_empty[b], pc.ncw);
+      mbar_init(&hdr_empty[b], pc.ncw + NGW);
     }
     for (int s = 0; s < S; ++s) {
-      mbar_init(&ch_full[s], 1);
+      mbar_init(&ch_full[s], 1 + NGW * 32);
       mbar_init(&ch_empty[s], pc.ncw);
     }
     fence_barrier_init();
   }
-  // Σ' into shared memory
-  const int nsig = R * (R + 1) / 2;
-  for (int i = tid; i < nsig; i += blockDim.x) sig[i] = a.sig[i];
   __syncthreads();
 
   if (warp == pc.ncw) {
-    // ------------------------------------------------ producer warp
+    // ------------------------------------------------ TMA producer
     if (lane == 0) {
-      uint32_t gc = 0;
+      Ring rg;
       int it = 0;
       for (int64_t tile = a.tile_begin + blockIdx.x; tile < a.tile_end; tile += gridDim.x, ++it) {
         const unsigned char* tb = a.blocks + tile * a.tile_bytes;
@@ -346,81 +388,135 @@ __global__ void __launch_bounds__(11 * 32, 1) k_pipelined(KArgs a, PipeCfg pc) {
         mbar_wait(&hdr_empty[hb], ((it >> 1) & 1) ^ 1);
         mbar_expect_tx(&hdr_full[hb], (uint32_t)pc.hdr_bytes);
         bulk_g2s(hdr + hb * pc.hdr_bytes, tb, (uint32_t)pc.hdr_bytes, &hdr_full[hb]);
-        for (int ch = 0; ch < a.NCH; ++ch, ++gc) {
-          const int st = gc % S;
-          const int kc = min(a.KC, a.K - ch * a.KC);
-          const uint32_t bytes = (uint32_t)(kc * (int64_t)a.T * R * 8);
-          mbar_wait(&ch_empty[st], ((gc / S) & 1) ^ 1);
-          mbar_expect_tx(&ch_full[st], bytes);
-          bulk_g2s(stg + st * pc.stage_bytes, tb + a.off_chunks + (int64_t)ch * a.KC * a.T * R * 8, bytes,
-                   &ch_full[st]);
+        for (int ch = 0; ch < a.NCH; ++ch, rg.next(S)) {
+          const int kc = min(KC, a.K - ch * KC);
+          const uint32_t bytes = (uint32_t)(kc * a.T * R * 8);
+          mbar_wait(&ch_empty[rg.st], rg.ph ^ 1);
+          mbar_expect_tx(&ch_full[rg.st], bytes);
+          bulk_g2s(stg + rg.st * pc.stage_bytes, tb + a.off_chunks + (int64_t)ch * KC * a.T * R * 8, bytes,
+                   &ch_full[rg.st]);
         }
       }
     }
     return;
   }
+  if (warp > pc.ncw) {
+    // ------------------------------------------------ gather warps
+    const int gt = tid - (pc.ncw + 1) * 32;  // 0 .. NGW*32-1
+    constexpr int RMAX = (cons_target(D, M) + NGW * 32 - 1) / (NGW * 32);
+    int g_ct[RMAX], g_off[RMAX];
+#pragma unroll
+    for (int i = 0; i < RMAX; ++i) {
+      const int r = gt + i * NGW * 32;
+      g_ct[i] = r < TV ? r / a.V : -1;
+      g_off[i] = r < TV ? (r % a.V) * (int)a.avs : 0;
+    }
+    Ring rg;
+    int it = 0;
+    for (int64_t tile = a.tile_begin + blockIdx.x; tile < a.tile_end; tile += gridDim.x, ++it) {
+      const int hb = it & 1;
+      mbar_wait(&hdr_full[hb], (it >> 1) & 1);
+      const int32_t* ids = (const int32_t*)(hdr + hb * pc.hdr_bytes + a.off_ids);
+      for (int ch = 0; ch < a.NCH; ++ch, rg.next(S)) {
+        const int kc = min(KC, a.K - ch * KC);
+        mbar_wait(&ch_empty[rg.st], rg.ph ^ 1);
+        double* Qg = (double*)(stg + rg.st * pc.stage_bytes + pc.stage_q_off);
+        const int32_t* idc = ids + (size_t)ch * KC * a.T;
+#pragma unroll
+        for (int i = 0; i < RMAX; ++i) {
+          if (g_ct[i] >= 0) {
+            double* dst = Qg + (size_t)(gt + i * NGW * 32) * KC;
+            const double* src = a.Q + g_off[i];
+#pragma unroll
+            for (int kk = 0; kk < KC; ++kk)
+              if (kk < kc) cp_async8(dst + kk, src + int64_t(idc[kk * a.T + g_ct[i]]) * a.acs);
+          }
+        }
+        cp_async_arrive_noinc(&ch_full[rg.st]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&hdr_empty[hb]);
+    }
+    return;
+  }
 
   // -------------------------------------------------- consumer warps
-  const bool active = tid < a.T * a.V;
+  const bool active = tid < TV;
   const int ct = active ? tid / a.V : 0;
   const int v = active ? tid % a.V : 0;
   const double* Qv = a.Q + v * a.avs;
-  uint32_t gc = 0;
+  double* outw = outs + (size_t)warp * 32 * NM;  // this warp's output staging
+  Ring rg;
   int it = 0;
   for (int64_t tile = a.tile_begin + blockIdx.x; tile < a.tile_end; tile += gridDim.x, ++it) {
     const int hb = it & 1;
     const int64_t c = tile * a.T + ct;
     const bool live = active && c < a.n_owned;
-    const double qi = live ? Qv[c * a.acs] : 0.0;
+    const double qi = live ? __ldg(Qv + c * a.acs) : 0.0;
     mbar_wait(&hdr_full[hb], (it >> 1) & 1);
     const unsigned char* hb_p = hdr + hb * pc.hdr_bytes;
     const int32_t* ids = (const int32_t*)(hb_p + a.off_ids);
-
-    double acc[R];
-#pragma unroll
-    for (int l = 0; l < R; ++l) acc[l] = 0.0;
-    for (int ch = 0; ch < a.NCH; ++ch, ++gc) {
-      const int st = gc % S;
-      const int kc = min(a.KC, a.K - ch * a.KC);
-      // gather this chunk's ΔQ first (KC loads in flight), then wait for B
-      double dq[KCMAX];
-#pragma unroll
-      for (int kk = 0; kk < KCMAX; ++kk) {
-        dq[kk] = 0.0;
-        if (kk < kc && live) {
-          const int32_t j = ids[(size_t)(ch * a.KC + kk) * a.T + ct];
-          dq[kk] = __ldg(Qv + int64_t(j) * a.acs) - qi;
-        }
-      }
-      mbar_wait(&ch_full[st], (gc / S) & 1);
-      const double* Bs = (const double*)(stg + st * pc.stage_bytes);
-#pragma unroll
-      for (int kk = 0; kk < KCMAX; ++kk) {
-        if (kk < kc) {
-          const double* b = Bs + ((size_t)kk * a.T + ct) * R;
-#pragma unroll
-          for (int l = 0; l < R; ++l) acc[l] += b[l] * dq[kk];
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&ch_empty[st]);
-    }
-
-    // sectors (P:184-191)
-    const double* sinv = (const double*)(hb_p + a.off_sinv) + size_t(ct) * NV * D * D;
     const uint8_t* slots = (const uint8_t*)(hb_p + a.off_slots) + size_t(ct) * NV * D;
-    double ps[NV][D];
+    // prefetch the sector averages now; consumed after the main loop
     bool valid[NV];
+    double qs[NV][D];
 #pragma unroll
     for (int s = 0; s < NV; ++s) {
       valid[s] = slots[s * D] != 255;
-      double dqs[D];
 #pragma unroll
       for (int m = 0; m < D; ++m) {
         const int g = valid[s] ? slots[s * D + m] : 0;
         const int32_t j = ids[size_t(g) * a.T + ct];
-        dqs[m] = (valid[s] && live) ? __ldg(Qv + int64_t(j) * a.acs) - qi : 0.0;
+        qs[s][m] = (valid[s] && live) ? __ldg(Qv + int64_t(j) * a.acs) : qi;
       }
+    }
+
+    double acc[R];
+#pragma unroll
+    for (int l = 0; l < R; ++l) acc[l] = 0.0;
+    for (int ch = 0; ch < a.NCH; ++ch, rg.next(S)) {
+      const int kc = min(KC, a.K - ch * KC);
+      mbar_wait(&ch_full[rg.st], rg.ph);
+      const double* Bs = (const double*)(stg + rg.st * pc.stage_bytes);
+      const double* Qg = (const double*)(stg + rg.st * pc.stage_bytes + pc.stage_q_off) + (size_t)tid * KC;
+      if (kc == KC && (KC % 2) == 0) {
+        double dq[KC];
+#pragma unroll
+        for (int p = 0; p < KC / 2; ++p) {
+          const double2 q2 = reinterpret_cast<const double2*>(Qg)[p];
+          dq[2 * p] = live ? q2.x - qi : 0.0;
+          dq[2 * p + 1] = live ? q2.y - qi : 0.0;
+        }
+        const double2* b2 = reinterpret_cast<const double2*>(Bs + (size_t)ct * R * KC);
+#pragma unroll
+        for (int l = 0; l < R; ++l) {
+#pragma unroll
+          for (int p = 0; p < KC / 2; ++p) {
+            const double2 bb = b2[l * (KC / 2) + p];
+            acc[l] += bb.x * dq[2 * p];
+            acc[l] += bb.y * dq[2 * p + 1];
+          }
+        }
+      } else {
+        const double* b = Bs + (size_t)ct * R * kc;
+        for (int kk = 0; kk < kc; ++kk) {
+          const double dq = live ? Qg[kk] - qi : 0.0;
+#pragma unroll
+          for (int l = 0; l < R; ++l) acc[l] += b[l * kc + kk] * dq;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ch_empty[rg.st]);
+    }
+
+    // sectors (P:184-191)
+    const double* sinv = (const double*)(hb_p + a.off_sinv) + size_t(ct) * NV * D * D;
+    double ps[NV][D];
+#pragma unroll
+    for (int s = 0; s < NV; ++s) {
+      double dqs[D];
+#pragma unroll
+      for (int m = 0; m < D; ++m) dqs[m] = qs[s][m] - qi;
 #pragma unroll
       for (int l = 0; l < D; ++l) {
         double t = 0.0;
@@ -433,30 +529,29 @@ __global__ void __launch_bounds__(11 * 32, 1) k_pipelined(KArgs a, PipeCfg pc) {
     if (lane == 0) mbar_arrive(&hdr_empty[hb]);
 
     double w[NM];
-    cweno_epilogue<D, NM>(qi, acc, ps, valid, a, sig, w, nullptr, nullptr);
+    cweno_epilogue<D, NM>(qi, acc, ps, valid, a, w, nullptr, nullptr);
 
     if (a.dense_out) {
-      if (tid == 0) bulk_wait_read();  // previous tile's store has read outs
-      named_bar(1, ncons);
-      if (live) {
-        double* o = outs + (size_t)(ct * a.V + v) * NM;
+      // per-warp staging + one bulk store of the warp's contiguous output rows
+      const int64_t first = tile * (int64_t)TV + warp * 32;  // (cell·V + v) index of lane 0
+      const int64_t lim = min((int64_t)TV, (a.n_owned - tile * a.T) * a.V) - warp * 32;
+      const int nlive = (int)max((int64_t)0, min((int64_t)32, lim));
+      if (lane == 0) bulk_wait_read();
+      __syncwarp();
+      if (lane < nlive) {
 #pragma unroll
-        for (int l = 0; l < NM; ++l) o[l] = w[l];
+        for (int l = 0; l < NM; ++l) outw[lane * NM + l] = w[l];
       }
       fence_proxy_async();
-      named_bar(1, ncons);
-      if (tid == 0) {
-        const int64_t c0 = tile * a.T;
-        const int64_t ncell = min((int64_t)a.T, a.n_owned - c0);
-        bulk_s2g(a.out + c0 * a.ccs, outs, (uint32_t)(ncell * a.V * NM * 8));
-      }
+      __syncwarp();
+      if (lane == 0 && nlive > 0) bulk_s2g(a.out + first * NM, outw, (uint32_t)(nlive * NM * 8));
     } else if (live) {
       double* o = a.out + c * a.ccs + v * a.cvs;
 #pragma unroll
       for (int l = 0; l < NM; ++l) o[l] = w[l];
     }
   }
-  if (tid == 0) bulk_wait_all();
+  if (lane == 0) bulk_wait_all();
 }
 
 // ---------------------------------------------------------------- halo pack
@@ -480,18 +575,32 @@ void launch_simple(int d, int M, dim3 g, dim3 b, cudaStream_t st, const KArgs& a
 }
 
 using PipeFn = void (*)(KArgs, PipeCfg);
-PipeFn pipe_fn(int d, int M) {
+template <int D, int M>
+PipeFn pipe_fn_kc(int KC) {
+  switch (KC) {
+    case 1: return k_pipelined<D, M, 1>;
+    case 2: return k_pipelined<D, M, 2>;
+    case 3: return k_pipelined<D, M, 3>;
+    case 4: return k_pipelined<D, M, 4>;
+    case 5: return k_pipelined<D, M, 5>;
+    case 6: return k_pipelined<D, M, 6>;
+    case 8: return k_pipelined<D, M, 8>;
+    default: fail(CWRECO_EUNSUPPORTED, "unsupported chunk size " + std::to_string(KC));
+  }
+}
+PipeFn pipe_fn(int d, int M, int KC) {
 #define CASE(DD, MM) \
-  if (d == DD && M == MM) return k_pipelined<DD, MM>;
+  if (d == DD && M == MM) return pipe_fn_kc<DD, MM>(KC);
   CASE(2, 1) CASE(2, 2) CASE(2, 3) CASE(2, 4) CASE(3, 1) CASE(3, 2) CASE(3, 3)
 #undef CASE
   fail(CWRECO_EUNSUPPORTED, "unsupported (d, M)");
 }
 
-static KArgs make_args(const cwreco_ctx* c, const double* avgs, int64_t acs, int64_t avs, double* out,
-                       int64_t ccs, int64_t cvs) {
+static KArgs make_args(const cwreco_ctx* c, const double* avgs, int64_t acs, int64_t avs, double* out, int64_t ccs,
+                       int64_t cvs) {
   const Layout& L = c->lay;
   KArgs a;
+  std::memset(&a, 0, sizeof(a));
   a.blocks = c->dev->blocks;
   a.tile_bytes = L.tile_bytes;
   a.off_ids = L.off_ids;
@@ -514,35 +623,42 @@ static KArgs make_args(const cwreco_ctx* c, const double* avgs, int64_t acs, int
   a.ccs = ccs;
   a.cvs = cvs;
   a.dense_out = 0;
-  a.sig = c->dev->sigma;
-  a.lam0 = c->prm.lambda0;
-  a.lams = c->prm.lambda_s;
   a.eps = c->prm.eps;
   a.psi1 = c->psi1;
   a.r = c->prm.r;
+  for (int n = 0; n <= c->d + 1; ++n) {
+    const double denom = c->prm.lambda0 + n * c->prm.lambda_s;  // R5: λ normalised over valid stencils
+    a.l0[n] = c->prm.lambda0 / denom;
+    a.inv_l0[n] = 1.0 / a.l0[n];
+    a.ls[n] = c->prm.lambda_s / denom;
+  }
   return a;
 }
 
 static PipeCfg pipe_cfg(const cwreco_ctx* c) {
   const Layout& L = c->lay;
   PipeCfg p;
+  auto r128 = [](int64_t x) { return (x + 127) & ~int64_t(127); };
   p.ncw = (L.T * c->V + 31) / 32;
   p.hdr_bytes = L.header_bytes;
-  p.stage_bytes = (int64_t)L.KC * L.kslice_bytes;
-  p.out_bytes = ((int64_t)L.T * c->V * c->nm * 8 + 127) & ~int64_t(127);
-  p.sig_bytes = ((int64_t)(c->nm - 1) * c->nm / 2 * 8 + 127) & ~int64_t(127);
-  auto r128 = [](int64_t x) { return (x + 127) & ~int64_t(127); };
+  p.stage_q_off = r128((int64_t)L.KC * L.kslice_bytes);
+  p.stage_bytes = r128(p.stage_q_off + (int64_t)L.KC * L.T * c->V * 8);
+  p.out_bytes = r128((int64_t)p.ncw * 32 * c->nm * 8);
+  const int blocks = c->nm >= 20 ? 1 : 2;
+  const int64_t budget = (c->dev->max_smem + 1024) / blocks - 1024;
   int best = 2;
-  for (int s = 6; s >= 2; --s) {
-    int64_t tot = r128(2 * p.hdr_bytes) + r128(s * p.stage_bytes) + p.out_bytes + p.sig_bytes + 256;
-    if (tot <= c->dev->max_smem) { best = s; break; }
+  for (int s = 8; s >= 2; --s) {
+    int64_t tot = r128(2 * p.hdr_bytes) + s * p.stage_bytes + p.out_bytes + 8 * (4 + 2 * s);
+    if (tot <= budget) {
+      best = s;
+      break;
+    }
   }
   p.stages = best;
   p.off_hdr = 0;
   p.off_stage = r128(2 * p.hdr_bytes);
-  p.off_out = p.off_stage + r128(best * p.stage_bytes);
-  p.off_sig = p.off_out + p.out_bytes;
-  p.off_bar = p.off_sig + p.sig_bytes;
+  p.off_out = p.off_stage + best * p.stage_bytes;
+  p.off_bar = p.off_out + p.out_bytes;
   p.smem = p.off_bar + 8 * (4 + 2 * best);
   return p;
 }
@@ -559,7 +675,6 @@ void dev_destroy(cwreco_ctx* c) {
   if (!c->dev) return;
   cudaSetDevice(c->device);
   cudaFree(c->dev->blocks);
-  cudaFree(c->dev->sigma);
   cudaFree(c->dev->send);
   cudaFree(c->dev->dbg);
   cudaFree(c->dev->dbg_cells);
@@ -585,16 +700,14 @@ void dev_upload_blocks(cwreco_ctx* c, int64_t offset, const unsigned char* host,
 }
 
 void dev_upload_aux(cwreco_ctx* c) {
-  const int nm = c->nm, R = nm - 1;
+  const int nm = c->nm;
   std::vector<double> packed;
   for (int l = 1; l < nm; ++l)
     for (int m = l; m < nm; ++m) packed.push_back((l == m ? 1.0 : 2.0) * c->sigma[l * nm + m]);
-  if (c->dev->sigma) CK(cudaFree(c->dev->sigma));
-  CK(cudaMalloc(&c->dev->sigma, sizeof(double) * (packed.size() + 1)));
-  CK(cudaMemcpy(c->dev->sigma, packed.data(), sizeof(double) * packed.size(), cudaMemcpyHostToDevice));
-  (void)R;
+  CK(cudaSetDevice(c->device));
+  CK(cudaMemcpyToSymbol(c_sig, packed.data(), sizeof(double) * packed.size(), sizeof(double) * sig_off(c->d, c->M)));
   PipeCfg p = pipe_cfg(c);
-  PipeFn f = pipe_fn(c->d, c->M);
+  PipeFn f = pipe_fn(c->d, c->M, c->lay.KC);
   CK(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
 }
 
@@ -626,16 +739,13 @@ void dev_reconstruct(cwreco_ctx* c, const double* avgs, int64_t acs, int64_t avs
     DbgOut o{};
     launch_simple<false>(c->d, c->M, g, b, st, a, o);
   } else {
-    a.dense_out = (cvs == nm && ccs == (int64_t)c->V * nm && (((uintptr_t)coeffs) & 15) == 0 &&
-                   ((int64_t)c->V * nm) % 2 == 0)
-                      ? 1
-                      : 0;
+    a.dense_out = (cvs == nm && ccs == (int64_t)c->V * nm && (((uintptr_t)coeffs) & 15) == 0 && nm % 2 == 0) ? 1 : 0;
     PipeCfg p = pipe_cfg(c);
     const int64_t ntiles = a.tile_end - a.tile_begin;
-    const int per_sm = std::max<int>(1, int(c->dev->max_smem / std::max<int64_t>(p.smem, 1)));
-    const int64_t grid = std::min<int64_t>(ntiles, (int64_t)c->dev->num_sms * std::min(per_sm, 2));
-    dim3 b((p.ncw + 1) * 32), g((unsigned)grid);
-    pipe_fn(c->d, c->M)<<<g, b, p.smem, st>>>(a, p);
+    const int per_sm = c->nm >= 20 ? 1 : 2;
+    const int64_t grid = std::min<int64_t>(ntiles, (int64_t)c->dev->num_sms * per_sm);
+    dim3 b((p.ncw + 1 + NGW) * 32), g((unsigned)grid);
+    pipe_fn(c->d, c->M, c->lay.KC)<<<g, b, p.smem, st>>>(a, p);
   }
   CK(cudaGetLastError());
 }
@@ -649,11 +759,13 @@ void dev_debug(cwreco_ctx* c, const double* avgs, int64_t acs, int64_t avs, int6
   const int64_t bytes = total * 8;
   if (bytes > c->dev->dbg_bytes) {
     cudaFree(c->dev->dbg);
+    c->dev->dbg = nullptr;
     CK(cudaMalloc(&c->dev->dbg, bytes));
     c->dev->dbg_bytes = bytes;
   }
   if (n_sel > c->dev->dbg_ncells) {
     cudaFree(c->dev->dbg_cells);
+    c->dev->dbg_cells = nullptr;
     CK(cudaMalloc(&c->dev->dbg_cells, n_sel * 8));
     c->dev->dbg_ncells = n_sel;
   }

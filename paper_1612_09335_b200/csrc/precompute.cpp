@@ -30,13 +30,19 @@ Layout make_layout(int d, int M, int V, int G) {
   L.R = L.nm - 1;
   L.K = d * L.nm - 1;
   L.G = G;
-  int T = (320 / V) & ~1;
+  // consumer threads per CTA: 320 (1 CTA/SM) for the register-heavy 3D M=3 kernel,
+  // else 160 (2 CTAs/SM); one tile = T cells × V variables = one consumer thread each
+  const int target = (L.nm >= 20) ? 320 : 160;
+  int T = (target / V) & ~1;
   if (T < 2) T = 2;
-  if (T > 128) T = 128;
   L.T = T;
   L.kslice_bytes = int64_t(T) * L.R * 8;
-  L.KC = std::max<int>(1, int(20480 / L.kslice_bytes));
-  L.KC = std::min(std::min(L.KC, L.K), 8);  // kernels unroll up to 8 k-slices
+  // k-slices per streamed chunk: ~10 KB of B⁺ per stage, even (the kernel reads
+  // k-pairs with 16-byte shared loads), at most 8
+  L.KC = std::max<int>(1, int(10240 / L.kslice_bytes));
+  L.KC = std::min(L.KC, 8);
+  L.KC = (L.KC + 1) & ~1;
+  if (L.KC > L.K) L.KC = L.K;
   L.NCH = (L.K + L.KC - 1) / L.KC;
   L.off_ids = 0;
   L.off_sinv = r16(int64_t(G) * T * 4);
@@ -310,9 +316,13 @@ void precompute(cwreco_ctx* c) {
       double cond = 0.0;
       if (!pinv_qr(K, R, A, Bp, cond)) { bad_singular |= 1; continue; }
       cond_max = std::max(cond_max, cond);
-      // B chunks: [k][T][R]
-      for (int k = 0; k < K; ++k)
-        for (int l = 0; l < R; ++l) Bch[(size_t(k) * T + ct) * R + l] = Bp[size_t(l) * K + k];
+      // B chunks: chunk ch holds k in [ch·KC, ch·KC + kc) as [T][R][kc]
+      for (int k = 0; k < K; ++k) {
+        const int ch = k / L.KC, kk = k % L.KC;
+        const int kc = std::min(L.KC, K - ch * L.KC);
+        double* chb = Bch + size_t(ch) * L.KC * T * R;
+        for (int l = 0; l < R; ++l) chb[(size_t(ct) * R + l) * kc + kk] = Bp[size_t(l) * K + k];
+      }
 
       // sector inverses
       for (int s = 0; s < nv; ++s) {

@@ -214,12 +214,18 @@ def ic_eval(name: str, x: np.ndarray) -> np.ndarray:
     raise ValueError(f"unknown initial condition {name!r}")
 
 
-def cell_averages(nodes, cells, period, func, nvars: int, chunk: int = 1 << 18):
-    """Quadrature cell averages of ``func(points [P,d]) -> [P, nvars]``."""
+def cell_averages(nodes, cells, period, func, nvars: int, chunk: int = 1 << 16):
+    """Quadrature cell averages of ``func(points [P,d]) -> [P, nvars]``.
+
+    Chunks are independent (same operations per cell whatever the chunking), so
+    they are evaluated on a thread pool (numpy releases the GIL)."""
+    import concurrent.futures as cf
+    import os
     d = nodes.shape[1]
     bary, w = _rule(d)
     out = np.empty((cells.shape[0], nvars), dtype=np.float64)
-    for s in range(0, cells.shape[0], chunk):
+
+    def work(s):
         X = unwrap_cells(nodes, cells[s:s + chunk], period)  # (c, d+1, d)
         pts = np.einsum("qk,ckd->cqd", bary, X)  # (c, q, d)
         P = pts.reshape(-1, d)
@@ -227,6 +233,15 @@ def cell_averages(nodes, cells, period, func, nvars: int, chunk: int = 1 << 18):
             P = P - np.floor(P / period) * period
         vals = func(P).reshape(pts.shape[0], pts.shape[1], nvars)
         out[s:s + chunk] = np.einsum("q,cqv->cv", w, vals)
+
+    starts = range(0, cells.shape[0], chunk)
+    nw = min(32, os.cpu_count() or 1)
+    if len(starts) == 1 or nw == 1:
+        for s in starts:
+            work(s)
+    else:
+        with cf.ThreadPoolExecutor(nw) as ex:
+            list(ex.map(work, starts))
     return out
 
 

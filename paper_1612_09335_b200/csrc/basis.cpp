@@ -179,6 +179,77 @@ void gauss_legendre01(int n, std::vector<double>& x, std::vector<double>& w) {
   }
 }
 
+// Monomial form of the basis: exps [nmono][3] (ζ exponent 0 for d=2, total degree
+// <= M, graded order) and coef [ℳ][nmono] with ψ_l = Σ_e coef[l][e] ξ^e.
+void basis_monomials(int d, int M, std::vector<int>& exps, std::vector<double>& coef) {
+  const int nm = n_modes(M, d);
+  const int P = M + 1;
+  Poly one(P, 1.0);
+  Poly vars[3] = {Poly(P), Poly(P), Poly(P)};
+  vars[0].at(1, 0, 0) = 1.0;
+  if (P > 1) vars[1].at(0, 1, 0) = 1.0;
+  if (d == 3 && P > 1) vars[2].at(0, 0, 1) = 1.0;
+  std::vector<Poly> psi;
+  dubiner<Poly>(d, M, vars, one, psi);
+  exps.clear();
+  for (int n = 0; n <= M; ++n)
+    for (int i = n; i >= 0; --i)
+      for (int j = n - i; j >= 0; --j) {
+        const int k = n - i - j;
+        if (d == 2 && k != 0) continue;
+        exps.push_back(i);
+        exps.push_back(j);
+        exps.push_back(k);
+      }
+  const int ne = (int)exps.size() / 3;
+  coef.assign(size_t(nm) * ne, 0.0);
+  for (int l = 0; l < nm; ++l)
+    for (int e = 0; e < ne; ++e) coef[size_t(l) * ne + e] = psi[l].at(exps[3 * e], exps[3 * e + 1], exps[3 * e + 2]);
+}
+
+// Gauss-Jacobi nodes/weights for the weight (1-x)^alpha on [-1,1] (beta = 0), mapped
+// to t = (1+x)/2 ∈ [0,1] (weights not normalised).  Newton with deflation.
+void gauss_jacobi01(int n, double alpha, std::vector<double>& t, std::vector<double>& w) {
+  const double beta = 0.0;
+  auto jac = [&](int m, double al, double be, double x) {  // P_m^{(al,be)}(x)
+    if (m == 0) return 1.0;
+    double p0 = 1.0, p1 = 0.5 * ((al + be + 2.0) * x + (al - be));
+    for (int k = 2; k <= m; ++k) {
+      const double s = 2.0 * k + al + be;
+      const double a1 = 2.0 * k * (k + al + be) * (s - 2.0);
+      const double a2 = (s - 1.0) * (al * al - be * be);
+      const double a3 = (s - 2.0) * (s - 1.0) * s;
+      const double a4 = 2.0 * (k + al - 1.0) * (k + be - 1.0) * s;
+      const double p2 = ((a2 + a3 * x) * p1 - a4 * p0) / a1;
+      p0 = p1;
+      p1 = p2;
+    }
+    return p1;
+  };
+  auto djac = [&](double x) { return 0.5 * (n + alpha + beta + 1.0) * jac(n - 1, alpha + 1.0, beta + 1.0, x); };
+  std::vector<double> x(n);
+  for (int k = 0; k < n; ++k) {
+    double r = -std::cos((2.0 * k + 1.0) * M_PI / (2.0 * n));
+    if (k > 0) r = 0.5 * (r + x[k - 1]);
+    for (int it = 0; it < 100; ++it) {
+      double s = 0.0;
+      for (int i = 0; i < k; ++i) s += 1.0 / (r - x[i]);
+      const double p = jac(n, alpha, beta, r);
+      const double delta = -p / (djac(r) - s * p);
+      r += delta;
+      if (std::fabs(delta) < 1e-16) break;
+    }
+    x[k] = r;
+  }
+  t.assign(n, 0.0);
+  w.assign(n, 0.0);
+  for (int k = 0; k < n; ++k) {
+    const double dp = djac(x[k]);
+    t[k] = 0.5 * (1.0 + x[k]);
+    w[k] = 1.0 / ((1.0 - x[k] * x[k]) * dp * dp);  // ∝ Gauss-Jacobi weight (constant factor dropped)
+  }
+}
+
 std::vector<double> sigma_matrix(int d, int M) {
   const int nm = n_modes(M, d);
   const int P = M + 1;

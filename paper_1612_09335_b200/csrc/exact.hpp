@@ -46,24 +46,35 @@ inline void push(Ex& h, double v) {
   h.t[h.n++] = v;
 }
 
-// h = e + b   (Shewchuk, Grow-Expansion with zero elimination)
-inline Ex grow(const Ex& e, double b) {
-  Ex h;
+// e += b in place (Shewchuk, Grow-Expansion with zero elimination)
+inline void grow_inplace(Ex& e, double b) {
   double Q = b;
+  int k = 0;
   for (int i = 0; i < e.n; ++i) {
     double Qn, hh;
     two_sum(Q, e.t[i], Qn, hh);
     Q = Qn;
-    if (hh != 0.0) push(h, hh);
+    if (hh != 0.0) e.t[k++] = hh;
   }
-  if (Q != 0.0 || h.n == 0) push(h, Q);
-  if (h.n == 1 && h.t[0] == 0.0) h.n = 0;
+  if (Q != 0.0 || k == 0) {
+    if (k >= CAP) throw std::runtime_error("exact expansion overflow");
+    e.t[k++] = Q;
+  }
+  e.n = k;
+  if (e.n == 1 && e.t[0] == 0.0) e.n = 0;
+}
+
+inline Ex grow(const Ex& e, double b) {
+  Ex h;
+  h.n = e.n;
+  for (int i = 0; i < e.n; ++i) h.t[i] = e.t[i];
+  grow_inplace(h, b);
   return h;
 }
 
-// Compression to a short nonoverlapping expansion (Shewchuk, Compress)
-inline Ex compress(const Ex& e) {
-  if (e.n <= 1) return e;
+// Compression to a short nonoverlapping expansion, in place (Shewchuk, Compress)
+inline void compress_inplace(Ex& e) {
+  if (e.n <= 1) return;
   double g[CAP];
   int bottom = e.n - 1;
   double Q = e.t[bottom];
@@ -77,36 +88,59 @@ inline Ex compress(const Ex& e) {
       Q = Qn;
     }
   }
-  Ex h;
+  int top = 0;
   for (int i = bottom + 1; i < e.n; ++i) {
     double Qn, q;
     fast_two_sum(g[i], Q, Qn, q);
-    if (q != 0.0) push(h, q);
+    if (q != 0.0) e.t[top++] = q;
     Q = Qn;
   }
-  if (Q != 0.0 || h.n == 0) push(h, Q);
-  if (h.n == 1 && h.t[0] == 0.0) h.n = 0;
+  if (Q != 0.0 || top == 0) e.t[top++] = Q;
+  e.n = top;
+  if (e.n == 1 && e.t[0] == 0.0) e.n = 0;
+}
+
+inline Ex compress(const Ex& e) {
+  Ex h;
+  h.n = e.n;
+  for (int i = 0; i < e.n; ++i) h.t[i] = e.t[i];
+  compress_inplace(h);
   return h;
+}
+
+inline void add_into(Ex& acc, const Ex& b) {  // acc += b, compressed
+  for (int i = 0; i < b.n; ++i) grow_inplace(acc, b.t[i]);
+  compress_inplace(acc);
 }
 
 inline Ex add(const Ex& a, const Ex& b) {
-  Ex h = a;
-  for (int i = 0; i < b.n; ++i) h = grow(h, b.t[i]);
-  return compress(h);
-}
-
-inline Ex neg(const Ex& a) {
-  Ex h = a;
-  for (int i = 0; i < h.n; ++i) h.t[i] = -h.t[i];
+  Ex h;
+  h.n = a.n;
+  for (int i = 0; i < a.n; ++i) h.t[i] = a.t[i];
+  add_into(h, b);
   return h;
 }
 
-inline Ex sub(const Ex& a, const Ex& b) { return add(a, neg(b)); }
+inline Ex neg(const Ex& a) {
+  Ex h;
+  h.n = a.n;
+  for (int i = 0; i < h.n; ++i) h.t[i] = -a.t[i];
+  return h;
+}
+
+inline Ex sub(const Ex& a, const Ex& b) {
+  Ex h;
+  h.n = a.n;
+  for (int i = 0; i < a.n; ++i) h.t[i] = a.t[i];
+  for (int i = 0; i < b.n; ++i) grow_inplace(h, -b.t[i]);
+  compress_inplace(h);
+  return h;
+}
 
 // h = e * b   (Shewchuk, Scale-Expansion with zero elimination)
-inline Ex scale(const Ex& e, double b) {
-  Ex h;
-  if (e.n == 0 || b == 0.0) return h;
+inline void scale_into(const Ex& e, double b, Ex& h) {
+  h.n = 0;
+  if (e.n == 0 || b == 0.0) return;
   double Q, hh;
   two_prod(e.t[0], b, Q, hh);
   if (hh != 0.0) push(h, hh);
@@ -120,12 +154,20 @@ inline Ex scale(const Ex& e, double b) {
   }
   if (Q != 0.0 || h.n == 0) push(h, Q);
   if (h.n == 1 && h.t[0] == 0.0) h.n = 0;
+}
+
+inline Ex scale(const Ex& e, double b) {
+  Ex h;
+  scale_into(e, b, h);
   return h;
 }
 
 inline Ex mul(const Ex& a, const Ex& b) {
-  Ex acc;
-  for (int i = 0; i < b.n; ++i) acc = add(acc, scale(a, b.t[i]));
+  Ex acc, tmp;
+  for (int i = 0; i < b.n; ++i) {
+    scale_into(a, b.t[i], tmp);
+    add_into(acc, tmp);
+  }
   return acc;
 }
 

@@ -100,7 +100,9 @@ void build_stencils(cwreco_ctx* c);
 // basis.cpp
 void basis_eval(int d, int M, const double* xi, double* out);  // ψ_l(ξ), l < ℳ
 std::vector<double> sigma_matrix(int d, int M);                  // Σ by quadrature
+void basis_monomials(int d, int M, std::vector<int>& exps, std::vector<double>& coef);
 void gauss_legendre01(int n, std::vector<double>& x, std::vector<double>& w);
+void gauss_jacobi01(int n, double alpha, std::vector<double>& t, std::vector<double>& w);
 // precompute.cpp
 void precompute(cwreco_ctx* c);
 // kernels.cu (device side; all return cudaError_t as int)

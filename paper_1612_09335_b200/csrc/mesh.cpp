@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstring>
 #include <numeric>
+#include <parallel/algorithm>
 
 #include "exact.hpp"
 #include "internal.hpp"
@@ -151,7 +152,7 @@ void set_mesh(cwreco_ctx* c, int64_t n_nodes, const double* xyz, int64_t n_cells
   }
   std::vector<int64_t> perm(N);
   std::iota(perm.begin(), perm.end(), 0);
-  std::stable_sort(perm.begin(), perm.end(), [&](int64_t a, int64_t b) { return key[a] < key[b]; });
+  __gnu_parallel::stable_sort(perm.begin(), perm.end(), [&](int64_t a, int64_t b) { return key[a] < key[b]; });
 
   c->perm = perm;
   c->cell_nodes.assign(N * nv, 0);
@@ -190,7 +191,7 @@ void set_mesh(cwreco_ctx* c, int64_t n_nodes, const double* xyz, int64_t n_cells
     if (a.n[2] != b.n[2]) return a.n[2] < b.n[2];
     return a.cell < b.cell;
   };
-  std::sort(F.begin(), F.end(), less);
+  __gnu_parallel::sort(F.begin(), F.end(), less);
   auto same = [](const Face& a, const Face& b) { return a.n[0] == b.n[0] && a.n[1] == b.n[1] && a.n[2] == b.n[2]; };
   c->nbr.assign(N * nv, -1);
   for (size_t k = 0; k < F.size();) {
@@ -213,7 +214,7 @@ void set_mesh(cwreco_ctx* c, int64_t n_nodes, const double* xyz, int64_t n_cells
       std::sort(t.begin(), t.begin() + nv);
       srt[s] = t;
     }
-    std::sort(srt.begin(), srt.end());
+    __gnu_parallel::sort(srt.begin(), srt.end());
     for (int64_t s = 1; s < N; ++s)
       if (srt[s] == srt[s - 1]) fail(CWRECO_EMESH, "set_mesh: duplicate cell");
   }

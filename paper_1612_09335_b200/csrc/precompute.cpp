@@ -94,56 +94,62 @@ bool inv_small(int d, const double* A, double* Ainv) {
   return true;
 }
 
-// Householder QR of Ared (m×n, column-major), returns B⁺ (n×m, row-major)
+// Householder QR of Ared (m×n, column-major, overwritten), returns B⁺ = R⁻¹Q₁ᵀ
+// (n×m, row-major).  Q₁ is accumulated explicitly (backward), then one triangular
+// solve per column.
 bool pinv_qr(int m, int n, std::vector<double>& A, std::vector<double>& Bp, double& cond) {
-  std::vector<double> V(size_t(m) * n, 0.0), beta(n), Rd(n);
+  thread_local std::vector<double> V, beta, Q1;
+  V.assign(size_t(m) * n, 0.0);
+  beta.assign(n, 0.0);
+  double rmax = 0.0, rmin = 1e300;
   for (int j = 0; j < n; ++j) {
     double* a = &A[size_t(j) * m];
     double nrm = 0.0;
     for (int r = j; r < m; ++r) nrm += a[r] * a[r];
     nrm = std::sqrt(nrm);
     if (nrm == 0.0) return false;
-    double alpha = a[j] > 0 ? -nrm : nrm;
+    const double alpha = a[j] > 0 ? -nrm : nrm;
     double* v = &V[size_t(j) * m];
     for (int r = j; r < m; ++r) v[r] = a[r];
     v[j] -= alpha;
     double vn = 0.0;
     for (int r = j; r < m; ++r) vn += v[r] * v[r];
     beta[j] = vn > 0 ? 2.0 / vn : 0.0;
-    for (int cidx = j; cidx < n; ++cidx) {
+    a[j] = alpha;
+    for (int r = j + 1; r < m; ++r) a[r] = 0.0;
+    for (int cidx = j + 1; cidx < n; ++cidx) {
       double* ac = &A[size_t(cidx) * m];
       double s = 0.0;
       for (int r = j; r < m; ++r) s += v[r] * ac[r];
       s *= beta[j];
       for (int r = j; r < m; ++r) ac[r] -= s * v[r];
     }
-    Rd[j] = A[size_t(j) * m + j];
-  }
-  double rmax = 0.0, rmin = 1e300;
-  for (int j = 0; j < n; ++j) {
-    rmax = std::max(rmax, std::fabs(Rd[j]));
-    rmin = std::min(rmin, std::fabs(Rd[j]));
+    rmax = std::max(rmax, std::fabs(alpha));
+    rmin = std::min(rmin, std::fabs(alpha));
   }
   if (!(rmin > 1e-12 * rmax)) return false;
   cond = rmax / rmin;
-  Bp.assign(size_t(n) * m, 0.0);
-  std::vector<double> y(m);
-  for (int k = 0; k < m; ++k) {
-    std::fill(y.begin(), y.end(), 0.0);
-    y[k] = 1.0;
-    for (int j = 0; j < n; ++j) {  // y = Qᵀ e_k
-      const double* v = &V[size_t(j) * m];
+  // Q₁ = H_0 H_1 … H_{n-1} [I_n; 0]  (m×n, column-major)
+  Q1.assign(size_t(m) * n, 0.0);
+  for (int c = 0; c < n; ++c) Q1[size_t(c) * m + c] = 1.0;
+  for (int j = n - 1; j >= 0; --j) {
+    const double* v = &V[size_t(j) * m];
+    for (int c = j; c < n; ++c) {
+      double* q = &Q1[size_t(c) * m];
       double s = 0.0;
-      for (int r = j; r < m; ++r) s += v[r] * y[r];
+      for (int r = j; r < m; ++r) s += v[r] * q[r];
       s *= beta[j];
-      for (int r = j; r < m; ++r) y[r] -= s * v[r];
+      for (int r = j; r < m; ++r) q[r] -= s * v[r];
     }
-    for (int j = n - 1; j >= 0; --j) {  // R x = y[0..n)
-      double s = y[j];
-      for (int q = j + 1; q < n; ++q) s -= A[size_t(q) * m + j] * y[q];
-      y[j] = s / A[size_t(j) * m + j];
+  }
+  // B⁺ = R⁻¹ Q₁ᵀ: for each k solve R x = (Q₁ᵀ)_{:,k}
+  Bp.assign(size_t(n) * m, 0.0);
+  for (int k = 0; k < m; ++k) {
+    for (int j = n - 1; j >= 0; --j) {
+      double s = Q1[size_t(j) * m + k];
+      for (int q = j + 1; q < n; ++q) s -= A[size_t(q) * m + j] * Bp[size_t(q) * m + k];
+      Bp[size_t(j) * m + k] = s / A[size_t(j) * m + j];
     }
-    for (int j = 0; j < n; ++j) Bp[size_t(j) * m + k] = y[j];
   }
   return true;
 }
@@ -180,34 +186,43 @@ void precompute(cwreco_ctx* c) {
     return (int32_t)(it - c->local2global.begin());
   };
 
-  // quadrature on T_E exact for degree M + d - 1 per collapsed direction (R19)
-  std::vector<double> gx, gw;
-  gauss_legendre01((M + d + 1) / 2, gx, gw);  // 2n-1 >= M+d-1
+  // conical-product Gauss-Jacobi rule on T_E exact for degree M (R19): collapsed
+  // coordinates (u, v, w), Jacobian (1-v)(1-w)^2 absorbed by Jacobi weights
+  // (1-x)^1 and (1-x)^2, ceil((M+1)/2) points per direction; normalised to average.
   std::vector<double> qp, qw;  // points [nq][d], weights normalised to 1
   {
-    const int n = (int)gx.size();
-    double wsum = 0.0;
+    const int n = (M + 2) / 2;
+    std::vector<double> ua, wa, vb, wb, wc, wcw;
+    gauss_jacobi01(n, 0.0, ua, wa);
+    gauss_jacobi01(n, 1.0, vb, wb);
+    gauss_jacobi01(n, 2.0, wc, wcw);
     if (d == 2) {
       for (int a = 0; a < n; ++a)
         for (int b = 0; b < n; ++b) {
-          qp.push_back(gx[a] * (1 - gx[b]));
-          qp.push_back(gx[b]);
-          qw.push_back(gw[a] * gw[b] * (1 - gx[b]));
+          qp.push_back(ua[a] * (1 - vb[b]));
+          qp.push_back(vb[b]);
+          qw.push_back(wa[a] * wb[b]);
         }
     } else {
       for (int a = 0; a < n; ++a)
         for (int b = 0; b < n; ++b)
           for (int e = 0; e < n; ++e) {
-            qp.push_back(gx[a] * (1 - gx[b]) * (1 - gx[e]));
-            qp.push_back(gx[b] * (1 - gx[e]));
-            qp.push_back(gx[e]);
-            qw.push_back(gw[a] * gw[b] * gw[e] * (1 - gx[b]) * (1 - gx[e]) * (1 - gx[e]));
+            qp.push_back(ua[a] * (1 - vb[b]) * (1 - wc[e]));
+            qp.push_back(vb[b] * (1 - wc[e]));
+            qp.push_back(wc[e]);
+            qw.push_back(wa[a] * wb[b] * wcw[e]);
           }
     }
+    double wsum = 0.0;
     for (double w : qw) wsum += w;
     for (double& w : qw) w /= wsum;
   }
   const int nq = (int)qw.size();
+  // monomial form of the basis: A row of stencil cell j = coef · (monomial averages over T_j)
+  std::vector<int> mexp;
+  std::vector<double> mcoef;
+  basis_monomials(d, M, mexp, mcoef);
+  const int nmono = (int)mexp.size() / 3;
 
   const int64_t TILES_PER_BATCH = std::max<int64_t>(1, (int64_t(256) << 20) / L.tile_bytes);
   const bool keep_host = c->device < 0;
@@ -280,7 +295,8 @@ void precompute(cwreco_ctx* c) {
         for (int m = 0; m < d; ++m) slots[(size_t(ct) * nv + s) * d + m] = sl[s][m];
 
       // central reduced LSQ matrix A[1:,1:] (column-major, K rows)
-      std::vector<double> A(size_t(K) * R);
+      thread_local std::vector<double> A;
+      A.assign(size_t(K) * R, 0.0);
       double psi[64], xi[3], sh[3];
       for (int k = 1; k < ne; ++k) {
         const int64_t j = cen[k];
@@ -300,19 +316,29 @@ void precompute(cwreco_ctx* c) {
             Cm[a * d + e] = s2;
           }
         }
-        double acc[64] = {0};
+        // monomial averages over the stencil cell, ξ = t + C ξ'_q (quadrature exact for degree M)
+        double mom[64] = {0};
         for (int qq = 0; qq < nq; ++qq) {
+          double pw[3][8];
           for (int a = 0; a < d; ++a) {
             double s = t[a];
             for (int e = 0; e < d; ++e) s += Cm[a * d + e] * qp[qq * d + e];
-            xi[a] = s;
+            pw[a][0] = 1.0;
+            for (int p = 1; p <= M; ++p) pw[a][p] = pw[a][p - 1] * s;
           }
-          basis_eval(d, M, xi, psi);
-          for (int l = 1; l < nm; ++l) acc[l] += qw[qq] * psi[l];
+          if (d == 2) pw[2][0] = 1.0;
+          const double wq = qw[qq];
+          for (int e = 0; e < nmono; ++e)
+            mom[e] += wq * (pw[0][mexp[3 * e]] * pw[1][mexp[3 * e + 1]] * pw[2][mexp[3 * e + 2]]);
         }
-        for (int l = 1; l < nm; ++l) A[size_t(l - 1) * K + (k - 1)] = acc[l];
+        for (int l = 1; l < nm; ++l) {
+          double s = 0.0;
+          const double* cl = &mcoef[size_t(l) * nmono];
+          for (int e = 0; e < nmono; ++e) s += cl[e] * mom[e];
+          A[size_t(l - 1) * K + (k - 1)] = s;
+        }
       }
-      std::vector<double> Bp;
+      thread_local std::vector<double> Bp;
       double cond = 0.0;
       if (!pinv_qr(K, R, A, Bp, cond)) { bad_singular |= 1; continue; }
       cond_max = std::max(cond_max, cond);

@@ -58,6 +58,11 @@ IV iv_orient(int d, const IV* const* p) {
 // Geometry of one owner cell i, in coordinates scaled by (d+1) and centred on
 // the owner's barycentre: W_k = (d+1) X_{i,k} − S_i, and for a cell j
 // D_j = S_j + (d+1) n L − S_i  (S_c = Σ_k X_{c,k}; n the periodic image shift).
+struct ExData {  // exact displacement and squared distance of one candidate
+  exact::Ex De[3];
+  exact::Ex keye;
+};
+
 struct Owner {
   const cwreco_ctx* c;
   int d;
@@ -66,6 +71,7 @@ struct Owner {
   exact::Ex Si[3];
   exact::Ex W[4][3];
   bool have_exactW = false;
+  std::vector<ExData> pool;  // exact data of candidates that needed it
 
   Owner(const cwreco_ctx* c_, int64_t i_) : c(c_), d(c_->d), i(i_) {
     const double* X = &c->X[i * (d + 1) * d];
@@ -93,9 +99,8 @@ struct Cand {
   int n[3];     // periodic shift
   IV D[3];      // filter value of D_j
   IV key;       // Σ D_a²
-  bool have_exact = false;
-  exact::Ex De[3];
-  exact::Ex keye;
+  int ex = -1;  // index into Owner::pool once the exact values were needed
+  int8_t lam[4] = {2, 2, 2, 2};  // cached signs of the owner barycentric coordinates (2 = unknown)
 };
 
 void shift_of(const cwreco_ctx* c, int64_t i, int64_t j, int* n) {
@@ -114,7 +119,7 @@ void make_cand(Owner& o, int64_t j, Cand& cd) {
   const cwreco_ctx* c = o.c;
   const int d = o.d;
   cd.j = j;
-  cd.have_exact = false;
+  cd.ex = -1;
   shift_of(c, o.i, j, cd.n);
   const double* Xi = &c->X[o.i * (d + 1) * d];
   const double* Xj = &c->X[j * (d + 1) * d];
@@ -132,23 +137,24 @@ void make_cand(Owner& o, int64_t j, Cand& cd) {
   cd.key = key;
 }
 
-void ensure_exact(Owner& o, Cand& cd) {
-  if (cd.have_exact) return;
+const ExData& ensure_exact(Owner& o, Cand& cd) {
+  if (cd.ex >= 0) return o.pool[cd.ex];
   o.ensure_exactW();
   const cwreco_ctx* c = o.c;
   const int d = o.d;
   const double* Xj = &c->X[cd.j * (d + 1) * d];
-  exact::Ex key;
+  ExData x;
   for (int a = 0; a < d; ++a) {
     exact::Ex s;
     for (int k = 0; k <= d; ++k) s = exact::grow(s, Xj[k * d + a]);
     s = exact::compress(s);
     if (c->periodic && cd.n[a] != 0) s = exact::add(s, exact::scale(exact::Ex(c->L[a]), double((d + 1) * cd.n[a])));
-    cd.De[a] = exact::sub(s, o.Si[a]);
-    key = exact::add(key, exact::mul(cd.De[a], cd.De[a]));
+    x.De[a] = exact::sub(s, o.Si[a]);
+    x.keye = exact::add(x.keye, exact::mul(x.De[a], x.De[a]));
   }
-  cd.keye = key;
-  cd.have_exact = true;
+  cd.ex = (int)o.pool.size();
+  o.pool.push_back(x);
+  return o.pool[cd.ex];
 }
 
 // strict-weak "less" by (exact squared distance, id)
@@ -157,22 +163,29 @@ bool key_less(Owner& o, Cand& a, Cand& b) {
   if (std::fabs(df.v) > df.r) return df.v < 0;
   ensure_exact(o, a);
   ensure_exact(o, b);
-  int s = exact::sign(exact::sub(a.keye, b.keye));
+  int s = exact::sign(exact::sub(o.pool[a.ex].keye, o.pool[b.ex].keye));
   if (s != 0) return s < 0;
   return a.j < b.j;
 }
 
 // sign of the owner barycentric coordinate λ_w at D (orientation with W_w -> D)
 int lambda_sign(Owner& o, Cand& cd, int w) {
+  if (cd.lam[w] != 2) return cd.lam[w];
   const int d = o.d;
   const IV* p[4];
   for (int k = 0; k <= d; ++k) p[k] = (k == w) ? cd.D : o.Wiv[k];
   IV det = iv_orient(d, p);
-  if (std::fabs(det.v) > det.r) return det.v > 0 ? 1 : -1;
-  ensure_exact(o, cd);
-  const exact::Ex* pe[4];
-  for (int k = 0; k <= d; ++k) pe[k] = (k == w) ? cd.De : o.W[k];
-  return exact::orient_sign(d, pe);
+  int sg;
+  if (std::fabs(det.v) > det.r) {
+    sg = det.v > 0 ? 1 : -1;
+  } else {
+    const ExData& x = ensure_exact(o, cd);
+    const exact::Ex* pe[4];
+    for (int k = 0; k <= d; ++k) pe[k] = (k == w) ? x.De : o.W[k];
+    sg = exact::orient_sign(d, pe);
+  }
+  cd.lam[w] = (int8_t)sg;
+  return sg;
 }
 
 bool in_cone(Owner& o, Cand& cd, int v) {  // R13: λ_w > 0 for all w != v
@@ -183,21 +196,37 @@ bool in_cone(Owner& o, Cand& cd, int v) {  // R13: λ_w > 0 for all w != v
   return true;
 }
 
-bool affinely_independent(Owner& o, std::vector<Cand>& cs) {
+// candidate cache of one owner (shared by the central and the d+1 sector searches)
+struct Cache {
+  Owner& o;
+  std::vector<Cand> cs;
+  explicit Cache(Owner& o_) : o(o_) { cs.reserve(256); }
+  int get(int64_t j) {
+    for (size_t q = 0; q < cs.size(); ++q)
+      if (cs[q].j == j) return (int)q;
+    cs.emplace_back();
+    make_cand(o, j, cs.back());
+    return (int)cs.size() - 1;
+  }
+  void sort(std::vector<int>& idx) {
+    std::sort(idx.begin(), idx.end(), [&](int a, int b) { return key_less(o, cs[a], cs[b]); });
+  }
+};
+
+bool affinely_independent(Cache& cc, const std::vector<int>& idx) {
+  Owner& o = cc.o;
   const int d = o.d;
   IV zero[3] = {{0, 0}, {0, 0}, {0, 0}};
   const IV* p[4];
   p[0] = zero;
-  for (int k = 0; k < d; ++k) p[k + 1] = cs[k].D;
+  for (int k = 0; k < d; ++k) p[k + 1] = cc.cs[idx[k]].D;
   IV det = iv_orient(d, p);
   if (std::fabs(det.v) > det.r) return true;
   exact::Ex ze[3];
   const exact::Ex* pe[4];
   pe[0] = ze;
-  for (int k = 0; k < d; ++k) {
-    ensure_exact(o, cs[k]);
-    pe[k + 1] = cs[k].De;
-  }
+  for (int k = 0; k < d; ++k) ensure_exact(o, cc.cs[idx[k]]);  // pool may grow: take pointers after
+  for (int k = 0; k < d; ++k) pe[k + 1] = o.pool[cc.cs[idx[k]].ex].De;
   return exact::orient_sign(d, pe) != 0;
 }
 
@@ -205,16 +234,13 @@ inline bool contains(const std::vector<int64_t>& v, int64_t x) {
   return std::find(v.begin(), v.end(), x) != v.end();
 }
 
-void sort_cands(Owner& o, std::vector<Cand>& cs) {
-  std::sort(cs.begin(), cs.end(), [&](Cand& a, Cand& b) { return key_less(o, a, b); });
-}
-
 // returns false if exhausted
-bool central_stencil(const cwreco_ctx* c, int64_t i, int32_t* out) {
+bool central_stencil(Cache& cc, int32_t* out) {
+  const cwreco_ctx* c = cc.o.c;
   const int d = c->d, ne = c->ne;
-  Owner o(c, i);
+  const int64_t i = cc.o.i;
   std::vector<int64_t> S{i}, frontier{i}, cand;
-  std::vector<Cand> cs;
+  std::vector<int> idx;
   while ((int)S.size() < ne) {
     cand.clear();
     for (int64_t f : frontier)
@@ -223,27 +249,29 @@ bool central_stencil(const cwreco_ctx* c, int64_t i, int32_t* out) {
         if (nb >= 0 && !contains(S, nb) && !contains(cand, nb)) cand.push_back(nb);
       }
     if (cand.empty()) return false;
-    cs.resize(cand.size());
-    for (size_t q = 0; q < cand.size(); ++q) make_cand(o, cand[q], cs[q]);
-    sort_cands(o, cs);
-    const size_t take = std::min(cs.size(), size_t(ne) - S.size());
+    idx.clear();
+    for (int64_t x : cand) idx.push_back(cc.get(x));
+    cc.sort(idx);
+    const size_t take = std::min(idx.size(), size_t(ne) - S.size());
     frontier.clear();
     for (size_t q = 0; q < take; ++q) {
-      S.push_back(cs[q].j);
-      frontier.push_back(cs[q].j);
+      S.push_back(cc.cs[idx[q]].j);
+      frontier.push_back(cc.cs[idx[q]].j);
     }
   }
   for (int k = 0; k < ne; ++k) out[k] = (int32_t)S[k];
   return true;
 }
 
+bool in_cone_idx(Cache& cc, int q, int v) { return in_cone(cc.o, cc.cs[q], v); }
+
 // P:156 + R14.  out: d+1 entries (self first, -1 padded); returns validity.
-bool sector_stencil(const cwreco_ctx* c, int64_t i, int v, int32_t* out) {
+bool sector_stencil(Cache& cc, int v, int32_t* out) {
+  const cwreco_ctx* c = cc.o.c;
   const int d = c->d;
-  Owner o(c, i);
+  const int64_t i = cc.o.i;
   std::vector<int64_t> S{i}, seen{i}, frontier{i}, cand;
-  std::vector<Cand> taken, acc;
-  Cand tmp;
+  std::vector<int> taken, acc;
   while ((int)S.size() < d + 1) {
     cand.clear();
     for (int64_t f : frontier)
@@ -254,8 +282,8 @@ bool sector_stencil(const cwreco_ctx* c, int64_t i, int v, int32_t* out) {
     for (int64_t x : cand) seen.push_back(x);
     acc.clear();
     for (int64_t x : cand) {
-      make_cand(o, x, tmp);
-      if (in_cone(o, tmp, v)) acc.push_back(tmp);
+      const int q = cc.get(x);
+      if (in_cone_idx(cc, q, v)) acc.push_back(q);
     }
     if (acc.empty()) {
       // fallback: node (Voronoi) neighbours of all selected sector cells
@@ -269,24 +297,25 @@ bool sector_stencil(const cwreco_ctx* c, int64_t i, int v, int32_t* out) {
           }
       }
       for (int64_t x : cand) {
-        make_cand(o, x, tmp);
-        if (in_cone(o, tmp, v)) acc.push_back(tmp);
+        const int q = cc.get(x);
+        if (in_cone_idx(cc, q, v)) acc.push_back(q);
       }
       if (acc.empty()) break;
     }
-    sort_cands(o, acc);
+    cc.sort(acc);
     const size_t take = std::min(acc.size(), size_t(d + 1) - S.size());
     frontier.clear();
     for (size_t q = 0; q < take; ++q) {
-      S.push_back(acc[q].j);
-      if (!contains(seen, acc[q].j)) seen.push_back(acc[q].j);
-      frontier.push_back(acc[q].j);
+      const int64_t j = cc.cs[acc[q]].j;
+      S.push_back(j);
+      if (!contains(seen, j)) seen.push_back(j);
+      frontier.push_back(j);
       taken.push_back(acc[q]);
     }
   }
   for (int k = 0; k <= d; ++k) out[k] = k < (int)S.size() ? (int32_t)S[k] : -1;
   if ((int)S.size() < d + 1) return false;
-  return affinely_independent(o, taken);
+  return affinely_independent(cc, taken);
 }
 
 int owner_rank(const cwreco_ctx* c, int64_t g) {
@@ -312,13 +341,15 @@ void build_stencils(cwreco_ctx* c) {
   for (int64_t q = 0; q < n_own; ++q) {
     const int64_t i = lo + q;
     try {
-      if (!central_stencil(c, i, &c->central[q * ne])) {
+      Owner o(c, i);
+      Cache cc(o);
+      if (!central_stencil(cc, &c->central[q * ne])) {
 #pragma omp critical
         exhausted = std::max<int64_t>(exhausted, i);
         continue;
       }
       for (int v = 0; v < nv; ++v)
-        c->valid[q * nv + v] = sector_stencil(c, i, v, &c->sectors[(q * nv + v) * nv]) ? 1 : 0;
+        c->valid[q * nv + v] = sector_stencil(cc, v, &c->sectors[(q * nv + v) * nv]) ? 1 : 0;
     } catch (const std::exception& e) {
 #pragma omp critical
       err = e.what();

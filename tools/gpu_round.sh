@@ -23,6 +23,15 @@ if [[ $what == bench || $what == all ]]; then
     echo "bench $c exit $?"; cat gpurun_out/bench_$c.json
   done
 fi
+if [[ $what == ncufull ]]; then
+  for c in $ncfg; do
+    cmd="python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline"
+    $cmd > gpurun_out/ncu_plain_$c.log 2>&1 && \
+    ncu --set full --clock-control none --import-source on -k regex:k_pipelined -s 3 -c 1 \
+        -o gpurun_out/prof_$c -f $cmd > gpurun_out/ncu_full_$c.log 2>&1
+    echo "ncu full $c exit $?"; tail -3 gpurun_out/ncu_full_$c.log
+  done
+fi
 if [[ $what == ncu || $what == all ]]; then
   cmd="python bench.py --config $ncfg --steps 3 --warmup 3 --no-cpu-baseline"
   $cmd > gpurun_out/ncu_plain_$ncfg.log 2>&1 && \

@@ -90,7 +90,8 @@ enum {
 typedef struct {
   int32_t dim, degree_M, nvars, n_modes; /* ℳ(M,d) = (1/d!) Π (M+l) */
   int32_t n_e;                           /* d·ℳ */
-  int32_t gather_len;                    /* n_e − 1 + extra sector cells outside S_i^0 */
+  int32_t gather_len;                    /* gather positions per cell: max((d+1)·d, n_e − 1 +
+                                            extra sector cells outside S_i^0) */
   int32_t tile_cells;                    /* cells per tile of the packed matrix stream */
   int32_t chunk_k;                       /* stencil columns per streamed chunk */
   int64_t n_cells;                       /* global cells */
@@ -146,10 +147,14 @@ cwreco_status cwreco_get_local_cells(const cwreco_ctx* ctx, int64_t* local_to_gl
 cwreco_status cwreco_precompute(cwreco_ctx* ctx);
 /* The universal oscillation matrix Σ [ℳ][ℳ] as used by the kernels. */
 cwreco_status cwreco_get_sigma(const cwreco_ctx* ctx, double* out);
-/* Export the packed matrices of selected owned cells (local ids) for tests:
- * bplus [n][ℳ-1][n_e-1], sinv [n][dim+1][dim][dim], gather [n][gather_len]
- * (local ids), slots [n][dim+1][dim] (index into gather, 255 = invalid sector).
- * Any output may be NULL. */
+/* Export the packed matrices of selected owned cells (local ids) for tests.
+ * gather [n][gather_len]: local ids in gather order — positions s·dim+m hold
+ * member m of sector s (fillers from S_i^0 or the cell itself when the sector is
+ * invalid), then the remaining cells of S_i^0, then the cell itself as padding;
+ * bplus [n][ℳ-1][gather_len]: the reduced pseudo-inverse B⁺ with its columns in
+ * gather order (zero for positions outside S_i^0), so p̂_opt[1..] = B⁺ (Q_g − Q_i);
+ * sinv [n][dim+1][dim][dim]; slots [n][dim+1][dim]: gather position of each
+ * sector member, 255 = invalid sector.  Any output may be NULL. */
 cwreco_status cwreco_get_blocks(const cwreco_ctx* ctx, int64_t n_sel, const int64_t* cells,
                                 double* bplus, double* sinv, int32_t* gather, uint8_t* slots);
 

@@ -179,7 +179,7 @@ class Context:
         cells = np.ascontiguousarray(cells, dtype=np.int64)
         inf = self.info()
         n, d = len(cells), self.dim
-        bp = np.empty((n, self.nm - 1, inf["n_e"] - 1))
+        bp = np.empty((n, self.nm - 1, inf["gather_len"]))
         sv = np.empty((n, d + 1, d, d))
         ga = np.empty((n, inf["gather_len"]), dtype=np.int32)
         sl = np.empty((n, d + 1, d), dtype=np.uint8)

@@ -208,7 +208,7 @@ cwreco_status cwreco_get_blocks(const cwreco_ctx* c, int64_t n_sel, const int64_
     need(c && (n_sel == 0 || cells), CWRECO_EINVAL, "get_blocks: NULL");
     need(c->has_blocks, CWRECO_ESTATE, "get_blocks: call cwreco_precompute first");
     const cwr::Layout& L = c->lay;
-    const int T = L.T, R = L.R, K = L.K, G = L.G, d = c->d, nv = d + 1;
+    const int T = L.T, R = L.R, G = L.G, d = c->d, nv = d + 1;
     std::vector<unsigned char> tile(L.tile_bytes);
     int64_t cur = -1;
     for (int64_t s = 0; s < n_sel; ++s) {
@@ -228,18 +228,20 @@ cwreco_status cwreco_get_blocks(const cwreco_ctx* c, int64_t n_sel, const int64_
       }
       const int32_t* ids = (const int32_t*)(tb + L.off_ids);
       const double* sv = (const double*)(tb + L.off_sinv);
-      const uint8_t* sl = (const uint8_t*)(tb + L.off_slots);
+      const uint8_t vm = *((const uint8_t*)(tb + L.off_vmask) + ct);
       const double* B = (const double*)(tb + L.off_chunks);
       if (bplus)
         for (int l = 0; l < R; ++l)
-          for (int k = 0; k < K; ++k) {
-            const int ch = k / L.KC, kk = k % L.KC, kc = std::min(L.KC, K - ch * L.KC);
-            bplus[(s * R + l) * K + k] = B[size_t(ch) * L.KC * T * R + (size_t(ct) * R + l) * kc + kk];
+          for (int k = 0; k < G; ++k) {
+            const int ch = k / L.KC, kk = k % L.KC, kc = std::min(L.KC, G - ch * L.KC);
+            bplus[(s * R + l) * G + k] = B[size_t(ch) * L.KC * T * R + (size_t(ct) * R + l) * kc + kk];
           }
       if (sinv) std::memcpy(sinv + s * nv * d * d, sv + (size_t)ct * nv * d * d, sizeof(double) * nv * d * d);
       if (gather)
         for (int k = 0; k < G; ++k) gather[s * G + k] = ids[(size_t)k * T + ct];
-      if (slots) std::memcpy(slots + s * nv * d, sl + (size_t)ct * nv * d, nv * d);
+      if (slots)
+        for (int q = 0; q < nv; ++q)
+          for (int m = 0; m < d; ++m) slots[(s * nv + q) * d + m] = ((vm >> q) & 1) ? uint8_t(q * d + m) : 255;
     }
   });
 }

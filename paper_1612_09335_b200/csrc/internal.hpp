@@ -26,14 +26,18 @@ inline int n_modes(int M, int d) {  // ℳ(M,d) = (1/d!) Π_{l=1..d} (M+l)   (P:
 }
 
 // Layout of one packed tile of the matrix stream.
-//   header:  ids   int32  [G][T]          gather list (local cell ids), k-major
+//   header:  ids   int32  [G][T]          gather list (local cell ids), position-major.
+//                                         Positions [0, (d+1)d): sector s, member m at
+//                                         s·d+m (R15; filler if the sector is invalid);
+//                                         then the remaining cells of S_i^0; self-padded.
 //            sinv  double [T][d+1][d][d]  sector inverses
-//            slots uint8  [T][d+1][d]     sector cell -> gather index, 255 = invalid
-//   chunks:  B     chunk ch = k ∈ [ch·KC, ch·KC+kc): double [T][R][kc]  (reduced
-//                  pseudo-inverse; kc = KC except for a shorter last chunk)
+//            vmask uint8  [T]             bit s = sector s valid (R14)
+//   chunks:  B     chunk ch = positions [ch·KC, ch·KC+kc): double [T][R][kc]  (reduced
+//                  pseudo-inverse columns in gather order, 0 for positions outside
+//                  S_i^0; kc = KC except for a shorter last chunk)
 struct Layout {
   int d = 0, M = 0, V = 0, nm = 0, R = 0, K = 0, G = 0, T = 0, KC = 0, NCH = 0;
-  int64_t off_ids = 0, off_sinv = 0, off_slots = 0, header_bytes = 0;
+  int64_t off_ids = 0, off_sinv = 0, off_vmask = 0, header_bytes = 0;
   int64_t off_chunks = 0, kslice_bytes = 0, tile_bytes = 0;
 };
 

@@ -16,6 +16,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <type_traits>
 #include <cstdint>
 #include <cstring>
 #include <string>
@@ -66,7 +68,7 @@ __constant__ double c_sig[SIG_TOTAL];
 
 struct KArgs {
   const unsigned char* blocks;
-  int64_t tile_bytes, off_ids, off_sinv, off_slots, off_chunks;
+  int64_t tile_bytes, off_ids, off_sinv, off_vmask, off_chunks;
   int T, G, K, KC, NCH, V;
   int64_t n_owned, tile_begin, tile_end;
   const double* Q;
@@ -74,6 +76,7 @@ struct KArgs {
   double* out;
   int64_t ccs, cvs;
   int dense_out;
+  int exp_flags;  // bottleneck experiments only (CWRECO_EXP_FLAGS): 1 no gather, 2 no math, 4 no B⁺ stream
   double eps, psi1;
   int r;
   // normalised linear weights (R5, R14) indexed by the number of valid sectors
@@ -102,7 +105,8 @@ struct ModeOf {  // M from (D, ℳ)
 };
 
 // Fused epilogue.  acc[l-1] = p̂_opt[l] (l >= 1); ps[s][l-1] = p̂_s[l]
-// (l = 1..D).  On return w[] holds the blended coefficients.
+// (l = 1..D).  The blended coefficients are written to w[0..NM) as they are formed
+// (w may be shared or global memory).
 template <int D, int NM>
 __device__ __forceinline__ void cweno_epilogue(double qi, double* acc, const double (&ps)[D + 1][D],
                                                const bool (&valid)[D + 1], const KArgs& a, double* w,
@@ -189,9 +193,24 @@ __device__ __forceinline__ void cweno_epilogue(double qi, double* acc, const dou
 }
 
 // ---------------------------------------------------------------- simple kernel
+// Sector products from the captured ΔQ of gather positions [0, (D+1)·D).
+template <int D>
+__device__ __forceinline__ void sector_apply(const double* sinv, const double (&dqs)[(D + 1) * D],
+                                             double (&ps)[D + 1][D]) {
+#pragma unroll
+  for (int s = 0; s <= D; ++s)
+#pragma unroll
+    for (int l = 0; l < D; ++l) {
+      double t = 0.0;
+#pragma unroll
+      for (int m = 0; m < D; ++m) t += sinv[(s * D + l) * D + m] * dqs[s * D + m];
+      ps[s][l] = t;
+    }
+}
+
 template <int D, int M, bool DEBUG>
 __global__ void __launch_bounds__(256) k_simple(KArgs a, DbgOut dbg) {
-  constexpr int NM = nmodes(M, D), R = NM - 1, NV = D + 1;
+  constexpr int NM = nmodes(M, D), R = NM - 1, NV = D + 1, NCAP = NV * D;
   const int64_t gid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t item = gid / a.V;
   const int v = int(gid % a.V);
@@ -208,7 +227,7 @@ __global__ void __launch_bounds__(256) k_simple(KArgs a, DbgOut dbg) {
   const unsigned char* tb = a.blocks + tile * a.tile_bytes;
   const int32_t* ids = (const int32_t*)(tb + a.off_ids);
   const double* sinv = (const double*)(tb + a.off_sinv) + size_t(ct) * NV * D * D;
-  const uint8_t* slots = (const uint8_t*)(tb + a.off_slots) + size_t(ct) * NV * D;
+  const uint8_t vmask = *((const uint8_t*)(tb + a.off_vmask) + ct);
   const double* B = (const double*)(tb + a.off_chunks);
   const double* Qv = a.Q + v * a.avs;
   const double qi = Qv[c * a.acs];
@@ -216,36 +235,26 @@ __global__ void __launch_bounds__(256) k_simple(KArgs a, DbgOut dbg) {
   double acc[R];
 #pragma unroll
   for (int l = 0; l < R; ++l) acc[l] = 0.0;
+  double dqs[NCAP];
   for (int ch = 0; ch < a.NCH; ++ch) {
-    const int kc = min(a.KC, a.K - ch * a.KC);
+    const int kc = min(a.KC, a.G - ch * a.KC);
     const double* Bc = B + (size_t)ch * a.KC * a.T * R + (size_t)ct * R * kc;  // chunk [T][R][kc]
     for (int kk = 0; kk < kc; ++kk) {
-      const int32_t j = ids[size_t(ch * a.KC + kk) * a.T + ct];
+      const int p = ch * a.KC + kk;
+      const int32_t j = ids[size_t(p) * a.T + ct];
       const double dq = Qv[int64_t(j) * a.acs] - qi;
+#pragma unroll
+      for (int q = 0; q < NCAP; ++q)
+        if (p == q) dqs[q] = dq;
 #pragma unroll
       for (int l = 0; l < R; ++l) acc[l] += Bc[l * kc + kk] * dq;
     }
   }
-  double ps[NV][D];
   bool valid[NV];
 #pragma unroll
-  for (int s = 0; s < NV; ++s) {
-    valid[s] = slots[s * D] != 255;
-    double dq[D];
-#pragma unroll
-    for (int m = 0; m < D; ++m) {
-      const int g = valid[s] ? slots[s * D + m] : 0;
-      const int32_t j = ids[size_t(g) * a.T + ct];
-      dq[m] = (valid[s] ? Qv[int64_t(j) * a.acs] : qi) - qi;
-    }
-#pragma unroll
-    for (int l = 0; l < D; ++l) {
-      double t = 0.0;
-#pragma unroll
-      for (int m = 0; m < D; ++m) t += sinv[(s * D + l) * D + m] * dq[m];
-      ps[s][l] = t;
-    }
-  }
+  for (int s = 0; s < NV; ++s) valid[s] = (vmask >> s) & 1;
+  double ps[NV][D];
+  sector_apply<D>(sinv, dqs, ps);
   if (DEBUG) {
     double* po = dbg.popt + (item * a.V + v) * NM;
     po[0] = qi / a.psi1;
@@ -253,23 +262,17 @@ __global__ void __launch_bounds__(256) k_simple(KArgs a, DbgOut dbg) {
     for (int s = 0; s < NV; ++s) {
       double* pp = dbg.psec + ((item * NV + s) * a.V + v) * NV;
       pp[0] = valid[s] ? qi / a.psi1 : 0.0;
-      for (int l = 0; l < D; ++l) pp[l + 1] = ps[s][l];
+      for (int l = 0; l < D; ++l) pp[l + 1] = valid[s] ? ps[s][l] : 0.0;
     }
   }
-  double w[NM];
   double sg[NV + 1], om[NV + 1];
-  cweno_epilogue<D, NM>(qi, acc, ps, valid, a, w, DEBUG ? sg : nullptr, DEBUG ? om : nullptr);
+  double* wout = DEBUG ? dbg.w + (item * a.V + v) * NM : a.out + c * a.ccs + v * a.cvs;
+  cweno_epilogue<D, NM>(qi, acc, ps, valid, a, wout, DEBUG ? sg : nullptr, DEBUG ? om : nullptr);
   if (DEBUG) {
     for (int s = 0; s <= NV; ++s) {
       dbg.sigma[(item * (NV + 1) + s) * a.V + v] = sg[s];
       dbg.omega[(item * (NV + 1) + s) * a.V + v] = om[s];
     }
-    double* wo = dbg.w + (item * a.V + v) * NM;
-    for (int l = 0; l < NM; ++l) wo[l] = w[l];
-  } else {
-    double* o = a.out + c * a.ccs + v * a.cvs;
-#pragma unroll
-    for (int l = 0; l < NM; ++l) o[l] = w[l];
   }
 }
 
@@ -316,23 +319,30 @@ __device__ __forceinline__ void fence_barrier_init() { asm volatile("fence.mbarr
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-constexpr int NGW = 2;  // gather warps per CTA
 __host__ __device__ constexpr int cons_target(int D, int M) { return nmodes(M, D) >= 20 ? 320 : 160; }
 __host__ __device__ constexpr int min_blocks(int D, int M) { return nmodes(M, D) >= 20 ? 1 : 2; }
-__host__ __device__ constexpr int max_threads(int D, int M) { return cons_target(D, M) + 32 * (1 + NGW); }
+// consumers + one producer warp
+__host__ __device__ constexpr int max_threads(int D, int M) { return cons_target(D, M) + 32; }
+constexpr int PF = 2;       // gather prefetch distance, in chunks
+constexpr int NQ = PF + 2;  // per-warp gather ring slots
 
 struct PipeCfg {
-  int stages;
-  int64_t stage_bytes, stage_q_off, hdr_bytes, out_bytes;
-  int64_t off_hdr, off_stage, off_out, off_bar, smem;
+  int stages, hslots;
+  int64_t stage_bytes, hdr_bytes, out_bytes, q_bytes;
+  int64_t off_hdr, off_stage, off_q, off_out, off_bar, smem;
   int ncw;  // consumer warps
 };
 
-struct Ring {  // stage index + mbarrier phase of a ring of S stages
+struct Ring {  // slot index + mbarrier phase of a ring of S slots
   int st = 0;
   uint32_t ph = 0;
   __device__ __forceinline__ void next(int S) {
@@ -344,33 +354,43 @@ struct Ring {  // stage index + mbarrier phase of a ring of S stages
 };
 
 // ---------------------------------------------------------------- pipelined kernel
-// Warp roles: [0, ncw) consumers, thread tid ↔ (ct, v) = (tid / V, tid % V);
-// warp ncw: TMA producer (lane 0); warps ncw+1 .. ncw+NGW: gathers.
-// Stage = B⁺ chunk [T][R][kc] (one bulk copy) + gathered Q [T·V][KC] (cp.async).
+// Persistent, warp-specialised.  Warp roles: [0, ncw) consumers, thread
+// tid ↔ (ct, v) = (tid / V, tid % V); warp ncw: TMA producer (lane 0) — per
+// tile, the B⁺ chunks [T][R][kc] into a ring of S shared-memory stages (1-D bulk
+// copies, mbarrier transaction counts), then the header (gather ids, sector
+// inverses, validity) of the tile H−1 ahead into the header ring.
+// Consumers gather their own stencil averages: each thread cp.async-copies the
+// Q_j of its (cell, variable) for chunk g+PF into a per-warp ring while chunk g
+// is multiplied (the prefetch cursor crosses tile boundaries), so the only
+// cross-warp synchronisation per chunk is the stage's full/empty pair.
+// Gather positions [0, (D+1)·D) are the sector cells (precompute.cpp): their ΔQ
+// is captured from the first chunks of the stream.
 template <int D, int M, int KC>
 __global__ void __launch_bounds__(max_threads(D, M), min_blocks(D, M)) k_pipelined(KArgs a, PipeCfg pc) {
   constexpr int NM = nmodes(M, D), R = NM - 1, NV = D + 1;
+  constexpr int NCAP = NV * D, NCAPCH = (NCAP + KC - 1) / KC;  // captured positions / chunks
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned char* hdr = smem + pc.off_hdr;
   unsigned char* stg = smem + pc.off_stage;
   double* outs = (double*)(smem + pc.off_out);
   uint64_t* bars = (uint64_t*)(smem + pc.off_bar);
-  uint64_t* hdr_full = bars;                  // [2]
-  uint64_t* hdr_empty = bars + 2;             // [2]
-  uint64_t* ch_full = bars + 4;               // [S]
-  uint64_t* ch_empty = bars + 4 + pc.stages;  // [S]
-  const int S = pc.stages;
+  const int S = pc.stages, H = pc.hslots;
+  uint64_t* hdr_full = bars;              // [H]
+  uint64_t* hdr_empty = bars + H;         // [H]
+  uint64_t* ch_full = bars + 2 * H;       // [S]
+  uint64_t* ch_empty = bars + 2 * H + S;  // [S]
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int TV = a.T * a.V;
+  const int64_t t0 = a.tile_begin + blockIdx.x;  // this CTA's tiles: t0, t0 + grid, …
 
   if (tid == 0) {
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < H; ++b) {
       mbar_init(&hdr_full[b], 1);
-      mbar_init(&hdr_empty[b], pc.ncw + NGW);
+      mbar_init(&hdr_empty[b], pc.ncw);
     }
     for (int s = 0; s < S; ++s) {
-      mbar_init(&ch_full[s], 1 + NGW * 32);
+      mbar_init(&ch_full[s], 1);
       mbar_init(&ch_empty[s], pc.ncw);
     }
     fence_barrier_init();
@@ -380,62 +400,31 @@ __global__ void __launch_bounds__(max_threads(D, M), min_blocks(D, M)) k_pipelin
   if (warp == pc.ncw) {
     // ------------------------------------------------ TMA producer
     if (lane == 0) {
-      Ring rg;
-      int it = 0;
-      for (int64_t tile = a.tile_begin + blockIdx.x; tile < a.tile_end; tile += gridDim.x, ++it) {
-        const unsigned char* tb = a.blocks + tile * a.tile_bytes;
-        const int hb = it & 1;
-        mbar_wait(&hdr_empty[hb], ((it >> 1) & 1) ^ 1);
-        mbar_expect_tx(&hdr_full[hb], (uint32_t)pc.hdr_bytes);
-        bulk_g2s(hdr + hb * pc.hdr_bytes, tb, (uint32_t)pc.hdr_bytes, &hdr_full[hb]);
+      Ring rg, hw;
+      int64_t th = t0;  // next header to issue
+      auto issue_header = [&]() {
+        mbar_wait(&hdr_empty[hw.st], hw.ph ^ 1);
+        mbar_expect_tx(&hdr_full[hw.st], (uint32_t)pc.hdr_bytes);
+        bulk_g2s(hdr + hw.st * pc.hdr_bytes, a.blocks + th * a.tile_bytes, (uint32_t)pc.hdr_bytes, &hdr_full[hw.st]);
+        hw.next(H);
+        th += gridDim.x;
+      };
+      for (int k = 0; k < H - 1 && th < a.tile_end; ++k) issue_header();
+      for (int64_t tile = t0; tile < a.tile_end; tile += gridDim.x) {
+        const unsigned char* tb = a.blocks + tile * a.tile_bytes + a.off_chunks;
         for (int ch = 0; ch < a.NCH; ++ch, rg.next(S)) {
-          const int kc = min(KC, a.K - ch * KC);
+          const int kc = min(KC, a.G - ch * KC);
           const uint32_t bytes = (uint32_t)(kc * a.T * R * 8);
           mbar_wait(&ch_empty[rg.st], rg.ph ^ 1);
-          mbar_expect_tx(&ch_full[rg.st], bytes);
-          bulk_g2s(stg + rg.st * pc.stage_bytes, tb + a.off_chunks + (int64_t)ch * KC * a.T * R * 8, bytes,
-                   &ch_full[rg.st]);
-        }
-      }
-    }
-    return;
-  }
-  if (warp > pc.ncw) {
-    // ------------------------------------------------ gather warps
-    const int gt = tid - (pc.ncw + 1) * 32;  // 0 .. NGW*32-1
-    constexpr int RMAX = (cons_target(D, M) + NGW * 32 - 1) / (NGW * 32);
-    int g_ct[RMAX], g_off[RMAX];
-#pragma unroll
-    for (int i = 0; i < RMAX; ++i) {
-      const int r = gt + i * NGW * 32;
-      g_ct[i] = r < TV ? r / a.V : -1;
-      g_off[i] = r < TV ? (r % a.V) * (int)a.avs : 0;
-    }
-    Ring rg;
-    int it = 0;
-    for (int64_t tile = a.tile_begin + blockIdx.x; tile < a.tile_end; tile += gridDim.x, ++it) {
-      const int hb = it & 1;
-      mbar_wait(&hdr_full[hb], (it >> 1) & 1);
-      const int32_t* ids = (const int32_t*)(hdr + hb * pc.hdr_bytes + a.off_ids);
-      for (int ch = 0; ch < a.NCH; ++ch, rg.next(S)) {
-        const int kc = min(KC, a.K - ch * KC);
-        mbar_wait(&ch_empty[rg.st], rg.ph ^ 1);
-        double* Qg = (double*)(stg + rg.st * pc.stage_bytes + pc.stage_q_off);
-        const int32_t* idc = ids + (size_t)ch * KC * a.T;
-#pragma unroll
-        for (int i = 0; i < RMAX; ++i) {
-          if (g_ct[i] >= 0) {
-            double* dst = Qg + (size_t)(gt + i * NGW * 32) * KC;
-            const double* src = a.Q + g_off[i];
-#pragma unroll
-            for (int kk = 0; kk < KC; ++kk)
-              if (kk < kc) cp_async8(dst + kk, src + int64_t(idc[kk * a.T + g_ct[i]]) * a.acs);
+          if (a.exp_flags & 4) {
+            mbar_arrive(&ch_full[rg.st]);
+            continue;
           }
+          mbar_expect_tx(&ch_full[rg.st], bytes);
+          bulk_g2s(stg + rg.st * pc.stage_bytes, tb + (int64_t)ch * KC * a.T * R * 8, bytes, &ch_full[rg.st]);
         }
-        cp_async_arrive_noinc(&ch_full[rg.st]);
+        if (th < a.tile_end) issue_header();
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&hdr_empty[hb]);
     }
     return;
   }
@@ -445,112 +434,164 @@ __global__ void __launch_bounds__(max_threads(D, M), min_blocks(D, M)) k_pipelin
   const int ct = active ? tid / a.V : 0;
   const int v = active ? tid % a.V : 0;
   const double* Qv = a.Q + v * a.avs;
-  double* outw = outs + (size_t)warp * 32 * NM;  // this warp's output staging
-  Ring rg;
-  int it = 0;
-  for (int64_t tile = a.tile_begin + blockIdx.x; tile < a.tile_end; tile += gridDim.x, ++it) {
-    const int hb = it & 1;
-    const int64_t c = tile * a.T + ct;
-    const bool live = active && c < a.n_owned;
-    const double qi = live ? __ldg(Qv + c * a.acs) : 0.0;
-    mbar_wait(&hdr_full[hb], (it >> 1) & 1);
-    const unsigned char* hb_p = hdr + hb * pc.hdr_bytes;
-    const int32_t* ids = (const int32_t*)(hb_p + a.off_ids);
-    const uint8_t* slots = (const uint8_t*)(hb_p + a.off_slots) + size_t(ct) * NV * D;
-    // prefetch the sector averages now; consumed after the main loop
-    bool valid[NV];
-    double qs[NV][D];
+  double* outw = outs + (size_t)warp * 32 * NM;                                   // output staging
+  double* qring = (double*)(smem + pc.off_q) + (size_t)warp * NQ * KC * 32 + lane;  // [NQ][KC][32]
+
+  // prefetch cursor: gathers of chunk (pf_tile, pf_ch) into ring slot pf_q
+  int64_t pf_tile = t0;
+  int pf_ch = 0, pf_q = 0;
+  Ring pf_hr;
+  const int32_t* pf_ids = nullptr;
+  bool pf_live = false;
+  auto pf_begin_tile = [&]() {
+    if (pf_tile < a.tile_end) {
+      mbar_wait(&hdr_full[pf_hr.st], pf_hr.ph);
+      pf_ids = (const int32_t*)(hdr + pf_hr.st * pc.hdr_bytes + a.off_ids) + ct;
+      pf_live = active && pf_tile * a.T + ct < a.n_owned && !(a.exp_flags & 1);
+    }
+  };
+  auto pf_issue = [&]() {
+    if (pf_tile < a.tile_end) {
+      const int kc = min(KC, a.G - pf_ch * KC);
+      double* dst = qring + pf_q * KC * 32;
+      const int32_t* idc = pf_ids + (size_t)pf_ch * KC * a.T;
+      if (pf_live) {
 #pragma unroll
-    for (int s = 0; s < NV; ++s) {
-      valid[s] = slots[s * D] != 255;
-#pragma unroll
-      for (int m = 0; m < D; ++m) {
-        const int g = valid[s] ? slots[s * D + m] : 0;
-        const int32_t j = ids[size_t(g) * a.T + ct];
-        qs[s][m] = (valid[s] && live) ? __ldg(Qv + int64_t(j) * a.acs) : qi;
+        for (int kk = 0; kk < KC; ++kk)
+          if (kk < kc) cp_async8(dst + kk * 32, Qv + int64_t(idc[kk * a.T]) * a.acs);
+      }
+      if (++pf_ch == a.NCH) {
+        pf_ch = 0;
+        pf_tile += gridDim.x;
+        pf_hr.next(H);
+        pf_begin_tile();
       }
     }
+    cp_async_commit();
+    if (++pf_q == NQ) pf_q = 0;
+  };
+  pf_begin_tile();
+#pragma unroll
+  for (int k = 0; k < PF; ++k) pf_issue();
+
+  Ring rg, hr;
+  int cq = 0;  // ring slot of the chunk being consumed
+  // Q_i of the first tile; later tiles' Q_i is prefetched one tile ahead
+  double qi = 0.0;
+  if (active && t0 < a.tile_end && t0 * a.T + ct < a.n_owned) qi = __ldg(Qv + (t0 * a.T + ct) * a.acs);
+  for (int64_t tile = t0; tile < a.tile_end; tile += gridDim.x, hr.next(H)) {
+    const int64_t c = tile * a.T + ct;
+    const bool live = active && c < a.n_owned;
+    const int64_t cn = c + (int64_t)gridDim.x * a.T;
+    const double qn = (active && tile + gridDim.x < a.tile_end && cn < a.n_owned) ? __ldg(Qv + cn * a.acs) : 0.0;
 
     double acc[R];
 #pragma unroll
     for (int l = 0; l < R; ++l) acc[l] = 0.0;
-    for (int ch = 0; ch < a.NCH; ++ch, rg.next(S)) {
-      const int kc = min(KC, a.K - ch * KC);
+    double dqs[NCAP];
+    // one full stage (kc == KC): ΔQ of KC positions, B⁺ columns accumulated in
+    // registers; CAP: capture the sector ΔQ (positions < NCAP; only the first
+    // NCAPCH chunks, which make_layout guarantees to be full)
+    auto stage_full = [&](int ch, auto cap) {
+      pf_issue();
+      cp_async_wait<PF>();
+      const double* Qg = qring + cq * KC * 32;
+      if (++cq == NQ) cq = 0;
       mbar_wait(&ch_full[rg.st], rg.ph);
       const double* Bs = (const double*)(stg + rg.st * pc.stage_bytes);
-      const double* Qg = (const double*)(stg + rg.st * pc.stage_bytes + pc.stage_q_off) + (size_t)tid * KC;
-      if (kc == KC && (KC % 2) == 0) {
+      if (a.exp_flags & 2) {
+        acc[0] += Qg[0];
+      } else {
         double dq[KC];
 #pragma unroll
-        for (int p = 0; p < KC / 2; ++p) {
-          const double2 q2 = reinterpret_cast<const double2*>(Qg)[p];
-          dq[2 * p] = live ? q2.x - qi : 0.0;
-          dq[2 * p + 1] = live ? q2.y - qi : 0.0;
+        for (int kk = 0; kk < KC; ++kk) dq[kk] = live ? Qg[kk * 32] - qi : 0.0;
+        if (decltype(cap)::value) {
+#pragma unroll
+          for (int kk = 0; kk < KC; ++kk)
+            if (ch * KC + kk < NCAP) dqs[ch * KC + kk] = dq[kk];
         }
-        const double2* b2 = reinterpret_cast<const double2*>(Bs + (size_t)ct * R * KC);
+        if (KC % 2 == 0) {
+          const double2* b2 = reinterpret_cast<const double2*>(Bs + (size_t)ct * R * KC);
 #pragma unroll
-        for (int l = 0; l < R; ++l) {
+          for (int l = 0; l < R; ++l) {
 #pragma unroll
-          for (int p = 0; p < KC / 2; ++p) {
-            const double2 bb = b2[l * (KC / 2) + p];
-            acc[l] += bb.x * dq[2 * p];
-            acc[l] += bb.y * dq[2 * p + 1];
+            for (int p = 0; p < KC / 2; ++p) {
+              const double2 bb = b2[l * (KC / 2) + p];
+              acc[l] += bb.x * dq[2 * p];
+              acc[l] += bb.y * dq[2 * p + 1];
+            }
           }
-        }
-      } else {
-        const double* b = Bs + (size_t)ct * R * kc;
-        for (int kk = 0; kk < kc; ++kk) {
-          const double dq = live ? Qg[kk] - qi : 0.0;
+        } else {
+          const double* b = Bs + (size_t)ct * R * KC;
 #pragma unroll
-          for (int l = 0; l < R; ++l) acc[l] += b[l * kc + kk] * dq;
+          for (int l = 0; l < R; ++l)
+#pragma unroll
+            for (int kk = 0; kk < KC; ++kk) acc[l] += b[l * KC + kk] * dq[kk];
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&ch_empty[rg.st]);
-    }
-
-    // sectors
-    const double* sinv = (const double*)(hb_p + a.off_sinv) + size_t(ct) * NV * D * D;
-    double ps[NV][D];
+      rg.next(S);
+    };
+    // the shorter last chunk
+    auto stage_tail = [&](int kc) {
+      pf_issue();
+      cp_async_wait<PF>();
+      const double* Qg = qring + cq * KC * 32;
+      if (++cq == NQ) cq = 0;
+      mbar_wait(&ch_full[rg.st], rg.ph);
+      const double* b = (const double*)(stg + rg.st * pc.stage_bytes) + (size_t)ct * R * kc;
+      for (int kk = 0; kk < kc; ++kk) {
+        const double dq = live ? Qg[kk * 32] - qi : 0.0;
 #pragma unroll
-    for (int s = 0; s < NV; ++s) {
-      double dqs[D];
-#pragma unroll
-      for (int m = 0; m < D; ++m) dqs[m] = qs[s][m] - qi;
-#pragma unroll
-      for (int l = 0; l < D; ++l) {
-        double t = 0.0;
-#pragma unroll
-        for (int m = 0; m < D; ++m) t += sinv[(s * D + l) * D + m] * dqs[m];
-        ps[s][l] = t;
+        for (int l = 0; l < R; ++l) acc[l] += b[l * kc + kk] * dq;
       }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&hdr_empty[hb]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ch_empty[rg.st]);
+      rg.next(S);
+    };
+    // first chunks (sector positions): fully unrolled so dqs[] stays in registers
+#pragma unroll
+    for (int ch = 0; ch < NCAPCH; ++ch) stage_full(ch, std::true_type{});
+    const int nfull = a.G / KC;
+    for (int ch = NCAPCH; ch < nfull; ++ch) stage_full(ch, std::false_type{});
+    if (nfull < a.NCH) stage_tail(a.G - nfull * KC);
 
-    double w[NM];
-    cweno_epilogue<D, NM>(qi, acc, ps, valid, a, w, nullptr, nullptr);
+    // sectors; the header is resident (the prefetch cursor waited on it)
+    mbar_wait(&hdr_full[hr.st], hr.ph);
+    const unsigned char* hb_p = hdr + hr.st * pc.hdr_bytes;
+    const uint8_t vmask = *((const uint8_t*)(hb_p + a.off_vmask) + ct);
+    bool valid[NV];
+#pragma unroll
+    for (int s = 0; s < NV; ++s) valid[s] = (vmask >> s) & 1;
+    double ps[NV][D];
+    sector_apply<D>((const double*)(hb_p + a.off_sinv) + size_t(ct) * NV * D * D, dqs, ps);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&hdr_empty[hr.st]);
 
     if (a.dense_out) {
       // per-warp staging + one bulk store of the warp's contiguous output rows
       const int64_t first = tile * (int64_t)TV + warp * 32;  // (cell·V + v) index of lane 0
       const int64_t lim = min((int64_t)TV, (a.n_owned - tile * a.T) * a.V) - warp * 32;
       const int nlive = (int)max((int64_t)0, min((int64_t)32, lim));
-      if (lane == 0) bulk_wait_read();
+      if (lane == 0) bulk_wait_read();  // the staging rows are free again
       __syncwarp();
-      if (lane < nlive) {
-#pragma unroll
-        for (int l = 0; l < NM; ++l) outw[lane * NM + l] = w[l];
-      }
+      cweno_epilogue<D, NM>(qi, acc, ps, valid, a, outw + lane * NM, nullptr, nullptr);
       fence_proxy_async();
       __syncwarp();
       if (lane == 0 && nlive > 0) bulk_s2g(a.out + first * NM, outw, (uint32_t)(nlive * NM * 8));
-    } else if (live) {
-      double* o = a.out + c * a.ccs + v * a.cvs;
+    } else {
+      double scratch[NM];
+      cweno_epilogue<D, NM>(qi, acc, ps, valid, a, scratch, nullptr, nullptr);
+      if (live) {
+        double* o = a.out + c * a.ccs + v * a.cvs;
 #pragma unroll
-      for (int l = 0; l < NM; ++l) o[l] = w[l];
+        for (int l = 0; l < NM; ++l) o[l] = scratch[l];
+      }
     }
+    qi = qn;
   }
+  cp_async_wait<0>();
   if (lane == 0) bulk_wait_all();
 }
 
@@ -605,7 +646,7 @@ static KArgs make_args(const cwreco_ctx* c, const double* avgs, int64_t acs, int
   a.tile_bytes = L.tile_bytes;
   a.off_ids = L.off_ids;
   a.off_sinv = L.off_sinv;
-  a.off_slots = L.off_slots;
+  a.off_vmask = L.off_vmask;
   a.off_chunks = L.off_chunks;
   a.T = L.T;
   a.G = L.G;
@@ -623,6 +664,10 @@ static KArgs make_args(const cwreco_ctx* c, const double* avgs, int64_t acs, int
   a.ccs = ccs;
   a.cvs = cvs;
   a.dense_out = 0;
+  {
+    const char* e = std::getenv("CWRECO_EXP_FLAGS");  // bottleneck experiments (tools/exp_bench.py)
+    a.exp_flags = e ? std::atoi(e) : 0;
+  }
   a.eps = c->prm.eps;
   a.psi1 = c->psi1;
   a.r = c->prm.r;
@@ -641,25 +686,38 @@ static PipeCfg pipe_cfg(const cwreco_ctx* c) {
   auto r128 = [](int64_t x) { return (x + 127) & ~int64_t(127); };
   p.ncw = (L.T * c->V + 31) / 32;
   p.hdr_bytes = L.header_bytes;
-  p.stage_q_off = r128((int64_t)L.KC * L.kslice_bytes);
-  p.stage_bytes = r128(p.stage_q_off + (int64_t)L.KC * L.T * c->V * 8);
+  p.stage_bytes = r128((int64_t)L.KC * L.kslice_bytes);
+  p.q_bytes = r128((int64_t)p.ncw * NQ * L.KC * 32 * 8);
   p.out_bytes = r128((int64_t)p.ncw * 32 * c->nm * 8);
   const int blocks = c->nm >= 20 ? 1 : 2;
-  const int64_t budget = (c->dev->max_smem + 1024) / blocks - 1024;
-  int best = 2;
-  for (int s = 8; s >= 2; --s) {
-    int64_t tot = r128(2 * p.hdr_bytes) + s * p.stage_bytes + p.out_bytes + 8 * (4 + 2 * s);
-    if (tot <= budget) {
-      best = s;
-      break;
-    }
+  auto total = [&](int hs, int s) {
+    return r128(hs * p.hdr_bytes) + s * p.stage_bytes + p.q_bytes + p.out_bytes + 8 * (2 * hs + 2 * s);
+  };
+  // header slots: 3 (two tiles of header lookahead) when affordable, else 2; then
+  // as many stages as fit the per-CTA budget (2 CTAs/SM for ℳ < 20); a tile too
+  // large for that budget runs at 1 CTA/SM with the whole shared memory.  The
+  // prefetch cursor needs stages > PF (it waits on the next tile's header, which
+  // the producer issues after the current tile's last chunk).
+  int hs = 0, st = 0;
+  for (int64_t budget : {(int64_t)(c->dev->max_smem + 1024) / blocks - 1024, (int64_t)c->dev->max_smem}) {
+    for (int h = 3; h >= 2 && !st; --h)
+      for (int s = 12; s >= PF + 1; --s)
+        if (total(h, s) <= budget && (h == 2 || s >= 4)) {
+          hs = h;
+          st = s;
+          break;
+        }
+    if (st) break;
   }
-  p.stages = best;
+  if (!st) fail(CWRECO_EUNSUPPORTED, "pipelined kernel: tile does not fit in shared memory");
+  p.hslots = hs;
+  p.stages = st;
   p.off_hdr = 0;
-  p.off_stage = r128(2 * p.hdr_bytes);
-  p.off_out = p.off_stage + best * p.stage_bytes;
+  p.off_stage = r128(hs * p.hdr_bytes);
+  p.off_q = p.off_stage + st * p.stage_bytes;
+  p.off_out = p.off_q + p.q_bytes;
   p.off_bar = p.off_out + p.out_bytes;
-  p.smem = p.off_bar + 8 * (4 + 2 * best);
+  p.smem = p.off_bar + 8 * (2 * hs + 2 * st);
   return p;
 }
 
@@ -744,7 +802,7 @@ void dev_reconstruct(cwreco_ctx* c, const double* avgs, int64_t acs, int64_t avs
     const int64_t ntiles = a.tile_end - a.tile_begin;
     const int per_sm = c->nm >= 20 ? 1 : 2;
     const int64_t grid = std::min<int64_t>(ntiles, (int64_t)c->dev->num_sms * per_sm);
-    dim3 b((p.ncw + 1 + NGW) * 32), g((unsigned)grid);
+    dim3 b((p.ncw + 1) * 32), g((unsigned)grid);
     pipe_fn(c->d, c->M, c->lay.KC)<<<g, b, p.smem, st>>>(a, p);
   }
   CK(cudaGetLastError());

@@ -42,14 +42,18 @@ Layout make_layout(int d, int M, int V, int G) {
   L.KC = std::max<int>(1, int(10240 / L.kslice_bytes));
   L.KC = std::min(L.KC, 8);
   L.KC = (L.KC + 1) & ~1;
-  if (L.KC > L.K) L.KC = L.K;
-  L.NCH = (L.K + L.KC - 1) / L.KC;
+  if (L.KC > G) L.KC = G;
+  // the chunks holding the (d+1)·d sector positions must be full (the kernel
+  // captures their ΔQ with static indices)
+  // (and KC must be one of the compiled chunk sizes 1-6, 8)
+  while (L.KC > 1 && (L.KC == 7 || ((d + 1) * d + L.KC - 1) / L.KC * L.KC > G)) --L.KC;
+  L.NCH = (G + L.KC - 1) / L.KC;
   L.off_ids = 0;
   L.off_sinv = r16(int64_t(G) * T * 4);
-  L.off_slots = L.off_sinv + int64_t(T) * (d + 1) * d * d * 8;
-  L.header_bytes = r16(L.off_slots + int64_t(T) * (d + 1) * d);
+  L.off_vmask = L.off_sinv + int64_t(T) * (d + 1) * d * d * 8;
+  L.header_bytes = r16(L.off_vmask + int64_t(T));
   L.off_chunks = L.header_bytes;
-  L.tile_bytes = r16(L.off_chunks + int64_t(L.K) * L.kslice_bytes);
+  L.tile_bytes = r16(L.off_chunks + int64_t(G) * L.kslice_bytes);
   return L;
 }
 
@@ -248,7 +252,7 @@ void precompute(cwreco_ctx* c) {
       unsigned char* tb = base + size_t(tile - t0) * L.tile_bytes;
       int32_t* ids = (int32_t*)(tb + L.off_ids);
       double* sinv = (double*)(tb + L.off_sinv);
-      uint8_t* slots = (uint8_t*)(tb + L.off_slots);
+      uint8_t* vmask = (uint8_t*)(tb + L.off_vmask);
       double* Bch = (double*)(tb + L.off_chunks);
       const int64_t g = c->local2global[li];
       const int64_t q = g - c->own_lo;
@@ -263,36 +267,49 @@ void precompute(cwreco_ctx* c) {
         for (int k = 0; k < d; ++k) J[a * d + k] = Xi[(k + 1) * d + a] - Xi[a];
       if (!inv_small(d, J, Ji)) { bad_singular |= 1; continue; }
 
-      // gather list: central[1..] then sector extras, padded with self
-      int32_t glist[256];
+      // gather order: sector cells at s·d+m, then the rest of S_i^0, then self.
+      // col[p] = column of B⁺ (index into S_i^0 ∖ i) of position p, -1 if none.
       int64_t gglob[256];
-      int ng = 0;
-      for (int k = 1; k < ne; ++k) gglob[ng++] = cen[k];
-      uint8_t sl[4][3];
+      int col[256];
+      bool used[256] = {false};
+      const int front = nv * d;
+      for (int p = 0; p < front; ++p) { gglob[p] = -1; col[p] = -1; }
       for (int s = 0; s < nv; ++s) {
-        for (int m = 0; m < d; ++m) sl[s][m] = 255;
         if (!val[s]) continue;
         for (int m = 0; m < d; ++m) {
-          int64_t x = sec[s * nv + 1 + m];
-          int pos = -1;
-          for (int k = 0; k < ng; ++k)
-            if (gglob[k] == x) { pos = k; break; }
-          if (pos < 0) { pos = ng; gglob[ng++] = x; }
-          sl[s][m] = (uint8_t)pos;
+          const int64_t x = sec[s * nv + 1 + m];
+          gglob[s * d + m] = x;
+          for (int k = 1; k < ne; ++k)
+            if (cen[k] == x) { col[s * d + m] = k - 1; used[k] = true; break; }
         }
       }
-      const int32_t self_local = (int32_t)li;
-      for (int k = 0; k < G; ++k) {
-        if (k < ng) {
-          glist[k] = to_local(gglob[k]);
-          if (glist[k] < 0) bad_local |= 1;
+      int ng = front;
+      int next = 1;  // next unused central cell for invalid-sector fillers
+      for (int p = 0; p < front; ++p) {
+        if (gglob[p] >= 0) continue;
+        while (next < ne && used[next]) ++next;
+        if (next < ne) {
+          gglob[p] = cen[next];
+          col[p] = next - 1;
+          used[next] = true;
         } else {
-          glist[k] = self_local;
+          gglob[p] = g;  // self: ΔQ = 0
         }
-        ids[size_t(k) * T + ct] = glist[k];
       }
-      for (int s = 0; s < nv; ++s)
-        for (int m = 0; m < d; ++m) slots[(size_t(ct) * nv + s) * d + m] = sl[s][m];
+      for (int k = 1; k < ne; ++k)
+        if (!used[k]) { gglob[ng] = cen[k]; col[ng] = k - 1; ++ng; }
+      if (ng > G) { bad_local |= 1; continue; }
+      const int32_t self_local = (int32_t)li;
+      for (int p = 0; p < G; ++p) {
+        int32_t lid = self_local;
+        if (p < ng && gglob[p] != g) {
+          lid = to_local(gglob[p]);
+          if (lid < 0) bad_local |= 1;
+        }
+        ids[size_t(p) * T + ct] = lid;
+      }
+      uint8_t vm = 0;
+      for (int s = 0; s < nv; ++s) vm |= val[s] ? uint8_t(1u << s) : 0;
 
       // central reduced LSQ matrix A[1:,1:] (column-major, K rows)
       thread_local std::vector<double> A;
@@ -342,12 +359,13 @@ void precompute(cwreco_ctx* c) {
       double cond = 0.0;
       if (!pinv_qr(K, R, A, Bp, cond)) { bad_singular |= 1; continue; }
       cond_max = std::max(cond_max, cond);
-      // B chunks: chunk ch holds k in [ch·KC, ch·KC + kc) as [T][R][kc]
-      for (int k = 0; k < K; ++k) {
-        const int ch = k / L.KC, kk = k % L.KC;
-        const int kc = std::min(L.KC, K - ch * L.KC);
+      // B chunks: chunk ch holds positions p in [ch·KC, ch·KC + kc) as [T][R][kc]
+      for (int p = 0; p < G; ++p) {
+        const int ch = p / L.KC, kk = p % L.KC;
+        const int kc = std::min(L.KC, G - ch * L.KC);
         double* chb = Bch + size_t(ch) * L.KC * T * R;
-        for (int l = 0; l < R; ++l) chb[(size_t(ct) * R + l) * kc + kk] = Bp[size_t(l) * K + k];
+        const int k = p < ng ? col[p] : -1;
+        for (int l = 0; l < R; ++l) chb[(size_t(ct) * R + l) * kc + kk] = k >= 0 ? Bp[size_t(l) * K + k] : 0.0;
       }
 
       // sector inverses
@@ -370,11 +388,12 @@ void precompute(cwreco_ctx* c) {
         // p_l = Σ_m S[l][m] ΔQ_m with S = As⁻¹ where As[m][l]
         double Ai[9];
         if (!inv_small(d, As, Ai)) {
-          for (int m = 0; m < d; ++m) slots[(size_t(ct) * nv + s) * d + m] = 255;
+          vm &= uint8_t(~(1u << s));
           continue;
         }
         for (int e = 0; e < d * d; ++e) Sd[e] = Ai[e];
       }
+      vmask[ct] = vm;
     }
     if (bad_singular || bad_local) break;
     if (!keep_host) dev_upload_blocks(c, t0 * L.tile_bytes, batch.data(), int64_t(t1 - t0) * L.tile_bytes);

@@ -410,7 +410,8 @@ void build_stencils(cwreco_ctx* c) {
   }
   c->n_extra = n_extra;
   c->n_invalid = n_inv;
-  c->G = (ne - 1) + max_extra;
+  // gather positions: sector cells first ((d+1)·d slots), then the rest of S_i^0 (R15)
+  c->G = std::max(nv * d, (ne - 1) + max_extra);
   c->has_stencils = true;
   c->has_blocks = false;
 }

@@ -106,7 +106,10 @@ def test_precompute_parity_host(case):
         r = R.reconstruct_cell(m, int(i), Q, M)
         g = blk["gather"][q]
         scale = np.abs(Q[r["central"]]).max()
-        popt = blk["bplus"][q] @ (Q[g[: n_e - 1]] - Q[i])
+        popt = blk["bplus"][q] @ (Q[g] - Q[i])
+        # every cell of S_i^0 ∖ i appears exactly once in the gather list
+        assert sorted(set(g.tolist()) - {int(i)}) == sorted(set(r["central"][1:])) or \
+            set(r["central"][1:]) <= set(g.tolist())
         assert np.abs(popt.T - r["popt"][:, 1:]).max() <= 1e-12 * scale, (name, i)
         for s in range(d + 1):
             sl = blk["slots"][q][s]

@@ -42,11 +42,14 @@ for cfg in sys.argv[1:]:
     out = torch.empty((inf["n_owned"], w["V"], ctx.nm), dtype=torch.float64, device="cuda")
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     res = {}
-    for flags in (0, 1, 2, 3, 4, 5, 6, 7):
+    for flags in [int(f) for f in os.environ.get("EXP_FLAGS_LIST", "0,1,2,3,4,5,6,7").split(",")]:
         os.environ["CWRECO_EXP_FLAGS"] = str(flags)
         ms = time_pass(ctx, A, out, flush)
         res[flags] = ms
     os.environ["CWRECO_EXP_FLAGS"] = "0"
+    ctx.set_kernel("simple")
+    res["simple"] = time_pass(ctx, A, out, flush)
+    ctx.set_kernel("pipelined")
     B = inf["algorithmic_bytes_per_cell"] * inf["n_owned"]
     print(json.dumps({"config": cfg, "info": {k: inf[k] for k in ("tile_cells", "chunk_k", "tile_bytes", "n_tiles")},
                       "ms": res, "GBps_alg": {k: B / v / 1e6 for k, v in res.items()}}), flush=True)

@@ -1,0 +1,49 @@
+#!/usr/bin/env python
+"""Join an ncu SASS source page (per-instruction stall samples / executed
+instructions) with nvdisasm line info to get per-CUDA-line totals.
+
+    python tools/sass_lines.py gpurun_out/prof_C5.ncu-rep <kernel cubin> <mangled name> [top]
+"""
+import csv
+import io
+import re
+import subprocess
+import sys
+from collections import defaultdict
+
+rep, cubin, fn = sys.argv[1:4]
+top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                     capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(out)))
+hdr = rows[1]
+data = rows[2:]
+si = hdr.index("Warp Stall Sampling (All Samples)")
+ie = hdr.index("Instructions Executed")
+base = int(data[0][0], 16)
+dis = subprocess.run(["nvdisasm", "-g", "-c", cubin], capture_output=True, text=True).stdout
+lines = dis.splitlines()
+start = next(i for i, ln in enumerate(lines) if ln.startswith("//---") and (".text." + fn + " ") in ln)
+end = next((i for i in range(start + 1, len(lines)) if lines[i].startswith("//---")), len(lines))
+line_of = {}
+cur = None
+for ln in lines[start:end]:
+    m = re.search(r'line (\d+)', ln)
+    if ln.strip().startswith("//##") and m:
+        cur = int(m.group(1))
+        continue
+    m = re.match(r'\s*/\*([0-9a-f]+)\*/', ln)
+    if m and cur is not None:
+        line_of[int(m.group(1), 16)] = cur
+st, ins = defaultdict(float), defaultdict(float)
+for r in data:
+    off = int(r[0], 16) - base
+    l = line_of.get(off, -1)
+    st[l] += float(r[si] or 0)
+    ins[l] += float(r[ie] or 0)
+ts, ti = sum(st.values()), sum(ins.values())
+src = open("paper_1612_09335_b200/csrc/kernels.cu").read().splitlines()
+print(f"{'line':>5} {'stall%':>7} {'inst%':>7}  source")
+for l in sorted(st, key=lambda k: -st[k])[:top]:
+    s = src[l - 1].strip()[:90] if 0 < l <= len(src) else "?"
+    print(f"{l:5d} {100 * st[l] / ts:7.1f} {100 * ins[l] / ti:7.1f}  {s}")

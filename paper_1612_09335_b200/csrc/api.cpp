@@ -226,19 +226,19 @@ cwreco_status cwreco_get_blocks(const cwreco_ctx* c, int64_t n_sel, const int64_
         }
         tb = tile.data();
       }
-      const int32_t* ids = (const int32_t*)(tb + L.off_ids);
-      const double* sv = (const double*)(tb + L.off_sinv);
-      const uint8_t vm = *((const uint8_t*)(tb + L.off_vmask) + ct);
-      const double* B = (const double*)(tb + L.off_chunks);
+      const double* sv = (const double*)(tb + L.off_sector);
+      const uint8_t vm = *((const uint8_t*)(tb + L.off_sector + L.sinv_bytes) + ct);
       if (bplus)
         for (int l = 0; l < R; ++l)
           for (int k = 0; k < G; ++k) {
-            const int ch = k / L.KC, kk = k % L.KC, kc = std::min(L.KC, G - ch * L.KC);
-            bplus[(s * R + l) * G + k] = B[size_t(ch) * L.KC * T * R + (size_t(ct) * R + l) * kc + kk];
+            const int ch = k / L.KC, kk = k % L.KC, kc = L.kc_of(ch);
+            const double* B = (const double*)(tb + L.off_chunk(ch) + L.ids_bytes);
+            bplus[(s * R + l) * G + k] = B[(size_t(ct) * R + l) * kc + kk];
           }
       if (sinv) std::memcpy(sinv + s * nv * d * d, sv + (size_t)ct * nv * d * d, sizeof(double) * nv * d * d);
       if (gather)
-        for (int k = 0; k < G; ++k) gather[s * G + k] = ids[(size_t)k * T + ct];
+        for (int k = 0; k < G; ++k)
+          gather[s * G + k] = ((const int32_t*)(tb + L.off_chunk(k / L.KC)))[size_t(k % L.KC) * T + ct];
       if (slots)
         for (int q = 0; q < nv; ++q)
           for (int m = 0; m < d; ++m) slots[(s * nv + q) * d + m] = ((vm >> q) & 1) ? uint8_t(q * d + m) : 255;

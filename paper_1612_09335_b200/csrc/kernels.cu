@@ -68,7 +68,7 @@ __constant__ double c_sig[SIG_TOTAL];
 
 struct KArgs {
   const unsigned char* blocks;
-  int64_t tile_bytes, off_ids, off_sinv, off_vmask, off_chunks;
+  int64_t tile_bytes, ids_bytes, chunk_bytes, kslice_bytes, off_sector, sinv_bytes, sector_bytes;
   int T, G, K, KC, NCH, V;
   int64_t n_owned, tile_begin, tile_end;
   const double* Q;
@@ -76,7 +76,8 @@ struct KArgs {
   double* out;
   int64_t ccs, cvs;
   int dense_out;
-  int exp_flags;  // bottleneck experiments only (CWRECO_EXP_FLAGS): 1 no gather, 2 no math, 4 no B⁺ stream
+  int exp_flags;  // bottleneck experiments only (CWRECO_EXP_FLAGS): 1 no gather, 2 no math, 4 no B⁺ stream,
+                 // 8 no gather bookkeeping, 16 no epilogue
   double eps, psi1;
   int r;
   // normalised linear weights (R5, R14) indexed by the number of valid sectors
@@ -225,10 +226,8 @@ __global__ void __launch_bounds__(256) k_simple(KArgs a, DbgOut dbg) {
   const int64_t tile = c / a.T;
   const int ct = int(c % a.T);
   const unsigned char* tb = a.blocks + tile * a.tile_bytes;
-  const int32_t* ids = (const int32_t*)(tb + a.off_ids);
-  const double* sinv = (const double*)(tb + a.off_sinv) + size_t(ct) * NV * D * D;
-  const uint8_t vmask = *((const uint8_t*)(tb + a.off_vmask) + ct);
-  const double* B = (const double*)(tb + a.off_chunks);
+  const double* sinv = (const double*)(tb + a.off_sector) + size_t(ct) * NV * D * D;
+  const uint8_t vmask = *((const uint8_t*)(tb + a.off_sector + a.sinv_bytes) + ct);
   const double* Qv = a.Q + v * a.avs;
   const double qi = Qv[c * a.acs];
 
@@ -238,10 +237,12 @@ __global__ void __launch_bounds__(256) k_simple(KArgs a, DbgOut dbg) {
   double dqs[NCAP];
   for (int ch = 0; ch < a.NCH; ++ch) {
     const int kc = min(a.KC, a.G - ch * a.KC);
-    const double* Bc = B + (size_t)ch * a.KC * a.T * R + (size_t)ct * R * kc;  // chunk [T][R][kc]
+    const unsigned char* cb = tb + ch * a.chunk_bytes;
+    const int32_t* ids = (const int32_t*)cb;                                          // [kc][T]
+    const double* Bc = (const double*)(cb + a.ids_bytes) + (size_t)ct * R * kc;   // [T][R][kc]
     for (int kk = 0; kk < kc; ++kk) {
       const int p = ch * a.KC + kk;
-      const int32_t j = ids[size_t(p) * a.T + ct];
+      const int32_t j = ids[size_t(kk) * a.T + ct];
       const double dq = Qv[int64_t(j) * a.acs] - qi;
 #pragma unroll
       for (int q = 0; q < NCAP; ++q)
@@ -328,17 +329,18 @@ __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// (must agree with cons_threads / ctas_per_sm in internal.hpp)
 __host__ __device__ constexpr int cons_target(int D, int M) { return nmodes(M, D) >= 20 ? 320 : 160; }
 __host__ __device__ constexpr int min_blocks(int D, int M) { return nmodes(M, D) >= 20 ? 1 : 2; }
 // consumers + one producer warp
 __host__ __device__ constexpr int max_threads(int D, int M) { return cons_target(D, M) + 32; }
-constexpr int PF = 2;       // gather prefetch distance, in chunks
-constexpr int NQ = PF + 2;  // per-warp gather ring slots
+constexpr int PF = kPrefetch;  // gather prefetch distance, in chunks
+constexpr int NQ = kQSlots;     // per-thread gather ring slots
 
 struct PipeCfg {
-  int stages, hslots;
-  int64_t stage_bytes, hdr_bytes, out_bytes, q_bytes;
-  int64_t off_hdr, off_stage, off_q, off_out, off_bar, smem;
+  int stages;
+  int64_t stage_bytes, q_bytes, out_bytes;
+  int64_t off_stage, off_q, off_out, off_bar, smem;
   int ncw;  // consumer warps
 };
 
@@ -355,43 +357,36 @@ struct Ring {  // slot index + mbarrier phase of a ring of S slots
 
 // ---------------------------------------------------------------- pipelined kernel
 // Persistent, warp-specialised.  Warp roles: [0, ncw) consumers, thread
-// tid ↔ (ct, v) = (tid / V, tid % V); warp ncw: TMA producer (lane 0) — per
-// tile, the B⁺ chunks [T][R][kc] into a ring of S shared-memory stages (1-D bulk
-// copies, mbarrier transaction counts), then the header (gather ids, sector
-// inverses, validity) of the tile H−1 ahead into the header ring.
-// Consumers gather their own stencil averages: each thread cp.async-copies the
-// Q_j of its (cell, variable) for chunk g+PF into a per-warp ring while chunk g
-// is multiplied (the prefetch cursor crosses tile boundaries), so the only
-// cross-warp synchronisation per chunk is the stage's full/empty pair.
-// Gather positions [0, (D+1)·D) are the sector cells (precompute.cpp): their ΔQ
-// is captured from the first chunks of the stream.
+// tid ↔ (ct, v) = (tid / V, tid % V); warp ncw: TMA producer (lane 0) — streams
+// each tile's chunks (gather ids + B⁺ columns) and its sector chunk (sector
+// inverses + validity) into a ring of S shared-memory stages with 1-D bulk
+// copies completing on mbarrier transaction counts.
+// Consumers gather their own stencil averages: for chunk g+PF each thread reads
+// the gather ids from that chunk's (already resident) stage and cp.async-copies
+// the Q_j of its (cell, variable) into a private ring while chunk g is
+// multiplied; the prefetch cursor runs over the flat chunk sequence across tile
+// boundaries.  Gather positions [0, (D+1)·D) are the sector cells
+// (precompute.cpp), so their ΔQ is captured from the first chunks.
 template <int D, int M, int KC>
 __global__ void __launch_bounds__(max_threads(D, M), min_blocks(D, M)) k_pipelined(KArgs a, PipeCfg pc) {
   constexpr int NM = nmodes(M, D), R = NM - 1, NV = D + 1;
   constexpr int NCAP = NV * D, NCAPCH = (NCAP + KC - 1) / KC;  // captured positions / chunks
   extern __shared__ __align__(128) unsigned char smem[];
-  unsigned char* hdr = smem + pc.off_hdr;
   unsigned char* stg = smem + pc.off_stage;
   double* outs = (double*)(smem + pc.off_out);
   uint64_t* bars = (uint64_t*)(smem + pc.off_bar);
-  const int S = pc.stages, H = pc.hslots;
-  uint64_t* hdr_full = bars;              // [H]
-  uint64_t* hdr_empty = bars + H;         // [H]
-  uint64_t* ch_full = bars + 2 * H;       // [S]
-  uint64_t* ch_empty = bars + 2 * H + S;  // [S]
+  const int S = pc.stages;
+  uint64_t* full = bars;       // [S]
+  uint64_t* empty = bars + S;  // [S]
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int TV = a.T * a.V;
   const int64_t t0 = a.tile_begin + blockIdx.x;  // this CTA's tiles: t0, t0 + grid, …
 
   if (tid == 0) {
-    for (int b = 0; b < H; ++b) {
-      mbar_init(&hdr_full[b], 1);
-      mbar_init(&hdr_empty[b], pc.ncw);
-    }
     for (int s = 0; s < S; ++s) {
-      mbar_init(&ch_full[s], 1);
-      mbar_init(&ch_empty[s], pc.ncw);
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], pc.ncw);
     }
     fence_barrier_init();
   }
@@ -400,30 +395,22 @@ __global__ void __launch_bounds__(max_threads(D, M), min_blocks(D, M)) k_pipelin
   if (warp == pc.ncw) {
     // ------------------------------------------------ TMA producer
     if (lane == 0) {
-      Ring rg, hw;
-      int64_t th = t0;  // next header to issue
-      auto issue_header = [&]() {
-        mbar_wait(&hdr_empty[hw.st], hw.ph ^ 1);
-        mbar_expect_tx(&hdr_full[hw.st], (uint32_t)pc.hdr_bytes);
-        bulk_g2s(hdr + hw.st * pc.hdr_bytes, a.blocks + th * a.tile_bytes, (uint32_t)pc.hdr_bytes, &hdr_full[hw.st]);
-        hw.next(H);
-        th += gridDim.x;
-      };
-      for (int k = 0; k < H - 1 && th < a.tile_end; ++k) issue_header();
-      for (int64_t tile = t0; tile < a.tile_end; tile += gridDim.x) {
-        const unsigned char* tb = a.blocks + tile * a.tile_bytes + a.off_chunks;
-        for (int ch = 0; ch < a.NCH; ++ch, rg.next(S)) {
-          const int kc = min(KC, a.G - ch * KC);
-          const uint32_t bytes = (uint32_t)(kc * a.T * R * 8);
-          mbar_wait(&ch_empty[rg.st], rg.ph ^ 1);
-          if (a.exp_flags & 4) {
-            mbar_arrive(&ch_full[rg.st]);
-            continue;
-          }
-          mbar_expect_tx(&ch_full[rg.st], bytes);
-          bulk_g2s(stg + rg.st * pc.stage_bytes, tb + (int64_t)ch * KC * a.T * R * 8, bytes, &ch_full[rg.st]);
+      Ring rg;
+      auto issue = [&](const unsigned char* src, uint32_t bytes) {
+        mbar_wait(&empty[rg.st], rg.ph ^ 1);
+        if (a.exp_flags & 4) {
+          mbar_arrive(&full[rg.st]);
+        } else {
+          mbar_expect_tx(&full[rg.st], bytes);
+          bulk_g2s(stg + rg.st * pc.stage_bytes, src, bytes, &full[rg.st]);
         }
-        if (th < a.tile_end) issue_header();
+        rg.next(S);
+      };
+      for (int64_t tile = t0; tile < a.tile_end; tile += gridDim.x) {
+        const unsigned char* tb = a.blocks + tile * a.tile_bytes;
+        for (int ch = 0; ch < a.NCH; ++ch)
+          issue(tb + ch * a.chunk_bytes, (uint32_t)(a.ids_bytes + min(KC, a.G - ch * KC) * a.kslice_bytes));
+        issue(tb + a.off_sector, (uint32_t)a.sector_bytes);
       }
     }
     return;
@@ -434,52 +421,48 @@ __global__ void __launch_bounds__(max_threads(D, M), min_blocks(D, M)) k_pipelin
   const int ct = active ? tid / a.V : 0;
   const int v = active ? tid % a.V : 0;
   const double* Qv = a.Q + v * a.avs;
-  double* outw = outs + (size_t)warp * 32 * NM;                                   // output staging
   double* qring = (double*)(smem + pc.off_q) + (size_t)warp * NQ * KC * 32 + lane;  // [NQ][KC][32]
+  double* outw = outs + (size_t)warp * 32 * NM;                                      // output staging
 
-  // prefetch cursor: gathers of chunk (pf_tile, pf_ch) into ring slot pf_q
+  // prefetch cursor over the flat chunk sequence: chunk pf_ch of tile pf_tile sits
+  // in stage pr (each tile = NCH chunks + 1 sector chunk)
   int64_t pf_tile = t0;
   int pf_ch = 0, pf_q = 0;
-  Ring pf_hr;
-  const int32_t* pf_ids = nullptr;
-  bool pf_live = false;
-  auto pf_begin_tile = [&]() {
-    if (pf_tile < a.tile_end) {
-      mbar_wait(&hdr_full[pf_hr.st], pf_hr.ph);
-      pf_ids = (const int32_t*)(hdr + pf_hr.st * pc.hdr_bytes + a.off_ids) + ct;
-      pf_live = active && pf_tile * a.T + ct < a.n_owned && !(a.exp_flags & 1);
-    }
-  };
+  Ring pr;
+  bool pf_live = active && t0 < a.tile_end && t0 * a.T + ct < a.n_owned && !(a.exp_flags & 1);
   auto pf_issue = [&]() {
     if (pf_tile < a.tile_end) {
       const int kc = min(KC, a.G - pf_ch * KC);
-      double* dst = qring + pf_q * KC * 32;
-      const int32_t* idc = pf_ids + (size_t)pf_ch * KC * a.T;
+      mbar_wait(&full[pr.st], pr.ph);  // the chunk (and its gather ids) is resident
       if (pf_live) {
+        const int32_t* idc = (const int32_t*)(stg + pr.st * pc.stage_bytes) + ct;
+        double* dst = qring + pf_q * KC * 32;
 #pragma unroll
         for (int kk = 0; kk < KC; ++kk)
           if (kk < kc) cp_async8(dst + kk * 32, Qv + int64_t(idc[kk * a.T]) * a.acs);
       }
-      if (++pf_ch == a.NCH) {
+      pr.next(S);
+      if (++pf_ch == a.NCH) {  // skip the sector chunk, move to the next tile
+        pr.next(S);
         pf_ch = 0;
         pf_tile += gridDim.x;
-        pf_hr.next(H);
-        pf_begin_tile();
+        pf_live = active && pf_tile < a.tile_end && pf_tile * a.T + ct < a.n_owned && !(a.exp_flags & 1);
       }
     }
     cp_async_commit();
     if (++pf_q == NQ) pf_q = 0;
   };
-  pf_begin_tile();
+  if (!(a.exp_flags & 8)) {
 #pragma unroll
-  for (int k = 0; k < PF; ++k) pf_issue();
+    for (int k = 0; k < PF; ++k) pf_issue();
+  }
 
-  Ring rg, hr;
+  Ring rg;
   int cq = 0;  // ring slot of the chunk being consumed
   // Q_i of the first tile; later tiles' Q_i is prefetched one tile ahead
   double qi = 0.0;
   if (active && t0 < a.tile_end && t0 * a.T + ct < a.n_owned) qi = __ldg(Qv + (t0 * a.T + ct) * a.acs);
-  for (int64_t tile = t0; tile < a.tile_end; tile += gridDim.x, hr.next(H)) {
+  for (int64_t tile = t0; tile < a.tile_end; tile += gridDim.x) {
     const int64_t c = tile * a.T + ct;
     const bool live = active && c < a.n_owned;
     const int64_t cn = c + (int64_t)gridDim.x * a.T;
@@ -489,19 +472,25 @@ __global__ void __launch_bounds__(max_threads(D, M), min_blocks(D, M)) k_pipelin
 #pragma unroll
     for (int l = 0; l < R; ++l) acc[l] = 0.0;
     double dqs[NCAP];
-    // one full stage (kc == KC): ΔQ of KC positions, B⁺ columns accumulated in
-    // registers; CAP: capture the sector ΔQ (positions < NCAP; only the first
-    // NCAPCH chunks, which make_layout guarantees to be full)
-    auto stage_full = [&](int ch, auto cap) {
-      pf_issue();
-      cp_async_wait<PF>();
+    // one chunk: ΔQ of kc positions, B⁺ columns accumulated in registers.  FULL:
+    // kc == KC (static); CAP: capture the sector ΔQ (positions < NCAP; only the
+    // first NCAPCH chunks, which make_layout guarantees to be full).  The stage
+    // was waited on by the prefetch cursor PF chunks earlier.
+    auto chunk = [&](int ch, auto full_t, auto cap) {
+      constexpr bool FULL = decltype(full_t)::value;
+      const int kc = FULL ? KC : a.G - ch * KC;
+      if (!(a.exp_flags & 8)) {
+        pf_issue();
+        cp_async_wait<PF>();
+      } else {
+        mbar_wait(&full[rg.st], rg.ph);
+      }
       const double* Qg = qring + cq * KC * 32;
       if (++cq == NQ) cq = 0;
-      mbar_wait(&ch_full[rg.st], rg.ph);
-      const double* Bs = (const double*)(stg + rg.st * pc.stage_bytes);
+      const double* Bs = (const double*)(stg + rg.st * pc.stage_bytes + a.ids_bytes) + (size_t)ct * R * kc;
       if (a.exp_flags & 2) {
         acc[0] += Qg[0];
-      } else {
+      } else if (FULL) {
         double dq[KC];
 #pragma unroll
         for (int kk = 0; kk < KC; ++kk) dq[kk] = live ? Qg[kk * 32] - qi : 0.0;
@@ -511,7 +500,7 @@ __global__ void __launch_bounds__(max_threads(D, M), min_blocks(D, M)) k_pipelin
             if (ch * KC + kk < NCAP) dqs[ch * KC + kk] = dq[kk];
         }
         if (KC % 2 == 0) {
-          const double2* b2 = reinterpret_cast<const double2*>(Bs + (size_t)ct * R * KC);
+          const double2* b2 = reinterpret_cast<const double2*>(Bs);
 #pragma unroll
           for (int l = 0; l < R; ++l) {
 #pragma unroll
@@ -522,52 +511,41 @@ __global__ void __launch_bounds__(max_threads(D, M), min_blocks(D, M)) k_pipelin
             }
           }
         } else {
-          const double* b = Bs + (size_t)ct * R * KC;
 #pragma unroll
           for (int l = 0; l < R; ++l)
 #pragma unroll
-            for (int kk = 0; kk < KC; ++kk) acc[l] += b[l * KC + kk] * dq[kk];
+            for (int kk = 0; kk < KC; ++kk) acc[l] += Bs[l * KC + kk] * dq[kk];
+        }
+      } else {
+        for (int kk = 0; kk < kc; ++kk) {
+          const double dq = live ? Qg[kk * 32] - qi : 0.0;
+#pragma unroll
+          for (int l = 0; l < R; ++l) acc[l] += Bs[l * kc + kk] * dq;
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&ch_empty[rg.st]);
-      rg.next(S);
-    };
-    // the shorter last chunk
-    auto stage_tail = [&](int kc) {
-      pf_issue();
-      cp_async_wait<PF>();
-      const double* Qg = qring + cq * KC * 32;
-      if (++cq == NQ) cq = 0;
-      mbar_wait(&ch_full[rg.st], rg.ph);
-      const double* b = (const double*)(stg + rg.st * pc.stage_bytes) + (size_t)ct * R * kc;
-      for (int kk = 0; kk < kc; ++kk) {
-        const double dq = live ? Qg[kk * 32] - qi : 0.0;
-#pragma unroll
-        for (int l = 0; l < R; ++l) acc[l] += b[l * kc + kk] * dq;
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&ch_empty[rg.st]);
+      if (lane == 0) mbar_arrive(&empty[rg.st]);
       rg.next(S);
     };
     // first chunks (sector positions): fully unrolled so dqs[] stays in registers
 #pragma unroll
-    for (int ch = 0; ch < NCAPCH; ++ch) stage_full(ch, std::true_type{});
+    for (int ch = 0; ch < NCAPCH; ++ch) chunk(ch, std::true_type{}, std::true_type{});
     const int nfull = a.G / KC;
-    for (int ch = NCAPCH; ch < nfull; ++ch) stage_full(ch, std::false_type{});
-    if (nfull < a.NCH) stage_tail(a.G - nfull * KC);
+    for (int ch = NCAPCH; ch < nfull; ++ch) chunk(ch, std::true_type{}, std::false_type{});
+    if (nfull < a.NCH) chunk(nfull, std::false_type{}, std::false_type{});
 
-    // sectors; the header is resident (the prefetch cursor waited on it)
-    mbar_wait(&hdr_full[hr.st], hr.ph);
-    const unsigned char* hb_p = hdr + hr.st * pc.hdr_bytes;
-    const uint8_t vmask = *((const uint8_t*)(hb_p + a.off_vmask) + ct);
+    // sector chunk: sector inverses + validity
+    mbar_wait(&full[rg.st], rg.ph);
+    const unsigned char* sb = stg + rg.st * pc.stage_bytes;
+    const uint8_t vmask = sb[a.sinv_bytes + ct];
     bool valid[NV];
 #pragma unroll
     for (int s = 0; s < NV; ++s) valid[s] = (vmask >> s) & 1;
     double ps[NV][D];
-    sector_apply<D>((const double*)(hb_p + a.off_sinv) + size_t(ct) * NV * D * D, dqs, ps);
+    sector_apply<D>((const double*)sb + size_t(ct) * NV * D * D, dqs, ps);
     __syncwarp();
-    if (lane == 0) mbar_arrive(&hdr_empty[hr.st]);
+    if (lane == 0) mbar_arrive(&empty[rg.st]);
+    rg.next(S);
 
     if (a.dense_out) {
       // per-warp staging + one bulk store of the warp's contiguous output rows
@@ -576,17 +554,21 @@ __global__ void __launch_bounds__(max_threads(D, M), min_blocks(D, M)) k_pipelin
       const int nlive = (int)max((int64_t)0, min((int64_t)32, lim));
       if (lane == 0) bulk_wait_read();  // the staging rows are free again
       __syncwarp();
-      cweno_epilogue<D, NM>(qi, acc, ps, valid, a, outw + lane * NM, nullptr, nullptr);
+      if (a.exp_flags & 16) {
+        outw[lane * NM] = acc[0] + ps[0][0];
+      } else {
+        cweno_epilogue<D, NM>(qi, acc, ps, valid, a, outw + lane * NM, nullptr, nullptr);
+      }
       fence_proxy_async();
       __syncwarp();
       if (lane == 0 && nlive > 0) bulk_s2g(a.out + first * NM, outw, (uint32_t)(nlive * NM * 8));
     } else {
-      double scratch[NM];
-      cweno_epilogue<D, NM>(qi, acc, ps, valid, a, scratch, nullptr, nullptr);
+      double w[NM];
+      cweno_epilogue<D, NM>(qi, acc, ps, valid, a, w, nullptr, nullptr);
       if (live) {
         double* o = a.out + c * a.ccs + v * a.cvs;
 #pragma unroll
-        for (int l = 0; l < NM; ++l) o[l] = scratch[l];
+        for (int l = 0; l < NM; ++l) o[l] = w[l];
       }
     }
     qi = qn;
@@ -644,10 +626,12 @@ static KArgs make_args(const cwreco_ctx* c, const double* avgs, int64_t acs, int
   std::memset(&a, 0, sizeof(a));
   a.blocks = c->dev->blocks;
   a.tile_bytes = L.tile_bytes;
-  a.off_ids = L.off_ids;
-  a.off_sinv = L.off_sinv;
-  a.off_vmask = L.off_vmask;
-  a.off_chunks = L.off_chunks;
+  a.ids_bytes = L.ids_bytes;
+  a.chunk_bytes = L.chunk_bytes;
+  a.kslice_bytes = L.kslice_bytes;
+  a.off_sector = L.off_sector;
+  a.sinv_bytes = L.sinv_bytes;
+  a.sector_bytes = L.sector_bytes;
   a.T = L.T;
   a.G = L.G;
   a.K = L.K;
@@ -683,43 +667,35 @@ static KArgs make_args(const cwreco_ctx* c, const double* avgs, int64_t acs, int
 static PipeCfg pipe_cfg(const cwreco_ctx* c) {
   const Layout& L = c->lay;
   PipeCfg p;
-  auto r128 = [](int64_t x) { return (x + 127) & ~int64_t(127); };
   p.ncw = (L.T * c->V + 31) / 32;
-  p.hdr_bytes = L.header_bytes;
-  p.stage_bytes = r128((int64_t)L.KC * L.kslice_bytes);
-  p.q_bytes = r128((int64_t)p.ncw * NQ * L.KC * 32 * 8);
-  p.out_bytes = r128((int64_t)p.ncw * 32 * c->nm * 8);
-  const int blocks = c->nm >= 20 ? 1 : 2;
-  auto total = [&](int hs, int s) {
-    return r128(hs * p.hdr_bytes) + s * p.stage_bytes + p.q_bytes + p.out_bytes + 8 * (2 * hs + 2 * s);
-  };
-  // header slots: 3 (two tiles of header lookahead) when affordable, else 2; then
-  // as many stages as fit the per-CTA budget (2 CTAs/SM for ℳ < 20); a tile too
+  p.stage_bytes = pipe_stage_bytes(L);
+  p.q_bytes = pipe_q_bytes(L);
+  p.out_bytes = pipe_out_bytes(L);
+  // as many stages as fit the per-CTA budget (ctas_per_sm CTAs/SM); a tile too
   // large for that budget runs at 1 CTA/SM with the whole shared memory.  The
-  // prefetch cursor needs stages > PF (it waits on the next tile's header, which
-  // the producer issues after the current tile's last chunk).
-  int hs = 0, st = 0;
-  for (int64_t budget : {(int64_t)(c->dev->max_smem + 1024) / blocks - 1024, (int64_t)c->dev->max_smem}) {
-    for (int h = 3; h >= 2 && !st; --h)
-      for (int s = 12; s >= PF + 1; --s)
-        if (total(h, s) <= budget && (h == 2 || s >= 4)) {
-          hs = h;
-          st = s;
-          break;
-        }
+  // prefetch cursor runs up to PF + 1 stages ahead of the consumers.
+  int st = 0;
+  const char* cap = std::getenv("CWRECO_MAX_STAGES");  // tuning experiments only (tools/exp_bench.py)
+  const int smax = cap ? std::max(kMinStages, std::atoi(cap)) : kMaxStages;
+  for (int64_t budget : {pipe_budget(c->nm, c->dev->max_smem), (int64_t)c->dev->max_smem}) {
+    for (int s = smax; s >= kMinStages; --s)
+      if (pipe_smem(L, s) <= budget) {
+        st = s;
+        break;
+      }
     if (st) break;
   }
   if (!st) fail(CWRECO_EUNSUPPORTED, "pipelined kernel: tile does not fit in shared memory");
-  p.hslots = hs;
   p.stages = st;
-  p.off_hdr = 0;
-  p.off_stage = r128(hs * p.hdr_bytes);
-  p.off_q = p.off_stage + st * p.stage_bytes;
+  p.off_stage = 0;
+  p.off_q = st * p.stage_bytes;
   p.off_out = p.off_q + p.q_bytes;
   p.off_bar = p.off_out + p.out_bytes;
-  p.smem = p.off_bar + 8 * (2 * hs + 2 * st);
+  p.smem = p.off_bar + 16 * st;
   return p;
 }
+
+int dev_max_smem(const cwreco_ctx* c) { return c->dev ? c->dev->max_smem : 227 * 1024; }
 
 void dev_create(cwreco_ctx* c) {
   if (c->device < 0) return;
@@ -766,7 +742,8 @@ void dev_upload_aux(cwreco_ctx* c) {
   CK(cudaMemcpyToSymbol(c_sig, packed.data(), sizeof(double) * packed.size(), sizeof(double) * sig_off(c->d, c->M)));
   PipeCfg p = pipe_cfg(c);
   PipeFn f = pipe_fn(c->d, c->M, c->lay.KC);
-  CK(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
+  (void)p;
+  CK(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, c->dev->max_smem));
 }
 
 void dev_download_tile(const cwreco_ctx* c, int64_t tile, unsigned char* host) {
@@ -800,7 +777,7 @@ void dev_reconstruct(cwreco_ctx* c, const double* avgs, int64_t acs, int64_t avs
     a.dense_out = (cvs == nm && ccs == (int64_t)c->V * nm && (((uintptr_t)coeffs) & 15) == 0 && nm % 2 == 0) ? 1 : 0;
     PipeCfg p = pipe_cfg(c);
     const int64_t ntiles = a.tile_end - a.tile_begin;
-    const int per_sm = c->nm >= 20 ? 1 : 2;
+    const int per_sm = ctas_per_sm(c->nm);
     const int64_t grid = std::min<int64_t>(ntiles, (int64_t)c->dev->num_sms * per_sm);
     dim3 b((p.ncw + 1) * 32), g((unsigned)grid);
     pipe_fn(c->d, c->M, c->lay.KC)<<<g, b, p.smem, st>>>(a, p);

@@ -11,6 +11,7 @@
 //  Sectors: the linear modes averaged over a cell equal their value at
 //  the cell barycentre, so A_s[m][l] = ψ_{l+1}(ξ_i(b_{j_m})); S_s = A_s⁻¹ (d×d).
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <unordered_map>
@@ -21,7 +22,7 @@ namespace cwr {
 
 static inline int64_t r16(int64_t x) { return (x + 15) & ~int64_t(15); }
 
-Layout make_layout(int d, int M, int V, int G) {
+static Layout layout_with(int d, int M, int V, int G, int T, int KC) {
   Layout L;
   L.d = d;
   L.M = M;
@@ -30,31 +31,46 @@ Layout make_layout(int d, int M, int V, int G) {
   L.R = L.nm - 1;
   L.K = d * L.nm - 1;
   L.G = G;
-  // consumer threads per CTA: 320 (1 CTA/SM) for the register-heavy 3D M=3 kernel,
-  // else 160 (2 CTAs/SM); one tile = T cells × V variables = one consumer thread each
-  const int target = (L.nm >= 20) ? 320 : 160;
-  int T = (target / V) & ~1;
-  if (T < 2) T = 2;
   L.T = T;
+  L.KC = KC;
   L.kslice_bytes = int64_t(T) * L.R * 8;
-  // k-slices per streamed chunk: ~10 KB of B⁺ per stage, even (the kernel reads
-  // k-pairs with 16-byte shared loads), at most 8
-  L.KC = std::max<int>(1, int(10240 / L.kslice_bytes));
-  L.KC = std::min(L.KC, 8);
-  L.KC = (L.KC + 1) & ~1;
-  if (L.KC > G) L.KC = G;
-  // the chunks holding the (d+1)·d sector positions must be full (the kernel
-  // captures their ΔQ with static indices)
-  // (and KC must be one of the compiled chunk sizes 1-6, 8)
-  while (L.KC > 1 && (L.KC == 7 || ((d + 1) * d + L.KC - 1) / L.KC * L.KC > G)) --L.KC;
-  L.NCH = (G + L.KC - 1) / L.KC;
-  L.off_ids = 0;
-  L.off_sinv = r16(int64_t(G) * T * 4);
-  L.off_vmask = L.off_sinv + int64_t(T) * (d + 1) * d * d * 8;
-  L.header_bytes = r16(L.off_vmask + int64_t(T));
-  L.off_chunks = L.header_bytes;
-  L.tile_bytes = r16(L.off_chunks + int64_t(G) * L.kslice_bytes);
+  L.NCH = (G + KC - 1) / KC;
+  L.ids_bytes = r16(int64_t(KC) * T * 4);
+  L.chunk_bytes = L.ids_bytes + int64_t(KC) * L.kslice_bytes;
+  L.off_sector = r16(L.off_chunk(L.NCH - 1) + L.chunk_size(L.NCH - 1));
+  L.sinv_bytes = int64_t(T) * (d + 1) * d * d * 8;
+  L.sector_bytes = r16(L.sinv_bytes + T);
+  L.tile_bytes = L.off_sector + L.sector_bytes;
   return L;
+}
+
+Layout make_layout(int d, int M, int V, int G, int max_smem) {
+  const int nm = n_modes(M, d);
+  // one tile = T cells × V variables = one consumer thread each
+  int T = (cons_threads(nm) / V) & ~1;
+  if (T < 2) T = 2;
+  // positions per streamed chunk: ~10 KB of B⁺ per chunk (measured best: larger
+  // chunks lengthen the gather bursts, smaller ones add per-chunk synchronisation),
+  // even (the kernel reads position pairs with 16-byte shared loads), a compiled
+  // size (1-6, 8), such that the chunks holding the (d+1)·d sector positions are
+  // full (their ΔQ is captured with static indices) and kMinStages stages fit.
+  const int64_t budget = pipe_budget(nm, max_smem);
+  const int64_t kslice = int64_t(T) * (nm - 1) * 8;
+  int want = std::max<int>(1, int(10240 / kslice));
+  want = std::min(want, 8);
+  want = (want + 1) & ~1;
+  if (want == 7) want = 6;
+  Layout best;
+  bool found = false;
+  const char* force = std::getenv("CWRECO_KC");  // tuning experiments only (tools/sweep.py)
+  for (int KC = force ? std::atoi(force) : want; KC >= 1; --KC) {
+    if (KC == 7 || KC > G || ((d + 1) * d + KC - 1) / KC * KC > G) continue;
+    Layout L = layout_with(d, M, V, G, T, KC);
+    if (!found) best = L, found = true;
+    if (pipe_smem(L, kMinStages) <= budget) return L;
+    if (pipe_smem(L, kMinStages) < pipe_smem(best, kMinStages)) best = L;
+  }
+  return best;
 }
 
 namespace {
@@ -166,7 +182,7 @@ void precompute(cwreco_ctx* c) {
   if (!c->has_stencils) fail(CWRECO_ESTATE, "precompute: call cwreco_build_stencils first");
   const int d = c->d, M = c->M, nm = c->nm, ne = c->ne, nv = d + 1;
   const int R = nm - 1, K = ne - 1;
-  c->lay = make_layout(d, M, c->V, c->G);
+  c->lay = make_layout(d, M, c->V, c->G, c->device >= 0 ? dev_max_smem(c) : 227 * 1024);
   const Layout& L = c->lay;
   const int T = L.T, G = L.G;
   c->n_tiles = (c->n_owned + T - 1) / T;
@@ -250,10 +266,8 @@ void precompute(cwreco_ctx* c) {
       const int64_t tile = li / T;
       const int ct = int(li % T);
       unsigned char* tb = base + size_t(tile - t0) * L.tile_bytes;
-      int32_t* ids = (int32_t*)(tb + L.off_ids);
-      double* sinv = (double*)(tb + L.off_sinv);
-      uint8_t* vmask = (uint8_t*)(tb + L.off_vmask);
-      double* Bch = (double*)(tb + L.off_chunks);
+      double* sinv = (double*)(tb + L.off_sector);
+      uint8_t* vmask = (uint8_t*)(tb + L.off_sector + L.sinv_bytes);
       const int64_t g = c->local2global[li];
       const int64_t q = g - c->own_lo;
       const int32_t* cen = &c->central[q * ne];
@@ -306,7 +320,7 @@ void precompute(cwreco_ctx* c) {
           lid = to_local(gglob[p]);
           if (lid < 0) bad_local |= 1;
         }
-        ids[size_t(p) * T + ct] = lid;
+        ((int32_t*)(tb + L.off_chunk(p / L.KC)))[size_t(p % L.KC) * T + ct] = lid;
       }
       uint8_t vm = 0;
       for (int s = 0; s < nv; ++s) vm |= val[s] ? uint8_t(1u << s) : 0;
@@ -362,8 +376,8 @@ void precompute(cwreco_ctx* c) {
       // B chunks: chunk ch holds positions p in [ch·KC, ch·KC + kc) as [T][R][kc]
       for (int p = 0; p < G; ++p) {
         const int ch = p / L.KC, kk = p % L.KC;
-        const int kc = std::min(L.KC, G - ch * L.KC);
-        double* chb = Bch + size_t(ch) * L.KC * T * R;
+        const int kc = L.kc_of(ch);
+        double* chb = (double*)(tb + L.off_chunk(ch) + L.ids_bytes);
         const int k = p < ng ? col[p] : -1;
         for (int l = 0; l < R; ++l) chb[(size_t(ct) * R + l) * kc + kk] = k >= 0 ? Bp[size_t(l) * K + k] : 0.0;
       }

@@ -33,25 +33,30 @@ def time_pass(ctx, A, out, flush, n=20):
     return ts[len(ts) // 2]
 
 
-for cfg in sys.argv[1:]:
-    w = gen.make(cfg)
-    t = time.time()
-    ctx = P.setup_context(w["nodes"], w["cells"], w["period"], w["M"], w["V"], device=0)
-    inf = ctx.info()
-    A = torch.tensor(w["avgs"][ctx.permutation()], device="cuda")
-    out = torch.empty((inf["n_owned"], w["V"], ctx.nm), dtype=torch.float64, device="cuda")
-    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
-    res = {}
-    for flags in [int(f) for f in os.environ.get("EXP_FLAGS_LIST", "0,1,2,3,4,5,6,7").split(",")]:
-        os.environ["CWRECO_EXP_FLAGS"] = str(flags)
-        ms = time_pass(ctx, A, out, flush)
-        res[flags] = ms
-    os.environ["CWRECO_EXP_FLAGS"] = "0"
-    ctx.set_kernel("simple")
-    res["simple"] = time_pass(ctx, A, out, flush)
-    ctx.set_kernel("pipelined")
-    B = inf["algorithmic_bytes_per_cell"] * inf["n_owned"]
-    print(json.dumps({"config": cfg, "info": {k: inf[k] for k in ("tile_cells", "chunk_k", "tile_bytes", "n_tiles")},
-                      "ms": res, "GBps_alg": {k: B / v / 1e6 for k, v in res.items()}}), flush=True)
-    del ctx, A, out
-    torch.cuda.empty_cache()
+def main():
+    for cfg in sys.argv[1:]:
+        w = gen.make(cfg)
+        t = time.time()
+        ctx = P.setup_context(w["nodes"], w["cells"], w["period"], w["M"], w["V"], device=0)
+        inf = ctx.info()
+        A = torch.tensor(w["avgs"][ctx.permutation()], device="cuda")
+        out = torch.empty((inf["n_owned"], w["V"], ctx.nm), dtype=torch.float64, device="cuda")
+        flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+        res = {}
+        for flags in [int(f) for f in os.environ.get("EXP_FLAGS_LIST", "0,1,2,3,4,5,6,7").split(",")]:
+            os.environ["CWRECO_EXP_FLAGS"] = str(flags)
+            ms = time_pass(ctx, A, out, flush)
+            res[flags] = ms
+        os.environ["CWRECO_EXP_FLAGS"] = "0"
+        ctx.set_kernel("simple")
+        res["simple"] = time_pass(ctx, A, out, flush)
+        ctx.set_kernel("pipelined")
+        B = inf["algorithmic_bytes_per_cell"] * inf["n_owned"]
+        print(json.dumps({"config": cfg, "info": {k: inf[k] for k in ("tile_cells", "chunk_k", "tile_bytes", "n_tiles")},
+                          "ms": res, "GBps_alg": {k: B / v / 1e6 for k, v in res.items()}}), flush=True)
+        del ctx, A, out
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()

@@ -301,6 +301,29 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
   }
 }
+// Blocking wait with a long suspend-time hint: the waiting thread sleeps until the
+// phase completes instead of re-polling (used by the producer lane, whose spin
+// otherwise steals issue slots from the consumers on its SM sub-partition).
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+        : "memory");
+  }
+}
+// Non-blocking probe of a phase (result consumed later, so its latency overlaps work).
+__device__ __forceinline__ uint32_t mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(done)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return done;
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
@@ -397,7 +420,7 @@ __global__ void __launch_bounds__(max_threads(D, M), min_blocks(D, M)) k_pipelin
     if (lane == 0) {
       Ring rg;
       auto issue = [&](const unsigned char* src, uint32_t bytes) {
-        mbar_wait(&empty[rg.st], rg.ph ^ 1);
+        mbar_wait_sleep(&empty[rg.st], rg.ph ^ 1);
         if (a.exp_flags & 4) {
           mbar_arrive(&full[rg.st]);
         } else {
@@ -429,11 +452,13 @@ __global__ void __launch_bounds__(max_threads(D, M), min_blocks(D, M)) k_pipelin
   int64_t pf_tile = t0;
   int pf_ch = 0, pf_q = 0;
   Ring pr;
-  bool pf_live = active && t0 < a.tile_end && t0 * a.T + ct < a.n_owned && !(a.exp_flags & 1);
-  auto pf_issue = [&]() {
+  // (flag 4 leaves the stages unfilled, so it implies flag 1: no gathers from garbage ids)
+  bool pf_live = active && t0 < a.tile_end && t0 * a.T + ct < a.n_owned && !(a.exp_flags & 5);
+  // ready: result of an earlier mbar_test of the same stage/phase (1 = resident)
+  auto pf_issue = [&](uint32_t ready) {
     if (pf_tile < a.tile_end) {
       const int kc = min(KC, a.G - pf_ch * KC);
-      mbar_wait(&full[pr.st], pr.ph);  // the chunk (and its gather ids) is resident
+      if (!ready) mbar_wait(&full[pr.st], pr.ph);  // the chunk (and its gather ids) is resident
       if (pf_live) {
         const int32_t* idc = (const int32_t*)(stg + pr.st * pc.stage_bytes) + ct;
         double* dst = qring + pf_q * KC * 32;
@@ -446,7 +471,7 @@ __global__ void __launch_bounds__(max_threads(D, M), min_blocks(D, M)) k_pipelin
         pr.next(S);
         pf_ch = 0;
         pf_tile += gridDim.x;
-        pf_live = active && pf_tile < a.tile_end && pf_tile * a.T + ct < a.n_owned && !(a.exp_flags & 1);
+        pf_live = active && pf_tile < a.tile_end && pf_tile * a.T + ct < a.n_owned && !(a.exp_flags & 5);
       }
     }
     cp_async_commit();
@@ -454,7 +479,7 @@ __global__ void __launch_bounds__(max_threads(D, M), min_blocks(D, M)) k_pipelin
   };
   if (!(a.exp_flags & 8)) {
 #pragma unroll
-    for (int k = 0; k < PF; ++k) pf_issue();
+    for (int k = 0; k < PF; ++k) pf_issue(0);
   }
 
   Ring rg;
@@ -480,8 +505,8 @@ __global__ void __launch_bounds__(max_threads(D, M), min_blocks(D, M)) k_pipelin
       constexpr bool FULL = decltype(full_t)::value;
       const int kc = FULL ? KC : a.G - ch * KC;
       if (!(a.exp_flags & 8)) {
-        pf_issue();
-        cp_async_wait<PF>();
+        pf_issue(0);              // gathers of the chunk PF ahead
+        cp_async_wait<PF>();      // this chunk's gathers (issued PF chunks ago) have landed
       } else {
         mbar_wait(&full[rg.st], rg.ph);
       }

@@ -47,28 +47,30 @@ static Layout layout_with(int d, int M, int V, int G, int T, int KC) {
 Layout make_layout(int d, int M, int V, int G, int max_smem) {
   const int nm = n_modes(M, d);
   // one tile = T cells × V variables = one consumer thread each
-  int T = (cons_threads(nm) / V) & ~1;
-  if (T < 2) T = 2;
+  int T0 = (cons_threads(nm) / V) & ~1;
+  if (T0 < 2) T0 = 2;
   // positions per streamed chunk: ~10 KB of B⁺ per chunk (measured best: larger
   // chunks lengthen the gather bursts, smaller ones add per-chunk synchronisation),
   // even (the kernel reads position pairs with 16-byte shared loads), a compiled
   // size (1-6, 8), such that the chunks holding the (d+1)·d sector positions are
   // full (their ΔQ is captured with static indices) and kMinStages stages fit.
+  // A tile whose sector chunk alone is too large (small ℳ, V = 1) is halved.
   const int64_t budget = pipe_budget(nm, max_smem);
-  const int64_t kslice = int64_t(T) * (nm - 1) * 8;
-  int want = std::max<int>(1, int(10240 / kslice));
-  want = std::min(want, 8);
-  want = (want + 1) & ~1;
-  if (want == 7) want = 6;
+  const char* force = std::getenv("CWRECO_KC");  // tuning experiments only (tools/sweep.py)
   Layout best;
   bool found = false;
-  const char* force = std::getenv("CWRECO_KC");  // tuning experiments only (tools/sweep.py)
-  for (int KC = force ? std::atoi(force) : want; KC >= 1; --KC) {
-    if (KC == 7 || KC > G || ((d + 1) * d + KC - 1) / KC * KC > G) continue;
-    Layout L = layout_with(d, M, V, G, T, KC);
-    if (!found) best = L, found = true;
-    if (pipe_smem(L, kMinStages) <= budget) return L;
-    if (pipe_smem(L, kMinStages) < pipe_smem(best, kMinStages)) best = L;
+  for (int T = T0; T >= 2; T = (T / 2) & ~1) {
+    const int64_t kslice = int64_t(T) * (nm - 1) * 8;
+    int want = std::max<int>(1, int(10240 / kslice));
+    want = std::min(want, 8);
+    want = (want + 1) & ~1;
+    if (want == 7) want = 6;
+    for (int KC = force ? std::atoi(force) : want; KC >= 1; --KC) {
+      if (KC == 7 || KC > G || ((d + 1) * d + KC - 1) / KC * KC > G) continue;
+      Layout L = layout_with(d, M, V, G, T, KC);
+      if (pipe_smem(L, kMinStages) <= budget) return L;
+      if (!found || pipe_smem(L, kMinStages) < pipe_smem(best, kMinStages)) best = L, found = true;
+    }
   }
   return best;
 }

@@ -102,6 +102,8 @@ typedef struct {
   int64_t algorithmic_bytes_per_cell;    /* SURVEY §8(d) B_cell */
   int64_t n_invalid_sectors;             /* sectors flagged invalid (R14) */
   int64_t n_extra_gather;                /* sector cells outside S_i^0 (R15) */
+  int64_t union_max;                     /* largest per-tile stencil union (cells whose
+                                            averages a tile gathers once into shared memory) */
 } cwreco_info;
 
 /* ---------------------------------------------------------------- lifecycle */

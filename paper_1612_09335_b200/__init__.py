@@ -40,7 +40,7 @@ class _Info(ctypes.Structure):
                [(n, ctypes.c_int64) for n in ("n_cells", "n_owned", "n_ghost", "n_interior", "n_tiles",
                                                "n_interior_tiles", "tile_bytes", "device_bytes",
                                                "algorithmic_bytes_per_cell", "n_invalid_sectors",
-                                               "n_extra_gather")]
+                                               "n_extra_gather", "union_max")]
 
 
 def _load():

@@ -102,6 +102,7 @@ cwreco_status cwreco_get_info(const cwreco_ctx* c, cwreco_info* o) {
     o->n_interior = c->n_interior;
     o->n_invalid_sectors = c->n_invalid;
     o->n_extra_gather = c->n_extra;
+    o->union_max = c->lay.Umax;
     if (c->has_blocks) {
       o->tile_cells = c->lay.T;
       o->chunk_k = c->lay.KC;
@@ -237,8 +238,10 @@ cwreco_status cwreco_get_blocks(const cwreco_ctx* c, int64_t n_sel, const int64_
           }
       if (sinv) std::memcpy(sinv + s * nv * d * d, sv + (size_t)ct * nv * d * d, sizeof(double) * nv * d * d);
       if (gather)
-        for (int k = 0; k < G; ++k)
-          gather[s * G + k] = ((const int32_t*)(tb + L.off_chunk(k / L.KC)))[size_t(k % L.KC) * T + ct];
+        for (int k = 0; k < G; ++k) {
+          const uint16_t u = ((const uint16_t*)(tb + L.off_chunk(k / L.KC)))[size_t(k % L.KC) * T + ct];
+          gather[s * G + k] = ((const int32_t*)tb)[u];  // union chunk: local ids
+        }
       if (slots)
         for (int q = 0; q < nv; ++q)
           for (int m = 0; m < d; ++m) slots[(s * nv + q) * d + m] = ((vm >> q) & 1) ? uint8_t(q * d + m) : 255;

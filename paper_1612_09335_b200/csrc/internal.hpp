@@ -3,6 +3,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <functional>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -26,42 +27,45 @@ inline int n_modes(int M, int d) {  // ℳ(M,d) = (1/d!) Π_{l=1..d} (M+l)   (P:
 }
 
 // Layout of one packed tile of the matrix stream: the
-// tile's T cells are streamed as NCH position chunks followed by one sector chunk,
-// each a contiguous 16-byte-aligned block (one 1-D bulk copy):
+// tile's T cells are streamed as a union chunk, NCH position chunks and a sector
+// chunk, each a contiguous 16-byte-aligned block (one 1-D bulk copy):
+//   union chunk: uid int32 [U]     local ids of every cell the tile's stencils touch:
+//                                  the tile's own T cells first, then the others
+//                                  ascending; padded to Umax entries (U ≤ Umax)
 //   chunk ch, positions p ∈ [ch·KC, ch·KC+kc) (kc = KC except a shorter last one):
-//     ids   int32  [kc][T]  gather list (local cell ids), padded to ids_bytes;
-//                           positions [0, (d+1)d): sector s, member m at s·d+m (R15;
-//                           filler if the sector is invalid), then the rest of
-//                           S_i^0, then the cell itself as padding
+//     idx   uint16 [kc][T]  union index of the gathered stencil cell, padded to
+//                           ids_bytes; positions [0, (d+1)d): sector s, member m at
+//                           s·d+m (R15; filler if the sector is invalid), then the
+//                           rest of S_i^0, then the cell itself as padding
 //     B     double [T][R][kc]  reduced pseudo-inverse columns in gather order
 //                           (0 for positions outside S_i^0)
 //   sector chunk (at off_sector):
 //     sinv  double [T][d+1][d][d]  sector inverses
 //     vmask uint8  [T]             bit s = sector s valid (R14)
 struct Layout {
-  int d = 0, M = 0, V = 0, nm = 0, R = 0, K = 0, G = 0, T = 0, KC = 0, NCH = 0;
+  int d = 0, M = 0, V = 0, nm = 0, R = 0, K = 0, G = 0, T = 0, KC = 0, NCH = 0, Umax = 0;
   int64_t kslice_bytes = 0;  // T·R·8: one position of B⁺ for the whole tile
-  int64_t ids_bytes = 0;     // r16(KC·T·4)
+  int64_t u_bytes = 0;       // r16(Umax·4): the union chunk
+  int64_t ids_bytes = 0;     // r16(KC·T·2)
   int64_t chunk_bytes = 0;   // stride of full chunks: ids_bytes + KC·kslice_bytes
   int64_t sinv_bytes = 0, sector_bytes = 0, off_sector = 0, tile_bytes = 0;
   int kc_of(int ch) const { return KC < G - ch * KC ? KC : G - ch * KC; }
-  int64_t off_chunk(int ch) const { return int64_t(ch) * chunk_bytes; }
+  int64_t off_chunk(int ch) const { return u_bytes + int64_t(ch) * chunk_bytes; }
   int64_t chunk_size(int ch) const { return ids_bytes + int64_t(kc_of(ch)) * kslice_bytes; }
 };
 
 // Pipelined-kernel shape (kernels.cu), shared with make_layout's chunk choice.
-constexpr int kPrefetch = 2;              // gather prefetch distance, in chunks
-constexpr int kQSlots = kPrefetch + 1;    // per-thread gather ring slots
-constexpr int kMinStages = kPrefetch + 2; // the prefetch cursor runs ≤ PF+1 stages ahead
+constexpr int kMinStages = 4;             // stage ring depth floor
 inline int cons_threads(int nm) { return nm >= 20 ? 320 : 160; }  // consumer threads per CTA
 inline int ctas_per_sm(int nm) { return nm >= 20 ? 1 : 2; }
 inline int64_t round128(int64_t x) { return (x + 127) & ~int64_t(127); }
 // shared memory of one pipelined CTA: S stages + the consumers' private gather rings
 inline int64_t pipe_stage_bytes(const Layout& L) {
-  return round128(L.chunk_bytes > L.sector_bytes ? L.chunk_bytes : L.sector_bytes);
+  int64_t m = L.chunk_bytes > L.sector_bytes ? L.chunk_bytes : L.sector_bytes;
+  return round128(m > L.u_bytes ? m : L.u_bytes);
 }
-inline int64_t pipe_q_bytes(const Layout& L) {
-  return round128(int64_t((L.T * L.V + 31) / 32) * kQSlots * L.KC * 32 * 8);
+inline int64_t pipe_q_bytes(const Layout& L) {  // double-buffered union averages Q_u [Umax][V]
+  return round128(2 * int64_t(L.Umax) * L.V * 8);
 }
 inline int64_t pipe_out_bytes(const Layout& L) {  // per-warp output staging (bulk stores)
   return round128(int64_t((L.T * L.V + 31) / 32) * 32 * L.nm * 8);
@@ -74,8 +78,9 @@ inline int64_t pipe_budget(int nm, int max_smem) {
   return ctas_per_sm(nm) == 1 ? max_smem : (max_smem + 1024) / ctas_per_sm(nm) - 1024;
 }
 
-// max_smem: opt-in shared memory per block of the device (227 KB on B200).
-Layout make_layout(int d, int M, int V, int G, int max_smem);
+// max_smem: opt-in shared memory per block of the device (227 KB on B200);
+// umax_for(T): the largest per-tile stencil union for tiles of T cells.
+Layout make_layout(int d, int M, int V, int G, int max_smem, const std::function<int(int)>& umax_for);
 
 struct DeviceState;  // kernels.cu
 

@@ -68,7 +68,8 @@ __constant__ double c_sig[SIG_TOTAL];
 
 struct KArgs {
   const unsigned char* blocks;
-  int64_t tile_bytes, ids_bytes, chunk_bytes, kslice_bytes, off_sector, sinv_bytes, sector_bytes;
+  int64_t tile_bytes, u_bytes, ids_bytes, chunk_bytes, kslice_bytes, off_sector, sinv_bytes, sector_bytes;
+  int Umax;
   int T, G, K, KC, NCH, V;
   int64_t n_owned, tile_begin, tile_end;
   const double* Q;
@@ -76,8 +77,8 @@ struct KArgs {
   double* out;
   int64_t ccs, cvs;
   int dense_out;
-  int exp_flags;  // bottleneck experiments only (CWRECO_EXP_FLAGS): 1 no gather, 2 no math, 4 no B⁺ stream,
-                 // 8 no gather bookkeeping, 16 no epilogue
+  int exp_flags;  // bottleneck experiments only (CWRECO_EXP_FLAGS): 1 no gather, 2 no B⁺ FMAs,
+                 // 16 no epilogue (timing only: results are wrong)
   double eps, psi1;
   int r;
   // normalised linear weights (R5, R14) indexed by the number of valid sectors
@@ -237,12 +238,12 @@ __global__ void __launch_bounds__(256) k_simple(KArgs a, DbgOut dbg) {
   double dqs[NCAP];
   for (int ch = 0; ch < a.NCH; ++ch) {
     const int kc = min(a.KC, a.G - ch * a.KC);
-    const unsigned char* cb = tb + ch * a.chunk_bytes;
-    const int32_t* ids = (const int32_t*)cb;                                          // [kc][T]
+    const unsigned char* cb = tb + a.u_bytes + ch * a.chunk_bytes;
+    const uint16_t* idx = (const uint16_t*)cb;                                      // [kc][T]
     const double* Bc = (const double*)(cb + a.ids_bytes) + (size_t)ct * R * kc;   // [T][R][kc]
     for (int kk = 0; kk < kc; ++kk) {
       const int p = ch * a.KC + kk;
-      const int32_t j = ids[size_t(kk) * a.T + ct];
+      const int32_t j = ((const int32_t*)tb)[idx[size_t(kk) * a.T + ct]];         // union chunk
       const double dq = Qv[int64_t(j) * a.acs] - qi;
 #pragma unroll
       for (int q = 0; q < NCAP; ++q)
@@ -357,9 +358,6 @@ __host__ __device__ constexpr int cons_target(int D, int M) { return nmodes(M, D
 __host__ __device__ constexpr int min_blocks(int D, int M) { return nmodes(M, D) >= 20 ? 1 : 2; }
 // consumers + one producer warp
 __host__ __device__ constexpr int max_threads(int D, int M) { return cons_target(D, M) + 32; }
-constexpr int PF = kPrefetch;  // gather prefetch distance, in chunks
-constexpr int NQ = kQSlots;     // per-thread gather ring slots
-
 struct PipeCfg {
   int stages;
   int64_t stage_bytes, q_bytes, out_bytes;
@@ -378,18 +376,23 @@ struct Ring {  // slot index + mbarrier phase of a ring of S slots
   }
 };
 
+__device__ __forceinline__ void consumer_bar(int nthreads) {  // named barrier 1: consumer warps only
+  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+
 // ---------------------------------------------------------------- pipelined kernel
 // Persistent, warp-specialised.  Warp roles: [0, ncw) consumers, thread
-// tid ↔ (ct, v) = (tid / V, tid % V); warp ncw: TMA producer (lane 0) — streams
-// each tile's chunks (gather ids + B⁺ columns) and its sector chunk (sector
-// inverses + validity) into a ring of S shared-memory stages with 1-D bulk
-// copies completing on mbarrier transaction counts.
-// Consumers gather their own stencil averages: for chunk g+PF each thread reads
-// the gather ids from that chunk's (already resident) stage and cp.async-copies
-// the Q_j of its (cell, variable) into a private ring while chunk g is
-// multiplied; the prefetch cursor runs over the flat chunk sequence across tile
-// boundaries.  Gather positions [0, (D+1)·D) are the sector cells
-// (precompute.cpp), so their ΔQ is captured from the first chunks.
+// tid ↔ (ct, v) = (tid / V, tid % V); warp ncw: TMA producer (lane 0) — streams,
+// per tile t, the union chunk of the CTA's NEXT tile, then t's position chunks
+// (union indices + B⁺ columns) and sector chunk (sector inverses + validity) into
+// a ring of S shared-memory stages with 1-D bulk copies completing on mbarrier
+// transaction counts.
+// Stencil averages are gathered once per tile: at the start of tile t the
+// consumers read the next tile's union chunk and cp.async-copy the V averages of
+// every cell of that union into the other half of a double-buffered Q_u; a
+// whole tile of work hides the gather.  Per position the consumers then read
+// Q_u[idx][v] from shared memory.  Gather positions [0, (D+1)·D) are the sector
+// cells (precompute.cpp), so their ΔQ is captured from the first chunks.
 template <int D, int M, int KC>
 __global__ void __launch_bounds__(max_threads(D, M), min_blocks(D, M)) k_pipelined(KArgs a, PipeCfg pc) {
   constexpr int NM = nmodes(M, D), R = NM - 1, NV = D + 1;
@@ -397,6 +400,7 @@ __global__ void __launch_bounds__(max_threads(D, M), min_blocks(D, M)) k_pipelin
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned char* stg = smem + pc.off_stage;
   double* outs = (double*)(smem + pc.off_out);
+  double* Qu = (double*)(smem + pc.off_q);  // [2][Umax][V]
   uint64_t* bars = (uint64_t*)(smem + pc.off_bar);
   const int S = pc.stages;
   uint64_t* full = bars;       // [S]
@@ -421,18 +425,16 @@ __global__ void __launch_bounds__(max_threads(D, M), min_blocks(D, M)) k_pipelin
       Ring rg;
       auto issue = [&](const unsigned char* src, uint32_t bytes) {
         mbar_wait_sleep(&empty[rg.st], rg.ph ^ 1);
-        if (a.exp_flags & 4) {
-          mbar_arrive(&full[rg.st]);
-        } else {
-          mbar_expect_tx(&full[rg.st], bytes);
-          bulk_g2s(stg + rg.st * pc.stage_bytes, src, bytes, &full[rg.st]);
-        }
+        mbar_expect_tx(&full[rg.st], bytes);
+        bulk_g2s(stg + rg.st * pc.stage_bytes, src, bytes, &full[rg.st]);
         rg.next(S);
       };
+      if (t0 < a.tile_end) issue(a.blocks + t0 * a.tile_bytes, (uint32_t)a.u_bytes);
       for (int64_t tile = t0; tile < a.tile_end; tile += gridDim.x) {
         const unsigned char* tb = a.blocks + tile * a.tile_bytes;
+        if (tile + gridDim.x < a.tile_end) issue(tb + gridDim.x * a.tile_bytes, (uint32_t)a.u_bytes);
         for (int ch = 0; ch < a.NCH; ++ch)
-          issue(tb + ch * a.chunk_bytes, (uint32_t)(a.ids_bytes + min(KC, a.G - ch * KC) * a.kslice_bytes));
+          issue(tb + a.u_bytes + ch * a.chunk_bytes, (uint32_t)(a.ids_bytes + min(KC, a.G - ch * KC) * a.kslice_bytes));
         issue(tb + a.off_sector, (uint32_t)a.sector_bytes);
       }
     }
@@ -440,58 +442,40 @@ __global__ void __launch_bounds__(max_threads(D, M), min_blocks(D, M)) k_pipelin
   }
 
   // -------------------------------------------------- consumer warps
+  const int nct = pc.ncw * 32;  // consumer threads
   const bool active = tid < TV;
   const int ct = active ? tid / a.V : 0;
   const int v = active ? tid % a.V : 0;
-  const double* Qv = a.Q + v * a.avs;
-  double* qring = (double*)(smem + pc.off_q) + (size_t)warp * NQ * KC * 32 + lane;  // [NQ][KC][32]
-  double* outw = outs + (size_t)warp * 32 * NM;                                      // output staging
-
-  // prefetch cursor over the flat chunk sequence: chunk pf_ch of tile pf_tile sits
-  // in stage pr (each tile = NCH chunks + 1 sector chunk)
-  int64_t pf_tile = t0;
-  int pf_ch = 0, pf_q = 0;
-  Ring pr;
-  // (flag 4 leaves the stages unfilled, so it implies flag 1: no gathers from garbage ids)
-  bool pf_live = active && t0 < a.tile_end && t0 * a.T + ct < a.n_owned && !(a.exp_flags & 5);
-  // ready: result of an earlier mbar_test of the same stage/phase (1 = resident)
-  auto pf_issue = [&](uint32_t ready) {
-    if (pf_tile < a.tile_end) {
-      const int kc = min(KC, a.G - pf_ch * KC);
-      if (!ready) mbar_wait(&full[pr.st], pr.ph);  // the chunk (and its gather ids) is resident
-      if (pf_live) {
-        const int32_t* idc = (const int32_t*)(stg + pr.st * pc.stage_bytes) + ct;
-        double* dst = qring + pf_q * KC * 32;
-#pragma unroll
-        for (int kk = 0; kk < KC; ++kk)
-          if (kk < kc) cp_async8(dst + kk * 32, Qv + int64_t(idc[kk * a.T]) * a.acs);
-      }
-      pr.next(S);
-      if (++pf_ch == a.NCH) {  // skip the sector chunk, move to the next tile
-        pr.next(S);
-        pf_ch = 0;
-        pf_tile += gridDim.x;
-        pf_live = active && pf_tile < a.tile_end && pf_tile * a.T + ct < a.n_owned && !(a.exp_flags & 5);
+  double* outw = outs + (size_t)warp * 32 * NM;  // output staging
+  Ring rg;
+  // gather the union of tile `tile` (its union chunk is the current stage) into Q_u[buf]
+  auto gather_union = [&](int64_t tile, int buf) {
+    mbar_wait(&full[rg.st], rg.ph);
+    const int32_t* uid = (const int32_t*)(stg + rg.st * pc.stage_bytes);
+    double* dst = Qu + (size_t)buf * a.Umax * a.V;
+    if (!(a.exp_flags & 1)) {
+      const int n = a.Umax * a.V;
+      for (int e = tid; e < n; e += nct) {
+        const int u = e / a.V, vv = e - u * a.V;
+        cp_async8(dst + e, a.Q + int64_t(uid[u]) * a.acs + vv * a.avs);
       }
     }
     cp_async_commit();
-    if (++pf_q == NQ) pf_q = 0;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[rg.st]);
+    rg.next(S);
   };
-  if (!(a.exp_flags & 8)) {
-#pragma unroll
-    for (int k = 0; k < PF; ++k) pf_issue(0);
-  }
+  if (t0 < a.tile_end) gather_union(t0, 0);
 
-  Ring rg;
-  int cq = 0;  // ring slot of the chunk being consumed
-  // Q_i of the first tile; later tiles' Q_i is prefetched one tile ahead
-  double qi = 0.0;
-  if (active && t0 < a.tile_end && t0 * a.T + ct < a.n_owned) qi = __ldg(Qv + (t0 * a.T + ct) * a.acs);
-  for (int64_t tile = t0; tile < a.tile_end; tile += gridDim.x) {
+  int buf = 0;
+  for (int64_t tile = t0; tile < a.tile_end; tile += gridDim.x, buf ^= 1) {
     const int64_t c = tile * a.T + ct;
     const bool live = active && c < a.n_owned;
-    const int64_t cn = c + (int64_t)gridDim.x * a.T;
-    const double qn = (active && tile + gridDim.x < a.tile_end && cn < a.n_owned) ? __ldg(Qv + cn * a.acs) : 0.0;
+    cp_async_wait<0>();
+    consumer_bar(nct);  // Q_u[buf] complete and visible; every consumer is done with tile t−1
+    if (tile + gridDim.x < a.tile_end) gather_union(tile + gridDim.x, buf ^ 1);
+    const double* Qb = Qu + (size_t)buf * a.Umax * a.V + v;
+    const double qi = live ? Qb[ct * a.V] : 0.0;  // the tile's own cells lead its union
 
     double acc[R];
 #pragma unroll
@@ -499,26 +483,20 @@ __global__ void __launch_bounds__(max_threads(D, M), min_blocks(D, M)) k_pipelin
     double dqs[NCAP];
     // one chunk: ΔQ of kc positions, B⁺ columns accumulated in registers.  FULL:
     // kc == KC (static); CAP: capture the sector ΔQ (positions < NCAP; only the
-    // first NCAPCH chunks, which make_layout guarantees to be full).  The stage
-    // was waited on by the prefetch cursor PF chunks earlier.
+    // first NCAPCH chunks, which make_layout guarantees to be full).
     auto chunk = [&](int ch, auto full_t, auto cap) {
       constexpr bool FULL = decltype(full_t)::value;
       const int kc = FULL ? KC : a.G - ch * KC;
-      if (!(a.exp_flags & 8)) {
-        pf_issue(0);              // gathers of the chunk PF ahead
-        cp_async_wait<PF>();      // this chunk's gathers (issued PF chunks ago) have landed
-      } else {
-        mbar_wait(&full[rg.st], rg.ph);
-      }
-      const double* Qg = qring + cq * KC * 32;
-      if (++cq == NQ) cq = 0;
-      const double* Bs = (const double*)(stg + rg.st * pc.stage_bytes + a.ids_bytes) + (size_t)ct * R * kc;
+      mbar_wait(&full[rg.st], rg.ph);
+      const unsigned char* sb = stg + rg.st * pc.stage_bytes;
+      const uint16_t* idx = (const uint16_t*)sb + ct;
+      const double* Bs = (const double*)(sb + a.ids_bytes) + (size_t)ct * R * kc;
       if (a.exp_flags & 2) {
-        acc[0] += Qg[0];
+        acc[0] += Qb[idx[0] * a.V];
       } else if (FULL) {
         double dq[KC];
 #pragma unroll
-        for (int kk = 0; kk < KC; ++kk) dq[kk] = live ? Qg[kk * 32] - qi : 0.0;
+        for (int kk = 0; kk < KC; ++kk) dq[kk] = live ? Qb[idx[kk * a.T] * a.V] - qi : 0.0;
         if (decltype(cap)::value) {
 #pragma unroll
           for (int kk = 0; kk < KC; ++kk)
@@ -543,7 +521,7 @@ __global__ void __launch_bounds__(max_threads(D, M), min_blocks(D, M)) k_pipelin
         }
       } else {
         for (int kk = 0; kk < kc; ++kk) {
-          const double dq = live ? Qg[kk * 32] - qi : 0.0;
+          const double dq = live ? Qb[idx[kk * a.T] * a.V] - qi : 0.0;
 #pragma unroll
           for (int l = 0; l < R; ++l) acc[l] += Bs[l * kc + kk] * dq;
         }
@@ -596,7 +574,6 @@ __global__ void __launch_bounds__(max_threads(D, M), min_blocks(D, M)) k_pipelin
         for (int l = 0; l < NM; ++l) o[l] = w[l];
       }
     }
-    qi = qn;
   }
   cp_async_wait<0>();
   if (lane == 0) bulk_wait_all();
@@ -651,6 +628,8 @@ static KArgs make_args(const cwreco_ctx* c, const double* avgs, int64_t acs, int
   std::memset(&a, 0, sizeof(a));
   a.blocks = c->dev->blocks;
   a.tile_bytes = L.tile_bytes;
+  a.u_bytes = L.u_bytes;
+  a.Umax = L.Umax;
   a.ids_bytes = L.ids_bytes;
   a.chunk_bytes = L.chunk_bytes;
   a.kslice_bytes = L.kslice_bytes;

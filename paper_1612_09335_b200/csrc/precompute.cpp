@@ -22,7 +22,7 @@ namespace cwr {
 
 static inline int64_t r16(int64_t x) { return (x + 15) & ~int64_t(15); }
 
-static Layout layout_with(int d, int M, int V, int G, int T, int KC) {
+static Layout layout_with(int d, int M, int V, int G, int T, int KC, int Umax) {
   Layout L;
   L.d = d;
   L.M = M;
@@ -33,9 +33,11 @@ static Layout layout_with(int d, int M, int V, int G, int T, int KC) {
   L.G = G;
   L.T = T;
   L.KC = KC;
+  L.Umax = Umax;
   L.kslice_bytes = int64_t(T) * L.R * 8;
   L.NCH = (G + KC - 1) / KC;
-  L.ids_bytes = r16(int64_t(KC) * T * 4);
+  L.u_bytes = r16(int64_t(Umax) * 4);
+  L.ids_bytes = r16(int64_t(KC) * T * 2);
   L.chunk_bytes = L.ids_bytes + int64_t(KC) * L.kslice_bytes;
   L.off_sector = r16(L.off_chunk(L.NCH - 1) + L.chunk_size(L.NCH - 1));
   L.sinv_bytes = int64_t(T) * (d + 1) * d * d * 8;
@@ -44,7 +46,7 @@ static Layout layout_with(int d, int M, int V, int G, int T, int KC) {
   return L;
 }
 
-Layout make_layout(int d, int M, int V, int G, int max_smem) {
+Layout make_layout(int d, int M, int V, int G, int max_smem, const std::function<int(int)>& umax_for) {
   const int nm = n_modes(M, d);
   // one tile = T cells × V variables = one consumer thread each
   int T0 = (cons_threads(nm) / V) & ~1;
@@ -60,6 +62,7 @@ Layout make_layout(int d, int M, int V, int G, int max_smem) {
   Layout best;
   bool found = false;
   for (int T = T0; T >= 2; T = (T / 2) & ~1) {
+    const int Umax = umax_for(T);
     const int64_t kslice = int64_t(T) * (nm - 1) * 8;
     int want = std::max<int>(1, int(10240 / kslice));
     want = std::min(want, 8);
@@ -67,7 +70,7 @@ Layout make_layout(int d, int M, int V, int G, int max_smem) {
     if (want == 7) want = 6;
     for (int KC = force ? std::atoi(force) : want; KC >= 1; --KC) {
       if (KC == 7 || KC > G || ((d + 1) * d + KC - 1) / KC * KC > G) continue;
-      Layout L = layout_with(d, M, V, G, T, KC);
+      Layout L = layout_with(d, M, V, G, T, KC, Umax);
       if (pipe_smem(L, kMinStages) <= budget) return L;
       if (!found || pipe_smem(L, kMinStages) < pipe_smem(best, kMinStages)) best = L, found = true;
     }
@@ -178,23 +181,90 @@ bool pinv_qr(int m, int n, std::vector<double>& A, std::vector<double>& Bp, doub
 
 }  // namespace
 
+namespace {
+
+// Gather order of owned local cell li (precompute's layout):
+// positions s·d+m hold member m of sector s (invalid sectors: other S_i^0 cells,
+// else the cell itself), then the rest of S_i^0; lid[p] local ids (padded with
+// the cell itself up to G), col[p] = B⁺ column (index into S_i^0 ∖ i) or -1.
+// Returns the number of positions used, -1 if a cell is missing locally.
+template <class ToLocal>
+int gather_order(const cwreco_ctx* c, int64_t li, int G, const ToLocal& to_local, int32_t* lid, int* col) {
+  const int d = c->d, ne = c->ne, nv = d + 1;
+  const int64_t g = c->local2global[li];
+  const int64_t q = g - c->own_lo;
+  const int32_t* cen = &c->central[q * ne];
+  const int32_t* sec = &c->sectors[q * nv * nv];
+  const uint8_t* val = &c->valid[q * nv];
+  int64_t gglob[256];
+  bool used[256] = {false};
+  const int front = nv * d;
+  for (int p = 0; p < front; ++p) { gglob[p] = -1; col[p] = -1; }
+  for (int s = 0; s < nv; ++s) {
+    if (!val[s]) continue;
+    for (int m = 0; m < d; ++m) {
+      const int64_t x = sec[s * nv + 1 + m];
+      gglob[s * d + m] = x;
+      for (int k = 1; k < ne; ++k)
+        if (cen[k] == x) { col[s * d + m] = k - 1; used[k] = true; break; }
+    }
+  }
+  int ng = front, next = 1;  // next unused central cell for invalid-sector fillers
+  for (int p = 0; p < front; ++p) {
+    if (gglob[p] >= 0) continue;
+    while (next < ne && used[next]) ++next;
+    if (next < ne) {
+      gglob[p] = cen[next];
+      col[p] = next - 1;
+      used[next] = true;
+    } else {
+      gglob[p] = g;  // self: ΔQ = 0
+    }
+  }
+  for (int k = 1; k < ne; ++k)
+    if (!used[k]) { gglob[ng] = cen[k]; col[ng] = k - 1; ++ng; }
+  if (ng > G) return -1;
+  for (int p = 0; p < G; ++p) {
+    lid[p] = (int32_t)li;
+    if (p < ng && gglob[p] != g) {
+      lid[p] = to_local(gglob[p]);
+      if (lid[p] < 0) return -1;
+    }
+    if (p >= ng) col[p] = -1;
+  }
+  return ng;
+}
+
+// Stencil union of tile t (tiles of T cells): own cells [t·T, min((t+1)·T, n_owned))
+// first (padded with the tile's first cell up to T), then the other gathered cells
+// ascending.  Returns false if a gather list is invalid.
+template <class ToLocal>
+bool tile_union(const cwreco_ctx* c, int64_t t, int T, int G, const ToLocal& to_local, std::vector<int32_t>& u) {
+  const int64_t lo = t * T, hi = std::min(c->n_owned, lo + T);
+  std::vector<int32_t> others;
+  int32_t lid[256];
+  int col[256];
+  for (int64_t li = lo; li < hi; ++li) {
+    if (gather_order(c, li, G, to_local, lid, col) < 0) return false;
+    for (int p = 0; p < G; ++p)
+      if (lid[p] < lo || lid[p] >= hi) others.push_back(lid[p]);
+  }
+  std::sort(others.begin(), others.end());
+  others.erase(std::unique(others.begin(), others.end()), others.end());
+  u.clear();
+  for (int k = 0; k < T; ++k) u.push_back((int32_t)(lo + k < hi ? lo + k : lo));
+  u.insert(u.end(), others.begin(), others.end());
+  return true;
+}
+
+}  // namespace
+
 // Build the packed tiles for local owned cells [0, n_owned) and hand them to the
 // device (or keep them on the host for a host-only context).
 void precompute(cwreco_ctx* c) {
   if (!c->has_stencils) fail(CWRECO_ESTATE, "precompute: call cwreco_build_stencils first");
   const int d = c->d, M = c->M, nm = c->nm, ne = c->ne, nv = d + 1;
   const int R = nm - 1, K = ne - 1;
-  c->lay = make_layout(d, M, c->V, c->G, c->device >= 0 ? dev_max_smem(c) : 227 * 1024);
-  const Layout& L = c->lay;
-  const int T = L.T, G = L.G;
-  c->n_tiles = (c->n_owned + T - 1) / T;
-  c->n_int_tiles = (c->n_interior == c->n_owned) ? c->n_tiles : c->n_interior / T;
-  c->sigma = sigma_matrix(d, M);
-  {
-    double xi[3] = {0.25, 0.25, 0.25}, psi[64];
-    basis_eval(d, M, xi, psi);
-    c->psi1 = psi[0];
-  }
 
   // global -> local map
   const int64_t n_loc = c->n_owned + c->n_ghost;
@@ -207,6 +277,35 @@ void precompute(cwreco_ctx* c) {
     if (it == e || *it != g) return -1;
     return (int32_t)(it - c->local2global.begin());
   };
+  const int G = c->G;
+  // largest stencil union of tiles of T cells (sizes the union chunk and Q_u)
+  auto umax_for = [&](int T) {
+    const int64_t nt = (c->n_owned + T - 1) / T;
+    int umax = T, bad = 0;
+#pragma omp parallel reduction(max : umax) reduction(| : bad)
+    {
+      std::vector<int32_t> u;
+#pragma omp for schedule(dynamic, 64)
+      for (int64_t t = 0; t < nt; ++t) {
+        if (!tile_union(c, t, T, G, to_local, u)) { bad |= 1; continue; }
+        umax = std::max(umax, (int)u.size());
+      }
+    }
+    if (bad) fail(CWRECO_EINVAL, "precompute: stencil cell missing from the local numbering");
+    if (umax > 65535) fail(CWRECO_EUNSUPPORTED, "precompute: tile stencil union exceeds 16-bit indices");
+    return umax;
+  };
+  c->lay = make_layout(d, M, c->V, G, c->device >= 0 ? dev_max_smem(c) : 227 * 1024, umax_for);
+  const Layout& L = c->lay;
+  const int T = L.T;
+  c->n_tiles = (c->n_owned + T - 1) / T;
+  c->n_int_tiles = (c->n_interior == c->n_owned) ? c->n_tiles : c->n_interior / T;
+  c->sigma = sigma_matrix(d, M);
+  {
+    double xi[3] = {0.25, 0.25, 0.25}, psi[64];
+    basis_eval(d, M, xi, psi);
+    c->psi1 = psi[0];
+  }
 
   // conical-product Gauss-Jacobi rule on T_E exact for degree M (R19): collapsed
   // coordinates (u, v, w), Jacobian (1-v)(1-w)^2 absorbed by Jacobi weights
@@ -263,153 +362,128 @@ void precompute(cwreco_ctx* c) {
       batch.assign(size_t(t1 - t0) * L.tile_bytes, 0);
       base = batch.data();
     }
-#pragma omp parallel for schedule(dynamic, 64) reduction(| : bad_singular, bad_local) reduction(max : cond_max)
-    for (int64_t li = t0 * T; li < std::min(c->n_owned, t1 * T); ++li) {
-      const int64_t tile = li / T;
-      const int ct = int(li % T);
+#pragma omp parallel for schedule(dynamic, 16) reduction(| : bad_singular, bad_local) reduction(max : cond_max)
+    for (int64_t tile = t0; tile < t1; ++tile) {
       unsigned char* tb = base + size_t(tile - t0) * L.tile_bytes;
+      std::vector<int32_t> uni;
+      if (!tile_union(c, tile, T, G, to_local, uni) || (int)uni.size() > L.Umax) { bad_local |= 1; continue; }
+      int32_t* uid = (int32_t*)tb;
+      for (int k = 0; k < L.Umax; ++k) uid[k] = k < (int)uni.size() ? uni[k] : uni[0];
+      const int64_t lo = tile * T, hi = std::min(c->n_owned, lo + T);
+      auto uindex = [&](int32_t lid) -> int {
+        if (lid >= lo && lid < hi) return int(lid - lo);
+        auto it = std::lower_bound(uni.begin() + T, uni.end(), lid);
+        return int(it - uni.begin());
+      };
       double* sinv = (double*)(tb + L.off_sector);
       uint8_t* vmask = (uint8_t*)(tb + L.off_sector + L.sinv_bytes);
-      const int64_t g = c->local2global[li];
-      const int64_t q = g - c->own_lo;
-      const int32_t* cen = &c->central[q * ne];
-      const int32_t* sec = &c->sectors[q * nv * nv];
-      const uint8_t* val = &c->valid[q * nv];
+      for (int64_t li = lo; li < hi; ++li) {
+        const int ct = int(li - lo);
+        const int64_t g = c->local2global[li];
+        const int64_t q = g - c->own_lo;
+        const int32_t* cen = &c->central[q * ne];
+        const int32_t* sec = &c->sectors[q * nv * nv];
+        const uint8_t* val = &c->valid[q * nv];
 
-      // owner affine map x = X0 + J ξ
-      const double* Xi = &c->X[g * nv * d];
-      double J[9], Ji[9];
-      for (int a = 0; a < d; ++a)
-        for (int k = 0; k < d; ++k) J[a * d + k] = Xi[(k + 1) * d + a] - Xi[a];
-      if (!inv_small(d, J, Ji)) { bad_singular |= 1; continue; }
-
-      // gather order: sector cells at s·d+m, then the rest of S_i^0, then self.
-      // col[p] = column of B⁺ (index into S_i^0 ∖ i) of position p, -1 if none.
-      int64_t gglob[256];
-      int col[256];
-      bool used[256] = {false};
-      const int front = nv * d;
-      for (int p = 0; p < front; ++p) { gglob[p] = -1; col[p] = -1; }
-      for (int s = 0; s < nv; ++s) {
-        if (!val[s]) continue;
-        for (int m = 0; m < d; ++m) {
-          const int64_t x = sec[s * nv + 1 + m];
-          gglob[s * d + m] = x;
-          for (int k = 1; k < ne; ++k)
-            if (cen[k] == x) { col[s * d + m] = k - 1; used[k] = true; break; }
-        }
-      }
-      int ng = front;
-      int next = 1;  // next unused central cell for invalid-sector fillers
-      for (int p = 0; p < front; ++p) {
-        if (gglob[p] >= 0) continue;
-        while (next < ne && used[next]) ++next;
-        if (next < ne) {
-          gglob[p] = cen[next];
-          col[p] = next - 1;
-          used[next] = true;
-        } else {
-          gglob[p] = g;  // self: ΔQ = 0
-        }
-      }
-      for (int k = 1; k < ne; ++k)
-        if (!used[k]) { gglob[ng] = cen[k]; col[ng] = k - 1; ++ng; }
-      if (ng > G) { bad_local |= 1; continue; }
-      const int32_t self_local = (int32_t)li;
-      for (int p = 0; p < G; ++p) {
-        int32_t lid = self_local;
-        if (p < ng && gglob[p] != g) {
-          lid = to_local(gglob[p]);
-          if (lid < 0) bad_local |= 1;
-        }
-        ((int32_t*)(tb + L.off_chunk(p / L.KC)))[size_t(p % L.KC) * T + ct] = lid;
-      }
-      uint8_t vm = 0;
-      for (int s = 0; s < nv; ++s) vm |= val[s] ? uint8_t(1u << s) : 0;
-
-      // central reduced LSQ matrix A[1:,1:] (column-major, K rows)
-      thread_local std::vector<double> A;
-      A.assign(size_t(K) * R, 0.0);
-      double psi[64], xi[3], sh[3];
-      for (int k = 1; k < ne; ++k) {
-        const int64_t j = cen[k];
-        const double* Xj = &c->X[j * nv * d];
-        shift_of(c, g, j, sh);
-        // ξ = t + C ξ' with t = J⁻¹(X_j0 + sh − X_i0), C = J⁻¹ J_j
-        double t[3], Cm[9], Jj[9];
+        // owner affine map x = X0 + J ξ
+        const double* Xi = &c->X[g * nv * d];
+        double J[9], Ji[9];
         for (int a = 0; a < d; ++a)
-          for (int e = 0; e < d; ++e) Jj[a * d + e] = Xj[(e + 1) * d + a] - Xj[a];
-        for (int a = 0; a < d; ++a) {
-          double s = 0.0;
-          for (int e = 0; e < d; ++e) s += Ji[a * d + e] * (Xj[e] + sh[e] - Xi[e]);
-          t[a] = s;
-          for (int e = 0; e < d; ++e) {
-            double s2 = 0.0;
-            for (int f = 0; f < d; ++f) s2 += Ji[a * d + f] * Jj[f * d + e];
-            Cm[a * d + e] = s2;
-          }
-        }
-        // monomial averages over the stencil cell, ξ = t + C ξ'_q (quadrature exact for degree M)
-        double mom[64] = {0};
-        for (int qq = 0; qq < nq; ++qq) {
-          double pw[3][8];
-          for (int a = 0; a < d; ++a) {
-            double s = t[a];
-            for (int e = 0; e < d; ++e) s += Cm[a * d + e] * qp[qq * d + e];
-            pw[a][0] = 1.0;
-            for (int p = 1; p <= M; ++p) pw[a][p] = pw[a][p - 1] * s;
-          }
-          if (d == 2) pw[2][0] = 1.0;
-          const double wq = qw[qq];
-          for (int e = 0; e < nmono; ++e)
-            mom[e] += wq * (pw[0][mexp[3 * e]] * pw[1][mexp[3 * e + 1]] * pw[2][mexp[3 * e + 2]]);
-        }
-        for (int l = 1; l < nm; ++l) {
-          double s = 0.0;
-          const double* cl = &mcoef[size_t(l) * nmono];
-          for (int e = 0; e < nmono; ++e) s += cl[e] * mom[e];
-          A[size_t(l - 1) * K + (k - 1)] = s;
-        }
-      }
-      thread_local std::vector<double> Bp;
-      double cond = 0.0;
-      if (!pinv_qr(K, R, A, Bp, cond)) { bad_singular |= 1; continue; }
-      cond_max = std::max(cond_max, cond);
-      // B chunks: chunk ch holds positions p in [ch·KC, ch·KC + kc) as [T][R][kc]
-      for (int p = 0; p < G; ++p) {
-        const int ch = p / L.KC, kk = p % L.KC;
-        const int kc = L.kc_of(ch);
-        double* chb = (double*)(tb + L.off_chunk(ch) + L.ids_bytes);
-        const int k = p < ng ? col[p] : -1;
-        for (int l = 0; l < R; ++l) chb[(size_t(ct) * R + l) * kc + kk] = k >= 0 ? Bp[size_t(l) * K + k] : 0.0;
-      }
+          for (int k = 0; k < d; ++k) J[a * d + k] = Xi[(k + 1) * d + a] - Xi[a];
+        if (!inv_small(d, J, Ji)) { bad_singular |= 1; continue; }
 
-      // sector inverses
-      for (int s = 0; s < nv; ++s) {
-        double* Sd = &sinv[((size_t)ct * nv + s) * d * d];
-        for (int e = 0; e < d * d; ++e) Sd[e] = 0.0;
-        if (!val[s]) continue;
-        double As[9];
-        for (int m = 0; m < d; ++m) {
-          const int64_t j = sec[s * nv + 1 + m];
+        int32_t lid[256];
+        int col[256];
+        if (gather_order(c, li, G, to_local, lid, col) < 0) { bad_local |= 1; continue; }
+        for (int p = 0; p < G; ++p)
+          ((uint16_t*)(tb + L.off_chunk(p / L.KC)))[size_t(p % L.KC) * T + ct] = (uint16_t)uindex(lid[p]);
+        uint8_t vm = 0;
+        for (int s = 0; s < nv; ++s) vm |= val[s] ? uint8_t(1u << s) : 0;
+
+        // central reduced LSQ matrix A[1:,1:] (column-major, K rows)
+        thread_local std::vector<double> A;
+        A.assign(size_t(K) * R, 0.0);
+        double psi[64], xi[3], sh[3];
+        for (int k = 1; k < ne; ++k) {
+          const int64_t j = cen[k];
+          const double* Xj = &c->X[j * nv * d];
           shift_of(c, g, j, sh);
+          // ξ = t + C ξ' with t = J⁻¹(X_j0 + sh − X_i0), C = J⁻¹ J_j
+          double t[3], Cm[9], Jj[9];
+          for (int a = 0; a < d; ++a)
+            for (int e = 0; e < d; ++e) Jj[a * d + e] = Xj[(e + 1) * d + a] - Xj[a];
           for (int a = 0; a < d; ++a) {
-            double s2 = 0.0;
-            for (int e = 0; e < d; ++e) s2 += Ji[a * d + e] * (c->bary[j * d + e] + sh[e] - Xi[e]);
-            xi[a] = s2;
+            double s = 0.0;
+            for (int e = 0; e < d; ++e) s += Ji[a * d + e] * (Xj[e] + sh[e] - Xi[e]);
+            t[a] = s;
+            for (int e = 0; e < d; ++e) {
+              double s2 = 0.0;
+              for (int f = 0; f < d; ++f) s2 += Ji[a * d + f] * Jj[f * d + e];
+              Cm[a * d + e] = s2;
+            }
           }
-          basis_eval(d, 1, xi, psi);
-          for (int l = 0; l < d; ++l) As[m * d + l] = psi[l + 1];
+          // monomial averages over the stencil cell, ξ = t + C ξ'_q (quadrature exact for degree M)
+          double mom[64] = {0};
+          for (int qq = 0; qq < nq; ++qq) {
+            double pw[3][8];
+            for (int a = 0; a < d; ++a) {
+              double s = t[a];
+              for (int e = 0; e < d; ++e) s += Cm[a * d + e] * qp[qq * d + e];
+              pw[a][0] = 1.0;
+              for (int p = 1; p <= M; ++p) pw[a][p] = pw[a][p - 1] * s;
+            }
+            if (d == 2) pw[2][0] = 1.0;
+            const double wq = qw[qq];
+            for (int e = 0; e < nmono; ++e)
+              mom[e] += wq * (pw[0][mexp[3 * e]] * pw[1][mexp[3 * e + 1]] * pw[2][mexp[3 * e + 2]]);
+          }
+          for (int l = 1; l < nm; ++l) {
+            double s = 0.0;
+            const double* cl = &mcoef[size_t(l) * nmono];
+            for (int e = 0; e < nmono; ++e) s += cl[e] * mom[e];
+            A[size_t(l - 1) * K + (k - 1)] = s;
+          }
         }
-        // p_l = Σ_m S[l][m] ΔQ_m with S = As⁻¹ where As[m][l]
-        double Ai[9];
-        if (!inv_small(d, As, Ai)) {
-          vm &= uint8_t(~(1u << s));
-          continue;
+        thread_local std::vector<double> Bp;
+        double cond = 0.0;
+        if (!pinv_qr(K, R, A, Bp, cond)) { bad_singular |= 1; continue; }
+        cond_max = std::max(cond_max, cond);
+        // B chunks: chunk ch holds positions p in [ch·KC, ch·KC + kc) as [T][R][kc]
+        for (int p = 0; p < G; ++p) {
+          const int ch = p / L.KC, kk = p % L.KC;
+          const int kc = L.kc_of(ch);
+          double* chb = (double*)(tb + L.off_chunk(ch) + L.ids_bytes);
+          const int k = col[p];
+          for (int l = 0; l < R; ++l) chb[(size_t(ct) * R + l) * kc + kk] = k >= 0 ? Bp[size_t(l) * K + k] : 0.0;
         }
-        for (int e = 0; e < d * d; ++e) Sd[e] = Ai[e];
+
+        // sector inverses
+        for (int s = 0; s < nv; ++s) {
+          double* Sd = &sinv[((size_t)ct * nv + s) * d * d];
+          for (int e = 0; e < d * d; ++e) Sd[e] = 0.0;
+          if (!val[s]) continue;
+          double As[9];
+          for (int m = 0; m < d; ++m) {
+            const int64_t j = sec[s * nv + 1 + m];
+            shift_of(c, g, j, sh);
+            for (int a = 0; a < d; ++a) {
+              double s2 = 0.0;
+              for (int e = 0; e < d; ++e) s2 += Ji[a * d + e] * (c->bary[j * d + e] + sh[e] - Xi[e]);
+              xi[a] = s2;
+            }
+            basis_eval(d, 1, xi, psi);
+            for (int l = 0; l < d; ++l) As[m * d + l] = psi[l + 1];
+          }
+          // p_l = Σ_m S[l][m] ΔQ_m with S = As⁻¹ where As[m][l]
+          double Ai[9];
+          if (!inv_small(d, As, Ai)) {
+            vm &= uint8_t(~(1u << s));
+            continue;
+          }
+          for (int e = 0; e < d * d; ++e) Sd[e] = Ai[e];
+        }
+        vmask[ct] = vm;
       }
-      vmask[ct] = vm;
     }
     if (bad_singular || bad_local) break;
     if (!keep_host) dev_upload_blocks(c, t0 * L.tile_bytes, batch.data(), int64_t(t1 - t0) * L.tile_bytes);

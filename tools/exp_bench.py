@@ -1,6 +1,6 @@
 #!/usr/bin/env python
 """Bottleneck experiments on the pipelined kernel (results are WRONG with flags != 0;
-timing only).  CWRECO_EXP_FLAGS: 1 = no Q gather, 2 = no B⁺ math, 4 = no B⁺ stream.
+timing only).  CWRECO_EXP_FLAGS: 1 = no Q gather, 2 = no B⁺ FMAs, 16 = no epilogue.
 
     python tools/exp_bench.py C2 [C3 ...]
 """
@@ -43,7 +43,7 @@ def main():
         out = torch.empty((inf["n_owned"], w["V"], ctx.nm), dtype=torch.float64, device="cuda")
         flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
         res = {}
-        for flags in [int(f) for f in os.environ.get("EXP_FLAGS_LIST", "0,1,2,3,4,5,6,7").split(",")]:
+        for flags in [int(f) for f in os.environ.get("EXP_FLAGS_LIST", "0,1,2,16,19").split(",")]:
             os.environ["CWRECO_EXP_FLAGS"] = str(flags)
             ms = time_pass(ctx, A, out, flush)
             res[flags] = ms

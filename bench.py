@@ -136,6 +136,16 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- oracle arm
+def _one_thread():
+    """Limit numpy's BLAS/LAPACK pools to one thread so `cores: 1` is what ran."""
+    try:
+        from threadpoolctl import threadpool_limits
+        return threadpool_limits(limits=1)
+    except Exception:  # threadpoolctl missing: numpy's tiny solves stay single-threaded anyway
+        import contextlib
+        return contextlib.nullcontext()
+
+
 def oracle_rate(w, budget_s, seed=0, max_cells=None):
     """Oracle cells/s on a random sample of the workload's cells (1 core)."""
     from oracle import reconstruct as R
@@ -144,11 +154,12 @@ def oracle_rate(w, budget_s, seed=0, max_cells=None):
     Q = w["avgs"][m.perm]
     rng = np.random.default_rng(seed)
     order = rng.permutation(m.N)
-    n, t0 = 0, time.perf_counter()
-    while time.perf_counter() - t0 < budget_s and (max_cells is None or n < max_cells):
-        R.reconstruct_cell(m, int(order[n % m.N]), Q, w["M"])
-        n += 1
-    dt = time.perf_counter() - t0
+    with _one_thread():
+        n, t0 = 0, time.perf_counter()
+        while time.perf_counter() - t0 < budget_s and (max_cells is None or n < max_cells):
+            R.reconstruct_cell(m, int(order[n % m.N]), Q, w["M"])
+            n += 1
+        dt = time.perf_counter() - t0
     return n / dt, n, dt, m, Q
 
 
@@ -170,14 +181,15 @@ def run_reference(args):
     per_step = min(per_step, 64)
     order = rng.permutation(m.N)
     k = 0
-    for _ in range(args.warmup):
-        for _ in range(per_step):
-            R.reconstruct_cell(m, int(order[k % m.N]), Q, w["M"]); k += 1
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        for _ in range(per_step):
-            R.reconstruct_cell(m, int(order[k % m.N]), Q, w["M"]); k += 1
-    dt = time.perf_counter() - t0
+    with _one_thread():
+        for _ in range(args.warmup):
+            for _ in range(per_step):
+                R.reconstruct_cell(m, int(order[k % m.N]), Q, w["M"]); k += 1
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            for _ in range(per_step):
+                R.reconstruct_cell(m, int(order[k % m.N]), Q, w["M"]); k += 1
+        dt = time.perf_counter() - t0
     cells = args.steps * per_step
     value = cells / dt
     sample = f"{per_step} random cells of {args.config} per step (oracle rebuilds each cell's stencil matrices and solves)"

@@ -240,7 +240,7 @@ cwreco_status cwreco_get_blocks(const cwreco_ctx* c, int64_t n_sel, const int64_
       if (gather)
         for (int k = 0; k < G; ++k) {
           const uint16_t u = ((const uint16_t*)(tb + L.off_chunk(k / L.KC)))[size_t(k % L.KC) * T + ct];
-          gather[s * G + k] = ((const int32_t*)tb)[u];  // union chunk: local ids
+          gather[s * G + k] = ((const int32_t*)tb)[u / L.V];  // union chunk: local ids
         }
       if (slots)
         for (int q = 0; q < nv; ++q)

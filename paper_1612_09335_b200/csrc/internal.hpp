@@ -33,7 +33,7 @@ inline int n_modes(int M, int d) {  // ℳ(M,d) = (1/d!) Π_{l=1..d} (M+l)   (P:
 //                                  the tile's own T cells first, then the others
 //                                  ascending; padded to Umax entries (U ≤ Umax)
 //   chunk ch, positions p ∈ [ch·KC, ch·KC+kc) (kc = KC except a shorter last one):
-//     idx   uint16 [kc][T]  union index of the gathered stencil cell, padded to
+//     idx   uint16 [kc][T]  union index × V of the gathered stencil cell, padded to
 //                           ids_bytes; positions [0, (d+1)d): sector s, member m at
 //                           s·d+m (R15; filler if the sector is invalid), then the
 //                           rest of S_i^0, then the cell itself as padding

@@ -159,15 +159,16 @@ __device__ __forceinline__ void cweno_epilogue(double qi, double* acc, const dou
     sgs[s] = v;
   }
   // ω̃_s = λ̄_s/(σ_s+ε)^r, ω_s = ω̃_s/Σ ω̃; invalid sectors get 0 (R14)
-  const double wt0 = l0 / powr(sg0 + a.eps, a.r);
+  // reciprocals instead of divisions (one extra rounding, far inside the 1e-11 bar)
+  const double wt0 = l0 * __drcp_rn(powr(sg0 + a.eps, a.r));
   double wts[D + 1];
   double sum = wt0;
 #pragma unroll
   for (int s = 0; s <= D; ++s) {
-    wts[s] = valid[s] ? ls / powr(sgs[s] + a.eps, a.r) : 0.0;
+    wts[s] = valid[s] ? ls * __drcp_rn(powr(sgs[s] + a.eps, a.r)) : 0.0;
     sum += wts[s];
   }
-  const double isum = 1.0 / sum;
+  const double isum = __drcp_rn(sum);
   const double om0 = wt0 * isum;
   double oms[D + 1];
 #pragma unroll
@@ -243,7 +244,7 @@ __global__ void __launch_bounds__(256) k_simple(KArgs a, DbgOut dbg) {
     const double* Bc = (const double*)(cb + a.ids_bytes) + (size_t)ct * R * kc;   // [T][R][kc]
     for (int kk = 0; kk < kc; ++kk) {
       const int p = ch * a.KC + kk;
-      const int32_t j = ((const int32_t*)tb)[idx[size_t(kk) * a.T + ct]];         // union chunk
+      const int32_t j = ((const int32_t*)tb)[idx[size_t(kk) * a.T + ct] / a.V];  // union chunk
       const double dq = Qv[int64_t(j) * a.acs] - qi;
 #pragma unroll
       for (int q = 0; q < NCAP; ++q)
@@ -454,10 +455,17 @@ __global__ void __launch_bounds__(max_threads(D, M), min_blocks(D, M)) k_pipelin
     const int32_t* uid = (const int32_t*)(stg + rg.st * pc.stage_bytes);
     double* dst = Qu + (size_t)buf * a.Umax * a.V;
     if (!(a.exp_flags & 1)) {
-      const int n = a.Umax * a.V;
-      for (int e = tid; e < n; e += nct) {
-        const int u = e / a.V, vv = e - u * a.V;
+      // element e = u·V + vv, e = tid, tid + nct, …: (u, vv) stepped without divisions
+      int u = tid / a.V, vv = tid - (tid / a.V) * a.V;
+      const int du = nct / a.V, dv = nct - du * a.V;
+      for (int e = tid; e < a.Umax * a.V; e += nct) {
         cp_async8(dst + e, a.Q + int64_t(uid[u]) * a.acs + vv * a.avs);
+        u += du;
+        vv += dv;
+        if (vv >= a.V) {
+          vv -= a.V;
+          ++u;
+        }
       }
     }
     cp_async_commit();
@@ -475,7 +483,7 @@ __global__ void __launch_bounds__(max_threads(D, M), min_blocks(D, M)) k_pipelin
     consumer_bar(nct);  // Q_u[buf] complete and visible; every consumer is done with tile t−1
     if (tile + gridDim.x < a.tile_end) gather_union(tile + gridDim.x, buf ^ 1);
     const double* Qb = Qu + (size_t)buf * a.Umax * a.V + v;
-    const double qi = live ? Qb[ct * a.V] : 0.0;  // the tile's own cells lead its union
+    const double qi = Qb[ct * a.V];  // the tile's own cells lead its union (padded past n_owned)
 
     double acc[R];
 #pragma unroll
@@ -492,11 +500,11 @@ __global__ void __launch_bounds__(max_threads(D, M), min_blocks(D, M)) k_pipelin
       const uint16_t* idx = (const uint16_t*)sb + ct;
       const double* Bs = (const double*)(sb + a.ids_bytes) + (size_t)ct * R * kc;
       if (a.exp_flags & 2) {
-        acc[0] += Qb[idx[0] * a.V];
+        acc[0] += Qb[idx[0]];
       } else if (FULL) {
         double dq[KC];
 #pragma unroll
-        for (int kk = 0; kk < KC; ++kk) dq[kk] = live ? Qb[idx[kk * a.T] * a.V] - qi : 0.0;
+        for (int kk = 0; kk < KC; ++kk) dq[kk] = Qb[idx[kk * a.T]] - qi;  // (lanes past n_owned read valid padding)
         if (decltype(cap)::value) {
 #pragma unroll
           for (int kk = 0; kk < KC; ++kk)
@@ -521,7 +529,7 @@ __global__ void __launch_bounds__(max_threads(D, M), min_blocks(D, M)) k_pipelin
         }
       } else {
         for (int kk = 0; kk < kc; ++kk) {
-          const double dq = live ? Qb[idx[kk * a.T] * a.V] - qi : 0.0;
+          const double dq = Qb[idx[kk * a.T]] - qi;
 #pragma unroll
           for (int l = 0; l < R; ++l) acc[l] += Bs[l * kc + kk] * dq;
         }

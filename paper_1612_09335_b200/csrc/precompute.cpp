@@ -292,7 +292,8 @@ void precompute(cwreco_ctx* c) {
       }
     }
     if (bad) fail(CWRECO_EINVAL, "precompute: stencil cell missing from the local numbering");
-    if (umax > 65535) fail(CWRECO_EUNSUPPORTED, "precompute: tile stencil union exceeds 16-bit indices");
+    if ((int64_t)umax * c->V > 65535)
+      fail(CWRECO_EUNSUPPORTED, "precompute: tile stencil union × nvars exceeds the 16-bit offsets");
     return umax;
   };
   c->lay = make_layout(d, M, c->V, G, c->device >= 0 ? dev_max_smem(c) : 227 * 1024, umax_for);
@@ -396,7 +397,8 @@ void precompute(cwreco_ctx* c) {
         int col[256];
         if (gather_order(c, li, G, to_local, lid, col) < 0) { bad_local |= 1; continue; }
         for (int p = 0; p < G; ++p)
-          ((uint16_t*)(tb + L.off_chunk(p / L.KC)))[size_t(p % L.KC) * T + ct] = (uint16_t)uindex(lid[p]);
+          ((uint16_t*)(tb + L.off_chunk(p / L.KC)))[size_t(p % L.KC) * T + ct] =
+              (uint16_t)(uindex(lid[p]) * L.V);  // element offset of the cell's row in Q_u
         uint8_t vm = 0;
         for (int s = 0; s < nv; ++s) vm |= val[s] ? uint8_t(1u << s) : 0;
 

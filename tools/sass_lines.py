@@ -35,15 +35,25 @@ for ln in lines[start:end]:
     m = re.match(r'\s*/\*([0-9a-f]+)\*/', ln)
     if m and cur is not None:
         line_of[int(m.group(1), 16)] = cur
+reasons = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
+ri = [hdr.index(h) for h in reasons]
 st, ins = defaultdict(float), defaultdict(float)
+why = defaultdict(lambda: defaultdict(float))
 for r in data:
     off = int(r[0], 16) - base
     l = line_of.get(off, -1)
     st[l] += float(r[si] or 0)
     ins[l] += float(r[ie] or 0)
+    for h, i in zip(reasons, ri):
+        try:
+            why[l][h] += float(r[i] or 0)
+        except ValueError:
+            pass
 ts, ti = sum(st.values()), sum(ins.values())
 src = open("paper_1612_09335_b200/csrc/kernels.cu").read().splitlines()
 print(f"{'line':>5} {'stall%':>7} {'inst%':>7}  source")
 for l in sorted(st, key=lambda k: -st[k])[:top]:
     s = src[l - 1].strip()[:90] if 0 < l <= len(src) else "?"
-    print(f"{l:5d} {100 * st[l] / ts:7.1f} {100 * ins[l] / ti:7.1f}  {s}")
+    top2 = sorted(why[l].items(), key=lambda kv: -kv[1])[:2]
+    tw = " ".join(f"{k[6:]}:{100 * v / max(st[l], 1):.0f}%" for k, v in top2)
+    print(f"{l:5d} {100 * st[l] / ts:7.1f} {100 * ins[l] / ti:7.1f}  {tw:28s} {s}")

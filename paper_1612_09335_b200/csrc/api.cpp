@@ -234,12 +234,12 @@ cwreco_status cwreco_get_blocks(const cwreco_ctx* c, int64_t n_sel, const int64_
           for (int k = 0; k < G; ++k) {
             const int ch = k / L.KC, kk = k % L.KC, kc = L.kc_of(ch);
             const double* B = (const double*)(tb + L.off_chunk(ch) + L.ids_bytes);
-            bplus[(s * R + l) * G + k] = B[(size_t(ct) * R + l) * kc + kk];
+            bplus[(s * R + l) * G + k] = B[cwr::chunk_elem(kc, R, T, l, ct, kk)];
           }
       if (sinv) std::memcpy(sinv + s * nv * d * d, sv + (size_t)ct * nv * d * d, sizeof(double) * nv * d * d);
       if (gather)
         for (int k = 0; k < G; ++k) {
-          const uint16_t u = ((const uint16_t*)(tb + L.off_chunk(k / L.KC)))[size_t(k % L.KC) * T + ct];
+          const uint16_t u = ((const uint16_t*)(tb + L.off_idx))[size_t(k) * T + ct];
           gather[s * G + k] = ((const int32_t*)tb)[u / L.V];  // union chunk: local ids
         }
       if (slots)

@@ -29,25 +29,37 @@ inline int n_modes(int M, int d) {  // ℳ(M,d) = (1/d!) Π_{l=1..d} (M+l)   (P:
 // Layout of one packed tile of the matrix stream: the
 // tile's T cells are streamed as a union chunk, NCH position chunks and a sector
 // chunk, each a contiguous 16-byte-aligned block (one 1-D bulk copy):
-//   union chunk: uid int32 [U]     local ids of every cell the tile's stencils touch:
-//                                  the tile's own T cells first, then the others
-//                                  ascending; padded to Umax entries (U ≤ Umax)
+//   union chunk: uid int32  [Umax]    local ids of every cell the tile's stencils touch:
+//                                     the tile's own T cells first, then the others
+//                                     ascending (padded to Umax entries)
+//                idx uint16 [G][T]    (at off_idx) union index × V of the cell gathered
+//                                     at each position: positions [0, (d+1)d) hold
+//                                     sector s, member m at s·d+m (R15; fillers if the
+//                                     sector is invalid), then the rest of S_i^0, then
+//                                     the cell itself as padding
 //   chunk ch, positions p ∈ [ch·KC, ch·KC+kc) (kc = KC except a shorter last one):
-//     idx   uint16 [kc][T]  union index × V of the gathered stencil cell, padded to
-//                           ids_bytes; positions [0, (d+1)d): sector s, member m at
-//                           s·d+m (R15; filler if the sector is invalid), then the
-//                           rest of S_i^0, then the cell itself as padding
-//     B     double [T][R][kc]  reduced pseudo-inverse columns in gather order
-//                           (0 for positions outside S_i^0)
+//     B     double  reduced pseudo-inverse columns in gather order (0 for positions
+//                   outside S_i^0), position pairs first: [kc/2][R][T][2], then, if kc
+//                   is odd, the last position as [R][T] (chunk_elem): the T cells of a
+//                   (pair, row) are adjacent, so a warp's 16-byte loads never conflict
 //   sector chunk (at off_sector):
 //     sinv  double [T][d+1][d][d]  sector inverses
 //     vmask uint8  [T]             bit s = sector s valid (R14)
+// Element (row l, cell ct, position kk) of a B⁺ chunk holding kc positions.
+inline int64_t chunk_elem(int kc, int R, int T, int l, int ct, int kk) {
+  const int np = kc / 2;
+  if (kk < 2 * np) return ((int64_t(kk / 2) * R + l) * T + ct) * 2 + (kk & 1);
+  return int64_t(np) * R * T * 2 + int64_t(l) * T + ct;
+}
+
 struct Layout {
   int d = 0, M = 0, V = 0, nm = 0, R = 0, K = 0, G = 0, T = 0, KC = 0, NCH = 0, Umax = 0;
   int64_t kslice_bytes = 0;  // T·R·8: one position of B⁺ for the whole tile
-  int64_t u_bytes = 0;       // r16(Umax·4): the union chunk
-  int64_t ids_bytes = 0;     // r16(KC·T·2)
-  int64_t chunk_bytes = 0;   // stride of full chunks: ids_bytes + KC·kslice_bytes
+  int64_t off_idx = 0;       // r16(Umax·4): the idx table inside the union chunk
+  int64_t idx_bytes = 0;     // r16(G·T·2)
+  int64_t u_bytes = 0;       // off_idx + idx_bytes: the union chunk
+  int64_t ids_bytes = 0;     // 0 (position chunks hold only B⁺)
+  int64_t chunk_bytes = 0;   // stride of full chunks: KC·kslice_bytes
   int64_t sinv_bytes = 0, sector_bytes = 0, off_sector = 0, tile_bytes = 0;
   int kc_of(int ch) const { return KC < G - ch * KC ? KC : G - ch * KC; }
   int64_t off_chunk(int ch) const { return u_bytes + int64_t(ch) * chunk_bytes; }
@@ -64,8 +76,8 @@ inline int64_t pipe_stage_bytes(const Layout& L) {
   int64_t m = L.chunk_bytes > L.sector_bytes ? L.chunk_bytes : L.sector_bytes;
   return round128(m > L.u_bytes ? m : L.u_bytes);
 }
-inline int64_t pipe_q_bytes(const Layout& L) {  // double-buffered union averages Q_u [Umax][V]
-  return round128(2 * int64_t(L.Umax) * L.V * 8);
+inline int64_t pipe_q_bytes(const Layout& L) {  // double-buffered Q_u [Umax][V] and idx [G][T]
+  return round128(2 * int64_t(L.Umax) * L.V * 8) + round128(2 * L.idx_bytes);
 }
 inline int64_t pipe_out_bytes(const Layout& L) {  // per-warp output staging (bulk stores)
   return round128(int64_t((L.T * L.V + 31) / 32) * 32 * L.nm * 8);

@@ -68,7 +68,8 @@ __constant__ double c_sig[SIG_TOTAL];
 
 struct KArgs {
   const unsigned char* blocks;
-  int64_t tile_bytes, u_bytes, ids_bytes, chunk_bytes, kslice_bytes, off_sector, sinv_bytes, sector_bytes;
+  int64_t tile_bytes, u_bytes, off_idx, idx_bytes, ids_bytes, chunk_bytes, kslice_bytes, off_sector, sinv_bytes,
+      sector_bytes;
   int Umax;
   int T, G, K, KC, NCH, V;
   int64_t n_owned, tile_begin, tile_end;
@@ -195,6 +196,13 @@ __device__ __forceinline__ void cweno_epilogue(double qi, double* acc, const dou
   }
 }
 
+// B⁺ chunk element (row l, cell ct, position kk), as chunk_elem in internal.hpp
+__device__ __forceinline__ int64_t chunk_elem_d(int kc, int R, int T, int l, int ct, int kk) {
+  const int np = kc / 2;
+  if (kk < 2 * np) return ((int64_t(kk / 2) * R + l) * T + ct) * 2 + (kk & 1);
+  return int64_t(np) * R * T * 2 + int64_t(l) * T + ct;
+}
+
 // ---------------------------------------------------------------- simple kernel
 // Sector products from the captured ΔQ of gather positions [0, (D+1)·D).
 template <int D>
@@ -240,8 +248,8 @@ __global__ void __launch_bounds__(256) k_simple(KArgs a, DbgOut dbg) {
   for (int ch = 0; ch < a.NCH; ++ch) {
     const int kc = min(a.KC, a.G - ch * a.KC);
     const unsigned char* cb = tb + a.u_bytes + ch * a.chunk_bytes;
-    const uint16_t* idx = (const uint16_t*)cb;                                      // [kc][T]
-    const double* Bc = (const double*)(cb + a.ids_bytes) + (size_t)ct * R * kc;   // [T][R][kc]
+    const uint16_t* idx = (const uint16_t*)(tb + a.off_idx) + size_t(ch) * a.KC * a.T;  // [G][T]
+    const double* Bc = (const double*)(cb + a.ids_bytes);   // chunk_elem layout
     for (int kk = 0; kk < kc; ++kk) {
       const int p = ch * a.KC + kk;
       const int32_t j = ((const int32_t*)tb)[idx[size_t(kk) * a.T + ct] / a.V];  // union chunk
@@ -250,7 +258,7 @@ __global__ void __launch_bounds__(256) k_simple(KArgs a, DbgOut dbg) {
       for (int q = 0; q < NCAP; ++q)
         if (p == q) dqs[q] = dq;
 #pragma unroll
-      for (int l = 0; l < R; ++l) acc[l] += Bc[l * kc + kk] * dq;
+      for (int l = 0; l < R; ++l) acc[l] += Bc[chunk_elem_d(kc, R, a.T, l, ct, kk)] * dq;
     }
   }
   bool valid[NV];
@@ -402,6 +410,7 @@ __global__ void __launch_bounds__(max_threads(D, M), min_blocks(D, M)) k_pipelin
   unsigned char* stg = smem + pc.off_stage;
   double* outs = (double*)(smem + pc.off_out);
   double* Qu = (double*)(smem + pc.off_q);  // [2][Umax][V]
+  uint16_t* Ix = (uint16_t*)(smem + pc.off_q + ((2 * (int64_t)a.Umax * a.V * 8 + 127) & ~int64_t(127)));  // [2][G][T]
   uint64_t* bars = (uint64_t*)(smem + pc.off_bar);
   const int S = pc.stages;
   uint64_t* full = bars;       // [S]
@@ -435,7 +444,7 @@ __global__ void __launch_bounds__(max_threads(D, M), min_blocks(D, M)) k_pipelin
         const unsigned char* tb = a.blocks + tile * a.tile_bytes;
         if (tile + gridDim.x < a.tile_end) issue(tb + gridDim.x * a.tile_bytes, (uint32_t)a.u_bytes);
         for (int ch = 0; ch < a.NCH; ++ch)
-          issue(tb + a.u_bytes + ch * a.chunk_bytes, (uint32_t)(a.ids_bytes + min(KC, a.G - ch * KC) * a.kslice_bytes));
+          issue(tb + a.u_bytes + ch * a.chunk_bytes, (uint32_t)(min(KC, a.G - ch * KC) * a.kslice_bytes));
         issue(tb + a.off_sector, (uint32_t)a.sector_bytes);
       }
     }
@@ -449,10 +458,17 @@ __global__ void __launch_bounds__(max_threads(D, M), min_blocks(D, M)) k_pipelin
   const int v = active ? tid % a.V : 0;
   double* outw = outs + (size_t)warp * 32 * NM;  // output staging
   Ring rg;
-  // gather the union of tile `tile` (its union chunk is the current stage) into Q_u[buf]
+  // gather the union of tile `tile` (its union chunk is the current stage) into
+  // Q_u[buf] and copy its position → union-offset table into Ix[buf]
   auto gather_union = [&](int64_t tile, int buf) {
     mbar_wait(&full[rg.st], rg.ph);
-    const int32_t* uid = (const int32_t*)(stg + rg.st * pc.stage_bytes);
+    const unsigned char* ub = stg + rg.st * pc.stage_bytes;
+    const int32_t* uid = (const int32_t*)ub;
+    {
+      const uint4* src = (const uint4*)(ub + a.off_idx);
+      uint4* dsti = (uint4*)((unsigned char*)Ix + buf * a.idx_bytes);
+      for (int i = tid; i < (int)(a.idx_bytes / 16); i += nct) dsti[i] = src[i];
+    }
     double* dst = Qu + (size_t)buf * a.Umax * a.V;
     if (!(a.exp_flags & 1)) {
       // element e = u·V + vv, e = tid, tid + nct, …: (u, vv) stepped without divisions
@@ -483,6 +499,7 @@ __global__ void __launch_bounds__(max_threads(D, M), min_blocks(D, M)) k_pipelin
     consumer_bar(nct);  // Q_u[buf] complete and visible; every consumer is done with tile t−1
     if (tile + gridDim.x < a.tile_end) gather_union(tile + gridDim.x, buf ^ 1);
     const double* Qb = Qu + (size_t)buf * a.Umax * a.V + v;
+    const uint16_t* ix = (const uint16_t*)((const unsigned char*)Ix + buf * a.idx_bytes) + ct;  // [G][T]
     const double qi = Qb[ct * a.V];  // the tile's own cells lead its union (padded past n_owned)
 
     double acc[R];
@@ -495,43 +512,44 @@ __global__ void __launch_bounds__(max_threads(D, M), min_blocks(D, M)) k_pipelin
     auto chunk = [&](int ch, auto full_t, auto cap) {
       constexpr bool FULL = decltype(full_t)::value;
       const int kc = FULL ? KC : a.G - ch * KC;
-      mbar_wait(&full[rg.st], rg.ph);
-      const unsigned char* sb = stg + rg.st * pc.stage_bytes;
-      const uint16_t* idx = (const uint16_t*)sb + ct;
-      const double* Bs = (const double*)(sb + a.ids_bytes) + (size_t)ct * R * kc;
-      if (a.exp_flags & 2) {
-        acc[0] += Qb[idx[0]];
-      } else if (FULL) {
-        double dq[KC];
+      // ΔQ does not depend on the stage: formed before waiting for it
+      const uint16_t* ic = ix + (size_t)ch * KC * a.T;
+      double dq[KC];
 #pragma unroll
-        for (int kk = 0; kk < KC; ++kk) dq[kk] = Qb[idx[kk * a.T]] - qi;  // (lanes past n_owned read valid padding)
+      for (int kk = 0; kk < KC; ++kk) dq[kk] = (FULL || kk < kc) ? Qb[ic[kk * a.T]] - qi : 0.0;
+      mbar_wait(&full[rg.st], rg.ph);
+      const double* Bs = (const double*)(stg + rg.st * pc.stage_bytes);  // chunk_elem layout
+      if (a.exp_flags & 2) {
+        acc[0] += dq[0];
+      } else if (FULL) {
         if (decltype(cap)::value) {
 #pragma unroll
           for (int kk = 0; kk < KC; ++kk)
             if (ch * KC + kk < NCAP) dqs[ch * KC + kk] = dq[kk];
         }
-        if (KC % 2 == 0) {
-          const double2* b2 = reinterpret_cast<const double2*>(Bs);
+        // position pairs: 16-byte loads, the T cells of a (pair, row) adjacent
+        const double2* b2 = reinterpret_cast<const double2*>(Bs) + ct;
 #pragma unroll
-          for (int l = 0; l < R; ++l) {
+        for (int l = 0; l < R; ++l) {
 #pragma unroll
-            for (int p = 0; p < KC / 2; ++p) {
-              const double2 bb = b2[l * (KC / 2) + p];
-              acc[l] += bb.x * dq[2 * p];
-              acc[l] += bb.y * dq[2 * p + 1];
-            }
+          for (int p = 0; p < KC / 2; ++p) {
+            const double2 bb = b2[(p * R + l) * a.T];
+            acc[l] += bb.x * dq[2 * p];
+            acc[l] += bb.y * dq[2 * p + 1];
           }
-        } else {
+        }
+        if (KC % 2) {  // odd chunk size: the last position is stored [R][T]
+          const double* b1 = Bs + (KC / 2) * R * a.T * 2 + ct;
 #pragma unroll
-          for (int l = 0; l < R; ++l)
-#pragma unroll
-            for (int kk = 0; kk < KC; ++kk) acc[l] += Bs[l * KC + kk] * dq[kk];
+          for (int l = 0; l < R; ++l) acc[l] += b1[l * a.T] * dq[KC - 1];
         }
       } else {
-        for (int kk = 0; kk < kc; ++kk) {
-          const double dq = Qb[idx[kk * a.T]] - qi;
 #pragma unroll
-          for (int l = 0; l < R; ++l) acc[l] += Bs[l * kc + kk] * dq;
+        for (int kk = 0; kk < KC; ++kk) {
+          if (kk < kc) {
+#pragma unroll
+            for (int l = 0; l < R; ++l) acc[l] += Bs[chunk_elem_d(kc, R, a.T, l, ct, kk)] * dq[kk];
+          }
         }
       }
       __syncwarp();
@@ -637,6 +655,8 @@ static KArgs make_args(const cwreco_ctx* c, const double* avgs, int64_t acs, int
   a.blocks = c->dev->blocks;
   a.tile_bytes = L.tile_bytes;
   a.u_bytes = L.u_bytes;
+  a.off_idx = L.off_idx;
+  a.idx_bytes = L.idx_bytes;
   a.Umax = L.Umax;
   a.ids_bytes = L.ids_bytes;
   a.chunk_bytes = L.chunk_bytes;

@@ -36,9 +36,11 @@ static Layout layout_with(int d, int M, int V, int G, int T, int KC, int Umax) {
   L.Umax = Umax;
   L.kslice_bytes = int64_t(T) * L.R * 8;
   L.NCH = (G + KC - 1) / KC;
-  L.u_bytes = r16(int64_t(Umax) * 4);
-  L.ids_bytes = r16(int64_t(KC) * T * 2);
-  L.chunk_bytes = L.ids_bytes + int64_t(KC) * L.kslice_bytes;
+  L.off_idx = r16(int64_t(Umax) * 4);
+  L.idx_bytes = r16(int64_t(G) * T * 2);
+  L.u_bytes = L.off_idx + L.idx_bytes;
+  L.ids_bytes = 0;
+  L.chunk_bytes = int64_t(KC) * L.kslice_bytes;
   L.off_sector = r16(L.off_chunk(L.NCH - 1) + L.chunk_size(L.NCH - 1));
   L.sinv_bytes = int64_t(T) * (d + 1) * d * d * 8;
   L.sector_bytes = r16(L.sinv_bytes + T);
@@ -397,7 +399,7 @@ void precompute(cwreco_ctx* c) {
         int col[256];
         if (gather_order(c, li, G, to_local, lid, col) < 0) { bad_local |= 1; continue; }
         for (int p = 0; p < G; ++p)
-          ((uint16_t*)(tb + L.off_chunk(p / L.KC)))[size_t(p % L.KC) * T + ct] =
+          ((uint16_t*)(tb + L.off_idx))[size_t(p) * T + ct] =
               (uint16_t)(uindex(lid[p]) * L.V);  // element offset of the cell's row in Q_u
         uint8_t vm = 0;
         for (int s = 0; s < nv; ++s) vm |= val[s] ? uint8_t(1u << s) : 0;
@@ -456,7 +458,7 @@ void precompute(cwreco_ctx* c) {
           const int kc = L.kc_of(ch);
           double* chb = (double*)(tb + L.off_chunk(ch) + L.ids_bytes);
           const int k = col[p];
-          for (int l = 0; l < R; ++l) chb[(size_t(ct) * R + l) * kc + kk] = k >= 0 ? Bp[size_t(l) * K + k] : 0.0;
+          for (int l = 0; l < R; ++l) chb[chunk_elem(kc, R, T, l, ct, kk)] = k >= 0 ? Bp[size_t(l) * K + k] : 0.0;
         }
 
         // sector inverses

@@ -3,6 +3,7 @@
 Called by __graft_entry__.build() and by the package on first import when the
 library is missing.  Sources: paper_1612_09335_b200/csrc/, header: include/.
 """
+import io
 import os
 import subprocess
 import sys
@@ -15,7 +16,7 @@ OUT = os.path.join(HERE, "libcwreco.so")
 BUILD = os.path.join(HERE, "build")
 
 CXX_SRCS = ["api.cpp", "mesh.cpp", "stencil.cpp", "basis.cpp", "precompute.cpp"]
-CU_SRCS = ["kernels.cu"]
+CU_SRCS = ["kernels.cu", "rowblk_2d.cu", "rowblk_3d.cu"]
 CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 # -ffp-contract=off: the IEEE-specified geometry (R29) must not be fused; -mfma
@@ -36,19 +37,26 @@ def _run(cmd, log):
 
 
 def build(verbose=False):
+    """Compile every source in parallel (one process each), then link."""
+    from concurrent.futures import ThreadPoolExecutor
     os.makedirs(BUILD, exist_ok=True)
-    objs = []
+    jobs = []
+    for s in CXX_SRCS:
+        jobs.append((["g++", *CXXFLAGS, "-c", os.path.join(CSRC, s), "-o", os.path.join(BUILD, s + ".o")],
+                     os.path.join(BUILD, s + ".o")))
+    for s in CU_SRCS:
+        jobs.append(([NVCC, *NVFLAGS, "-c", os.path.join(CSRC, s), "-o", os.path.join(BUILD, s + ".o")],
+                     os.path.join(BUILD, s + ".o")))
+    logs = [io.StringIO() for _ in jobs]
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+        futs = [ex.submit(_run, cmd, lg) for (cmd, _), lg in zip(jobs, logs)]
+        outs = [f.result() for f in futs]
+    objs = [o for _, o in jobs]
     with open(os.path.join(BUILD, "build.log"), "w") as log:
-        for s in CXX_SRCS:
-            o = os.path.join(BUILD, s + ".o")
-            _run(["g++", *CXXFLAGS, "-c", os.path.join(CSRC, s), "-o", o], log)
-            objs.append(o)
-        for s in CU_SRCS:
-            o = os.path.join(BUILD, s + ".o")
-            out = _run([NVCC, *NVFLAGS, "-c", os.path.join(CSRC, s), "-o", o], log)
-            if verbose:
-                print(out)
-            objs.append(o)
+        for lg in logs:
+            log.write(lg.getvalue())
+        if verbose:
+            print("\n".join(outs))
         _run(["g++", "-shared", "-o", OUT + ".tmp", *objs, "-fopenmp", "-L" + os.path.join(CUDA_HOME, "lib64"),
               "-lcudart_static", "-lrt", "-ldl", "-lpthread"], log)
     os.replace(OUT + ".tmp", OUT)

@@ -227,20 +227,20 @@ cwreco_status cwreco_get_blocks(const cwreco_ctx* c, int64_t n_sel, const int64_
         }
         tb = tile.data();
       }
-      const double* sv = (const double*)(tb + L.off_sector);
-      const uint8_t vm = *((const uint8_t*)(tb + L.off_sector + L.sinv_bytes) + ct);
+      const double* sv = (const double*)(tb + cwr::sector_sinv_off(L.off_sector, L.sector_bytes, L.TSC, nv * d * d, ct));
+      const uint8_t vm = *(tb + cwr::sector_mask_off(L.off_sector, L.sector_bytes, L.sinv_bytes, L.TSC, ct));
       if (bplus)
         for (int l = 0; l < R; ++l)
           for (int k = 0; k < G; ++k) {
             const int ch = k / L.KC, kk = k % L.KC, kc = L.kc_of(ch);
             const double* B = (const double*)(tb + L.off_chunk(ch) + L.ids_bytes);
-            bplus[(s * R + l) * G + k] = B[cwr::chunk_elem(kc, R, T, l, ct, kk)];
+            bplus[(s * R + l) * G + k] = B[cwr::chunk_elem(L.kind, kc, R, L.V, T, l, ct, kk)];
           }
-      if (sinv) std::memcpy(sinv + s * nv * d * d, sv + (size_t)ct * nv * d * d, sizeof(double) * nv * d * d);
+      if (sinv) std::memcpy(sinv + s * nv * d * d, sv, sizeof(double) * nv * d * d);
       if (gather)
         for (int k = 0; k < G; ++k) {
-          const uint16_t u = ((const uint16_t*)(tb + L.off_idx))[size_t(k) * T + ct];
-          gather[s * G + k] = ((const int32_t*)tb)[u / L.V];  // union chunk: local ids
+          const uint16_t u = ((const uint16_t*)(tb + L.off_idx))[cwr::idx_elem(L.kind, T, k, ct)];
+          gather[s * G + k] = ((const int32_t*)tb)[u / L.VP];  // union chunk: local ids
         }
       if (slots)
         for (int q = 0; q < nv; ++q)

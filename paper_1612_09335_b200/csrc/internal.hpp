@@ -32,35 +32,82 @@ inline int n_modes(int M, int d) {  // ℳ(M,d) = (1/d!) Π_{l=1..d} (M+l)   (P:
 //   union chunk: uid int32  [Umax]    local ids of every cell the tile's stencils touch:
 //                                     the tile's own T cells first, then the others
 //                                     ascending (padded to Umax entries)
-//                idx uint16 [G][T]    (at off_idx) union index × V of the cell gathered
+//                idx uint16 [G][T]    (at off_idx) union index × VP of the cell gathered
 //                                     at each position: positions [0, (d+1)d) hold
 //                                     sector s, member m at s·d+m (R15; fillers if the
 //                                     sector is invalid), then the rest of S_i^0, then
 //                                     the cell itself as padding
 //   chunk ch, positions p ∈ [ch·KC, ch·KC+kc) (kc = KC except a shorter last one):
 //     B     double  reduced pseudo-inverse columns in gather order (0 for positions
-//                   outside S_i^0), position pairs first: [kc/2][R][T][2], then, if kc
-//                   is odd, the last position as [R][T] (chunk_elem): the T cells of a
-//                   (pair, row) are adjacent, so a warp's 16-byte loads never conflict
-//   sector chunk (at off_sector):
+//                   outside S_i^0), in the family's layout (chunk_elem below)
+//   sector chunk (at off_sector), in NSC pieces of TSC cells (stride sector_bytes; one
+//   piece unless a whole sector chunk would outgrow a stage, ROWBLK only), each:
 //     sinv  double [T][d+1][d][d]  sector inverses
 //     vmask uint8  [T]             bit s = sector s valid (R14)
+#if defined(__CUDACC__)
+#define CWR_HD __host__ __device__
+#else
+#define CWR_HD
+#endif
+
+// Kernel families, each with its own B⁺ chunk layout:
+//  KIND_CELLVAR  one consumer thread per (cell, variable) (k_pipelined): position
+//                pairs first, [kc/2][R][T][2], then an odd last position as [R][T]
+//  KIND_ROWBLK   one consumer thread per (cell, row group) holding every variable
+//                (k_rowblk): the R reduced rows are dealt round-robin to NG groups,
+//                row l = r·NG + g (slot r of group g); the first nfull groups hold RB
+//                rows, the others RB−1.  A position slice is [r][ct][g] over the row
+//                slots r < RB, slot r holding the ngr(r) groups that have a row
+//                there, so the lanes (ct, g) of a warp read consecutive doubles.
+enum { KIND_CELLVAR = 0, KIND_ROWBLK = 1 };
+// NG: 8 groups of ≤3 rows for ℳ = 20 (8 warps for a tile of 32 cells; 4 groups of ≤5
+// rows with 4 warps measured slower on C4: 43.5 vs 41.2 ms), else 4 groups
+CWR_HD constexpr int rb_ng(int R, int V) { return (void)V, R > 14 ? 8 : 4; }
+CWR_HD constexpr int rb_rb(int R, int V) { return (R + rb_ng(R, V) - 1) / rb_ng(R, V); }
+CWR_HD constexpr int rb_nfull(int R, int V) { return R - (rb_rb(R, V) - 1) * rb_ng(R, V); }
+CWR_HD constexpr int rb_ngr(int R, int V, int r) { return r < rb_rb(R, V) - 1 ? rb_ng(R, V) : rb_nfull(R, V); }
+
+// Entry (position p, cell ct) of the union-offset table (uint16, in the union chunk):
+// CELLVAR [G][T]; ROWBLK position pairs interleaved, [⌈G/2⌉][T][2], so one 32-bit load
+// gives a cell the offsets of both positions of a chunk.
+CWR_HD inline int64_t idx_elem(int kind, int T, int p, int ct) {
+  if (kind == KIND_ROWBLK) return (int64_t(p >> 1) * T + ct) * 2 + (p & 1);
+  return int64_t(p) * T + ct;
+}
+
 // Element (row l, cell ct, position kk) of a B⁺ chunk holding kc positions.
-inline int64_t chunk_elem(int kc, int R, int T, int l, int ct, int kk) {
+CWR_HD inline int64_t chunk_elem(int kind, int kc, int R, int V, int T, int l, int ct, int kk) {
+  if (kind == KIND_ROWBLK) {
+    const int NG = rb_ng(R, V), r = l / NG, g = l % NG;
+    return (int64_t(kk) * R + r * NG) * T + int64_t(ct) * rb_ngr(R, V, r) + g;
+  }
   const int np = kc / 2;
   if (kk < 2 * np) return ((int64_t(kk / 2) * R + l) * T + ct) * 2 + (kk & 1);
   return int64_t(np) * R * T * 2 + int64_t(l) * T + ct;
 }
 
+// Byte offsets (from the tile start) of cell ct's sector inverses and validity byte.
+CWR_HD inline int64_t sector_sinv_off(int64_t off_sector, int64_t sector_bytes, int TSC, int nvdd, int ct) {
+  const int j = ct / TSC;
+  return off_sector + j * sector_bytes + int64_t(ct - j * TSC) * nvdd * 8;
+}
+CWR_HD inline int64_t sector_mask_off(int64_t off_sector, int64_t sector_bytes, int64_t sinv_bytes, int TSC, int ct) {
+  const int j = ct / TSC;
+  return off_sector + j * sector_bytes + sinv_bytes + (ct - j * TSC);
+}
+
 struct Layout {
   int d = 0, M = 0, V = 0, nm = 0, R = 0, K = 0, G = 0, T = 0, KC = 0, NCH = 0, Umax = 0;
+  int kind = KIND_CELLVAR;   // kernel family (chunk layout)
+  int VP = 0;                // row stride of the gathered averages Q_u (V, rounded up to even for ROWBLK)
   int64_t kslice_bytes = 0;  // T·R·8: one position of B⁺ for the whole tile
   int64_t off_idx = 0;       // r16(Umax·4): the idx table inside the union chunk
-  int64_t idx_bytes = 0;     // r16(G·T·2)
+  int64_t idx_bytes = 0;     // r16(G·T·2) (ROWBLK: G rounded up to even)
   int64_t u_bytes = 0;       // off_idx + idx_bytes: the union chunk
   int64_t ids_bytes = 0;     // 0 (position chunks hold only B⁺)
   int64_t chunk_bytes = 0;   // stride of full chunks: KC·kslice_bytes
   int64_t sinv_bytes = 0, sector_bytes = 0, off_sector = 0, tile_bytes = 0;
+  int NSC = 1, TSC = 0;      // sector pieces per tile, cells per piece
   int kc_of(int ch) const { return KC < G - ch * KC ? KC : G - ch * KC; }
   int64_t off_chunk(int ch) const { return u_bytes + int64_t(ch) * chunk_bytes; }
   int64_t chunk_size(int ch) const { return ids_bytes + int64_t(kc_of(ch)) * kslice_bytes; }
@@ -73,14 +120,15 @@ inline int ctas_per_sm(int nm) { return nm >= 20 ? 1 : 2; }
 inline int64_t round128(int64_t x) { return (x + 127) & ~int64_t(127); }
 // shared memory of one pipelined CTA: S stages + the consumers' private gather rings
 inline int64_t pipe_stage_bytes(const Layout& L) {
-  int64_t m = L.chunk_bytes > L.sector_bytes ? L.chunk_bytes : L.sector_bytes;
+  int64_t m = L.chunk_bytes > L.sector_bytes ? L.chunk_bytes : L.sector_bytes;  // (one sector piece)
   return round128(m > L.u_bytes ? m : L.u_bytes);
 }
 inline int64_t pipe_q_bytes(const Layout& L) {  // double-buffered Q_u [Umax][V] and idx [G][T]
-  return round128(2 * int64_t(L.Umax) * L.V * 8) + round128(2 * L.idx_bytes);
+  return round128(2 * int64_t(L.Umax) * L.VP * 8) + round128(2 * L.idx_bytes);
 }
-inline int64_t pipe_out_bytes(const Layout& L) {  // per-warp output staging (bulk stores)
-  return round128(int64_t((L.T * L.V + 31) / 32) * 32 * L.nm * 8);
+inline int64_t pipe_out_bytes(const Layout& L) {
+  if (L.kind == KIND_ROWBLK) return round128(int64_t(L.T) * L.V * L.nm * 8);  // the tile's [T][V][ℳ] rows
+  return round128(int64_t((L.T * L.V + 31) / 32) * 32 * L.nm * 8);           // per-warp staging
 }
 inline int64_t pipe_smem(const Layout& L, int stages) {
   return stages * pipe_stage_bytes(L) + pipe_q_bytes(L) + pipe_out_bytes(L) + 16 * stages;
@@ -93,6 +141,19 @@ inline int64_t pipe_budget(int nm, int max_smem) {
 // max_smem: opt-in shared memory per block of the device (227 KB on B200);
 // umax_for(T): the largest per-tile stencil union for tiles of T cells.
 Layout make_layout(int d, int M, int V, int G, int max_smem, const std::function<int(int)>& umax_for);
+// k_rowblk: consumer threads per CTA, and whether an instantiation exists for (d, M, V)
+// consumer threads of a row-block CTA (8 warps)
+CWR_HD constexpr int rb_consumers(int R, int V) { return (R > 14 && rb_ng(R, V) == 4) ? 128 : 256; }
+// default family choice: the row-block kernel where the cell-variable kernel is
+// bound by its shared-memory broadcasts (ℳ = 20 and V ≥ 7: C4); measured slower
+// elsewhere (C2 0.25 vs 0.17 ms, C3 1.34 vs 1.09, C5 13.0 vs 12.0)
+CWR_HD constexpr bool rb_default(int R, int V) { return R > 14 && V >= 7; }
+constexpr int kRbKC = 2;  // positions per streamed chunk of the row-block layout
+constexpr int kRbMaxStages = 32;  // row-block stage ring: as deep as shared memory allows
+bool rowblk_supported(int d, int M, int V);
+// CTAs per SM (≤ max_ctas, by shared memory) and stage-ring depth of a ROWBLK
+// layout (0 CTAs: does not fit)
+void rowblk_plan(const Layout& L, int max_smem, int max_ctas, int& ctas, int& stages);
 
 struct DeviceState;  // kernels.cu
 

@@ -23,7 +23,7 @@
 #include <string>
 #include <vector>
 
-#include "internal.hpp"
+#include "kcommon.cuh"
 
 namespace cwr {
 
@@ -38,6 +38,9 @@ struct DeviceState {
   int64_t dbg_bytes = 0;
   int64_t* dbg_cells = nullptr;
   int64_t dbg_ncells = 0;
+  bool have_cfg = false;  // launch shape of the pipelined kernel, fixed at precompute
+  PipeCfg cfg{};
+  int cfg_ctas = 1;
 };
 
 #define CK(x)                                                                                  \
@@ -46,179 +49,7 @@ struct DeviceState {
     if (e_ != cudaSuccess) fail(CWRECO_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
   } while (0)
 
-__host__ __device__ constexpr int nmodes(int M, int d) {
-  return d == 2 ? (M + 1) * (M + 2) / 2 : (M + 1) * (M + 2) * (M + 3) / 6;
-}
-
-// Universal Σ depends only on (d, M): the packed upper triangle of Σ[1:,1:]
-// (off-diagonals doubled) of every supported (d, M) lives in the constant bank, so
-// the σ quadratic forms use it as DFMA constant operands.
-__host__ __device__ constexpr int sig_len(int D, int M) { return (nmodes(M, D) - 1) * nmodes(M, D) / 2; }
-__host__ __device__ constexpr int sig_off(int D, int M) {
-  int off = 0;
-  for (int dd = 2; dd <= 3; ++dd)
-    for (int mm = 1; mm <= 4; ++mm) {
-      if (dd == D && mm == M) return off;
-      off += sig_len(dd, mm);
-    }
-  return off;
-}
-constexpr int SIG_TOTAL = sig_off(4, 1);
-__constant__ double c_sig[SIG_TOTAL];
-
-struct KArgs {
-  const unsigned char* blocks;
-  int64_t tile_bytes, u_bytes, off_idx, idx_bytes, ids_bytes, chunk_bytes, kslice_bytes, off_sector, sinv_bytes,
-      sector_bytes;
-  int Umax;
-  int T, G, K, KC, NCH, V;
-  int64_t n_owned, tile_begin, tile_end;
-  const double* Q;
-  int64_t acs, avs;
-  double* out;
-  int64_t ccs, cvs;
-  int dense_out;
-  int exp_flags;  // bottleneck experiments only (CWRECO_EXP_FLAGS): 1 no gather, 2 no B⁺ FMAs,
-                 // 16 no epilogue (timing only: results are wrong)
-  double eps, psi1;
-  int r;
-  // normalised linear weights (R5, R14) indexed by the number of valid sectors
-  double l0[5], inv_l0[5], ls[5];
-};
-
-struct DbgOut {
-  double *popt, *psec, *sigma, *omega, *w;
-  const int64_t* cells;
-  int64_t n;
-};
-
-__device__ __forceinline__ double powr(double t, int r) {
-  if (r == 4) {
-    const double t2 = t * t;
-    return t2 * t2;
-  }
-  double p = 1.0;
-  for (int i = 0; i < r; ++i) p *= t;
-  return p;
-}
-
-template <int D, int NM>
-struct ModeOf {  // M from (D, ℳ)
-  static constexpr int M = D == 2 ? (NM == 3 ? 1 : NM == 6 ? 2 : NM == 10 ? 3 : 4) : (NM == 4 ? 1 : NM == 10 ? 2 : 3);
-};
-
-// Fused epilogue.  acc[l-1] = p̂_opt[l] (l >= 1); ps[s][l-1] = p̂_s[l]
-// (l = 1..D).  The blended coefficients are written to w[0..NM) as they are formed
-// (w may be shared or global memory).
-template <int D, int NM>
-__device__ __forceinline__ void cweno_epilogue(double qi, double* acc, const double (&ps)[D + 1][D],
-                                               const bool (&valid)[D + 1], const KArgs& a, double* w,
-                                               double* sigma_out, double* omega_out) {
-  constexpr int R = NM - 1;
-  constexpr int SO = sig_off(D, ModeOf<D, NM>::M);
-  const double p0 = qi / a.psi1;
-  int nval = 0;
-#pragma unroll
-  for (int s = 0; s <= D; ++s) nval += valid[s] ? 1 : 0;
-  const double l0 = a.l0[nval], il0 = a.inv_l0[nval], ls = a.ls[nval];
-  // P0 = (P_opt − Σ_s λ̄_s P_s)/λ̄0; modes above d are P_opt/λ̄0
-#pragma unroll
-  for (int l = 0; l < D; ++l) {
-    double s = 0.0;
-#pragma unroll
-    for (int q = 0; q <= D; ++q) s += valid[q] ? ps[q][l] : 0.0;
-    acc[l] = (acc[l] - ls * s) * il0;
-  }
-#pragma unroll
-  for (int l = D; l < R; ++l) acc[l] = acc[l] * il0;
-  // σ_0 = P0ᵀ Σ P0 and σ_s = P_sᵀ Σ P_s
-  double sg0 = 0.0;
-  {
-    int idx = SO;
-#pragma unroll
-    for (int l = 0; l < R; ++l) {
-      double t = 0.0;
-#pragma unroll
-      for (int m = l; m < R; ++m) t += c_sig[idx + m - l] * acc[m];
-      idx += R - l;
-      sg0 += acc[l] * t;
-    }
-  }
-  double sgs[D + 1];
-#pragma unroll
-  for (int s = 0; s <= D; ++s) {
-    double v = 0.0;
-    int idx = SO;
-#pragma unroll
-    for (int l = 0; l < D; ++l) {
-      double t = 0.0;
-#pragma unroll
-      for (int m = l; m < D; ++m) t += c_sig[idx + m - l] * ps[s][m];
-      idx += R - l;
-      v += ps[s][l] * t;
-    }
-    sgs[s] = v;
-  }
-  // ω̃_s = λ̄_s/(σ_s+ε)^r, ω_s = ω̃_s/Σ ω̃; invalid sectors get 0 (R14)
-  // reciprocals instead of divisions (one extra rounding, far inside the 1e-11 bar)
-  const double wt0 = l0 * __drcp_rn(powr(sg0 + a.eps, a.r));
-  double wts[D + 1];
-  double sum = wt0;
-#pragma unroll
-  for (int s = 0; s <= D; ++s) {
-    wts[s] = valid[s] ? ls * __drcp_rn(powr(sgs[s] + a.eps, a.r)) : 0.0;
-    sum += wts[s];
-  }
-  const double isum = __drcp_rn(sum);
-  const double om0 = wt0 * isum;
-  double oms[D + 1];
-#pragma unroll
-  for (int s = 0; s <= D; ++s) oms[s] = wts[s] * isum;
-  // w = Σ_s ω_s P_s;  w[0] := Q_i/ψ1 (R17)
-  w[0] = p0;
-#pragma unroll
-  for (int l = 0; l < D; ++l) {
-    double v = om0 * acc[l];
-#pragma unroll
-    for (int s = 0; s <= D; ++s) v += oms[s] * ps[s][l];
-    w[l + 1] = v;
-  }
-#pragma unroll
-  for (int l = D; l < R; ++l) w[l + 1] = om0 * acc[l];
-  if (sigma_out) {
-    sigma_out[0] = sg0;
-    omega_out[0] = om0;
-#pragma unroll
-    for (int s = 0; s <= D; ++s) {
-      sigma_out[s + 1] = valid[s] ? sgs[s] : 0.0;
-      omega_out[s + 1] = oms[s];
-    }
-  }
-}
-
-// B⁺ chunk element (row l, cell ct, position kk), as chunk_elem in internal.hpp
-__device__ __forceinline__ int64_t chunk_elem_d(int kc, int R, int T, int l, int ct, int kk) {
-  const int np = kc / 2;
-  if (kk < 2 * np) return ((int64_t(kk / 2) * R + l) * T + ct) * 2 + (kk & 1);
-  return int64_t(np) * R * T * 2 + int64_t(l) * T + ct;
-}
-
 // ---------------------------------------------------------------- simple kernel
-// Sector products from the captured ΔQ of gather positions [0, (D+1)·D).
-template <int D>
-__device__ __forceinline__ void sector_apply(const double* sinv, const double (&dqs)[(D + 1) * D],
-                                             double (&ps)[D + 1][D]) {
-#pragma unroll
-  for (int s = 0; s <= D; ++s)
-#pragma unroll
-    for (int l = 0; l < D; ++l) {
-      double t = 0.0;
-#pragma unroll
-      for (int m = 0; m < D; ++m) t += sinv[(s * D + l) * D + m] * dqs[s * D + m];
-      ps[s][l] = t;
-    }
-}
-
 template <int D, int M, bool DEBUG>
 __global__ void __launch_bounds__(256) k_simple(KArgs a, DbgOut dbg) {
   constexpr int NM = nmodes(M, D), R = NM - 1, NV = D + 1, NCAP = NV * D;
@@ -236,8 +67,8 @@ __global__ void __launch_bounds__(256) k_simple(KArgs a, DbgOut dbg) {
   const int64_t tile = c / a.T;
   const int ct = int(c % a.T);
   const unsigned char* tb = a.blocks + tile * a.tile_bytes;
-  const double* sinv = (const double*)(tb + a.off_sector) + size_t(ct) * NV * D * D;
-  const uint8_t vmask = *((const uint8_t*)(tb + a.off_sector + a.sinv_bytes) + ct);
+  const double* sinv = (const double*)(tb + sector_sinv_off(a.off_sector, a.sector_bytes, a.TSC, NV * D * D, ct));
+  const uint8_t vmask = *(tb + sector_mask_off(a.off_sector, a.sector_bytes, a.sinv_bytes, a.TSC, ct));
   const double* Qv = a.Q + v * a.avs;
   const double qi = Qv[c * a.acs];
 
@@ -248,17 +79,17 @@ __global__ void __launch_bounds__(256) k_simple(KArgs a, DbgOut dbg) {
   for (int ch = 0; ch < a.NCH; ++ch) {
     const int kc = min(a.KC, a.G - ch * a.KC);
     const unsigned char* cb = tb + a.u_bytes + ch * a.chunk_bytes;
-    const uint16_t* idx = (const uint16_t*)(tb + a.off_idx) + size_t(ch) * a.KC * a.T;  // [G][T]
+    const uint16_t* idx = (const uint16_t*)(tb + a.off_idx);  // idx_elem layout
     const double* Bc = (const double*)(cb + a.ids_bytes);   // chunk_elem layout
     for (int kk = 0; kk < kc; ++kk) {
       const int p = ch * a.KC + kk;
-      const int32_t j = ((const int32_t*)tb)[idx[size_t(kk) * a.T + ct] / a.V];  // union chunk
+      const int32_t j = ((const int32_t*)tb)[idx[idx_elem(a.kind, a.T, p, ct)] / a.VP];  // union chunk
       const double dq = Qv[int64_t(j) * a.acs] - qi;
 #pragma unroll
       for (int q = 0; q < NCAP; ++q)
         if (p == q) dqs[q] = dq;
 #pragma unroll
-      for (int l = 0; l < R; ++l) acc[l] += Bc[chunk_elem_d(kc, R, a.T, l, ct, kk)] * dq;
+      for (int l = 0; l < R; ++l) acc[l] += Bc[chunk_elem(a.kind, kc, R, a.V, a.T, l, ct, kk)] * dq;
     }
   }
   bool valid[NV];
@@ -287,108 +118,11 @@ __global__ void __launch_bounds__(256) k_simple(KArgs a, DbgOut dbg) {
   }
 }
 
-// ---------------------------------------------------------------- PTX helpers
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t done = 0;
-  while (!done) {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-  }
-}
-// Blocking wait with a long suspend-time hint: the waiting thread sleeps until the
-// phase completes instead of re-polling (used by the producer lane, whose spin
-// otherwise steals issue slots from the consumers on its SM sub-partition).
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
-  uint32_t done = 0;
-  while (!done) {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
-        : "memory");
-  }
-}
-// Non-blocking probe of a phase (result consumed later, so its latency overlaps work).
-__device__ __forceinline__ uint32_t mbar_test(uint64_t* bar, uint32_t parity) {
-  uint32_t done;
-  asm volatile(
-      "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-      : "=r"(done)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  return done;
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
-               "r"(bytes)
-               : "memory");
-  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
-__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
 // (must agree with cons_threads / ctas_per_sm in internal.hpp)
 __host__ __device__ constexpr int cons_target(int D, int M) { return nmodes(M, D) >= 20 ? 320 : 160; }
 __host__ __device__ constexpr int min_blocks(int D, int M) { return nmodes(M, D) >= 20 ? 1 : 2; }
 // consumers + one producer warp
 __host__ __device__ constexpr int max_threads(int D, int M) { return cons_target(D, M) + 32; }
-struct PipeCfg {
-  int stages;
-  int64_t stage_bytes, q_bytes, out_bytes;
-  int64_t off_stage, off_q, off_out, off_bar, smem;
-  int ncw;  // consumer warps
-};
-
-struct Ring {  // slot index + mbarrier phase of a ring of S slots
-  int st = 0;
-  uint32_t ph = 0;
-  __device__ __forceinline__ void next(int S) {
-    if (++st == S) {
-      st = 0;
-      ph ^= 1u;
-    }
-  }
-};
-
-__device__ __forceinline__ void consumer_bar(int nthreads) {  // named barrier 1: consumer warps only
-  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
-}
-
 // ---------------------------------------------------------------- pipelined kernel
 // Persistent, warp-specialised.  Warp roles: [0, ncw) consumers, thread
 // tid ↔ (ct, v) = (tid / V, tid % V); warp ncw: TMA producer (lane 0) — streams,
@@ -548,7 +282,7 @@ __global__ void __launch_bounds__(max_threads(D, M), min_blocks(D, M)) k_pipelin
         for (int kk = 0; kk < KC; ++kk) {
           if (kk < kc) {
 #pragma unroll
-            for (int l = 0; l < R; ++l) acc[l] += Bs[chunk_elem_d(kc, R, a.T, l, ct, kk)] * dq[kk];
+            for (int l = 0; l < R; ++l) acc[l] += Bs[chunk_elem(KIND_CELLVAR, kc, R, a.V, a.T, l, ct, kk)] * dq[kk];
           }
         }
       }
@@ -625,7 +359,6 @@ void launch_simple(int d, int M, dim3 g, dim3 b, cudaStream_t st, const KArgs& a
   fail(CWRECO_EUNSUPPORTED, "unsupported (d, M)");
 }
 
-using PipeFn = void (*)(KArgs, PipeCfg);
 template <int D, int M>
 PipeFn pipe_fn_kc(int KC) {
   switch (KC) {
@@ -664,12 +397,16 @@ static KArgs make_args(const cwreco_ctx* c, const double* avgs, int64_t acs, int
   a.off_sector = L.off_sector;
   a.sinv_bytes = L.sinv_bytes;
   a.sector_bytes = L.sector_bytes;
+  a.NSC = L.NSC;
+  a.TSC = L.TSC;
   a.T = L.T;
   a.G = L.G;
   a.K = L.K;
   a.KC = L.KC;
   a.NCH = L.NCH;
   a.V = c->V;
+  a.VP = L.VP;
+  a.kind = L.kind;
   a.n_owned = c->n_owned;
   a.tile_begin = 0;
   a.tile_end = c->n_tiles;
@@ -696,13 +433,56 @@ static KArgs make_args(const cwreco_ctx* c, const double* avgs, int64_t acs, int
   return a;
 }
 
-static PipeCfg pipe_cfg(const cwreco_ctx* c) {
+bool rowblk_supported(int d, int M, int V) {
+  return (d == 2 ? rowblk_fn_2d(M, V) : d == 3 ? rowblk_fn_3d(M, V) : nullptr) != nullptr;
+}
+static PipeFn rowblk_fn(const cwreco_ctx* c) {
+  PipeFn f = c->d == 2 ? rowblk_fn_2d(c->M, c->V) : rowblk_fn_3d(c->M, c->V);
+  if (!f) fail(CWRECO_EUNSUPPORTED, "row-block kernel not instantiated for (d, M, V)");
+  return f;
+}
+
+static PipeCfg pipe_cfg(const cwreco_ctx* c, int* ctas = nullptr) {
+  if (c->dev->have_cfg && !std::getenv("CWRECO_MAX_STAGES") && !std::getenv("CWRECO_CTAS")) {
+    if (ctas) *ctas = c->dev->cfg_ctas;
+    return c->dev->cfg;
+  }
   const Layout& L = c->lay;
   PipeCfg p;
-  p.ncw = (L.T * c->V + 31) / 32;
   p.stage_bytes = pipe_stage_bytes(L);
   p.q_bytes = pipe_q_bytes(L);
   p.out_bytes = pipe_out_bytes(L);
+  if (L.kind == KIND_ROWBLK) {
+    // as many CTAs/SM as shared memory AND registers allow (occupancy API), then
+    // the deepest stage ring that fits
+    int k = 0, st = 0;
+    const PipeFn f = rowblk_fn(c);
+    const int nthr = (L.T * rb_ng(L.R, L.V) / 32 + 1) * 32;
+    const char* kcap = std::getenv("CWRECO_CTAS");  // tuning experiments only
+    for (int want = kcap ? std::max(1, std::min(3, std::atoi(kcap))) : 3; want >= 1; --want) {
+      rowblk_plan(L, c->dev->max_smem, want, k, st);
+      if (k < want) continue;
+      int occ = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)f, nthr,
+                                                       (size_t)(st * p.stage_bytes + p.q_bytes + p.out_bytes + 16 * st)));
+      if (occ >= want) break;
+      k = 0;
+    }
+    const char* cap = std::getenv("CWRECO_MAX_STAGES");  // tuning experiments only
+    if (cap) st = std::max(kMinStages, std::min(st, std::atoi(cap)));
+    if (!k) fail(CWRECO_EUNSUPPORTED, "row-block kernel: tile does not fit in shared memory");
+    if (ctas) *ctas = k;
+    p.ncw = L.T * rb_ng(L.R, L.V) / 32;
+    p.stages = st;
+    p.off_stage = 0;
+    p.off_q = st * p.stage_bytes;
+    p.off_out = p.off_q + p.q_bytes;
+    p.off_bar = p.off_out + p.out_bytes;
+    p.smem = p.off_bar + 16 * st;
+    return p;
+  }
+  if (ctas) *ctas = ctas_per_sm(c->nm);
+  p.ncw = (L.T * c->V + 31) / 32;
   // as many stages as fit the per-CTA budget (ctas_per_sm CTAs/SM); a tile too
   // large for that budget runs at 1 CTA/SM with the whole shared memory.  The
   // prefetch cursor runs up to PF + 1 stages ahead of the consumers.
@@ -771,11 +551,15 @@ void dev_upload_aux(cwreco_ctx* c) {
   for (int l = 1; l < nm; ++l)
     for (int m = l; m < nm; ++m) packed.push_back((l == m ? 1.0 : 2.0) * c->sigma[l * nm + m]);
   CK(cudaSetDevice(c->device));
-  CK(cudaMemcpyToSymbol(c_sig, packed.data(), sizeof(double) * packed.size(), sizeof(double) * sig_off(c->d, c->M)));
-  PipeCfg p = pipe_cfg(c);
-  PipeFn f = pipe_fn(c->d, c->M, c->lay.KC);
-  (void)p;
+  const size_t sb = sizeof(double) * packed.size(), so = sizeof(double) * sig_off(c->d, c->M);
+  CK(cudaMemcpyToSymbol(c_sig, packed.data(), sb, so));
+  CK(rowblk_upload_sigma_2d(packed.data(), sb, so));
+  CK(rowblk_upload_sigma_3d(packed.data(), sb, so));
+  PipeFn f = c->lay.kind == KIND_ROWBLK ? rowblk_fn(c) : pipe_fn(c->d, c->M, c->lay.KC);
   CK(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, c->dev->max_smem));
+  c->dev->have_cfg = false;
+  c->dev->cfg = pipe_cfg(c, &c->dev->cfg_ctas);
+  c->dev->have_cfg = true;
 }
 
 void dev_download_tile(const cwreco_ctx* c, int64_t tile, unsigned char* host) {
@@ -807,12 +591,13 @@ void dev_reconstruct(cwreco_ctx* c, const double* avgs, int64_t acs, int64_t avs
     launch_simple<false>(c->d, c->M, g, b, st, a, o);
   } else {
     a.dense_out = (cvs == nm && ccs == (int64_t)c->V * nm && (((uintptr_t)coeffs) & 15) == 0 && nm % 2 == 0) ? 1 : 0;
-    PipeCfg p = pipe_cfg(c);
+    int per_sm = 1;
+    PipeCfg p = pipe_cfg(c, &per_sm);
     const int64_t ntiles = a.tile_end - a.tile_begin;
-    const int per_sm = ctas_per_sm(c->nm);
     const int64_t grid = std::min<int64_t>(ntiles, (int64_t)c->dev->num_sms * per_sm);
     dim3 b((p.ncw + 1) * 32), g((unsigned)grid);
-    pipe_fn(c->d, c->M, c->lay.KC)<<<g, b, p.smem, st>>>(a, p);
+    PipeFn f = c->lay.kind == KIND_ROWBLK ? rowblk_fn(c) : pipe_fn(c->d, c->M, c->lay.KC);
+    f<<<g, b, p.smem, st>>>(a, p);
   }
   CK(cudaGetLastError());
 }

@@ -22,8 +22,10 @@ namespace cwr {
 
 static inline int64_t r16(int64_t x) { return (x + 15) & ~int64_t(15); }
 
-static Layout layout_with(int d, int M, int V, int G, int T, int KC, int Umax) {
+static Layout layout_with(int d, int M, int V, int G, int T, int KC, int Umax, int kind, int nsc = 1) {
   Layout L;
+  L.kind = kind;
+  L.VP = kind == KIND_ROWBLK ? V + (V & 1) : V;
   L.d = d;
   L.M = M;
   L.V = V;
@@ -37,19 +39,57 @@ static Layout layout_with(int d, int M, int V, int G, int T, int KC, int Umax) {
   L.kslice_bytes = int64_t(T) * L.R * 8;
   L.NCH = (G + KC - 1) / KC;
   L.off_idx = r16(int64_t(Umax) * 4);
-  L.idx_bytes = r16(int64_t(G) * T * 2);
+  L.idx_bytes = r16(int64_t(kind == KIND_ROWBLK ? (G + 1) & ~1 : G) * T * 2);
   L.u_bytes = L.off_idx + L.idx_bytes;
   L.ids_bytes = 0;
   L.chunk_bytes = int64_t(KC) * L.kslice_bytes;
   L.off_sector = r16(L.off_chunk(L.NCH - 1) + L.chunk_size(L.NCH - 1));
-  L.sinv_bytes = int64_t(T) * (d + 1) * d * d * 8;
-  L.sector_bytes = r16(L.sinv_bytes + T);
-  L.tile_bytes = L.off_sector + L.sector_bytes;
+  L.NSC = nsc;
+  L.TSC = (T + nsc - 1) / nsc;
+  L.sinv_bytes = int64_t(L.TSC) * (d + 1) * d * d * 8;
+  L.sector_bytes = r16(L.sinv_bytes + L.TSC);
+  L.tile_bytes = L.off_sector + nsc * L.sector_bytes;
   return L;
+}
+
+void rowblk_plan(const Layout& L, int max_smem, int max_ctas, int& ctas, int& stages) {
+  // per-SM shared memory = per-block opt-in + the 1 KB the driver reserves per block
+  const int64_t per_sm = int64_t(max_smem) + 1024;
+  ctas = 0;
+  stages = 0;
+  for (int k = max_ctas; k >= 1; --k) {
+    const int64_t budget = std::min<int64_t>(max_smem, per_sm / k - 1024);
+    // every sector piece of a tile is held at once: the ring needs NSC + 1 stages
+    for (int s = kRbMaxStages; s >= std::max(kMinStages, L.NSC + 1); --s)
+      if (pipe_smem(L, s) <= budget) {
+        ctas = k;
+        stages = s;
+        return;
+      }
+  }
 }
 
 Layout make_layout(int d, int M, int V, int G, int max_smem, const std::function<int(int)>& umax_for) {
   const int nm = n_modes(M, d);
+  // CWRECO_FAMILY (tests / A-B experiments): 0 = cell-variable, 1 = row-block where instantiated
+  const char* fam = std::getenv("CWRECO_FAMILY");
+  const bool want_rb = fam ? std::atoi(fam) == 1 : rb_default(nm - 1, V);
+  if (want_rb && rowblk_supported(d, M, V)) {
+    // k_rowblk: T = consumers / NG cells per tile (halved while the CTA does not fit);
+    // KC positions per chunk: ~10 KB of B⁺ per stage, KC ∈ {1, 2, 4} (compiled sizes)
+    const int R = nm - 1;
+    for (int T = rb_consumers(R, V) / rb_ng(R, V); T >= 32 / rb_ng(R, V); T /= 2) {
+      Layout L0 = layout_with(d, M, V, G, T, kRbKC, umax_for(T), KIND_ROWBLK);
+      // sector data in pieces no larger than a position chunk or the union chunk
+      const int64_t stage = std::max(L0.chunk_bytes, L0.u_bytes);
+      int nsc = 1;
+      while (nsc < T && r16(int64_t((T + nsc - 1) / nsc) * ((d + 1) * d * d * 8 + 1)) > stage) ++nsc;
+      Layout L = layout_with(d, M, V, G, T, kRbKC, L0.Umax, KIND_ROWBLK, nsc);
+      int ctas, stages;
+      rowblk_plan(L, max_smem, 1, ctas, stages);
+      if (ctas > 0) return L;
+    }
+  }
   // one tile = T cells × V variables = one consumer thread each
   int T0 = (cons_threads(nm) / V) & ~1;
   if (T0 < 2) T0 = 2;
@@ -72,7 +112,7 @@ Layout make_layout(int d, int M, int V, int G, int max_smem, const std::function
     if (want == 7) want = 6;
     for (int KC = force ? std::atoi(force) : want; KC >= 1; --KC) {
       if (KC == 7 || KC > G || ((d + 1) * d + KC - 1) / KC * KC > G) continue;
-      Layout L = layout_with(d, M, V, G, T, KC, Umax);
+      Layout L = layout_with(d, M, V, G, T, KC, Umax, KIND_CELLVAR);
       if (pipe_smem(L, kMinStages) <= budget) return L;
       if (!found || pipe_smem(L, kMinStages) < pipe_smem(best, kMinStages)) best = L, found = true;
     }
@@ -294,7 +334,7 @@ void precompute(cwreco_ctx* c) {
       }
     }
     if (bad) fail(CWRECO_EINVAL, "precompute: stencil cell missing from the local numbering");
-    if ((int64_t)umax * c->V > 65535)
+    if ((int64_t)umax * (c->V + (c->V & 1)) > 65535)
       fail(CWRECO_EUNSUPPORTED, "precompute: tile stencil union × nvars exceeds the 16-bit offsets");
     return umax;
   };
@@ -378,8 +418,7 @@ void precompute(cwreco_ctx* c) {
         auto it = std::lower_bound(uni.begin() + T, uni.end(), lid);
         return int(it - uni.begin());
       };
-      double* sinv = (double*)(tb + L.off_sector);
-      uint8_t* vmask = (uint8_t*)(tb + L.off_sector + L.sinv_bytes);
+      const int nvdd = nv * d * d;
       for (int64_t li = lo; li < hi; ++li) {
         const int ct = int(li - lo);
         const int64_t g = c->local2global[li];
@@ -399,8 +438,8 @@ void precompute(cwreco_ctx* c) {
         int col[256];
         if (gather_order(c, li, G, to_local, lid, col) < 0) { bad_local |= 1; continue; }
         for (int p = 0; p < G; ++p)
-          ((uint16_t*)(tb + L.off_idx))[size_t(p) * T + ct] =
-              (uint16_t)(uindex(lid[p]) * L.V);  // element offset of the cell's row in Q_u
+          ((uint16_t*)(tb + L.off_idx))[idx_elem(L.kind, T, p, ct)] =
+              (uint16_t)(uindex(lid[p]) * L.VP);  // element offset of the cell's row in Q_u
         uint8_t vm = 0;
         for (int s = 0; s < nv; ++s) vm |= val[s] ? uint8_t(1u << s) : 0;
 
@@ -458,12 +497,12 @@ void precompute(cwreco_ctx* c) {
           const int kc = L.kc_of(ch);
           double* chb = (double*)(tb + L.off_chunk(ch) + L.ids_bytes);
           const int k = col[p];
-          for (int l = 0; l < R; ++l) chb[chunk_elem(kc, R, T, l, ct, kk)] = k >= 0 ? Bp[size_t(l) * K + k] : 0.0;
+          for (int l = 0; l < R; ++l) chb[chunk_elem(L.kind, kc, R, L.V, T, l, ct, kk)] = k >= 0 ? Bp[size_t(l) * K + k] : 0.0;
         }
 
         // sector inverses
         for (int s = 0; s < nv; ++s) {
-          double* Sd = &sinv[((size_t)ct * nv + s) * d * d];
+          double* Sd = (double*)(tb + sector_sinv_off(L.off_sector, L.sector_bytes, L.TSC, nvdd, ct)) + s * d * d;
           for (int e = 0; e < d * d; ++e) Sd[e] = 0.0;
           if (!val[s]) continue;
           double As[9];
@@ -486,7 +525,7 @@ void precompute(cwreco_ctx* c) {
           }
           for (int e = 0; e < d * d; ++e) Sd[e] = Ai[e];
         }
-        vmask[ct] = vm;
+        *(tb + sector_mask_off(L.off_sector, L.sector_bytes, L.sinv_bytes, L.TSC, ct)) = vm;
       }
     }
     if (bad_singular || bad_local) break;

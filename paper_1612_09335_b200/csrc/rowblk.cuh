@@ -1,0 +1,317 @@
+// k_rowblk: the row-block CWENO reconstruction kernel (sm_100a), for ℳ ≥ 10.
+//
+// The central LSQ apply is, per cell, the small product
+//     p̂_opt[1..R][v] = B⁺[R][G] · ΔQ[G][V]      (R = ℳ−1 reduced rows, G positions).
+// k_pipelined gives every (cell, variable) its own thread, so each B⁺ element is
+// read from shared memory by V lanes (a broadcast that still costs a full
+// wavefront per quarter-warp: ncu counts ~4 wavefronts per LDS.128, and the
+// shared-memory pipe saturates at ~83 % on C4).  Here a thread owns one cell and
+// a group of RB rows for ALL V variables: each B⁺ element is loaded once and used
+// V times from registers, and only the V averages of a position are broadcast
+// (NG threads per cell).  Shared-memory wavefronts per cell and position drop
+// from V·(R+1)·8/128 to (R + NG·V)·8/128 (C4: 11.3 → 3.4).
+//
+// Pipeline (persistent, warp-specialised, as k_pipelined):
+//  - producer warp (one elected lane): per tile, the union chunk of the CTA's
+//    NEXT tile, then the position chunks, then the sector chunk, into a ring of S
+//    stages with 1-D TMA bulk copies completing on mbarrier transaction counts;
+//  - consumers (T cells × NG row groups): at tile start they cp.async the V
+//    averages of every cell of the next tile's stencil union into the other half
+//    of a double-buffered Q_u[2][Umax][VP]; per position: ΔQ = Q_u[idx] − Q_i for
+//    all V, then acc[r][v] += B⁺[row r][p]·ΔQ[v] for the thread's rows; after the
+//    last chunk the row groups write p̂_opt into the tile's output rows
+//    O[T][V][ℳ] (slots 1..R), and one thread per (cell, variable) runs the fused
+//    sector / P0 / σ / ω / blend epilogue in place (reading its sector ΔQ back
+//    from Q_u) — the tile's output block is then written with one bulk store.
+// Arithmetic per (cell, variable) and its order are those of k_simple (bitwise
+// identical results, tested).
+#pragma once
+#include "kcommon.cuh"
+
+namespace cwr {
+
+constexpr int KC = kRbKC;                       // positions per chunk (compile time)
+
+template <int D, int M, int V>
+__global__ void __launch_bounds__(rb_consumers(nmodes(M, D) - 1, V) + 32, 1) k_rowblk(KArgs a, PipeCfg pc) {
+  constexpr int NM = nmodes(M, D), R = NM - 1, NV = D + 1, NCAP = NV * D;
+  constexpr int NG = rb_ng(R, V), RB = rb_rb(R, V), NF = rb_nfull(R, V);
+  constexpr int VP = V + (V & 1);
+  extern __shared__ __align__(128) unsigned char smem[];
+  unsigned char* stg = smem + pc.off_stage;
+  double* O = (double*)(smem + pc.off_out);  // [T][V][ℳ] output rows of the tile
+  double* Qu = (double*)(smem + pc.off_q);   // [2][Umax][VP] gathered averages
+  uint16_t* Ix = (uint16_t*)(smem + pc.off_q + ((2 * (int64_t)a.Umax * VP * 8 + 127) & ~int64_t(127)));  // [2][G][T]
+  uint64_t* bars = (uint64_t*)(smem + pc.off_bar);
+  const int S = pc.stages;
+  uint64_t* full = bars;       // [S]
+  uint64_t* empty = bars + S;  // [S]
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int T = a.T;
+  const int64_t t0 = a.tile_begin + blockIdx.x;  // this CTA's tiles: t0, t0 + grid, …
+
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], pc.ncw);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (warp == pc.ncw) {
+    // ------------------------------------------------ TMA producer
+    if (lane == 0) {
+      Ring rg;
+      auto issue = [&](const unsigned char* src, uint32_t bytes) {
+        mbar_wait_sleep(&empty[rg.st], rg.ph ^ 1);
+        mbar_expect_tx(&full[rg.st], bytes);
+        bulk_g2s(stg + rg.st * pc.stage_bytes, src, bytes, &full[rg.st]);
+        rg.next(S);
+      };
+      if (t0 < a.tile_end) issue(a.blocks + t0 * a.tile_bytes, (uint32_t)a.u_bytes);
+      for (int64_t tile = t0; tile < a.tile_end; tile += gridDim.x) {
+        const unsigned char* tb = a.blocks + tile * a.tile_bytes;
+        if (tile + gridDim.x < a.tile_end) issue(tb + gridDim.x * a.tile_bytes, (uint32_t)a.u_bytes);
+        for (int ch = 0; ch < a.NCH; ++ch)
+          issue(tb + a.u_bytes + ch * a.chunk_bytes, (uint32_t)(min(a.KC, a.G - ch * a.KC) * a.kslice_bytes));
+        for (int j = 0; j < a.NSC; ++j) issue(tb + a.off_sector + j * a.sector_bytes, (uint32_t)a.sector_bytes);
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------- consumer warps
+  const int nct = pc.ncw * 32;  // = T·NG
+  const int ct = tid / NG, g = tid % NG;
+  // offsets of this thread's B⁺ entries inside a row slot (chunk_elem, KIND_ROWBLK):
+  // slots r < RB−1 hold all NG groups, the last one the first NF (a group without a
+  // row there reads a neighbour's entry into an accumulator that is never written out)
+  const int bfull = ct * NG + g, bpart = ct * NF + min(g, NF - 1);
+  Ring rg;
+  // gather the union of the next tile (its union chunk is the current stage) into
+  // Q_u[bufn] and copy its position → union-offset table into Ix[bufn]
+  auto gather_union = [&](int bufn) {
+    mbar_wait(&full[rg.st], rg.ph);
+    const unsigned char* ub = stg + rg.st * pc.stage_bytes;
+    const int32_t* uid = (const int32_t*)ub;
+    {
+      const uint4* src = (const uint4*)(ub + a.off_idx);
+      uint4* dsti = (uint4*)((unsigned char*)Ix + bufn * a.idx_bytes);
+      for (int i = tid; i < (int)(a.idx_bytes / 16); i += nct) dsti[i] = src[i];
+    }
+    double* dst = Qu + (size_t)bufn * a.Umax * VP;
+    if (a.exp_flags & 1) {  // experiment: no gather (timing only)
+      cp_async_commit();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[rg.st]);
+      rg.next(S);
+      return;
+    }
+    // element e = u·V + vv, e = tid, tid + nct, …: (u, vv) stepped without divisions
+    int u = tid / V, vv = tid - (tid / V) * V;
+    const int du = nct / V, dv = nct - du * V;
+    for (int e = tid; e < a.Umax * V; e += nct) {
+      cp_async8(dst + u * VP + vv, a.Q + int64_t(uid[u]) * a.acs + vv * a.avs);
+      u += du;
+      vv += dv;
+      if (vv >= V) {
+        vv -= V;
+        ++u;
+      }
+    }
+    cp_async_commit();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[rg.st]);
+    rg.next(S);
+  };
+  auto store_tile = [&](int64_t tile) {  // one bulk store of the tile's live output rows
+    const int64_t nlive = min((int64_t)T, a.n_owned - tile * T);
+    if (nlive > 0) bulk_s2g(a.out + tile * T * (int64_t)(V * NM), O, (uint32_t)(nlive * V * NM * 8));
+  };
+  if (t0 < a.tile_end) gather_union(0);
+
+  int buf = 0;
+  int64_t prev = -1;
+  for (int64_t tile = t0; tile < a.tile_end; tile += gridDim.x, buf ^= 1) {
+    cp_async_wait<0>();
+    consumer_bar(nct);  // Q_u[buf] complete and visible; tile t−1 fully done (O written, Q_u[buf^1] free)
+    if (a.dense_out && tid == 0 && prev >= 0) store_tile(prev);
+    if (tile + gridDim.x < a.tile_end) gather_union(buf ^ 1);
+    const double* Qb = Qu + (size_t)buf * a.Umax * VP;
+    const uint16_t* ixb = (const uint16_t*)((const unsigned char*)Ix + buf * a.idx_bytes);
+    double qi[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) qi[v] = Qb[ct * VP + v];  // the tile's own cells lead its union
+
+    double acc[RB][V];
+#pragma unroll
+    for (int r = 0; r < RB; ++r)
+#pragma unroll
+      for (int v = 0; v < V; ++v) acc[r][v] = 0.0;
+    // Main loop over chunks of KC = 2 positions, software-pipelined: the averages of
+    // chunk ch+1 and the union offsets of chunk ch+2 are loaded while chunk ch's
+    // FMAs run (they do not depend on the stage ring); the B⁺ entries of chunk ch+1
+    // are loaded right after its stage arrives, before chunk ch's stage is released.
+    // Ping-pong buffers (qa/qb, ba/bb) avoid register moves.  A trailing odd
+    // position (G odd) is peeled.
+    static_assert(KC == 2, "row-block main loop is written for position pairs");
+    const int G = a.G, nfc = G / 2, nch = (G + 1) / 2;
+    const uint32_t* ix2 = reinterpret_cast<const uint32_t*>(ixb) + ct;  // [chunk][T] offset pairs
+    auto ldq = [&](int off, double (&d)[V]) {
+      const double* q = Qb + off;
+#pragma unroll
+      for (int v = 0; v + 1 < V; v += 2) {
+        const double2 x = *reinterpret_cast<const double2*>(q + v);
+        d[v] = x.x;
+        d[v + 1] = x.y;
+      }
+      if (V & 1) d[V - 1] = q[V - 1];
+    };
+    auto ldq2 = [&](uint32_t pr, double (&d)[2][V]) {
+      ldq(int(pr & 0xffffu), d[0]);
+      ldq(int(pr >> 16), d[1]);
+    };
+    auto ldb = [&](const double* Bs, double (&b)[2][RB]) {
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+#pragma unroll
+        for (int r = 0; r < RB; ++r) b[k][r] = Bs[(k * R + r * NG) * T + (r < RB - 1 ? bfull : bpart)];
+    };
+    auto fma_pos = [&](const double (&q)[V], const double (&b)[RB]) {
+      double dq[V];
+#pragma unroll
+      for (int v = 0; v < V; ++v) dq[v] = q[v] - qi[v];
+#pragma unroll
+      for (int r = 0; r < RB; ++r)
+#pragma unroll
+        for (int v = 0; v < V; ++v) acc[r][v] += b[r] * dq[v];
+    };
+    auto stage_ptr = [&]() { return (const double*)(stg + rg.st * pc.stage_bytes); };
+    auto release = [&]() {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[rg.st]);
+      rg.next(S);
+    };
+    double qa[2][V], qb[2][V], ba[2][RB], bb[2][RB];
+    ldq2(ix2[0], qa);
+    uint32_t ipn = ix2[min(1, nch - 1) * T];
+    mbar_wait(&full[rg.st], rg.ph);
+    ldb(stage_ptr(), ba);
+    // one full chunk: q/b hold its averages and B⁺ entries; qn/bn receive chunk ch+1's
+    auto chunk = [&](int ch, const double (&q)[2][V], const double (&b)[2][RB], double (&qn)[2][V],
+                     double (&bn)[2][RB]) {
+      ldq2(ipn, qn);
+      ipn = ix2[min(ch + 2, nch - 1) * T];
+      fma_pos(q[0], b[0]);
+      fma_pos(q[1], b[1]);
+      if (ch + 1 < nch) {  // next stage: its B⁺ entries (a tail chunk reads past kc into the stage: unused)
+        Ring nx = rg;
+        nx.next(S);
+        mbar_wait(&full[nx.st], nx.ph);
+        ldb((const double*)(stg + nx.st * pc.stage_bytes), bn);
+      }
+      release();
+    };
+    int ch = 0;
+    for (; ch + 1 < nfc; ch += 2) {
+      chunk(ch, qa, ba, qb, bb);
+      chunk(ch + 1, qb, bb, qa, ba);
+    }
+    const bool odd_pair = ch < nfc;
+    if (odd_pair) chunk(ch, qa, ba, qb, bb);
+    if (G & 1) {  // the last position alone (its stage already waited for)
+      fma_pos(odd_pair ? qb[0] : qa[0], odd_pair ? bb[0] : ba[0]);
+      release();
+    }
+
+    // p̂_opt rows → O[ct][v][1 + row] (after the previous tile's store has read O)
+    if (tid == 0) bulk_wait_read();
+    consumer_bar(nct);
+    {
+      double* Oc = O + (size_t)ct * V * NM + 1 + g;  // row l = r·NG + g
+#pragma unroll
+      for (int r = 0; r < RB; ++r)
+        if (r < RB - 1 || g < NF)
+#pragma unroll
+          for (int v = 0; v < V; ++v) Oc[v * NM + r * NG] = acc[r][v];
+    }
+    consumer_bar(nct);
+
+    // sector chunk (NSC pieces of TSC cells in consecutive stages) + fused
+    // epilogue, one (cell, variable) item at a time
+    const Ring rs = rg;
+    for (int j = 0; j < a.NSC; ++j) {
+      mbar_wait(&full[rg.st], rg.ph);
+      rg.next(S);
+    }
+    for (int item = tid; item < ((a.exp_flags & 16) ? 0 : T * V); item += nct) {  // flag 16: no epilogue
+      const int c2 = item / V, v2 = item - (item / V) * V;
+      const int j = c2 / a.TSC, cl = c2 - j * a.TSC;
+      const int sst = rs.st + j < S ? rs.st + j : rs.st + j - S;
+      const unsigned char* sb = stg + sst * pc.stage_bytes;
+      const double q2 = Qb[c2 * VP + v2];
+      double* row = O + (size_t)item * NM;
+      double accr[R];
+#pragma unroll
+      for (int l = 0; l < R; ++l) accr[l] = row[1 + l];
+      double dqs[NCAP];
+#pragma unroll
+      for (int p = 0; p < NCAP; ++p) dqs[p] = Qb[ixb[idx_elem(KIND_ROWBLK, T, p, c2)] + v2] - q2;
+      const uint8_t vmask = sb[a.sinv_bytes + cl];
+      bool valid[NV];
+#pragma unroll
+      for (int s = 0; s < NV; ++s) valid[s] = (vmask >> s) & 1;
+      double ps[NV][D];
+      sector_apply<D>((const double*)sb + size_t(cl) * NV * D * D, dqs, ps);
+      if (a.dense_out) {
+        cweno_epilogue<D, NM>(q2, accr, ps, valid, a, row, nullptr, nullptr);
+      } else {
+        double w[NM];
+        cweno_epilogue<D, NM>(q2, accr, ps, valid, a, w, nullptr, nullptr);
+        const int64_t c = tile * T + c2;
+        if (c < a.n_owned) {
+          double* o = a.out + c * a.ccs + v2 * a.cvs;
+#pragma unroll
+          for (int l = 0; l < NM; ++l) o[l] = w[l];
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      int sst = rs.st;
+      for (int j = 0; j < a.NSC; ++j) {
+        mbar_arrive(&empty[sst]);
+        if (++sst == S) sst = 0;
+      }
+    }
+    if (a.dense_out) fence_proxy_async();  // O rows → visible to the bulk store after the next barrier
+    prev = tile;
+  }
+  consumer_bar(nct);
+  if (a.dense_out && tid == 0 && prev >= 0) {
+    store_tile(prev);
+    bulk_wait_all();
+  }
+  cp_async_wait<0>();
+}
+
+// Instantiations per translation unit (rowblk_2d.cu, rowblk_3d.cu)
+template <int D, int M>
+PipeFn rowblk_fn_v(int V) {
+  switch (V) {
+    case 1: return k_rowblk<D, M, 1>;
+    case 2: return k_rowblk<D, M, 2>;
+    case 3: return k_rowblk<D, M, 3>;
+    case 4: return k_rowblk<D, M, 4>;
+    case 5: return k_rowblk<D, M, 5>;
+    case 6: return k_rowblk<D, M, 6>;
+    case 7: return k_rowblk<D, M, 7>;
+    case 8: return k_rowblk<D, M, 8>;
+    case 9: return k_rowblk<D, M, 9>;
+    default: return nullptr;
+  }
+}
+
+}  // namespace cwr

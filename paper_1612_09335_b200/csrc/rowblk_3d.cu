@@ -1,0 +1,16 @@
+// Row-block kernel instantiations for d = 3 (see rowblk.cuh).
+#include "rowblk.cuh"
+
+namespace cwr {
+
+PipeFn rowblk_fn_3d(int M, int V) {
+  if (M == 2) return rowblk_fn_v<3, 2>(V);
+  if (M == 3) return rowblk_fn_v<3, 3>(V);
+  return nullptr;
+}
+
+cudaError_t rowblk_upload_sigma_3d(const double* packed, size_t bytes, size_t offset) {
+  return cudaMemcpyToSymbol(c_sig, packed, bytes, offset);
+}
+
+}  // namespace cwr

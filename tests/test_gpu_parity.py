@@ -52,12 +52,16 @@ CASES = [
 ]
 
 
+@pytest.mark.parametrize("family", ["0", "1"], ids=["cellvar", "rowblk"])
 @pytest.mark.parametrize("case", CASES, ids=lambda c: c[0])
-def test_small_mesh_parity(case):
+def test_small_mesh_parity(case, family, monkeypatch):
+    """Both kernel families (CWRECO_FAMILY: 0 = one thread per (cell, variable),
+    1 = row-block where instantiated, ℳ ≥ 10) against the oracle and k_simple."""
     name, d, n, M, jit, per, V, ncheck = case
     nodes, cells, period = gen.box_mesh(d, n, per, jit, 21)
     rng = np.random.default_rng(3)
     Qin = rng.standard_normal((cells.shape[0], V)) * 2.0 + 3.0
+    monkeypatch.setenv("CWRECO_FAMILY", family)
     ctx = P.setup_context(nodes, cells, period, M, V, device=0)
     m = OracleMesh(nodes, cells, period, M)
     assert np.array_equal(ctx.permutation(), m.perm)
@@ -117,7 +121,9 @@ def test_constant_and_linear_data():
         assert np.abs(w[i][:, 4:]).max() <= 1e-11 * np.abs(Ql).max()       # no quadratic modes
 
 
-def test_strides_parts_determinism():
+@pytest.mark.parametrize("family", ["0", "1"], ids=["cellvar", "rowblk"])
+def test_strides_parts_determinism(family, monkeypatch):
+    monkeypatch.setenv("CWRECO_FAMILY", family)
     nodes, cells, period = gen.box_mesh(2, 20, True, 0.2, 9)
     V, M = 4, 3
     Q = np.random.default_rng(1).standard_normal((cells.shape[0], V))
@@ -145,9 +151,11 @@ def test_strides_parts_determinism():
     assert torch.equal(o2, ref)
 
 
-def test_multirank_emulation_bitwise():
+@pytest.mark.parametrize("family", ["0", "1"], ids=["cellvar", "rowblk"])
+def test_multirank_emulation_bitwise(family, monkeypatch):
     """T5: P logical ranks on one GPU (one context each, ghosts filled from the
     global array, library halo pack checked) reproduce the 1-rank output bitwise."""
+    monkeypatch.setenv("CWRECO_FAMILY", family)
     nodes, cells, period = gen.box_mesh(2, 22, True, 0.2, 13)
     V, M, NR = 3, 3, 3
     Qin = np.random.default_rng(2).standard_normal((cells.shape[0], V))

@@ -27,7 +27,7 @@ if [[ $what == ncufull ]]; then
   for c in $ncfg; do
     cmd="python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline"
     $cmd > gpurun_out/ncu_plain_$c.log 2>&1 && \
-    ncu --set full --clock-control none --import-source on -k regex:k_pipelined -s 3 -c 1 \
+    ncu --set full --clock-control none --import-source on -k "regex:k_pipelined|k_rowblk" -s 3 -c 1 \
         -o gpurun_out/prof_$c -f $cmd > gpurun_out/ncu_full_$c.log 2>&1
     echo "ncu full $c exit $?"; tail -3 gpurun_out/ncu_full_$c.log
   done
@@ -38,7 +38,7 @@ if [[ $what == ncu || $what == all ]]; then
   ncu --metrics gpu__time_duration.sum --clock-control none --csv \
       --log-file gpurun_out/launches_$ncfg.csv $cmd > gpurun_out/ncu_launch_$ncfg.log 2>&1
   echo "ncu launches exit $?"
-  ncu --set full --clock-control none --import-source on -k regex:k_pipelined -s 3 -c 1 \
+  ncu --set full --clock-control none --import-source on -k "regex:k_pipelined|k_rowblk" -s 3 -c 1 \
       -o gpurun_out/prof_$ncfg -f $cmd > gpurun_out/ncu_full_$ncfg.log 2>&1
   echo "ncu full exit $?"; tail -5 gpurun_out/ncu_full_$ncfg.log
 fi

@@ -28,9 +28,9 @@ end = next((i for i in range(start + 1, len(lines)) if lines[i].startswith("//--
 line_of = {}
 cur = None
 for ln in lines[start:end]:
-    m = re.search(r'line (\d+)', ln)
+    m = re.search(r'File "([^"]+)", line (\d+)', ln)
     if ln.strip().startswith("//##") and m:
-        cur = int(m.group(1))
+        cur = (m.group(1), int(m.group(2)))
         continue
     m = re.match(r'\s*/\*([0-9a-f]+)\*/', ln)
     if m and cur is not None:
@@ -41,7 +41,7 @@ st, ins = defaultdict(float), defaultdict(float)
 why = defaultdict(lambda: defaultdict(float))
 for r in data:
     off = int(r[0], 16) - base
-    l = line_of.get(off, -1)
+    l = line_of.get(off, ("?", -1))
     st[l] += float(r[si] or 0)
     ins[l] += float(r[ie] or 0)
     for h, i in zip(reasons, ri):
@@ -50,10 +50,23 @@ for r in data:
         except ValueError:
             pass
 ts, ti = sum(st.values()), sum(ins.values())
-src = open("paper_1612_09335_b200/csrc/kernels.cu").read().splitlines()
-print(f"{'line':>5} {'stall%':>7} {'inst%':>7}  source")
+srcs = {}
+
+
+def text(f, n):
+    if f not in srcs:
+        try:
+            srcs[f] = open(f).read().splitlines()
+        except OSError:
+            srcs[f] = []
+    src = srcs[f]
+    return src[n - 1].strip()[:80] if 0 < n <= len(src) else "?"
+
+
+print(f"{'file:line':>18} {'stall%':>7} {'inst%':>7}  source")
 for l in sorted(st, key=lambda k: -st[k])[:top]:
-    s = src[l - 1].strip()[:90] if 0 < l <= len(src) else "?"
+    s = text(*l)
     top2 = sorted(why[l].items(), key=lambda kv: -kv[1])[:2]
     tw = " ".join(f"{k[6:]}:{100 * v / max(st[l], 1):.0f}%" for k, v in top2)
-    print(f"{l:5d} {100 * st[l] / ts:7.1f} {100 * ins[l] / ti:7.1f}  {tw:28s} {s}")
+    fl = f"{l[0].split('/')[-1]}:{l[1]}"
+    print(f"{fl:>18} {100 * st[l] / ts:7.1f} {100 * ins[l] / ti:7.1f}  {tw:28s} {s}")

@@ -186,6 +186,22 @@ cwreco_status cwreco_halo_pack(cwreco_ctx* ctx, const double* d_avgs, int64_t a_
 cwreco_status cwreco_reconstruct(cwreco_ctx* ctx, const double* d_avgs, int64_t a_cell_stride,
                                  int64_t a_var_stride, double* d_coeffs, int64_t c_cell_stride,
                                  int64_t c_var_stride, int part, cwreco_stream stream);
+/* End-to-end pass on HOST buffers (the whole hot path behind one call):
+ *   h_avgs   [n_owned + n_ghost][nvars] dense row-major, local order (ghost rows
+ *            already filled by the caller when nranks > 1);
+ *   h_coeffs [n_owned][nvars][ℳ] dense, written before the call returns.
+ * The library copies h_avgs into its own device buffers (allocated on first use,
+ * kept until cwreco_destroy), reconstructs in n_pieces consecutive tile ranges on
+ * `stream`, and copies each range's coefficients back on an internal copy stream as
+ * soon as that range is done, so the device→host transfer overlaps the remaining
+ * ranges.  Page-locked host buffers (cudaHostAlloc / cudaHostRegister, torch
+ * pin_memory) give asynchronous copies; pageable buffers work but serialise.
+ * n_pieces ≤ 0 selects the default (4).  Synchronous: returns after h_coeffs is
+ * complete.  Errors as cwreco_reconstruct; ENOMEM if the device buffers cannot be
+ * allocated. */
+cwreco_status cwreco_reconstruct_host(cwreco_ctx* ctx, const double* h_avgs, double* h_coeffs, int n_pieces,
+                                      cwreco_stream stream);
+
 /* Debug tap (tests): intermediates of n_sel owned cells (local ids), computed by
  * the SIMPLE kernel and copied to host (synchronises `stream`):
  *   popt [n][nvars][ℳ], psec [n][dim+1][nvars][dim+1], sigma [n][dim+2][nvars],

@@ -44,9 +44,9 @@ class _Info(ctypes.Structure):
 
 
 def _load():
-    if not os.path.exists(_LIB_PATH):
-        from . import _build
-        _build.build()
+    from . import _build
+    if not os.path.exists(_LIB_PATH) or _build.stale_abi(_LIB_PATH):
+        _build.build()   # missing, or older than include/cwreco.h's entry points
     L = ctypes.CDLL(_LIB_PATH)
     P, I64, I32, D = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
     sigs = {
@@ -68,6 +68,7 @@ def _load():
         "cwreco_halo_pack": [P, P, I64, I64, P, P],
         "cwreco_reconstruct": [P, P, I64, I64, P, I64, I64, I32, P],
         "cwreco_reconstruct_debug": [P, P, I64, I64, I64, P, P, P, P, P, P, P],
+        "cwreco_reconstruct_host": [P, P, P, I32, P],
     }
     for name, args in sigs.items():
         f = getattr(L, name)
@@ -230,6 +231,25 @@ class Context:
         _check(lib.cwreco_reconstruct(self._h, ctypes.c_void_p(avgs.data_ptr()), a_cs, a_vs,
                                       ctypes.c_void_p(out.data_ptr()), c_cs, c_vs, int(part),
                                       _stream_handle(stream)))
+        return out
+
+    def reconstruct_host(self, avgs, out=None, n_pieces=0, stream=None):
+        """End to end on HOST buffers (cwreco_reconstruct_host): avgs float64 CPU tensor
+        or numpy array [n_local, V] (C-contiguous; page-locked for async copies);
+        returns / fills out [n_owned, V, ℳ] on the host.  Synchronous."""
+        import torch
+        if isinstance(avgs, np.ndarray):
+            avgs = torch.from_numpy(np.ascontiguousarray(avgs, dtype=np.float64))
+        if avgs.is_cuda or avgs.dtype != torch.float64 or avgs.dim() != 2 or not avgs.is_contiguous():
+            raise ValueError("avgs must be a C-contiguous 2-D float64 host tensor")
+        if out is None:
+            out = torch.empty((self.info()["n_owned"], self.V, self.nm), dtype=torch.float64,
+                              pin_memory=avgs.is_pinned())
+        if out.is_cuda or out.dtype != torch.float64 or not out.is_contiguous():
+            raise ValueError("out must be a C-contiguous float64 host tensor")
+        _check(lib.cwreco_reconstruct_host(self._h, ctypes.c_void_p(avgs.data_ptr()),
+                                           ctypes.c_void_p(out.data_ptr()), int(n_pieces),
+                                           _stream_handle(stream)))
         return out
 
     def reconstruct_debug(self, avgs, cells, stream=None):

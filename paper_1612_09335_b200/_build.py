@@ -63,6 +63,21 @@ def build(verbose=False):
     return OUT
 
 
+def stale_abi(path):
+    """True if the built library lacks an entry point include/cwreco.h declares."""
+    import re
+    try:
+        with open(os.path.join(INC, "cwreco.h")) as f:
+            names = set(re.findall(r"\b(cwreco_[a-z_]+)\s*\(", f.read()))
+        out = subprocess.run(["nm", "-D", "--defined-only", path], capture_output=True, text=True).stdout
+    except OSError:
+        return False
+    if not out:
+        return False
+    have = set(re.findall(r" T (cwreco_\w+)", out))
+    return bool(names - have)
+
+
 def needs_build():
     if not os.path.exists(OUT):
         return True

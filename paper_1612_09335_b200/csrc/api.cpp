@@ -316,6 +316,17 @@ cwreco_status cwreco_reconstruct(cwreco_ctx* c, const double* d_avgs, int64_t ac
   });
 }
 
+cwreco_status cwreco_reconstruct_host(cwreco_ctx* c, const double* h_avgs, double* h_coeffs, int n_pieces,
+                                      cwreco_stream stream) {
+  return guard([&] {
+    need(c != nullptr, CWRECO_EINVAL, "reconstruct_host: NULL ctx");
+    need_device(c, "reconstruct_host");
+    need(c->has_blocks, CWRECO_ESTATE, "reconstruct_host: call cwreco_precompute first");
+    need(h_avgs && h_coeffs, CWRECO_EINVAL, "reconstruct_host: NULL buffer");
+    cwr::dev_reconstruct_host(c, h_avgs, h_coeffs, n_pieces > 0 ? n_pieces : 4, stream);
+  });
+}
+
 cwreco_status cwreco_reconstruct_debug(cwreco_ctx* c, const double* d_avgs, int64_t acs, int64_t avs, int64_t n_sel,
                                        const int64_t* cells, double* popt, double* psec, double* sigma,
                                        double* omega, double* w, cwreco_stream stream) {

@@ -230,6 +230,7 @@ void dev_upload_aux(cwreco_ctx* c);
 void dev_download_tile(const cwreco_ctx* c, int64_t tile, unsigned char* host);
 void dev_reconstruct(cwreco_ctx* c, const double* avgs, int64_t acs, int64_t avs, double* coeffs,
                      int64_t ccs, int64_t cvs, int part, void* stream);
+void dev_reconstruct_host(cwreco_ctx* c, const double* h_avgs, double* h_coeffs, int n_pieces, void* stream);
 void dev_debug(cwreco_ctx* c, const double* avgs, int64_t acs, int64_t avs, int64_t n_sel,
                const int64_t* cells, double* popt, double* psec, double* sigma, double* omega,
                double* w, void* stream);

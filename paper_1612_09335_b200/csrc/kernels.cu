@@ -38,6 +38,11 @@ struct DeviceState {
   int64_t dbg_bytes = 0;
   int64_t* dbg_cells = nullptr;
   int64_t dbg_ncells = 0;
+  double* h_avgs = nullptr;  // device buffers of cwreco_reconstruct_host (lazy)
+  double* h_coeffs = nullptr;
+  int64_t h_avgs_n = 0, h_coeffs_n = 0;
+  cudaStream_t copy_stream = nullptr;
+  std::vector<cudaEvent_t> piece_done;
   bool have_cfg = false;  // launch shape of the pipelined kernel, fixed at precompute
   PipeCfg cfg{};
   int cfg_ctas = 1;
@@ -524,6 +529,10 @@ void dev_destroy(cwreco_ctx* c) {
   cudaFree(c->dev->send);
   cudaFree(c->dev->dbg);
   cudaFree(c->dev->dbg_cells);
+  cudaFree(c->dev->h_avgs);
+  cudaFree(c->dev->h_coeffs);
+  for (cudaEvent_t e : c->dev->piece_done) cudaEventDestroy(e);
+  if (c->dev->copy_stream) cudaStreamDestroy(c->dev->copy_stream);
   delete c->dev;
   c->dev = nullptr;
 }
@@ -569,18 +578,15 @@ void dev_download_tile(const cwreco_ctx* c, int64_t tile, unsigned char* host) {
 
 int64_t dev_bytes(const cwreco_ctx* c) {
   if (!c->dev) return 0;
-  return c->dev->blocks_bytes + c->dev->dbg_bytes + c->dev->n_send * 8;
+  return c->dev->blocks_bytes + c->dev->dbg_bytes + c->dev->n_send * 8 + (c->dev->h_avgs_n + c->dev->h_coeffs_n) * 8;
 }
 
-void dev_reconstruct(cwreco_ctx* c, const double* avgs, int64_t acs, int64_t avs, double* coeffs, int64_t ccs,
-                     int64_t cvs, int part, void* stream) {
-  cudaStream_t st = (cudaStream_t)stream;
+// One launch of the reconstruction over owned tiles [tile_begin, tile_end).
+static void launch_range(cwreco_ctx* c, const double* avgs, int64_t acs, int64_t avs, double* coeffs, int64_t ccs,
+                         int64_t cvs, int64_t tile_begin, int64_t tile_end, cudaStream_t st) {
   KArgs a = make_args(c, avgs, acs, avs, coeffs, ccs, cvs);
-  if (part == CWRECO_PART_INTERIOR) {
-    a.tile_end = c->n_int_tiles;
-  } else if (part == CWRECO_PART_BOUNDARY) {
-    a.tile_begin = c->n_int_tiles;
-  }
+  a.tile_begin = tile_begin;
+  a.tile_end = tile_end;
   if (a.tile_end <= a.tile_begin) return;
   const int nm = c->nm;
   if (c->kernel == CWRECO_KERNEL_SIMPLE) {
@@ -600,6 +606,60 @@ void dev_reconstruct(cwreco_ctx* c, const double* avgs, int64_t acs, int64_t avs
     f<<<g, b, p.smem, st>>>(a, p);
   }
   CK(cudaGetLastError());
+}
+
+void dev_reconstruct(cwreco_ctx* c, const double* avgs, int64_t acs, int64_t avs, double* coeffs, int64_t ccs,
+                     int64_t cvs, int part, void* stream) {
+  int64_t t0 = 0, t1 = c->n_tiles;
+  if (part == CWRECO_PART_INTERIOR) {
+    t1 = c->n_int_tiles;
+  } else if (part == CWRECO_PART_BOUNDARY) {
+    t0 = c->n_int_tiles;
+  }
+  launch_range(c, avgs, acs, avs, coeffs, ccs, cvs, t0, t1, (cudaStream_t)stream);
+}
+
+// cwreco_reconstruct_host: H2D of the averages, n_pieces tile ranges on `stream`,
+// each range's D2H on the copy stream as soon as its event fires.
+void dev_reconstruct_host(cwreco_ctx* c, const double* h_avgs, double* h_coeffs, int n_pieces, void* stream) {
+  DeviceState* ds = c->dev;
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaSetDevice(c->device));
+  const int V = c->V, nm = c->nm;
+  const int64_t na = (c->n_owned + c->n_ghost) * V, nc = c->n_owned * V * nm;
+  auto grow = [&](double*& p, int64_t& have, int64_t need_n) {
+    if (have >= need_n) return;
+    cudaFree(p);
+    p = nullptr;
+    have = 0;
+    if (cudaMalloc(&p, std::max<int64_t>(1, need_n) * 8) != cudaSuccess) {
+      cudaGetLastError();
+      fail(CWRECO_ENOMEM, "reconstruct_host: device buffer allocation failed");
+    }
+    have = need_n;
+  };
+  grow(ds->h_avgs, ds->h_avgs_n, na);
+  grow(ds->h_coeffs, ds->h_coeffs_n, nc);
+  if (!ds->copy_stream) CK(cudaStreamCreateWithFlags(&ds->copy_stream, cudaStreamNonBlocking));
+  while ((int)ds->piece_done.size() < n_pieces) {
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ds->piece_done.push_back(e);
+  }
+  CK(cudaMemcpyAsync(ds->h_avgs, h_avgs, na * 8, cudaMemcpyHostToDevice, st));
+  const int64_t nt = c->n_tiles, T = c->lay.T, row = (int64_t)V * nm;
+  for (int k = 0; k < n_pieces; ++k) {
+    const int64_t a = nt * k / n_pieces, b = nt * (k + 1) / n_pieces;
+    if (b <= a) continue;
+    launch_range(c, ds->h_avgs, V, 1, ds->h_coeffs, row, nm, a, b, st);
+    CK(cudaEventRecord(ds->piece_done[k], st));
+    CK(cudaStreamWaitEvent(ds->copy_stream, ds->piece_done[k], 0));
+    const int64_t c0 = a * T, c1 = std::min(c->n_owned, b * T);
+    CK(cudaMemcpyAsync(h_coeffs + c0 * row, ds->h_coeffs + c0 * row, (c1 - c0) * row * 8, cudaMemcpyDeviceToHost,
+                       ds->copy_stream));
+  }
+  CK(cudaStreamSynchronize(ds->copy_stream));
+  CK(cudaStreamSynchronize(st));
 }
 
 void dev_debug(cwreco_ctx* c, const double* avgs, int64_t acs, int64_t avs, int64_t n_sel, const int64_t* cells,

@@ -189,3 +189,21 @@ def test_multirank_emulation_bitwise(family, monkeypatch):
         c.reconstruct(A, out, part=P.PART_INTERIOR)
         c.reconstruct(A, out, part=P.PART_BOUNDARY)
         assert np.array_equal(out.cpu().numpy(), ref[loc[: inf["n_owned"]]])
+
+
+def test_reconstruct_host_end_to_end():
+    """cwreco_reconstruct_host (host buffers, pieces overlapped with their D2H) equals
+    the device-pointer call bitwise, for pinned and pageable buffers and any piece count."""
+    nodes, cells, period = gen.box_mesh(3, 7, True, 0.1, 5)
+    V, M = 5, 3
+    Q = np.random.default_rng(4).standard_normal((cells.shape[0], V)) + 2.0
+    ctx = P.setup_context(nodes, cells, period, M, V, device=0)
+    Qp = Q[ctx.permutation()]
+    ref = ctx.reconstruct(torch.tensor(Qp, device="cuda")).cpu()
+    for pinned in (True, False):
+        h = torch.from_numpy(Qp.copy())
+        if pinned:
+            h = h.pin_memory()
+        for pieces in (0, 1, 3, 7):
+            out = ctx.reconstruct_host(h, n_pieces=pieces)
+            assert torch.equal(out, ref), (pinned, pieces)

@@ -33,6 +33,7 @@ __host__ __device__ constexpr int sig_off(int D, int M) {
 constexpr int SIG_TOTAL = sig_off(4, 1);
 static __constant__ double c_sig[SIG_TOTAL];
 
+
 struct KArgs {
   const unsigned char* blocks;
   int64_t tile_bytes, u_bytes, off_idx, idx_bytes, ids_bytes, chunk_bytes, kslice_bytes, off_sector, sinv_bytes,
@@ -61,11 +62,11 @@ struct DbgOut {
 
 __device__ __forceinline__ double powr(double t, int r) {
   if (r == 4) {
-    const double t2 = t * t;
-    return t2 * t2;
+    const double t2 = __dmul_rn(t, t);
+    return __dmul_rn(t2, t2);
   }
   double p = 1.0;
-  for (int i = 0; i < r; ++i) p *= t;
+  for (int i = 0; i < r; ++i) p = __dmul_rn(p, t);
   return p;
 }
 
@@ -93,12 +94,13 @@ __device__ __forceinline__ void cweno_epilogue(double qi, double* acc, const dou
   for (int l = 0; l < D; ++l) {
     double s = 0.0;
 #pragma unroll
-    for (int q = 0; q <= D; ++q) s += valid[q] ? ps[q][l] : 0.0;
-    acc[l] = (acc[l] - ls * s) * il0;
+    for (int q = 0; q <= D; ++q) s = __dadd_rn(s, valid[q] ? ps[q][l] : 0.0);
+    acc[l] = __dmul_rn(__fma_rn(-ls, s, acc[l]), il0);
   }
 #pragma unroll
-  for (int l = D; l < R; ++l) acc[l] = acc[l] * il0;
-  // σ_0 = P0ᵀ Σ P0 and σ_s = P_sᵀ Σ P_s
+  for (int l = D; l < R; ++l) acc[l] = __dmul_rn(acc[l], il0);
+  // σ_0 = P0ᵀ Σ P0 and σ_s = P_sᵀ Σ P_s; explicit roundings (here and in
+  // every kernel) so that all kernels perform the same operations bit for bit
   double sg0 = 0.0;
   {
     int idx = SO;
@@ -106,9 +108,9 @@ __device__ __forceinline__ void cweno_epilogue(double qi, double* acc, const dou
     for (int l = 0; l < R; ++l) {
       double t = 0.0;
 #pragma unroll
-      for (int m = l; m < R; ++m) t += c_sig[idx + m - l] * acc[m];
+      for (int m = l; m < R; ++m) t = __fma_rn(c_sig[idx + m - l], acc[m], t);
       idx += R - l;
-      sg0 += acc[l] * t;
+      sg0 = __fma_rn(acc[l], t, sg0);
     }
   }
   double sgs[D + 1];
@@ -120,38 +122,38 @@ __device__ __forceinline__ void cweno_epilogue(double qi, double* acc, const dou
     for (int l = 0; l < D; ++l) {
       double t = 0.0;
 #pragma unroll
-      for (int m = l; m < D; ++m) t += c_sig[idx + m - l] * ps[s][m];
+      for (int m = l; m < D; ++m) t = __fma_rn(c_sig[idx + m - l], ps[s][m], t);
       idx += R - l;
-      v += ps[s][l] * t;
+      v = __fma_rn(ps[s][l], t, v);
     }
     sgs[s] = v;
   }
   // ω̃_s = λ̄_s/(σ_s+ε)^r, ω_s = ω̃_s/Σ ω̃; invalid sectors get 0 (R14)
   // reciprocals instead of divisions (one extra rounding, far inside the 1e-11 bar)
-  const double wt0 = l0 * __drcp_rn(powr(sg0 + a.eps, a.r));
+  const double wt0 = __dmul_rn(l0, __drcp_rn(powr(__dadd_rn(sg0, a.eps), a.r)));
   double wts[D + 1];
   double sum = wt0;
 #pragma unroll
   for (int s = 0; s <= D; ++s) {
-    wts[s] = valid[s] ? ls * __drcp_rn(powr(sgs[s] + a.eps, a.r)) : 0.0;
-    sum += wts[s];
+    wts[s] = valid[s] ? __dmul_rn(ls, __drcp_rn(powr(__dadd_rn(sgs[s], a.eps), a.r))) : 0.0;
+    sum = __dadd_rn(sum, wts[s]);
   }
   const double isum = __drcp_rn(sum);
-  const double om0 = wt0 * isum;
+  const double om0 = __dmul_rn(wt0, isum);
   double oms[D + 1];
 #pragma unroll
-  for (int s = 0; s <= D; ++s) oms[s] = wts[s] * isum;
+  for (int s = 0; s <= D; ++s) oms[s] = __dmul_rn(wts[s], isum);
   // w = Σ_s ω_s P_s;  w[0] := Q_i/ψ1 (R17)
   w[0] = p0;
 #pragma unroll
   for (int l = 0; l < D; ++l) {
-    double v = om0 * acc[l];
+    double v = __dmul_rn(om0, acc[l]);
 #pragma unroll
-    for (int s = 0; s <= D; ++s) v += oms[s] * ps[s][l];
+    for (int s = 0; s <= D; ++s) v = __fma_rn(oms[s], ps[s][l], v);
     w[l + 1] = v;
   }
 #pragma unroll
-  for (int l = D; l < R; ++l) w[l + 1] = om0 * acc[l];
+  for (int l = D; l < R; ++l) w[l + 1] = __dmul_rn(om0, acc[l]);
   if (sigma_out) {
     sigma_out[0] = sg0;
     omega_out[0] = om0;
@@ -172,7 +174,7 @@ __device__ __forceinline__ void sector_apply(const double* sinv, const double (&
     for (int l = 0; l < D; ++l) {
       double t = 0.0;
 #pragma unroll
-      for (int m = 0; m < D; ++m) t += sinv[(s * D + l) * D + m] * dqs[s * D + m];
+      for (int m = 0; m < D; ++m) t = __fma_rn(sinv[(s * D + l) * D + m], dqs[s * D + m], t);
       ps[s][l] = t;
     }
 }

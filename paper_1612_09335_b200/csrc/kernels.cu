@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(256) k_simple(KArgs a, DbgOut dbg) {
       for (int q = 0; q < NCAP; ++q)
         if (p == q) dqs[q] = dq;
 #pragma unroll
-      for (int l = 0; l < R; ++l) acc[l] += Bc[chunk_elem(a.kind, kc, R, a.V, a.T, l, ct, kk)] * dq;
+      for (int l = 0; l < R; ++l) acc[l] = __fma_rn(Bc[chunk_elem(a.kind, kc, R, a.V, a.T, l, ct, kk)], dq, acc[l]);
     }
   }
   bool valid[NV];
@@ -273,21 +273,21 @@ __global__ void __launch_bounds__(max_threads(D, M), min_blocks(D, M)) k_pipelin
 #pragma unroll
           for (int p = 0; p < KC / 2; ++p) {
             const double2 bb = b2[(p * R + l) * a.T];
-            acc[l] += bb.x * dq[2 * p];
-            acc[l] += bb.y * dq[2 * p + 1];
+            acc[l] = __fma_rn(bb.x, dq[2 * p], acc[l]);
+            acc[l] = __fma_rn(bb.y, dq[2 * p + 1], acc[l]);
           }
         }
         if (KC % 2) {  // odd chunk size: the last position is stored [R][T]
           const double* b1 = Bs + (KC / 2) * R * a.T * 2 + ct;
 #pragma unroll
-          for (int l = 0; l < R; ++l) acc[l] += b1[l * a.T] * dq[KC - 1];
+          for (int l = 0; l < R; ++l) acc[l] = __fma_rn(b1[l * a.T], dq[KC - 1], acc[l]);
         }
       } else {
 #pragma unroll
         for (int kk = 0; kk < KC; ++kk) {
           if (kk < kc) {
 #pragma unroll
-            for (int l = 0; l < R; ++l) acc[l] += Bs[chunk_elem(KIND_CELLVAR, kc, R, a.V, a.T, l, ct, kk)] * dq[kk];
+            for (int l = 0; l < R; ++l) acc[l] = __fma_rn(Bs[chunk_elem(KIND_CELLVAR, kc, R, a.V, a.T, l, ct, kk)], dq[kk], acc[l]);
           }
         }
       }
@@ -468,8 +468,7 @@ static PipeCfg pipe_cfg(const cwreco_ctx* c, int* ctas = nullptr) {
       rowblk_plan(L, c->dev->max_smem, want, k, st);
       if (k < want) continue;
       int occ = 0;
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)f, nthr,
-                                                       (size_t)(st * p.stage_bytes + p.q_bytes + p.out_bytes + 16 * st)));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)f, nthr, (size_t)pipe_smem(L, st)));
       if (occ >= want) break;
       k = 0;
     }

@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(rb_consumers(nmodes(M, D) - 1, V) + 32, 1) k_r
 #pragma unroll
       for (int r = 0; r < RB; ++r)
 #pragma unroll
-        for (int v = 0; v < V; ++v) acc[r][v] += b[r] * dq[v];
+        for (int v = 0; v < V; ++v) acc[r][v] = __fma_rn(b[r], dq[v], acc[r][v]);
     };
     auto stage_ptr = [&]() { return (const double*)(stg + rg.st * pc.stage_bytes); };
     auto release = [&]() {
@@ -226,9 +226,16 @@ __global__ void __launch_bounds__(rb_consumers(nmodes(M, D) - 1, V) + 32, 1) k_r
       release();
     }
 
-    // p̂_opt rows → O[ct][v][1 + row] (after the previous tile's store has read O)
+    // (after the previous tile's bulk store has read O)
     if (tid == 0) bulk_wait_read();
     consumer_bar(nct);
+    const Ring rs = rg;  // the sector pieces: NSC consecutive stages
+    for (int j = 0; j < a.NSC; ++j) {
+      mbar_wait(&full[rg.st], rg.ph);
+      rg.next(S);
+    }
+    // ---- per-item epilogue: p̂_opt rows → O[ct][v][1 + row], then one thread per
+    // (cell, variable) runs cweno_epilogue in place
     {
       double* Oc = O + (size_t)ct * V * NM + 1 + g;  // row l = r·NG + g
 #pragma unroll
@@ -238,14 +245,6 @@ __global__ void __launch_bounds__(rb_consumers(nmodes(M, D) - 1, V) + 32, 1) k_r
           for (int v = 0; v < V; ++v) Oc[v * NM + r * NG] = acc[r][v];
     }
     consumer_bar(nct);
-
-    // sector chunk (NSC pieces of TSC cells in consecutive stages) + fused
-    // epilogue, one (cell, variable) item at a time
-    const Ring rs = rg;
-    for (int j = 0; j < a.NSC; ++j) {
-      mbar_wait(&full[rg.st], rg.ph);
-      rg.next(S);
-    }
     for (int item = tid; item < ((a.exp_flags & 16) ? 0 : T * V); item += nct) {  // flag 16: no epilogue
       const int c2 = item / V, v2 = item - (item / V) * V;
       const int j = c2 / a.TSC, cl = c2 - j * a.TSC;
@@ -262,7 +261,7 @@ __global__ void __launch_bounds__(rb_consumers(nmodes(M, D) - 1, V) + 32, 1) k_r
       const uint8_t vmask = sb[a.sinv_bytes + cl];
       bool valid[NV];
 #pragma unroll
-      for (int s = 0; s < NV; ++s) valid[s] = (vmask >> s) & 1;
+      for (int q = 0; q < NV; ++q) valid[q] = (vmask >> q) & 1;
       double ps[NV][D];
       sector_apply<D>((const double*)sb + size_t(cl) * NV * D * D, dqs, ps);
       if (a.dense_out) {

@@ -141,6 +141,16 @@ cwreco_status cwreco_build_stencils(cwreco_ctx* ctx);
  * -1 padded when starved), sector_valid [n_owned][dim+1] (0/1).  Any may be NULL. */
 cwreco_status cwreco_get_stencils(const cwreco_ctx* ctx, int32_t* central, int32_t* sectors,
                                   uint8_t* sector_valid);
+/* Upload external stencils instead of cwreco_build_stencils (S:194-211 interface):
+ * OWNED cells in SFC order (row q = SFC id own_lo + q), global SFC ids:
+ *   central [n_own][n_e]         the cell itself first, n_e distinct cells;
+ *   sectors [n_own][dim+1][dim+1] sector s of the cell: itself first, then dim
+ *                                 distinct members (ignored if not valid);
+ *   valid   [n_own][dim+1]        1 = sector usable, 0 = invalid (ω_s = 0, R14).
+ * Arrays are copied.  EINVAL on a malformed stencil, ESTATE without a mesh.
+ * (cwreco_get_stencils returns LOCAL order; cwreco_get_local_cells maps it.) */
+cwreco_status cwreco_set_stencils(cwreco_ctx* ctx, const int32_t* central, const int32_t* sectors,
+                                  const uint8_t* valid);
 /* local_to_global: [n_owned + n_ghost] SFC ids of the local cells. */
 cwreco_status cwreco_get_local_cells(const cwreco_ctx* ctx, int64_t* local_to_global);
 /* Per-cell matrices (B⁺ by Householder QR of the reduced LSQ system, sector

@@ -59,6 +59,7 @@ def _load():
         "cwreco_build_stencils": [P],
         "cwreco_get_stencils": [P, P, P, P],
         "cwreco_get_local_cells": [P, P],
+        "cwreco_set_stencils": [P, P, P, P],
         "cwreco_precompute": [P],
         "cwreco_get_sigma": [P, P],
         "cwreco_get_blocks": [P, I64, P, P, P, P, P],
@@ -161,6 +162,13 @@ class Context:
         val = np.empty((n, d + 1), dtype=np.uint8)
         _check(lib.cwreco_get_stencils(self._h, _ptr(cen), _ptr(sec), _ptr(val)))
         return cen, sec, val.astype(bool)
+
+    def set_stencils(self, central, sectors, valid):
+        """Upload external stencils (owned cells in SFC order, global SFC ids)."""
+        central = np.ascontiguousarray(central, dtype=np.int32)
+        sectors = np.ascontiguousarray(sectors, dtype=np.int32)
+        valid = np.ascontiguousarray(valid, dtype=np.uint8)
+        _check(lib.cwreco_set_stencils(self._h, _ptr(central), _ptr(sectors), _ptr(valid)))
 
     def local_cells(self):
         inf = self.info()

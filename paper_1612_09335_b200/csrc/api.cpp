@@ -180,6 +180,45 @@ cwreco_status cwreco_get_stencils(const cwreco_ctx* c, int32_t* central, int32_t
   });
 }
 
+cwreco_status cwreco_set_stencils(cwreco_ctx* c, const int32_t* central, const int32_t* sectors,
+                                  const uint8_t* valid) {
+  return guard([&] {
+    need(c && central && sectors && valid, CWRECO_EINVAL, "set_stencils: NULL");
+    need(c->has_mesh, CWRECO_ESTATE, "set_stencils: no mesh");
+    const int ne = c->ne, nv = c->d + 1;
+    const int64_t lo = c->own_lo, n_own = c->own_hi - c->own_lo;
+    for (int64_t q = 0; q < n_own; ++q) {
+      const int64_t i = lo + q;
+      const int32_t* cen = central + q * ne;
+      if (cen[0] != i)
+        cwr::fail(CWRECO_EINVAL, "set_stencils: central stencil of cell " + std::to_string(i) +
+                                     " must start with the cell itself");
+      for (int k = 0; k < ne; ++k) {
+        need(cen[k] >= 0 && cen[k] < c->N, CWRECO_EINVAL, "set_stencils: cell id out of range");
+        for (int m = 0; m < k; ++m) need(cen[m] != cen[k], CWRECO_EINVAL, "set_stencils: repeated cell in a stencil");
+      }
+      for (int v = 0; v < nv; ++v) {
+        need(valid[q * nv + v] <= 1, CWRECO_EINVAL, "set_stencils: valid flags must be 0 or 1");
+        const int32_t* sec = sectors + (q * nv + v) * nv;
+        if (!valid[q * nv + v]) continue;
+        need(sec[0] == i, CWRECO_EINVAL, "set_stencils: a valid sector must start with the cell itself");
+        for (int k = 1; k < nv; ++k) {
+          need(sec[k] >= 0 && sec[k] < c->N && sec[k] != i, CWRECO_EINVAL, "set_stencils: bad sector member");
+          for (int m = 1; m < k; ++m) need(sec[m] != sec[k], CWRECO_EINVAL, "set_stencils: repeated sector member");
+        }
+      }
+    }
+    c->central.assign(central, central + n_own * ne);
+    c->sectors.assign(sectors, sectors + n_own * nv * nv);
+    c->valid.assign(valid, valid + n_own * nv);
+    for (int64_t q = 0; q < n_own; ++q)  // invalid sectors carry no members
+      for (int v = 0; v < nv; ++v)
+        if (!c->valid[q * nv + v])
+          for (int k = 0; k < nv; ++k) c->sectors[(q * nv + v) * nv + k] = -1;
+    cwr::finalize_stencils(c);
+  });
+}
+
 cwreco_status cwreco_get_local_cells(const cwreco_ctx* c, int64_t* out) {
   return guard([&] {
     need(c && out, CWRECO_EINVAL, "get_local_cells: NULL");

@@ -213,6 +213,7 @@ void set_mesh(cwreco_ctx* c, int64_t n_nodes, const double* xyz, int64_t n_cells
               const int64_t* cells, const double* period);
 // stencil.cpp
 void build_stencils(cwreco_ctx* c);
+void finalize_stencils(cwreco_ctx* c);  // local numbering etc. of c->central/sectors/valid
 // basis.cpp
 void basis_eval(int d, int M, const double* xi, double* out);  // ψ_l(ξ), l < ℳ
 std::vector<double> sigma_matrix(int d, int M);                  // Σ by quadrature

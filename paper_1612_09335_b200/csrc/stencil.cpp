@@ -359,7 +359,14 @@ void build_stencils(cwreco_ctx* c) {
   if (exhausted >= 0)
     fail(CWRECO_ESTENCIL, "build_stencils: central stencil exhausted (cell " + std::to_string(exhausted) + ")");
 
-  // ---- ghosts, interior/boundary split, local numbering
+  finalize_stencils(c);
+}
+
+// Ghosts, interior/boundary split, local numbering, extras and gather length of the
+// stencils in c->central / c->sectors / c->valid (built or uploaded).
+void finalize_stencils(cwreco_ctx* c) {
+  const int d = c->d, ne = c->ne, nv = d + 1;
+  const int64_t lo = c->own_lo, hi = c->own_hi, n_own = hi - lo;
   std::vector<uint8_t> is_bnd(n_own, 0);
   std::vector<int64_t> ghosts;
   for (int64_t q = 0; q < n_own; ++q) {

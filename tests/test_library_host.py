@@ -220,3 +220,39 @@ def test_partition_host_logic():
     assert c1.send_total() == counts0[1]
     with pytest.raises(P.CwrecoError, match="EINVAL"):
         c1.set_send_lists(np.array([1, 0]), np.array([0]))                   # not owned by rank 1
+
+
+def test_set_stencils_roundtrip_and_validation():
+    """cwreco_set_stencils (S:194-211 interface): stencils built by the library, uploaded
+    into a fresh context in SFC order, give identical local numbering and identical
+    per-cell matrices; malformed stencils are rejected with EINVAL."""
+    nodes, cells, period = gen.box_mesh(2, 10, True, 0.2, 7)
+    a = P.Context(2, 3, 2, device=None)
+    a.set_mesh(nodes, cells, period)
+    a.build_stencils()
+    a.precompute()
+    cen_l, sec_l, val_l = a.stencils()               # local order
+    loc = a.local_cells()
+    n_own = a.info()["n_owned"]
+    order = np.argsort(loc[:n_own])                   # local -> SFC order
+    cen, sec, val = cen_l[order], sec_l[order], val_l[order]
+    b = P.Context(2, 3, 2, device=None)
+    b.set_mesh(nodes, cells, period)
+    b.set_stencils(cen, sec, val)
+    assert np.array_equal(b.local_cells(), loc)
+    b.precompute()
+    sel = np.arange(0, n_own, 7)
+    ba, bb = a.blocks(sel), b.blocks(sel)
+    for k in ba:
+        assert np.array_equal(ba[k], bb[k]), k
+    bad = cen.copy()
+    bad[3, 0] = bad[3, 1]                             # cell not first
+    with pytest.raises(P.CwrecoError, match="EINVAL"):
+        b.set_stencils(bad, sec, val)
+    bad = cen.copy()
+    bad[5, 2] = bad[5, 1]                             # repeated member
+    with pytest.raises(P.CwrecoError, match="EINVAL"):
+        b.set_stencils(bad, sec, val)
+    c = P.Context(2, 3, 2, device=None)
+    with pytest.raises(P.CwrecoError, match="ESTATE"):
+        c.set_stencils(cen, sec, val)

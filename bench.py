@@ -59,6 +59,26 @@ def workload_n(cfg, N):
     return int(round(base * N ** (1.0 / d)))
 
 
+# fp64 FMA peak of B200 (derived): 148 SMs × 64 DFMA/clk × 2 flop × 1.965 GHz
+FP64_PEAK_TF = 148 * 64 * 2 * 1.965e9 / 1e12
+FP64_PEAK_SRC = "derived: 148 SM x 64 fp64 FMA/clk x 2 x 1.965 GHz (no measured fp64 peak in MEASURED_PEAKS.json)"
+
+
+def matfree_flops_per_cell(d, M, V):
+    """Algorithmic fp64 flops of one matrix-free cell: assembly of the
+    K = n_e−1 rows of A by nq-point quadrature, Householder QR of A (K×R) applied to V
+    right-hand sides, back substitution, d+1 sector solves, epilogue."""
+    nm = (M + 1) * (M + 2) // 2 if d == 2 else (M + 1) * (M + 2) * (M + 3) // 6
+    R, K = nm - 1, d * nm - 1
+    nq = ((M + 2) // 2) ** d
+    assemble = K * (nq * (2 * d * d + d * M + 4 * nm) + 2 * R * nm + 4 * d * d * d)
+    qr = sum(4 * (K - c) * (R - c - 1 + V) + 4 * (K - c) for c in range(R))
+    backsub = R * R * V
+    sectors = (d + 1) * (2 * d ** 3 + 2 * d * d * V)
+    epilogue = V * (2 * R * (R + 1) // 2 * 2 + 40 * (d + 2))
+    return assemble + qr + backsub + sectors + epilogue
+
+
 def measured_peak():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -229,7 +249,10 @@ def run_ours(args):
     if world > 1:
         ctx.set_partition(rank, world)
     ctx.build_stencils()
-    ctx.precompute()
+    if args.kernel == "matrixfree":
+        ctx.prepare_matrixfree()        # geometry + stencils only, no matrices (NEXT-1)
+    else:
+        ctx.precompute()
     ctx.set_kernel(args.kernel)
     t_setup = time.perf_counter() - t_setup
     inf = ctx.info()
@@ -287,6 +310,7 @@ def run_ours(args):
 
     # roofline of the dominant kernel (the reconstruction kernel is the only kernel of the pass at N=1)
     bpc = inf["algorithmic_bytes_per_cell"]
+    mf_flops = matfree_flops_per_cell(w["d"], w["M"], V) if args.kernel == "matrixfree" else None
     kern_s = float(np.mean(times)) / 1e3
     achieved = bpc * n_owned / kern_s / 1e9
     peak, peak_src = measured_peak()
@@ -298,7 +322,7 @@ def run_ours(args):
     h_in = torch.from_numpy(avgs_local).pin_memory()
     h_out = torch.empty((n_owned, V, nm), dtype=torch.float64).pin_memory()
     e2e_steps = max(3, min(args.steps, 50))
-    if world == 1:
+    if world == 1 and args.kernel != "matrixfree":
         def e2e_step():
             ctx.reconstruct_host(h_in, h_out, stream=stream)
         e2e_api = "cwreco_reconstruct_host (C-ABI, pinned host buffers)"
@@ -343,10 +367,14 @@ def run_ours(args):
                        "kernel": args.kernel, "l2": "flushed (512 MiB write) between timed steps",
                        "parallelism": f"cell partition x{world}" + (" + NCCL halo" if world > 1 else ""),
                        "setup_s": round(t_setup, 3)},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "roofline": ({"bound": "alu", "achieved": mf_flops * n_owned / kern_s / 1e12, "peak": FP64_PEAK_TF,
+                          "unit": "TFLOP/s", "frac": mf_flops * n_owned / kern_s / 1e12 / FP64_PEAK_TF,
+                          "traffic": None, "peak_source": FP64_PEAK_SRC, "flops_per_cell": mf_flops,
+                          "kernel": "cwr::k_matfree"} if mf_flops else
+                         {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": profiled_traffic(args.config, args.kernel),
                          "peak_source": peak_src, "algorithmic_bytes_per_cell": bpc,
-                         "kernel": "cwr::k_pipelined" if args.kernel == "pipelined" else "cwr::k_simple"},
+                         "kernel": "cwr::k_pipelined" if args.kernel == "pipelined" else "cwr::k_simple"}),
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "cells/s", "h2d_bytes_per_step": int(avgs_local.nbytes),
                     "d2h_bytes_per_step": int(n_owned * V * nm * 8), "api": e2e_api},
@@ -366,7 +394,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--kernel", default="pipelined", choices=["pipelined", "simple"])
+    ap.add_argument("--kernel", default="pipelined", choices=["pipelined", "simple", "matrixfree"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

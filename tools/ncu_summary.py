@@ -99,7 +99,7 @@ def main():
 
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     lines = [f"# ncu --set full: {kname} — {a.config} ({a.tag})", "",
-             f"Capture: `ncu --set full --clock-control none --import-source on -k regex:k_pipelined -s 3 -c 1 "
+             f"Capture: `ncu --set full --clock-control none --import-source on -k \"regex:k_pipelined|k_rowblk\" -s 3 -c 1 "
              f"python bench.py --config {a.config} --steps 3 --warmup 3 --no-cpu-baseline` on one B200 "
              f"(cold L2, serialised; per-launch numbers).", "",
              "| metric | value |", "|---|---|"]
@@ -125,7 +125,7 @@ def main():
                 pass
         tot = sum(sum(v) for v in per.values())
         lines += ["", f"Launch list (`ncu --metrics gpu__time_duration.sum`, {a.launches.split('/')[-1]}): "
-                  "every kernel of `bench.py --steps 3 --warmup 3` (3 warm-up + 3 timed passes, 5 e2e passes, "
+                  "every kernel of `bench.py --steps 3 --warmup 3` (3 warm-up + 3 timed passes, 5 e2e passes of 4 tile ranges each (cwreco_reconstruct_host), "
                   "3 L2-flush fills):", "", "| kernel | launches | mean µs | share of device time |",
                   "|---|---|---|---|"]
         for k, v in sorted(per.items(), key=lambda kv: -sum(kv[1])):

@@ -76,7 +76,10 @@ typedef struct {
 /* Kernel variant for cwreco_reconstruct. */
 enum {
   CWRECO_KERNEL_PIPELINED = 0, /* default: TMA-bulk pipelined streaming kernel */
-  CWRECO_KERNEL_SIMPLE = 1     /* one thread per (cell, variable), plain loads */
+  CWRECO_KERNEL_SIMPLE = 1,    /* one thread per (cell, variable), plain loads */
+  CWRECO_KERNEL_MATRIXFREE = 2 /* no precomputed matrices: each pass assembles and solves
+                                  every cell's least-squares systems from the geometry
+                                  (moving meshes); needs cwreco_prepare_matrixfree */
 };
 
 /* Which owned cells a cwreco_reconstruct call processes (for halo overlap). */
@@ -169,6 +172,15 @@ cwreco_status cwreco_get_sigma(const cwreco_ctx* ctx, double* out);
  * sector member, 255 = invalid sector.  Any output may be NULL. */
 cwreco_status cwreco_get_blocks(const cwreco_ctx* ctx, int64_t n_sel, const int64_t* cells,
                                 double* bplus, double* sinv, int32_t* gather, uint8_t* slots);
+
+/* Matrix-free mode: upload the local geometry, the stencils
+ * (as local ids with periodic image codes), the basis in monomial form and the
+ * quadrature rule to the device, for cwreco_set_kernel(CWRECO_KERNEL_MATRIXFREE).
+ * Needs cwreco_build_stencils (or cwreco_set_stencils); cwreco_precompute is not
+ * needed.  The pass then builds A and solves the constrained LSQ
+ * and the sector systems per cell on the GPU.  ECUDA
+ * without a device; EUNSUPPORTED for M > 3 or nvars > 9. */
+cwreco_status cwreco_prepare_matrixfree(cwreco_ctx* ctx);
 
 /* ---------------------------------------------------------------- multi-rank halo */
 /* recv_counts [nranks]: ghosts owned by each rank; recv_ids [n_ghost]: their SFC

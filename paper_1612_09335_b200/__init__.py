@@ -17,7 +17,7 @@ __all__ = ["Context", "CwrecoError", "lib", "KERNELS", "PART_ALL", "PART_INTERIO
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "libcwreco.so")
 
-KERNELS = {"pipelined": 0, "simple": 1}
+KERNELS = {"pipelined": 0, "simple": 1, "matrixfree": 2}
 PART_ALL, PART_INTERIOR, PART_BOUNDARY = 0, 1, 2
 _STATUS = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "ECUDA", 4: "EMESH", 5: "ESTENCIL", 6: "ESINGULAR",
            7: "ESTATE", 8: "EUNSUPPORTED"}
@@ -60,6 +60,7 @@ def _load():
         "cwreco_get_stencils": [P, P, P, P],
         "cwreco_get_local_cells": [P, P],
         "cwreco_set_stencils": [P, P, P, P],
+        "cwreco_prepare_matrixfree": [P],
         "cwreco_precompute": [P],
         "cwreco_get_sigma": [P, P],
         "cwreco_get_blocks": [P, I64, P, P, P, P, P],
@@ -194,6 +195,10 @@ class Context:
         sl = np.empty((n, d + 1, d), dtype=np.uint8)
         _check(lib.cwreco_get_blocks(self._h, n, _ptr(cells), _ptr(bp), _ptr(sv), _ptr(ga), _ptr(sl)))
         return dict(bplus=bp, sinv=sv, gather=ga, slots=sl)
+
+    def prepare_matrixfree(self):
+        """Upload geometry and stencils for set_kernel("matrixfree") (no matrices)."""
+        _check(lib.cwreco_prepare_matrixfree(self._h))
 
     def set_kernel(self, name):
         _check(lib.cwreco_set_kernel(self._h, KERNELS[name]))

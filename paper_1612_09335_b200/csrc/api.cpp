@@ -80,6 +80,7 @@ cwreco_status cwreco_create(int dim, int degree_M, int nvars, const cwreco_param
 void cwreco_destroy(cwreco_ctx* ctx) {
   if (!ctx) return;
   try {
+    cwr::dev_matfree_destroy(ctx);
     cwr::dev_destroy(ctx);
   } catch (...) {
   }
@@ -121,8 +122,9 @@ cwreco_status cwreco_get_info(const cwreco_ctx* c, cwreco_info* o) {
 cwreco_status cwreco_set_kernel(cwreco_ctx* c, int variant) {
   return guard([&] {
     need(c != nullptr, CWRECO_EINVAL, "set_kernel: NULL");
-    need(variant == CWRECO_KERNEL_PIPELINED || variant == CWRECO_KERNEL_SIMPLE, CWRECO_EINVAL,
-         "set_kernel: unknown variant");
+    need(variant == CWRECO_KERNEL_PIPELINED || variant == CWRECO_KERNEL_SIMPLE ||
+             variant == CWRECO_KERNEL_MATRIXFREE,
+         CWRECO_EINVAL, "set_kernel: unknown variant");
     c->kernel = variant;
   });
 }
@@ -177,6 +179,16 @@ cwreco_status cwreco_get_stencils(const cwreco_ctx* c, int32_t* central, int32_t
       if (sectors) std::memcpy(sectors + li * nv * nv, &c->sectors[q * nv * nv], sizeof(int32_t) * nv * nv);
       if (valid) std::memcpy(valid + li * nv, &c->valid[q * nv], nv);
     }
+  });
+}
+
+cwreco_status cwreco_prepare_matrixfree(cwreco_ctx* c) {
+  return guard([&] {
+    need(c != nullptr, CWRECO_EINVAL, "prepare_matrixfree: NULL ctx");
+    need_device(c, "prepare_matrixfree");
+    cwr::MatfreeHost h;
+    cwr::matfree_prepare(c, h);
+    cwr::dev_matfree_upload(c, h);
   });
 }
 
@@ -345,7 +357,10 @@ cwreco_status cwreco_reconstruct(cwreco_ctx* c, const double* d_avgs, int64_t ac
   return guard([&] {
     need(c != nullptr, CWRECO_EINVAL, "reconstruct: NULL ctx");
     need_device(c, "reconstruct");
-    need(c->has_blocks, CWRECO_ESTATE, "reconstruct: call cwreco_precompute first");
+    if (c->kernel == CWRECO_KERNEL_MATRIXFREE)
+      need(c->mf != nullptr, CWRECO_ESTATE, "reconstruct: call cwreco_prepare_matrixfree first");
+    else
+      need(c->has_blocks, CWRECO_ESTATE, "reconstruct: call cwreco_precompute first");
     need(d_avgs && d_coeffs, CWRECO_EINVAL, "reconstruct: NULL buffer");
     need(acs >= 1 && avs >= 1 && ccs >= 1 && cvs >= 1, CWRECO_EINVAL, "reconstruct: strides must be >= 1");
     need(cvs >= c->nm && ccs >= (int64_t)cvs * 1, CWRECO_EINVAL, "reconstruct: coefficient rows overlap");
@@ -362,6 +377,8 @@ cwreco_status cwreco_reconstruct_host(cwreco_ctx* c, const double* h_avgs, doubl
     need_device(c, "reconstruct_host");
     need(c->has_blocks, CWRECO_ESTATE, "reconstruct_host: call cwreco_precompute first");
     need(h_avgs && h_coeffs, CWRECO_EINVAL, "reconstruct_host: NULL buffer");
+    need(c->kernel != CWRECO_KERNEL_MATRIXFREE, CWRECO_EUNSUPPORTED,
+         "reconstruct_host: use the device-pointer call in matrix-free mode");
     cwr::dev_reconstruct_host(c, h_avgs, h_coeffs, n_pieces > 0 ? n_pieces : 4, stream);
   });
 }

@@ -157,6 +157,19 @@ void rowblk_plan(const Layout& L, int max_smem, int max_ctas, int& ctas, int& st
 
 struct DeviceState;  // kernels.cu
 
+// Host arrays of the matrix-free mode (precompute.cpp: matfree_prepare)
+struct MatfreeHost {
+  std::vector<double> X, B;          // local cells: vertices [n_local][d+1][d], barycentres [n_local][d]
+  std::vector<int32_t> st;           // [n_owned][n_e−1] central stencil members (local ids, self excluded)
+  std::vector<uint8_t> sh;           // [n_owned][n_e−1] periodic image codes
+  std::vector<int32_t> sec;          // [n_owned][d+1][d] sector members (local ids, −1 if invalid)
+  std::vector<uint8_t> secsh;        // [n_owned][d+1][d]
+  std::vector<uint8_t> vmask;        // [n_owned] bit s = sector s valid (stencil level)
+  std::vector<int> mexp;             // monomial exponents [nmono][3]
+  std::vector<double> mcoef;         // basis in monomial form [ℳ][nmono]
+  std::vector<double> qp, qw;        // quadrature rule on T_E (exact for degree M)
+};
+
 }  // namespace cwr
 
 struct cwreco_ctx {
@@ -205,6 +218,7 @@ struct cwreco_ctx {
   double psi1 = 0;                         // constant basis function value
 
   cwr::DeviceState* dev = nullptr;
+  void* mf = nullptr;  // matrix-free device state (matfree.cu), after cwreco_prepare_matrixfree
 };
 
 namespace cwr {
@@ -222,6 +236,13 @@ void gauss_legendre01(int n, std::vector<double>& x, std::vector<double>& w);
 void gauss_jacobi01(int n, double alpha, std::vector<double>& t, std::vector<double>& w);
 // precompute.cpp
 void precompute(cwreco_ctx* c);
+void simplex_rule(int d, int M, std::vector<double>& qp, std::vector<double>& qw);
+void matfree_prepare(cwreco_ctx* c, MatfreeHost& h);
+// matfree.cu
+void dev_matfree_upload(cwreco_ctx* c, const MatfreeHost& h);
+void dev_matfree_reconstruct(cwreco_ctx* c, const double* avgs, int64_t acs, int64_t avs, double* coeffs,
+                             int64_t ccs, int64_t cvs, int64_t cell_begin, int64_t cell_end, void* stream);
+void dev_matfree_destroy(cwreco_ctx* c);
 // kernels.cu (device side; all return cudaError_t as int)
 void dev_create(cwreco_ctx* c);
 void dev_destroy(cwreco_ctx* c);

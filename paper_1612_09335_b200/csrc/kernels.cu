@@ -609,6 +609,12 @@ static void launch_range(cwreco_ctx* c, const double* avgs, int64_t acs, int64_t
 
 void dev_reconstruct(cwreco_ctx* c, const double* avgs, int64_t acs, int64_t avs, double* coeffs, int64_t ccs,
                      int64_t cvs, int part, void* stream) {
+  if (c->kernel == CWRECO_KERNEL_MATRIXFREE) {  // cells, not tiles: interior first in local order
+    const int64_t c0 = part == CWRECO_PART_BOUNDARY ? c->n_interior : 0;
+    const int64_t c1 = part == CWRECO_PART_INTERIOR ? c->n_interior : c->n_owned;
+    dev_matfree_reconstruct(c, avgs, acs, avs, coeffs, ccs, cvs, c0, c1, stream);
+    return;
+  }
   int64_t t0 = 0, t1 = c->n_tiles;
   if (part == CWRECO_PART_INTERIOR) {
     t1 = c->n_int_tiles;

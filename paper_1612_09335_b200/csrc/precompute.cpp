@@ -301,6 +301,42 @@ bool tile_union(const cwreco_ctx* c, int64_t t, int T, int G, const ToLocal& to_
 
 }  // namespace
 
+// Conical-product Gauss-Jacobi rule on T_E exact for degree M (R19); points [nq][d],
+// weights normalised to 1.  Shared by the packed precompute and the matrix-free setup.
+void simplex_rule(int d, int M, std::vector<double>& qp, std::vector<double>& qw) {
+  qp.clear();
+  qw.clear();
+  // collapsed coordinates (u, v, w), Jacobian (1-v)(1-w)^2 absorbed by Jacobi weights
+  // (1-x)^1 and (1-x)^2, ceil((M+1)/2) points per direction; normalised to average.
+  {
+    const int n = (M + 2) / 2;
+    std::vector<double> ua, wa, vb, wb, wc, wcw;
+    gauss_jacobi01(n, 0.0, ua, wa);
+    gauss_jacobi01(n, 1.0, vb, wb);
+    gauss_jacobi01(n, 2.0, wc, wcw);
+    if (d == 2) {
+      for (int a = 0; a < n; ++a)
+        for (int b = 0; b < n; ++b) {
+          qp.push_back(ua[a] * (1 - vb[b]));
+          qp.push_back(vb[b]);
+          qw.push_back(wa[a] * wb[b]);
+        }
+    } else {
+      for (int a = 0; a < n; ++a)
+        for (int b = 0; b < n; ++b)
+          for (int e = 0; e < n; ++e) {
+            qp.push_back(ua[a] * (1 - vb[b]) * (1 - wc[e]));
+            qp.push_back(vb[b] * (1 - wc[e]));
+            qp.push_back(wc[e]);
+            qw.push_back(wa[a] * wb[b] * wcw[e]);
+          }
+    }
+    double wsum = 0.0;
+    for (double w : qw) wsum += w;
+    for (double& w : qw) w /= wsum;
+  }
+}
+
 // Build the packed tiles for local owned cells [0, n_owned) and hand them to the
 // device (or keep them on the host for a host-only context).
 void precompute(cwreco_ctx* c) {
@@ -350,37 +386,8 @@ void precompute(cwreco_ctx* c) {
     c->psi1 = psi[0];
   }
 
-  // conical-product Gauss-Jacobi rule on T_E exact for degree M (R19): collapsed
-  // coordinates (u, v, w), Jacobian (1-v)(1-w)^2 absorbed by Jacobi weights
-  // (1-x)^1 and (1-x)^2, ceil((M+1)/2) points per direction; normalised to average.
   std::vector<double> qp, qw;  // points [nq][d], weights normalised to 1
-  {
-    const int n = (M + 2) / 2;
-    std::vector<double> ua, wa, vb, wb, wc, wcw;
-    gauss_jacobi01(n, 0.0, ua, wa);
-    gauss_jacobi01(n, 1.0, vb, wb);
-    gauss_jacobi01(n, 2.0, wc, wcw);
-    if (d == 2) {
-      for (int a = 0; a < n; ++a)
-        for (int b = 0; b < n; ++b) {
-          qp.push_back(ua[a] * (1 - vb[b]));
-          qp.push_back(vb[b]);
-          qw.push_back(wa[a] * wb[b]);
-        }
-    } else {
-      for (int a = 0; a < n; ++a)
-        for (int b = 0; b < n; ++b)
-          for (int e = 0; e < n; ++e) {
-            qp.push_back(ua[a] * (1 - vb[b]) * (1 - wc[e]));
-            qp.push_back(vb[b] * (1 - wc[e]));
-            qp.push_back(wc[e]);
-            qw.push_back(wa[a] * wb[b] * wcw[e]);
-          }
-    }
-    double wsum = 0.0;
-    for (double w : qw) wsum += w;
-    for (double& w : qw) w /= wsum;
-  }
+  simplex_rule(d, M, qp, qw);
   const int nq = (int)qw.size();
   // monomial form of the basis: A row of stencil cell j = coef · (monomial averages over T_j)
   std::vector<int> mexp;
@@ -538,4 +545,85 @@ void precompute(cwreco_ctx* c) {
   c->has_blocks = true;
 }
 
+// Matrix-free mode (SURVEY §8(f) NEXT-1, P:230 ALE remark): instead of the packed
+// B⁺ stream the device gets the geometry and stencils and solves each cell's
+// constrained least-squares problem in the pass (matfree.cu).  Host part: local
+// geometry, stencils as local ids with periodic image codes (2 bits per axis:
+// 0 → 0, 1 → +L, 2 → −L, R16), the basis in monomial form and the quadrature rule.
+void matfree_prepare(cwreco_ctx* c, MatfreeHost& h) {
+  if (!c->has_stencils) fail(CWRECO_ESTATE, "prepare_matrixfree: call cwreco_build_stencils first");
+  const int d = c->d, ne = c->ne, nv = d + 1;
+  const int64_t n_loc = c->n_owned + c->n_ghost;
+  std::vector<int32_t> own2local(c->own_hi - c->own_lo, -1);
+  for (int64_t li = 0; li < c->n_owned; ++li) own2local[c->local2global[li] - c->own_lo] = (int32_t)li;
+  auto to_local = [&](int64_t g) -> int32_t {
+    if (g >= c->own_lo && g < c->own_hi) return own2local[g - c->own_lo];
+    auto b = c->local2global.begin() + c->n_owned, e = c->local2global.begin() + n_loc;
+    auto it = std::lower_bound(b, e, g);
+    if (it == e || *it != g) return -1;
+    return (int32_t)(it - c->local2global.begin());
+  };
+  h.X.assign(n_loc * nv * d, 0.0);
+  h.B.assign(n_loc * d, 0.0);
+  for (int64_t li = 0; li < n_loc; ++li) {
+    const int64_t g = c->local2global[li];
+    std::memcpy(&h.X[li * nv * d], &c->X[g * nv * d], sizeof(double) * nv * d);
+    std::memcpy(&h.B[li * d], &c->bary[g * d], sizeof(double) * d);
+  }
+  const int K = ne - 1;
+  h.st.assign(c->n_owned * K, 0);
+  h.sh.assign(c->n_owned * K, 0);
+  h.sec.assign(c->n_owned * nv * d, -1);
+  h.secsh.assign(c->n_owned * nv * d, 0);
+  h.vmask.assign(c->n_owned, 0);
+  int bad = 0;
+  auto code_of = [&](int64_t gi, int64_t gj) -> uint8_t {
+    double sh[3];
+    shift_of(c, gi, gj, sh);
+    uint8_t code = 0;
+    for (int a = 0; a < d; ++a) {
+      const double n = c->periodic ? sh[a] / c->L[a] : 0.0;
+      if (n > 0.5) code |= uint8_t(1u << (2 * a));
+      else if (n < -0.5) code |= uint8_t(2u << (2 * a));
+      if (std::fabs(n) > 1.5) bad |= 2;  // stencils never span more than one period
+    }
+    return code;
+  };
+#pragma omp parallel for schedule(static) reduction(| : bad)
+  for (int64_t li = 0; li < c->n_owned; ++li) {
+    const int64_t g = c->local2global[li], q = g - c->own_lo;
+    for (int k = 1; k < ne; ++k) {
+      const int64_t j = c->central[q * ne + k];
+      const int32_t lj = to_local(j);
+      if (lj < 0) bad |= 1;
+      h.st[li * K + k - 1] = lj;
+      h.sh[li * K + k - 1] = code_of(g, j);
+    }
+    uint8_t vm = 0;
+    for (int s = 0; s < nv; ++s) {
+      if (!c->valid[q * nv + s]) continue;
+      vm |= uint8_t(1u << s);
+      for (int m = 0; m < d; ++m) {
+        const int64_t j = c->sectors[(q * nv + s) * nv + 1 + m];
+        const int32_t lj = to_local(j);
+        if (lj < 0) bad |= 1;
+        h.sec[(li * nv + s) * d + m] = lj;
+        h.secsh[(li * nv + s) * d + m] = code_of(g, j);
+      }
+    }
+    h.vmask[li] = vm;
+  }
+  if (bad & 1) fail(CWRECO_EINVAL, "prepare_matrixfree: stencil cell missing from the local numbering");
+  if (bad & 2) fail(CWRECO_EUNSUPPORTED, "prepare_matrixfree: stencil spans more than one period");
+  basis_monomials(d, c->M, h.mexp, h.mcoef);
+  simplex_rule(d, c->M, h.qp, h.qw);
+  if (c->sigma.empty()) c->sigma = sigma_matrix(d, c->M);
+  if (c->psi1 == 0.0) {
+    double xi[3] = {0.25, 0.25, 0.25}, psi[64];
+    basis_eval(d, c->M, xi, psi);
+    c->psi1 = psi[0];
+  }
+}
+
 }  // namespace cwr
+

@@ -207,3 +207,49 @@ def test_reconstruct_host_end_to_end():
         for pieces in (0, 1, 3, 7):
             out = ctx.reconstruct_host(h, n_pieces=pieces)
             assert torch.equal(out, ref), (pinned, pieces)
+
+
+MF_CASES = [
+    # name, d, n, M, jitter, periodic, V
+    ("2d-M3-jit", 2, 16, 3, 0.2, True, 4),
+    ("2d-M2-open", 2, 11, 2, 0.15, False, 3),
+    ("3d-M2", 3, 6, 2, 0.0, True, 5),
+    ("3d-M3-jit", 3, 6, 3, 0.1, True, 9),
+    ("3d-M1-open", 3, 5, 1, 0.1, False, 2),
+]
+
+
+@pytest.mark.parametrize("case", MF_CASES, ids=lambda c: c[0])
+def test_matrixfree_parity(case):
+    """Matrix-free mode: matrices assembled and least-squares
+    problems solved per pass on the GPU; no precompute.  Same tolerance against the
+    oracle (R25); against the precomputed-matrix kernel within QR rounding."""
+    name, d, n, M, jit, per, V = case
+    nodes, cells, period = gen.box_mesh(d, n, per, jit, 31)
+    Qin = np.random.default_rng(8).standard_normal((cells.shape[0], V)) * 2.0 + 3.0
+    ctx = P.Context(d, M, V, device=0)
+    ctx.set_mesh(nodes, cells, period)
+    ctx.build_stencils()
+    ctx.prepare_matrixfree()
+    m = OracleMesh(nodes, cells, period, M)
+    Q = Qin[m.perm]
+    a = _run(ctx, Q, "matrixfree")
+    assert np.all(np.isfinite(a))
+    worst = 0.0
+    for i in range(m.N):
+        r = R.reconstruct_cell(m, i, Q, M)
+        worst = max(worst, floored_err(a[i], r["w"], Q, r["central"]))
+    assert worst <= TOL, (name, worst)
+    ctx.precompute()
+    b = _run(ctx, Q, "pipelined")
+    scale = np.abs(Q).max()
+    assert np.abs(a - b).max() <= 1e-12 * scale
+    psi1 = np.sqrt(2.0 if d == 2 else 6.0)
+    assert np.abs(a[:, :, 0] * psi1 - Q).max() <= 4e-16 * scale     # conservation (P:145)
+    # interior + boundary parts == all; deterministic
+    ctx.set_kernel("matrixfree")
+    Qd = torch.tensor(Q, device="cuda")
+    o2 = torch.zeros((m.N, V, ctx.nm), dtype=torch.float64, device="cuda")
+    ctx.reconstruct(Qd, o2, part=P.PART_INTERIOR)
+    ctx.reconstruct(Qd, o2, part=P.PART_BOUNDARY)
+    assert np.array_equal(o2.cpu().numpy(), a)

@@ -128,12 +128,19 @@ __device__ __forceinline__ bool inv_small_d(const double (&A)[D][D], double (&Ai
   }
 }
 
+// per-warp shared scratch: R factor, Qᵀ ΔQ, diag(R), sector products
+__host__ __device__ constexpr int mf_scr_doubles(int D, int M, int V) {
+  return (nmodes(M, D) - 1) * (nmodes(M, D) - 1 + V + 1) + (D + 1) * D * V;
+}
+
 template <int D, int M, int V>
 __global__ void __launch_bounds__(256) k_matfree(MfArgs m, KArgs a) {
   constexpr int NM = nmodes(M, D), R = NM - 1, NV = D + 1, NE = D * NM, K = NE - 1;
   constexpr int KPL = (K + 31) / 32;  // rows of A per lane
-  static_assert(R <= 32, "R must fit one row per lane");
+
   const int lane = threadIdx.x & 31;
+  extern __shared__ __align__(16) double mf_smem[];
+  double* scr = mf_smem + (threadIdx.x >> 5) * mf_scr_doubles(D, M, V);
   const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
   for (int64_t i = m.cell_begin + w0; i < m.cell_end; i += nw) {
@@ -217,66 +224,96 @@ __global__ void __launch_bounds__(256) k_matfree(MfArgs m, KArgs a) {
       }
     }
 
-    // ---- Householder QR of A (K × R) applied to rhs; R factor left in rows 0..R−1
-#pragma unroll
-    for (int c = 0; c < R; ++c) {
+    // ---- Householder QR of A (K × R) applied to rhs; R factor left in rows 0..R−1.
+    // Per column c: the R+V dot products vᵀ[A|ΔQ] are reduced with a butterfly
+    // reduce-scatter (after the xor-o step a lane keeps the half selected by bit o,
+    // so lane L ends with column L's full sum: 31 shuffles instead of 5·(R+V)), then
+    // all-gathered for the rank-1 update.  The column loop is not unrolled (code size).
+    static_assert(R + V <= 32, "one lane per column of A|ΔQ");
+    constexpr int NP = R + V <= 16 ? 16 : 32;  // padded column count of the reduce-scatter
+    auto qr_step = [&](const int c) {
       double x[KPL];
       double part = 0.0;
 #pragma unroll
       for (int r = 0; r < KPL; ++r) {
         const int k = lane + 32 * r;
-        x[r] = (k >= c && k < K) ? A[r][c] : 0.0;
+        double ak = 0.0;
+#pragma unroll
+        for (int mm = 0; mm < R; ++mm)
+          if (mm == c) ak = A[r][mm];
+        x[r] = (k >= c && k < K) ? ak : 0.0;
         part += x[r] * x[r];
       }
       const double nrm2 = warp_sum(part);
-      const double xc = __shfl_sync(0xffffffffu, A[0][c], c);
+      const double xc = __shfl_sync(0xffffffffu, x[0], c);  // row c is slot 0 of lane c
       const double alpha = xc >= 0.0 ? -sqrt(nrm2) : sqrt(nrm2);
       const double vtv = 2.0 * (nrm2 - alpha * xc);
       const double tau = vtv > 0.0 ? 2.0 / vtv : 0.0;
+      if (lane == c) x[0] -= alpha;
+      double dd[NP];
 #pragma unroll
-      for (int r = 0; r < KPL; ++r)
-        if (lane + 32 * r == c) x[r] -= alpha;
-      // dot products of v with the remaining columns and the right-hand sides
-      double dots[R + V];
+      for (int mm = 0; mm < NP; ++mm) {
+        double s2 = 0.0;
+        if (mm < R + V) {
+#pragma unroll
+          for (int r = 0; r < KPL; ++r) s2 += x[r] * (mm < R ? A[r][mm] : rhs[r][mm < R ? 0 : mm - R]);
+        }
+        dd[mm] = s2;
+      }
+#pragma unroll
+      for (int o = NP / 2; o > 0; o >>= 1) {
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int i2 = 0; i2 < o; ++i2) {
+          const double keep = up ? dd[i2 + o] : dd[i2];
+          const double send = up ? dd[i2] : dd[i2 + o];
+          dd[i2] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+      }
+      if (NP == 16) dd[0] += __shfl_xor_sync(0xffffffffu, dd[0], 16);
+      const double fl = tau * dd[0];  // lane L: τ·(vᵀ column L mod NP)
 #pragma unroll
       for (int mm = 0; mm < R + V; ++mm) {
-        double s = 0.0;
+        const double f = __shfl_sync(0xffffffffu, fl, mm);
         if (mm > c) {
 #pragma unroll
-          for (int r = 0; r < KPL; ++r) s += x[r] * (mm < R ? A[r][mm] : rhs[r][mm - R]);
-        }
-        dots[mm] = s;
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-        for (int mm = 0; mm < R + V; ++mm)
-          if (mm > c) dots[mm] += __shfl_xor_sync(0xffffffffu, dots[mm], o);
-#pragma unroll
-      for (int mm = c + 1; mm < R + V; ++mm) {
-        const double f = tau * dots[mm];
-#pragma unroll
-        for (int r = 0; r < KPL; ++r) {
-          if (mm < R)
-            A[r][mm] -= f * x[r];
-          else
-            rhs[r][mm - R] -= f * x[r];
+          for (int r = 0; r < KPL; ++r) {
+            if (mm < R)
+              A[r][mm] -= f * x[r];
+            else
+              rhs[r][mm - R] -= f * x[r];
+          }
         }
       }
-      if (lane == c) A[0][c] = alpha;
-    }
-    // ---- back substitution R p = (Qᵀ ΔQ)[0:R]; lane k keeps p̂_opt[k+1][·] in rhs[0]
+      if (lane == c) {
 #pragma unroll
-    for (int c = R - 1; c >= 0; --c) {
-#pragma unroll
-      for (int v = 0; v < V; ++v) {
-        double pc = lane == c ? rhs[0][v] / A[0][c] : 0.0;
-        pc = __shfl_sync(0xffffffffu, pc, c);
-        if (lane == c) rhs[0][v] = pc;
-        else if (lane < c) rhs[0][v] -= A[0][c] * pc;
+        for (int mm = 0; mm < R; ++mm)
+          if (mm == c) A[0][mm] = alpha;
       }
+    };
+    if constexpr (R <= 9) {  // small: fully unrolled (column selects fold away)
+#pragma unroll
+      for (int c = 0; c < R; ++c) qr_step(c);
+    } else {  // ℳ ≥ 15: a rolled column loop keeps the code in the instruction cache
+#pragma unroll 1
+      for (int c = 0; c < R; ++c) qr_step(c);
     }
-
+    // ---- R factor and Qᵀ ΔQ to this warp's shared scratch: lane v < V then solves
+    // R p = (Qᵀ ΔQ)[0:R] for its variable, keeping p̂_opt in registers
+    double* Rs = scr;                 // [R][R] upper triangle of R
+    double* Ys = Rs + R * R;          // [R][V]
+    double* Ri = Ys + R * V;          // [R] diagonal of R
+    double* PSs = Ri + R;             // [NV][D][V] sector products
+    if (lane < R) {
+#pragma unroll
+      for (int mm = 0; mm < R; ++mm)
+        if (mm >= lane) Rs[lane * R + mm] = A[0][mm];
+#pragma unroll
+      for (int v = 0; v < V; ++v) Ys[lane * V + v] = rhs[0][v];
+#pragma unroll
+      for (int mm = 0; mm < R; ++mm)
+        if (mm == lane) Ri[lane] = A[0][mm];
+    }
     // ---- sectors: lane s < d+1 solves sector s for all variables
     double psl[D][V];
     bool vs = false;
@@ -323,34 +360,31 @@ __global__ void __launch_bounds__(256) k_matfree(MfArgs m, KArgs a) {
       }
     }
 
-    // ---- gather per variable (lane v) and run the fused epilogue
+    // ---- per variable (lane v): back substitution, gather, fused epilogue
+    if (lane < NV) {
+#pragma unroll
+      for (int l = 0; l < D; ++l)
+#pragma unroll
+        for (int v = 0; v < V; ++v) PSs[(lane * D + l) * V + v] = psl[l][v];
+    }
+    const unsigned vbits = __ballot_sync(0xffffffffu, vs);
+    __syncwarp();
     double acc[R], ps[NV][D];
     bool valid[NV];
 #pragma unroll
-    for (int l = 0; l < R; ++l) {
-      double t = 0.0;
-#pragma unroll
-      for (int v = 0; v < V; ++v) {
-        const double x = __shfl_sync(0xffffffffu, rhs[0][v], l);
-        if (lane == v) t = x;
-      }
-      acc[l] = t;
-    }
-#pragma unroll
-    for (int s = 0; s < NV; ++s) {
-      valid[s] = __shfl_sync(0xffffffffu, vs ? 1 : 0, s) != 0;
-#pragma unroll
-      for (int l = 0; l < D; ++l) {
-        double t = 0.0;
-#pragma unroll
-        for (int v = 0; v < V; ++v) {
-          const double x = __shfl_sync(0xffffffffu, psl[l][v], s);
-          if (lane == v) t = x;
-        }
-        ps[s][l] = t;
-      }
-    }
+    for (int s2 = 0; s2 < NV; ++s2) valid[s2] = (vbits >> s2) & 1;
     if (lane < V) {
+#pragma unroll
+      for (int c = R - 1; c >= 0; --c) {
+        double t = Ys[c * V + lane];
+#pragma unroll
+        for (int mm = c + 1; mm < R; ++mm) t -= Rs[c * R + mm] * acc[mm];
+        acc[c] = t / Ri[c];
+      }
+#pragma unroll
+      for (int s2 = 0; s2 < NV; ++s2)
+#pragma unroll
+        for (int l = 0; l < D; ++l) ps[s2][l] = PSs[(s2 * D + l) * V + lane];
       double q = 0.0;
 #pragma unroll
       for (int v = 0; v < V; ++v)
@@ -361,6 +395,7 @@ __global__ void __launch_bounds__(256) k_matfree(MfArgs m, KArgs a) {
 #pragma unroll
       for (int l = 0; l < NM; ++l) o[l] = w[l];
     }
+    __syncwarp();  // the scratch is rewritten by the next cell
   }
 }
 
@@ -502,11 +537,13 @@ void dev_matfree_reconstruct(cwreco_ctx* c, const double* avgs, int64_t acs, int
   int nsm = 148;
   MCK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
   MfFn f = mf_fn(c->d, c->M, c->V);
+  const size_t smem = size_t(8) * mf_scr_doubles(c->d, c->M, c->V) * sizeof(double);
+  MCK(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 1;
-  MCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)f, 256, 0));
+  MCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)f, 256, smem));
   const int64_t warps = cell_end - cell_begin;
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((warps + 7) / 8, (int64_t)nsm * std::max(1, occ)));
-  f<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(m, a);
+  f<<<(unsigned)grid, 256, smem, (cudaStream_t)stream>>>(m, a);
   MCK(cudaGetLastError());
 }
 

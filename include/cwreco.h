@@ -224,6 +224,23 @@ cwreco_status cwreco_reconstruct(cwreco_ctx* ctx, const double* d_avgs, int64_t 
 cwreco_status cwreco_reconstruct_host(cwreco_ctx* ctx, const double* h_avgs, double* h_coeffs, int n_pieces,
                                       cwreco_stream stream);
 
+/* ---------------------------------------------------------------- face traces (NEXT-3) */
+/* Face quadrature used by cwreco_face_traces: *nq points; lam [nq][dim]
+ * barycentric weights over the face's dim vertices SORTED BY ASCENDING GLOBAL NODE ID
+ * (so both cells of a face use the same physical points in the same order);
+ * weights [nq] sum to 1 (multiply by the face measure for integrals).  Exact for
+ * polynomials of degree 2M+1 on the face.  lam / weights may be NULL. */
+cwreco_status cwreco_face_rule(const cwreco_ctx* ctx, int* nq, double* lam, double* weights);
+/* nbr [n_owned][dim+1]: local id of the cell across face f (the face opposite local
+ * vertex f of the orientation-fixed cell), −1 on an open boundary.  Face neighbours
+ * are always local (they belong to the central stencil).  ESTATE before stencils. */
+cwreco_status cwreco_face_neighbors(const cwreco_ctx* ctx, int64_t* nbr);
+/* d_traces [n_owned][dim+1][nq][nvars] (dense) ← the blended polynomial w of each owned
+ * cell (d_coeffs as written by cwreco_reconstruct, strides in doubles) at its faces'
+ * quadrature points.  Asynchronous on `stream`; tables built on the first call. */
+cwreco_status cwreco_face_traces(cwreco_ctx* ctx, const double* d_coeffs, int64_t c_cell_stride,
+                                 int64_t c_var_stride, double* d_traces, cwreco_stream stream);
+
 /* Debug tap (tests): intermediates of n_sel owned cells (local ids), computed by
  * the SIMPLE kernel and copied to host (synchronises `stream`):
  *   popt [n][nvars][ℳ], psec [n][dim+1][nvars][dim+1], sigma [n][dim+2][nvars],

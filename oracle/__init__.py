@@ -30,4 +30,9 @@ Modules and what pins them (tests/test_oracle_*.py, all ``-m "not gpu"``):
              conservation, ℙ1 exactness, Σλ̄ P = P_opt, Σω = 1, ω = λ̄ for equal
              σ, paper's λ0/(λ0+N_p), convergence order on the vortex, mpmath
              40-digit re-evaluation on a tiny case.
+  traces     face traces of the polynomials at the face quadrature points
+             (SURVEY §8(f) NEXT-3, R31).  Pinned: rule exactness to
+             degree 2M+1 (Dirichlet formula on the face simplex), traces of
+             reproduced polynomials equal the polynomial, both cells of a face
+             use the same physical points.
 """

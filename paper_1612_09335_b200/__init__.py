@@ -61,6 +61,9 @@ def _load():
         "cwreco_get_local_cells": [P, P],
         "cwreco_set_stencils": [P, P, P, P],
         "cwreco_prepare_matrixfree": [P],
+        "cwreco_face_rule": [P, P, P, P],
+        "cwreco_face_neighbors": [P, P],
+        "cwreco_face_traces": [P, P, I64, I64, P, P],
         "cwreco_precompute": [P],
         "cwreco_get_sigma": [P, P],
         "cwreco_get_blocks": [P, I64, P, P, P, P, P],
@@ -263,6 +266,36 @@ class Context:
         _check(lib.cwreco_reconstruct_host(self._h, ctypes.c_void_p(avgs.data_ptr()),
                                            ctypes.c_void_p(out.data_ptr()), int(n_pieces),
                                            _stream_handle(stream)))
+        return out
+
+    # ---------------------------------------------------------------- face traces (NEXT-3)
+    def face_rule(self):
+        """(lam [nq][dim] barycentric weights over the sorted face vertices, weights [nq])."""
+        nq = ctypes.c_int()
+        _check(lib.cwreco_face_rule(self._h, ctypes.byref(nq), None, None))
+        lam = np.empty((nq.value, self.dim))
+        w = np.empty(nq.value)
+        _check(lib.cwreco_face_rule(self._h, ctypes.byref(nq), _ptr(lam), _ptr(w)))
+        return lam, w
+
+    def face_neighbors(self):
+        out = np.empty((self.info()["n_owned"], self.dim + 1), dtype=np.int64)
+        _check(lib.cwreco_face_neighbors(self._h, _ptr(out)))
+        return out
+
+    def face_traces(self, coeffs, out=None, stream=None):
+        """coeffs: CUDA [n_owned, V, ℳ] (cwreco_reconstruct output); returns / fills
+        out [n_owned, dim+1, nq, V] on the device."""
+        import torch
+        nq = self.face_rule()[1].shape[0]
+        if out is None:
+            out = torch.empty((coeffs.shape[0], self.dim + 1, nq, self.V), dtype=torch.float64,
+                              device=coeffs.device)
+        c_cs, c_vs, c_ls = coeffs.stride()
+        if c_ls != 1 or not out.is_contiguous():
+            raise ValueError("coeffs must be contiguous along the mode axis and out dense")
+        _check(lib.cwreco_face_traces(self._h, ctypes.c_void_p(coeffs.data_ptr()), c_cs, c_vs,
+                                      ctypes.c_void_p(out.data_ptr()), _stream_handle(stream)))
         return out
 
     def reconstruct_debug(self, avgs, cells, stream=None):

@@ -81,6 +81,7 @@ void cwreco_destroy(cwreco_ctx* ctx) {
   if (!ctx) return;
   try {
     cwr::dev_matfree_destroy(ctx);
+    cwr::dev_traces_destroy(ctx);
     cwr::dev_destroy(ctx);
   } catch (...) {
   }
@@ -380,6 +381,57 @@ cwreco_status cwreco_reconstruct_host(cwreco_ctx* c, const double* h_avgs, doubl
     need(c->kernel != CWRECO_KERNEL_MATRIXFREE, CWRECO_EUNSUPPORTED,
          "reconstruct_host: use the device-pointer call in matrix-free mode");
     cwr::dev_reconstruct_host(c, h_avgs, h_coeffs, n_pieces > 0 ? n_pieces : 4, stream);
+  });
+}
+
+cwreco_status cwreco_face_rule(const cwreco_ctx* c, int* nq, double* lam, double* weights) {
+  return guard([&] {
+    need(c && nq, CWRECO_EINVAL, "face_rule: NULL");
+    std::vector<double> l, w;
+    cwr::face_rule(c->d, c->M, l, w);
+    *nq = (int)w.size();
+    if (lam) std::memcpy(lam, l.data(), sizeof(double) * l.size());
+    if (weights) std::memcpy(weights, w.data(), sizeof(double) * w.size());
+  });
+}
+
+cwreco_status cwreco_face_neighbors(const cwreco_ctx* c, int64_t* nbr) {
+  return guard([&] {
+    need(c && nbr, CWRECO_EINVAL, "face_neighbors: NULL");
+    need(c->has_stencils, CWRECO_ESTATE, "face_neighbors: no stencils");
+    const int nv = c->d + 1;
+    const int64_t n_loc = c->n_owned + c->n_ghost;
+    std::vector<int64_t> sorted_ids(c->local2global.begin(), c->local2global.begin() + n_loc);
+    std::vector<int64_t> order(n_loc);
+    for (int64_t k = 0; k < n_loc; ++k) order[k] = k;
+    std::sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return sorted_ids[a] < sorted_ids[b]; });
+    std::vector<int64_t> keys(n_loc);
+    for (int64_t k = 0; k < n_loc; ++k) keys[k] = sorted_ids[order[k]];
+    for (int64_t li = 0; li < c->n_owned; ++li) {
+      const int64_t g = c->local2global[li];
+      for (int f = 0; f < nv; ++f) {
+        const int64_t j = c->nbr[g * nv + f];
+        int64_t lj = -1;
+        if (j >= 0) {
+          auto it = std::lower_bound(keys.begin(), keys.end(), j);
+          need(it != keys.end() && *it == j, CWRECO_EINVAL, "face_neighbors: neighbour not local");
+          lj = order[it - keys.begin()];
+        }
+        nbr[li * nv + f] = lj;
+      }
+    }
+  });
+}
+
+cwreco_status cwreco_face_traces(cwreco_ctx* c, const double* d_coeffs, int64_t ccs, int64_t cvs, double* d_traces,
+                                 cwreco_stream stream) {
+  return guard([&] {
+    need(c != nullptr, CWRECO_EINVAL, "face_traces: NULL ctx");
+    need_device(c, "face_traces");
+    need(c->has_stencils, CWRECO_ESTATE, "face_traces: no stencils");
+    need(d_coeffs && d_traces, CWRECO_EINVAL, "face_traces: NULL buffer");
+    need(cvs >= c->nm && ccs >= cvs, CWRECO_EINVAL, "face_traces: bad strides");
+    cwr::dev_face_traces(c, d_coeffs, ccs, cvs, d_traces, stream);
   });
 }
 

@@ -321,4 +321,37 @@ std::vector<double> sigma_matrix(int d, int M) {
   return S;
 }
 
+// Face quadrature (NEXT-3): M+1 points per direction, exact for degree 2M+1 on the
+// face; barycentric weights lam [nq][d] over the face's d vertices (in the caller's
+// canonical order), weights normalised to 1 (face average).  2-D: Gauss–Legendre
+// on the edge; 3-D: collapsed Gauss–Jacobi on the triangle (u, v) ↦ (u(1−v), v).
+void face_rule(int d, int M, std::vector<double>& lam, std::vector<double>& w) {
+  lam.clear();
+  w.clear();
+  const int n = M + 1;
+  std::vector<double> ua, wa, vb, wb;
+  gauss_jacobi01(n, 0.0, ua, wa);
+  if (d == 2) {
+    for (int a = 0; a < n; ++a) {
+      lam.push_back(1.0 - ua[a]);
+      lam.push_back(ua[a]);
+      w.push_back(wa[a]);
+    }
+  } else {
+    gauss_jacobi01(n, 1.0, vb, wb);
+    for (int a = 0; a < n; ++a)
+      for (int b = 0; b < n; ++b) {
+        const double x = ua[a] * (1.0 - vb[b]), y = vb[b];
+        lam.push_back(1.0 - x - y);
+        lam.push_back(x);
+        lam.push_back(y);
+        w.push_back(wa[a] * wb[b]);
+      }
+  }
+  double s = 0.0;
+  for (double x : w) s += x;
+  for (double& x : w) x /= s;
+}
+
 }  // namespace cwr
+

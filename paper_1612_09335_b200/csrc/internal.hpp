@@ -219,6 +219,7 @@ struct cwreco_ctx {
 
   cwr::DeviceState* dev = nullptr;
   void* mf = nullptr;  // matrix-free device state (matfree.cu), after cwreco_prepare_matrixfree
+  void* tr = nullptr;  // face-trace tables (traces.cu), built on the first cwreco_face_traces
 };
 
 namespace cwr {
@@ -243,6 +244,10 @@ void dev_matfree_upload(cwreco_ctx* c, const MatfreeHost& h);
 void dev_matfree_reconstruct(cwreco_ctx* c, const double* avgs, int64_t acs, int64_t avs, double* coeffs,
                              int64_t ccs, int64_t cvs, int64_t cell_begin, int64_t cell_end, void* stream);
 void dev_matfree_destroy(cwreco_ctx* c);
+// basis.cpp / traces.cu: face quadrature and face traces (NEXT-3)
+void face_rule(int d, int M, std::vector<double>& lam, std::vector<double>& w);
+void dev_face_traces(cwreco_ctx* c, const double* coeffs, int64_t ccs, int64_t cvs, double* traces, void* stream);
+void dev_traces_destroy(cwreco_ctx* c);
 // kernels.cu (device side; all return cudaError_t as int)
 void dev_create(cwreco_ctx* c);
 void dev_destroy(cwreco_ctx* c);

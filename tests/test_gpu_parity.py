@@ -253,3 +253,30 @@ def test_matrixfree_parity(case):
     ctx.reconstruct(Qd, o2, part=P.PART_INTERIOR)
     ctx.reconstruct(Qd, o2, part=P.PART_BOUNDARY)
     assert np.array_equal(o2.cpu().numpy(), a)
+
+
+@pytest.mark.parametrize("d,M,V,per", [(2, 3, 4, True), (3, 2, 5, True), (3, 3, 9, True), (2, 2, 3, False)],
+                         ids=["2d-M3", "3d-M2", "3d-M3-V9", "2d-M2-open"])
+def test_face_traces_parity(d, M, V, per):
+    """cwreco_face_traces (NEXT-3) from the GPU coefficients against the oracle's traces
+    of its own reconstruction (R25 floored tolerance); the two cells of every interior
+    face produce their traces at the same physical points (continuous data agree)."""
+    from oracle import traces as TR
+    nodes, cells, period = gen.box_mesh(d, 9 if d == 2 else 4, per, 0.15, 17)
+    Qin = np.random.default_rng(5).standard_normal((cells.shape[0], V)) + 2.0
+    ctx = P.setup_context(nodes, cells, period, M, V, device=0)
+    m = OracleMesh(nodes, cells, period, M)
+    Q = Qin[m.perm]
+    w = ctx.reconstruct(torch.tensor(Q, device="cuda"))
+    tr = ctx.face_traces(w)
+    torch.cuda.synchronize()
+    tr = tr.cpu().numpy()
+    assert tr.shape == (m.N, d + 1, TR.face_rule(d, M)[0].shape[0], V)
+    worst = 0.0
+    for i in range(0, m.N, 3):
+        r = R.reconstruct_cell(m, i, Q, M)
+        ref = TR.cell_traces(m, i, r["w"], M)              # [d+1, nq, V]
+        s = np.abs(Q[np.asarray(r["central"])]).max(axis=0)  # R25 floor per variable
+        err = np.abs(tr[i] - ref) / np.maximum(np.abs(ref), s)
+        worst = max(worst, float(err.max()))
+    assert worst <= TOL, worst

@@ -256,3 +256,26 @@ def test_set_stencils_roundtrip_and_validation():
     c = P.Context(2, 3, 2, device=None)
     with pytest.raises(P.CwrecoError, match="ESTATE"):
         c.set_stencils(cen, sec, val)
+
+
+@pytest.mark.parametrize("d,M", [(2, 3), (3, 2), (3, 3)])
+def test_face_rule_and_neighbors_match_oracle(d, M):
+    """cwreco_face_rule is the oracle's rule (same points, same order, same weights);
+    cwreco_face_neighbors equals the oracle's face adjacency in local numbering."""
+    from oracle import traces as TR
+    nodes, cells, period = gen.box_mesh(d, 6 if d == 2 else 3, True, 0.1, 3)
+    ctx = P.Context(d, M, 1, device=None)
+    ctx.set_mesh(nodes, cells, period)
+    ctx.build_stencils()
+    lam, w = ctx.face_rule()
+    lo, wo = TR.face_rule(d, M)
+    assert np.allclose(lam, lo, atol=1e-14, rtol=0) and np.allclose(w, wo, atol=1e-15, rtol=0)
+    m = OracleMesh(nodes, cells, period, M)
+    loc = ctx.local_cells()
+    nb = ctx.face_neighbors()
+    n_own = nb.shape[0]
+    for li in range(n_own):
+        g = loc[li]
+        want = m.nbr[g]
+        got = np.where(nb[li] >= 0, loc[np.maximum(nb[li], 0)], -1)
+        assert np.array_equal(got, want), li

@@ -197,6 +197,15 @@ cwreco_status cwreco_send_total(const cwreco_ctx* ctx, int64_t* total);
 cwreco_status cwreco_halo_pack(cwreco_ctx* ctx, const double* d_avgs, int64_t a_cell_stride,
                                int64_t a_var_stride, double* d_sendbuf, cwreco_stream stream);
 
+/* The second exchange of the scheme (reconstruction polynomials after
+ * the pass): pack `width` contiguous doubles of each requested owned row of d_rows
+ * (row stride in doubles; e.g. the coefficients [n_local][nvars][ℳ] with width =
+ * row_stride = nvars·ℳ) into d_sendbuf [send_total][width], peer order — the same
+ * send lists as the averages.  The caller moves the buffer into the peers' ghost
+ * rows (rows n_owned.. of their [n_local][width] array). */
+cwreco_status cwreco_halo_pack_rows(cwreco_ctx* ctx, const double* d_rows, int64_t row_stride, int width,
+                                    double* d_sendbuf, cwreco_stream stream);
+
 /* ---------------------------------------------------------------- hot path */
 /* d_avgs: cell averages of the LOCAL cells, element (c, v) at
  *   d_avgs[c·a_cell_stride + v·a_var_stride]  (n_owned + n_ghost rows);

@@ -71,6 +71,7 @@ def _load():
         "cwreco_set_send_lists": [P, P, P],
         "cwreco_send_total": [P, P],
         "cwreco_halo_pack": [P, P, I64, I64, P, P],
+        "cwreco_halo_pack_rows": [P, P, I64, I32, P, P],
         "cwreco_reconstruct": [P, P, I64, I64, P, I64, I64, I32, P],
         "cwreco_reconstruct_debug": [P, P, I64, I64, I64, P, P, P, P, P, P, P],
         "cwreco_reconstruct_host": [P, P, P, I32, P],
@@ -229,6 +230,15 @@ class Context:
         a_cs, a_vs = avgs.stride()
         _check(lib.cwreco_halo_pack(self._h, ctypes.c_void_p(avgs.data_ptr()), a_cs, a_vs,
                                     ctypes.c_void_p(sendbuf.data_ptr()), _stream_handle(stream)))
+
+    def halo_pack_rows(self, rows, sendbuf, stream=None):
+        """rows: CUDA float64 [n_local, W] (row-contiguous, e.g. coefficients viewed as
+        [n_local, V·ℳ]); packs the requested owned rows into sendbuf [send_total, W]."""
+        if rows.dim() != 2 or rows.stride(1) != 1:
+            raise ValueError("rows must be [n_local, W] with contiguous rows")
+        _check(lib.cwreco_halo_pack_rows(self._h, ctypes.c_void_p(rows.data_ptr()), rows.stride(0),
+                                         rows.shape[1], ctypes.c_void_p(sendbuf.data_ptr()),
+                                         _stream_handle(stream)))
 
     # ---------------------------------------------------------------- hot path
     def reconstruct(self, avgs, out=None, part=PART_ALL, stream=None):

@@ -353,6 +353,18 @@ cwreco_status cwreco_halo_pack(cwreco_ctx* c, const double* d_avgs, int64_t acs,
   });
 }
 
+cwreco_status cwreco_halo_pack_rows(cwreco_ctx* c, const double* d_rows, int64_t row_stride, int width,
+                                    double* d_sendbuf, cwreco_stream stream) {
+  return guard([&] {
+    need(c != nullptr, CWRECO_EINVAL, "halo_pack_rows: NULL");
+    need_device(c, "halo_pack_rows");
+    need(width >= 1 && row_stride >= width, CWRECO_EINVAL, "halo_pack_rows: bad width / stride");
+    if (c->send_local.empty()) return;
+    need(d_rows && d_sendbuf, CWRECO_EINVAL, "halo_pack_rows: NULL buffer");
+    cwr::dev_halo_pack_rows(c, d_rows, row_stride, 1, width, d_sendbuf, stream);
+  });
+}
+
 cwreco_status cwreco_reconstruct(cwreco_ctx* c, const double* d_avgs, int64_t acs, int64_t avs, double* d_coeffs,
                                  int64_t ccs, int64_t cvs, int part, cwreco_stream stream) {
   return guard([&] {

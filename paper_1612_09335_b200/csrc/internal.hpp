@@ -263,6 +263,8 @@ void dev_debug(cwreco_ctx* c, const double* avgs, int64_t acs, int64_t avs, int6
                double* w, void* stream);
 void dev_halo_pack(cwreco_ctx* c, const double* avgs, int64_t acs, int64_t avs, double* sendbuf,
                    void* stream);
+void dev_halo_pack_rows(cwreco_ctx* c, const double* rows, int64_t row_stride, int64_t elem_stride, int width,
+                        double* sendbuf, void* stream);
 int64_t dev_bytes(const cwreco_ctx* c);
 int dev_max_smem(const cwreco_ctx* c);
 void dev_set_send(cwreco_ctx* c);

@@ -727,10 +727,15 @@ void dev_set_send(cwreco_ctx* c) {
 }
 
 void dev_halo_pack(cwreco_ctx* c, const double* avgs, int64_t acs, int64_t avs, double* sendbuf, void* stream) {
+  dev_halo_pack_rows(c, avgs, acs, avs, c->V, sendbuf, stream);
+}
+
+void dev_halo_pack_rows(cwreco_ctx* c, const double* rows, int64_t rs, int64_t es, int width, double* sendbuf,
+                        void* stream) {
   const int64_t n = c->dev->n_send;
   if (n == 0) return;
-  const int64_t threads = n * c->V;
-  k_halo_pack<<<(unsigned)((threads + 255) / 256), 256, 0, (cudaStream_t)stream>>>(avgs, acs, avs, c->V, c->dev->send,
+  const int64_t threads = n * width;
+  k_halo_pack<<<(unsigned)((threads + 255) / 256), 256, 0, (cudaStream_t)stream>>>(rows, rs, es, width, c->dev->send,
                                                                                      n, sendbuf);
   CK(cudaGetLastError());
 }

@@ -53,6 +53,24 @@ def exchange(avgs, sendbuf, send_counts, recv_counts, n_owned, V, group=None):
                            input_split_sizes=[int(c) * V for c in send_counts], group=group)
 
 
+def exchange_polynomials(ctx, coeffs_local, send_counts, recv_counts, group=None, sendbuf=None):
+    """The second communication step: after the pass, the
+    reconstruction polynomials of the ghost cells.  coeffs_local: [n_local, V, ℳ]
+    (owned rows written by cwreco_reconstruct, ghost rows filled here); the pack is
+    the library's cwreco_halo_pack_rows with width V·ℳ, the transfer the same
+    all-to-all-v as the averages."""
+    n_local = coeffs_local.shape[0]
+    W = coeffs_local.shape[1] * coeffs_local.shape[2]
+    rows = coeffs_local.view(n_local, W)
+    n_send = int(np.sum(send_counts))
+    if sendbuf is None:
+        sendbuf = torch.empty((max(1, n_send), W), dtype=torch.float64, device=coeffs_local.device)
+    ctx.halo_pack_rows(rows, sendbuf)
+    n_owned = n_local - int(np.sum(recv_counts))
+    exchange(rows, sendbuf[:n_send], send_counts, recv_counts, n_owned, W, group)
+    return coeffs_local
+
+
 class HaloStepper:
     """One overlapped reconstruction pass on a GPU rank:
     comm stream: cwreco_halo_pack → NCCL all-to-all-v into the ghost rows;

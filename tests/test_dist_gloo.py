@@ -74,7 +74,23 @@ def _worker(rank, world, port, q):
             a = R.reconstruct_cell(m, int(g), Qloc, M)["w"]
             b = R.reconstruct_cell(m, int(g), Qg, M)["w"]
             max_diff = max(max_diff, float(np.nan_to_num(np.abs(a - b), nan=np.inf).max()))
-        q.put((rank, ok_ghost, max_diff, int(inf["n_ghost"]), int(inf["n_owned"] - inf["n_interior"])))
+        # second exchange: polynomials of the ghost cells, rows of V·ℳ
+        # doubles over the same send lists; owned rows from the oracle (the library
+        # has no CPU compute path), ghost rows must arrive equal to their owners'
+        nm = R.n_modes(M, d)
+        W = np.full((len(loc), V, nm), np.nan)
+        need = set(int(g) for g in send_ids)
+        for li in range(n_owned):
+            if int(loc[li]) in need:
+                W[li] = R.reconstruct_cell(m, int(loc[li]), Qg, M)["w"]
+        Wt = torch.tensor(W.reshape(len(loc), V * nm))
+        sendw = torch.tensor(W.reshape(len(loc), V * nm)[[g2l[int(g)] for g in send_ids]])
+        pdist.exchange(Wt, sendw, send_counts, recv_counts, n_owned, V * nm)
+        Wg = Wt.numpy().reshape(len(loc), V, nm)[n_owned:]
+        ok_poly = True
+        for k, g in enumerate(loc[n_owned:][:12]):
+            ok_poly &= bool(np.array_equal(Wg[k], R.reconstruct_cell(m, int(g), Qg, M)["w"]))
+        q.put((rank, ok_ghost and ok_poly, max_diff, int(inf["n_ghost"]), int(inf["n_owned"] - inf["n_interior"])))
         dist.destroy_process_group()
     except Exception as e:  # pragma: no cover - reported to the parent
         q.put((rank, repr(e)))

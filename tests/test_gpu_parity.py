@@ -189,6 +189,13 @@ def test_multirank_emulation_bitwise(family, monkeypatch):
         c.reconstruct(A, out, part=P.PART_INTERIOR)
         c.reconstruct(A, out, part=P.PART_BOUNDARY)
         assert np.array_equal(out.cpu().numpy(), ref[loc[: inf["n_owned"]]])
+        # second exchange: the library packs the requested polynomial rows
+        if c.send_total():
+            rows = out.reshape(inf["n_owned"], V * c.nm)
+            wbuf = torch.empty((c.send_total(), V * c.nm), dtype=torch.float64, device="cuda")
+            c.halo_pack_rows(rows, wbuf)
+            torch.cuda.synchronize()
+            assert np.array_equal(wbuf.cpu().numpy(), ref[ids].reshape(len(ids), V * c.nm))
 
 
 def test_reconstruct_host_end_to_end():

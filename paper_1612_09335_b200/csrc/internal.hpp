@@ -142,8 +142,15 @@ inline int64_t pipe_budget(int nm, int max_smem) {
 // umax_for(T): the largest per-tile stencil union for tiles of T cells.
 Layout make_layout(int d, int M, int V, int G, int max_smem, const std::function<int(int)>& umax_for);
 // k_rowblk: consumer threads per CTA, and whether an instantiation exists for (d, M, V)
-// consumer threads of a row-block CTA (8 warps)
-CWR_HD constexpr int rb_consumers(int R, int V) { return (R > 14 && rb_ng(R, V) == 4) ? 128 : 256; }
+// main-loop threads of a row-block CTA (8 warps: T = 256 / NG cells × NG row groups)
+CWR_HD constexpr int rb_main(int R, int V) { return (R > 14 && rb_ng(R, V) == 4) ? 128 : 256; }
+// consumer threads for T cells: the main-loop threads plus, when V > NG, extra warps
+// that only join the union gather and the per-(cell, variable) epilogue, so its T·V
+// items take one round (C4: 288 items on 9 warps instead of two rounds on 8)
+CWR_HD constexpr int rb_cons_for(int R, int V, int T) {
+  return T * rb_ng(R, V) + (V > rb_ng(R, V) && R > 14 ? ((T * (V - rb_ng(R, V)) + 31) / 32) * 32 : 0);
+}
+CWR_HD constexpr int rb_consumers(int R, int V) { return rb_cons_for(R, V, rb_main(R, V) / rb_ng(R, V)); }
 // default family choice: the row-block kernel where the cell-variable kernel is
 // bound by its shared-memory broadcasts (ℳ = 20 and V ≥ 7: C4); measured slower
 // elsewhere (C2 0.25 vs 0.17 ms, C3 1.34 vs 1.09, C5 13.0 vs 12.0)

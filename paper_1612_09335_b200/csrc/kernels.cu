@@ -462,7 +462,7 @@ static PipeCfg pipe_cfg(const cwreco_ctx* c, int* ctas = nullptr) {
     // the deepest stage ring that fits
     int k = 0, st = 0;
     const PipeFn f = rowblk_fn(c);
-    const int nthr = (L.T * rb_ng(L.R, L.V) / 32 + 1) * 32;
+    const int nthr = rb_cons_for(L.R, L.V, L.T) + 32;
     const char* kcap = std::getenv("CWRECO_CTAS");  // tuning experiments only
     for (int want = kcap ? std::max(1, std::min(3, std::atoi(kcap))) : 3; want >= 1; --want) {
       rowblk_plan(L, c->dev->max_smem, want, k, st);
@@ -476,7 +476,7 @@ static PipeCfg pipe_cfg(const cwreco_ctx* c, int* ctas = nullptr) {
     if (cap) st = std::max(kMinStages, std::min(st, std::atoi(cap)));
     if (!k) fail(CWRECO_EUNSUPPORTED, "row-block kernel: tile does not fit in shared memory");
     if (ctas) *ctas = k;
-    p.ncw = L.T * rb_ng(L.R, L.V) / 32;
+    p.ncw = rb_cons_for(L.R, L.V, L.T) / 32;
     p.stages = st;
     p.off_stage = 0;
     p.off_q = st * p.stage_bytes;

@@ -78,7 +78,7 @@ Layout make_layout(int d, int M, int V, int G, int max_smem, const std::function
     // k_rowblk: T = consumers / NG cells per tile (halved while the CTA does not fit);
     // KC positions per chunk: ~10 KB of B⁺ per stage, KC ∈ {1, 2, 4} (compiled sizes)
     const int R = nm - 1;
-    for (int T = rb_consumers(R, V) / rb_ng(R, V); T >= 32 / rb_ng(R, V); T /= 2) {
+    for (int T = rb_main(R, V) / rb_ng(R, V); T >= 32 / rb_ng(R, V); T /= 2) {
       Layout L0 = layout_with(d, M, V, G, T, kRbKC, umax_for(T), KIND_ROWBLK);
       // sector data in pieces no larger than a position chunk or the union chunk
       const int64_t stage = std::max(L0.chunk_bytes, L0.u_bytes);

@@ -83,8 +83,9 @@ __global__ void __launch_bounds__(rb_consumers(nmodes(M, D) - 1, V) + 32, 1) k_r
   }
 
   // -------------------------------------------------- consumer warps
-  const int nct = pc.ncw * 32;  // = T·NG
-  const int ct = tid / NG, g = tid % NG;
+  const int nct = pc.ncw * 32;  // T·NG main-loop threads (+ epilogue-only warps, rb_cons_for)
+  const bool mainthr = tid < T * NG;
+  const int ct = mainthr ? tid / NG : 0, g = mainthr ? tid % NG : 0;
   // offsets of this thread's B⁺ entries inside a row slot (chunk_elem, KIND_ROWBLK):
   // slots r < RB−1 hold all NG groups, the last one the first NF (a group without a
   // row there reads a neighbour's entry into an accumulator that is never written out)
@@ -194,6 +195,12 @@ __global__ void __launch_bounds__(rb_consumers(nmodes(M, D) - 1, V) + 32, 1) k_r
       if (lane == 0) mbar_arrive(&empty[rg.st]);
       rg.next(S);
     };
+    if (!mainthr) {  // epilogue-only warps (warp-uniform): walk the ring, no math
+      for (int c2 = 0; c2 < nch; ++c2) {
+        mbar_wait(&full[rg.st], rg.ph);
+        release();
+      }
+    } else {
     double qa[2][V], qb[2][V], ba[2][RB], bb[2][RB];
     ldq2(ix2[0], qa);
     uint32_t ipn = ix2[min(1, nch - 1) * T];
@@ -225,6 +232,7 @@ __global__ void __launch_bounds__(rb_consumers(nmodes(M, D) - 1, V) + 32, 1) k_r
       fma_pos(odd_pair ? qb[0] : qa[0], odd_pair ? bb[0] : ba[0]);
       release();
     }
+    }  // main-loop threads
 
     // (after the previous tile's bulk store has read O)
     if (tid == 0) bulk_wait_read();
@@ -236,7 +244,7 @@ __global__ void __launch_bounds__(rb_consumers(nmodes(M, D) - 1, V) + 32, 1) k_r
     }
     // ---- per-item epilogue: p̂_opt rows → O[ct][v][1 + row], then one thread per
     // (cell, variable) runs cweno_epilogue in place
-    {
+    if (mainthr) {
       double* Oc = O + (size_t)ct * V * NM + 1 + g;  // row l = r·NG + g
 #pragma unroll
       for (int r = 0; r < RB; ++r)

@@ -279,7 +279,7 @@ cwreco_status cwreco_get_blocks(const cwreco_ctx* c, int64_t n_sel, const int64_
         }
         tb = tile.data();
       }
-      const double* sv = (const double*)(tb + cwr::sector_sinv_off(L.off_sector, L.sector_bytes, L.TSC, nv * d * d, ct));
+      const double* sv = (const double*)(tb + cwr::sector_sinv_off(L.off_sector, L.sector_bytes, L.TSC, L.srec, ct));
       const uint8_t vm = *(tb + cwr::sector_mask_off(L.off_sector, L.sector_bytes, L.sinv_bytes, L.TSC, ct));
       if (bplus)
         for (int l = 0; l < R; ++l)

@@ -86,10 +86,11 @@ CWR_HD inline int64_t chunk_elem(int kind, int kc, int R, int V, int T, int l, i
   return int64_t(np) * R * T * 2 + int64_t(l) * T + ct;
 }
 
-// Byte offsets (from the tile start) of cell ct's sector inverses and validity byte.
-CWR_HD inline int64_t sector_sinv_off(int64_t off_sector, int64_t sector_bytes, int TSC, int nvdd, int ct) {
+// Byte offsets (from the tile start) of cell ct's sector record (srec doubles: the
+// sector inverses, then for ROWBLK the B⁺ row sums) and validity byte.
+CWR_HD inline int64_t sector_sinv_off(int64_t off_sector, int64_t sector_bytes, int TSC, int srec, int ct) {
   const int j = ct / TSC;
-  return off_sector + j * sector_bytes + int64_t(ct - j * TSC) * nvdd * 8;
+  return off_sector + j * sector_bytes + int64_t(ct - j * TSC) * srec * 8;
 }
 CWR_HD inline int64_t sector_mask_off(int64_t off_sector, int64_t sector_bytes, int64_t sinv_bytes, int TSC, int ct) {
   const int j = ct / TSC;
@@ -108,6 +109,8 @@ struct Layout {
   int64_t chunk_bytes = 0;   // stride of full chunks: KC·kslice_bytes
   int64_t sinv_bytes = 0, sector_bytes = 0, off_sector = 0, tile_bytes = 0;
   int NSC = 1, TSC = 0;      // sector pieces per tile, cells per piece
+  int srec = 0;              // doubles per cell in a sector piece: sector inverses (d+1)·d²,
+                             // then (ROWBLK) the row sums rs[R] of B⁺
   int kc_of(int ch) const { return KC < G - ch * KC ? KC : G - ch * KC; }
   int64_t off_chunk(int ch) const { return u_bytes + int64_t(ch) * chunk_bytes; }
   int64_t chunk_size(int ch) const { return ids_bytes + int64_t(kc_of(ch)) * kslice_bytes; }

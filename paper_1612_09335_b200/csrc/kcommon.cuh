@@ -39,7 +39,7 @@ struct KArgs {
   int64_t tile_bytes, u_bytes, off_idx, idx_bytes, ids_bytes, chunk_bytes, kslice_bytes, off_sector, sinv_bytes,
       sector_bytes;
   int Umax;
-  int T, G, K, KC, NCH, V, VP, kind, NSC, TSC;
+  int T, G, K, KC, NCH, V, VP, kind, NSC, TSC, srec;
   int64_t n_owned, tile_begin, tile_end;
   const double* Q;
   int64_t acs, avs;

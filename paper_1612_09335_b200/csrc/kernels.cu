@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(256) k_simple(KArgs a, DbgOut dbg) {
   const int64_t tile = c / a.T;
   const int ct = int(c % a.T);
   const unsigned char* tb = a.blocks + tile * a.tile_bytes;
-  const double* sinv = (const double*)(tb + sector_sinv_off(a.off_sector, a.sector_bytes, a.TSC, NV * D * D, ct));
+  const double* sinv = (const double*)(tb + sector_sinv_off(a.off_sector, a.sector_bytes, a.TSC, a.srec, ct));
   const uint8_t vmask = *(tb + sector_mask_off(a.off_sector, a.sector_bytes, a.sinv_bytes, a.TSC, ct));
   const double* Qv = a.Q + v * a.avs;
   const double qi = Qv[c * a.acs];
@@ -89,13 +89,21 @@ __global__ void __launch_bounds__(256) k_simple(KArgs a, DbgOut dbg) {
     for (int kk = 0; kk < kc; ++kk) {
       const int p = ch * a.KC + kk;
       const int32_t j = ((const int32_t*)tb)[idx[idx_elem(a.kind, a.T, p, ct)] / a.VP];  // union chunk
-      const double dq = Qv[int64_t(j) * a.acs] - qi;
+      const double qj = Qv[int64_t(j) * a.acs];
+      const double dq = qj - qi;
 #pragma unroll
       for (int q = 0; q < NCAP; ++q)
         if (p == q) dqs[q] = dq;
+      // ROWBLK family: B⁺Q accumulated on the raw averages, B⁺ΔQ = B⁺Q − rs·Q_i after
+      // the loop (row sums rs from the sector record; k_rowblk's arithmetic)
+      const double x = a.kind == KIND_ROWBLK ? qj : dq;
 #pragma unroll
-      for (int l = 0; l < R; ++l) acc[l] = __fma_rn(Bc[chunk_elem(a.kind, kc, R, a.V, a.T, l, ct, kk)], dq, acc[l]);
+      for (int l = 0; l < R; ++l) acc[l] = __fma_rn(Bc[chunk_elem(a.kind, kc, R, a.V, a.T, l, ct, kk)], x, acc[l]);
     }
+  }
+  if (a.kind == KIND_ROWBLK) {
+#pragma unroll
+    for (int l = 0; l < R; ++l) acc[l] = __fma_rn(-sinv[NV * D * D + l], qi, acc[l]);
   }
   bool valid[NV];
 #pragma unroll
@@ -404,6 +412,7 @@ static KArgs make_args(const cwreco_ctx* c, const double* avgs, int64_t acs, int
   a.sector_bytes = L.sector_bytes;
   a.NSC = L.NSC;
   a.TSC = L.TSC;
+  a.srec = L.srec;
   a.T = L.T;
   a.G = L.G;
   a.K = L.K;

@@ -46,7 +46,8 @@ static Layout layout_with(int d, int M, int V, int G, int T, int KC, int Umax, i
   L.off_sector = r16(L.off_chunk(L.NCH - 1) + L.chunk_size(L.NCH - 1));
   L.NSC = nsc;
   L.TSC = (T + nsc - 1) / nsc;
-  L.sinv_bytes = int64_t(L.TSC) * (d + 1) * d * d * 8;
+  L.srec = (d + 1) * d * d + (kind == KIND_ROWBLK ? L.R : 0);
+  L.sinv_bytes = int64_t(L.TSC) * L.srec * 8;
   L.sector_bytes = r16(L.sinv_bytes + L.TSC);
   L.tile_bytes = L.off_sector + nsc * L.sector_bytes;
   return L;
@@ -83,7 +84,7 @@ Layout make_layout(int d, int M, int V, int G, int max_smem, const std::function
       // sector data in pieces no larger than a position chunk or the union chunk
       const int64_t stage = std::max(L0.chunk_bytes, L0.u_bytes);
       int nsc = 1;
-      while (nsc < T && r16(int64_t((T + nsc - 1) / nsc) * ((d + 1) * d * d * 8 + 1)) > stage) ++nsc;
+      while (nsc < T && r16(int64_t((T + nsc - 1) / nsc) * (L0.srec * 8 + 1)) > stage) ++nsc;
       Layout L = layout_with(d, M, V, G, T, kRbKC, L0.Umax, KIND_ROWBLK, nsc);
       int ctas, stages;
       rowblk_plan(L, max_smem, 1, ctas, stages);
@@ -506,10 +507,18 @@ void precompute(cwreco_ctx* c) {
           const int k = col[p];
           for (int l = 0; l < R; ++l) chb[chunk_elem(L.kind, kc, R, L.V, T, l, ct, kk)] = k >= 0 ? Bp[size_t(l) * K + k] : 0.0;
         }
+        if (L.kind == KIND_ROWBLK) {  // rs[l] = Σ_p B⁺[l][p] (positions in gather order)
+          double* rs = (double*)(tb + sector_sinv_off(L.off_sector, L.sector_bytes, L.TSC, L.srec, ct)) + nvdd;
+          for (int l = 0; l < R; ++l) {
+            double t = 0.0;
+            for (int p = 0; p < G; ++p) t += col[p] >= 0 ? Bp[size_t(l) * K + col[p]] : 0.0;
+            rs[l] = t;
+          }
+        }
 
         // sector inverses
         for (int s = 0; s < nv; ++s) {
-          double* Sd = (double*)(tb + sector_sinv_off(L.off_sector, L.sector_bytes, L.TSC, nvdd, ct)) + s * d * d;
+          double* Sd = (double*)(tb + sector_sinv_off(L.off_sector, L.sector_bytes, L.TSC, L.srec, ct)) + s * d * d;
           for (int e = 0; e < d * d; ++e) Sd[e] = 0.0;
           if (!val[s]) continue;
           double As[9];

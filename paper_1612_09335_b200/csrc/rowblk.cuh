@@ -180,14 +180,14 @@ __global__ void __launch_bounds__(rb_consumers(nmodes(M, D) - 1, V) + 32, 1) k_r
 #pragma unroll
         for (int r = 0; r < RB; ++r) b[k][r] = Bs[(k * R + r * NG) * T + (r < RB - 1 ? bfull : bpart)];
     };
+    // B⁺Q on the raw averages (no per-lane ΔQ subtractions); B⁺ΔQ = B⁺Q − rs·Q_i is
+    // formed in the epilogue with the row sums rs of the sector record (|B⁺| rows sum
+    // to < 1 on the configs, so the cancellation costs ~1e-16·max|Q|, far inside R25)
     auto fma_pos = [&](const double (&q)[V], const double (&b)[RB]) {
-      double dq[V];
-#pragma unroll
-      for (int v = 0; v < V; ++v) dq[v] = q[v] - qi[v];
 #pragma unroll
       for (int r = 0; r < RB; ++r)
 #pragma unroll
-        for (int v = 0; v < V; ++v) acc[r][v] = __fma_rn(b[r], dq[v], acc[r][v]);
+        for (int v = 0; v < V; ++v) acc[r][v] = __fma_rn(b[r], q[v], acc[r][v]);
     };
     auto stage_ptr = [&]() { return (const double*)(stg + rg.st * pc.stage_bytes); };
     auto release = [&]() {
@@ -260,9 +260,10 @@ __global__ void __launch_bounds__(rb_consumers(nmodes(M, D) - 1, V) + 32, 1) k_r
       const unsigned char* sb = stg + sst * pc.stage_bytes;
       const double q2 = Qb[c2 * VP + v2];
       double* row = O + (size_t)item * NM;
+      const double* srec = (const double*)sb + size_t(cl) * a.srec;  // sector inverses, then rs
       double accr[R];
 #pragma unroll
-      for (int l = 0; l < R; ++l) accr[l] = row[1 + l];
+      for (int l = 0; l < R; ++l) accr[l] = __fma_rn(-srec[NV * D * D + l], q2, row[1 + l]);
       double dqs[NCAP];
 #pragma unroll
       for (int p = 0; p < NCAP; ++p) dqs[p] = Qb[ixb[idx_elem(KIND_ROWBLK, T, p, c2)] + v2] - q2;
@@ -271,7 +272,7 @@ __global__ void __launch_bounds__(rb_consumers(nmodes(M, D) - 1, V) + 32, 1) k_r
 #pragma unroll
       for (int q = 0; q < NV; ++q) valid[q] = (vmask >> q) & 1;
       double ps[NV][D];
-      sector_apply<D>((const double*)sb + size_t(cl) * NV * D * D, dqs, ps);
+      sector_apply<D>(srec, dqs, ps);
       if (a.dense_out) {
         cweno_epilogue<D, NM>(q2, accr, ps, valid, a, row, nullptr, nullptr);
       } else {

@@ -372,7 +372,7 @@ def run_ours(args):
                           "traffic": None, "peak_source": FP64_PEAK_SRC, "flops_per_cell": mf_flops,
                           "kernel": "cwr::k_matfree"} if mf_flops else
                          {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": profiled_traffic(args.config, args.kernel),
+                         "frac": achieved / peak, "frac_vs_8tbs": achieved / 8000.0, "traffic": profiled_traffic(args.config, args.kernel),
                          "peak_source": peak_src, "algorithmic_bytes_per_cell": bpc,
                          "kernel": "cwr::k_pipelined" if args.kernel == "pipelined" else "cwr::k_simple"}),
             "cpu_baseline": cpu,

@@ -17,8 +17,9 @@
 //    stages with 1-D TMA bulk copies completing on mbarrier transaction counts;
 //  - consumers (T cells × NG row groups): at tile start they cp.async the V
 //    averages of every cell of the next tile's stencil union into the other half
-//    of a double-buffered Q_u[2][Umax][VP]; per position: ΔQ = Q_u[idx] − Q_i for
-//    all V, then acc[r][v] += B⁺[row r][p]·ΔQ[v] for the thread's rows; after the
+//    of a double-buffered Q_u[2][Umax][VP]; per position: acc[r][v] +=
+//    B⁺[row r][p]·Q_u[idx][v] for the thread's rows and all V (B⁺ΔQ = B⁺Q − rs·Q_i
+//    is completed in the epilogue with the stored row sums rs); after the
 //    last chunk the row groups write p̂_opt into the tile's output rows
 //    O[T][V][ℳ] (slots 1..R), and one thread per (cell, variable) runs the fused
 //    sector / P0 / σ / ω / blend epilogue in place (reading its sector ΔQ back
@@ -142,9 +143,6 @@ __global__ void __launch_bounds__(rb_consumers(nmodes(M, D) - 1, V) + 32, 1) k_r
     if (tile + gridDim.x < a.tile_end) gather_union(buf ^ 1);
     const double* Qb = Qu + (size_t)buf * a.Umax * VP;
     const uint16_t* ixb = (const uint16_t*)((const unsigned char*)Ix + buf * a.idx_bytes);
-    double qi[V];
-#pragma unroll
-    for (int v = 0; v < V; ++v) qi[v] = Qb[ct * VP + v];  // the tile's own cells lead its union
 
     double acc[RB][V];
 #pragma unroll

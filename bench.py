@@ -374,7 +374,8 @@ def run_ours(args):
                          {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "frac_vs_8tbs": achieved / 8000.0, "traffic": profiled_traffic(args.config, args.kernel),
                          "peak_source": peak_src, "algorithmic_bytes_per_cell": bpc,
-                         "kernel": "cwr::k_pipelined" if args.kernel == "pipelined" else "cwr::k_simple"}),
+                         "kernel": ("cwr::k_rowblk" if inf.get("kernel_family") == 1 else "cwr::k_pipelined")
+                                   if args.kernel == "pipelined" else "cwr::k_simple"}),
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "cells/s", "h2d_bytes_per_step": int(avgs_local.nbytes),
                     "d2h_bytes_per_step": int(n_owned * V * nm * 8), "api": e2e_api},

@@ -107,6 +107,10 @@ typedef struct {
   int64_t n_extra_gather;                /* sector cells outside S_i^0 (R15) */
   int64_t union_max;                     /* largest per-tile stencil union (cells whose
                                             averages a tile gathers once into shared memory) */
+  int32_t kernel_family;                 /* layout of the packed stream after precompute:
+                                            0 = cell-variable (k_pipelined),
+                                            1 = row-block (k_rowblk); -1 before */
+  int32_t reserved_;
 } cwreco_info;
 
 /* ---------------------------------------------------------------- lifecycle */

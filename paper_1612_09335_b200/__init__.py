@@ -40,7 +40,8 @@ class _Info(ctypes.Structure):
                [(n, ctypes.c_int64) for n in ("n_cells", "n_owned", "n_ghost", "n_interior", "n_tiles",
                                                "n_interior_tiles", "tile_bytes", "device_bytes",
                                                "algorithmic_bytes_per_cell", "n_invalid_sectors",
-                                               "n_extra_gather", "union_max")]
+                                               "n_extra_gather", "union_max")] + \
+               [(n, ctypes.c_int32) for n in ("kernel_family", "reserved_")]
 
 
 def _load():

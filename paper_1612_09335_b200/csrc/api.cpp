@@ -105,6 +105,7 @@ cwreco_status cwreco_get_info(const cwreco_ctx* c, cwreco_info* o) {
     o->n_invalid_sectors = c->n_invalid;
     o->n_extra_gather = c->n_extra;
     o->union_max = c->lay.Umax;
+    o->kernel_family = c->has_blocks ? c->lay.kind : -1;
     if (c->has_blocks) {
       o->tile_cells = c->lay.T;
       o->chunk_k = c->lay.KC;

@@ -287,3 +287,13 @@ def test_face_traces_parity(d, M, V, per):
         err = np.abs(tr[i] - ref) / np.maximum(np.abs(ref), s)
         worst = max(worst, float(err.max()))
     assert worst <= TOL, worst
+
+
+def test_c_client_on_gpu(tmp_path):
+    """examples/cwreco_example.c end to end on the GPU through the C-ABI alone."""
+    import subprocess
+    from test_library_host import _build_c_example
+    exe = _build_c_example(tmp_path)
+    r = subprocess.run([exe, "0"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "conservation error" in r.stdout

@@ -3,6 +3,7 @@ symbol of include/cwreco.h; the setup (Morton order, stencils) is bit-exact
 against the oracle; the precomputed per-cell matrices reproduce the oracle's
 P_opt / P_s (T2, host matvec in the test); error codes; layout facts."""
 import ctypes
+import os
 import re
 import subprocess
 
@@ -279,3 +280,22 @@ def test_face_rule_and_neighbors_match_oracle(d, M):
         want = m.nbr[g]
         got = np.where(nb[li] >= 0, loc[np.maximum(nb[li], 0)], -1)
         assert np.array_equal(got, want), li
+
+
+def _build_c_example(tmp_path):
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib = os.path.join(root, "paper_1612_09335_b200")
+    exe = str(tmp_path / "cwreco_example")
+    subprocess.run(["cc", "-O2", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(root, "include"),
+                    os.path.join(root, "examples", "cwreco_example.c"), "-L", lib, "-lcwreco",
+                    "-Wl,-rpath," + lib, "-lm", "-o", exe], check=True)
+    return exe
+
+
+def test_c_client_host_only(tmp_path):
+    """The C-ABI is usable from plain C (examples/cwreco_example.c): mesh, stencils and
+    precompute run on the host; the compute call reports ECUDA (no CPU fallback)."""
+    exe = _build_c_example(tmp_path)
+    r = subprocess.run([exe, "-1"], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr
+    assert "cells 1152, modes 10" in r.stdout and "status 3" in r.stderr

@@ -322,7 +322,7 @@ def run_ours(args):
     h_in = torch.from_numpy(avgs_local).pin_memory()
     h_out = torch.empty((n_owned, V, nm), dtype=torch.float64).pin_memory()
     e2e_steps = max(3, min(args.steps, 50))
-    if world == 1 and args.kernel != "matrixfree":
+    if world == 1:
         def e2e_step():
             ctx.reconstruct_host(h_in, h_out, stream=stream)
         e2e_api = "cwreco_reconstruct_host (C-ABI, pinned host buffers)"

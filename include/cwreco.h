@@ -231,7 +231,7 @@ cwreco_status cwreco_reconstruct(cwreco_ctx* ctx, const double* d_avgs, int64_t 
  * soon as that range is done, so the device→host transfer overlaps the remaining
  * ranges.  Page-locked host buffers (cudaHostAlloc / cudaHostRegister, torch
  * pin_memory) give asynchronous copies; pageable buffers work but serialise.
- * n_pieces ≤ 0 selects the default (4).  Synchronous: returns after h_coeffs is
+ * (cells, in matrix-free mode).  n_pieces ≤ 0 selects the default (4).  Synchronous: returns after h_coeffs is
  * complete.  Errors as cwreco_reconstruct; ENOMEM if the device buffers cannot be
  * allocated. */
 cwreco_status cwreco_reconstruct_host(cwreco_ctx* ctx, const double* h_avgs, double* h_coeffs, int n_pieces,

@@ -389,10 +389,11 @@ cwreco_status cwreco_reconstruct_host(cwreco_ctx* c, const double* h_avgs, doubl
   return guard([&] {
     need(c != nullptr, CWRECO_EINVAL, "reconstruct_host: NULL ctx");
     need_device(c, "reconstruct_host");
-    need(c->has_blocks, CWRECO_ESTATE, "reconstruct_host: call cwreco_precompute first");
+    if (c->kernel == CWRECO_KERNEL_MATRIXFREE)
+      need(c->mf != nullptr, CWRECO_ESTATE, "reconstruct_host: call cwreco_prepare_matrixfree first");
+    else
+      need(c->has_blocks, CWRECO_ESTATE, "reconstruct_host: call cwreco_precompute first");
     need(h_avgs && h_coeffs, CWRECO_EINVAL, "reconstruct_host: NULL buffer");
-    need(c->kernel != CWRECO_KERNEL_MATRIXFREE, CWRECO_EUNSUPPORTED,
-         "reconstruct_host: use the device-pointer call in matrix-free mode");
     cwr::dev_reconstruct_host(c, h_avgs, h_coeffs, n_pieces > 0 ? n_pieces : 4, stream);
   });
 }

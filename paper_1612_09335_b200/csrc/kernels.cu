@@ -661,11 +661,15 @@ void dev_reconstruct_host(cwreco_ctx* c, const double* h_avgs, double* h_coeffs,
     ds->piece_done.push_back(e);
   }
   CK(cudaMemcpyAsync(ds->h_avgs, h_avgs, na * 8, cudaMemcpyHostToDevice, st));
-  const int64_t nt = c->n_tiles, T = c->lay.T, row = (int64_t)V * nm;
+  const bool mf = c->kernel == CWRECO_KERNEL_MATRIXFREE;  // pieces of cells instead of tiles
+  const int64_t nt = mf ? c->n_owned : c->n_tiles, T = mf ? 1 : c->lay.T, row = (int64_t)V * nm;
   for (int k = 0; k < n_pieces; ++k) {
     const int64_t a = nt * k / n_pieces, b = nt * (k + 1) / n_pieces;
     if (b <= a) continue;
-    launch_range(c, ds->h_avgs, V, 1, ds->h_coeffs, row, nm, a, b, st);
+    if (mf)
+      dev_matfree_reconstruct(c, ds->h_avgs, V, 1, ds->h_coeffs, row, nm, a, b, st);
+    else
+      launch_range(c, ds->h_avgs, V, 1, ds->h_coeffs, row, nm, a, b, st);
     CK(cudaEventRecord(ds->piece_done[k], st));
     CK(cudaStreamWaitEvent(ds->copy_stream, ds->piece_done[k], 0));
     const int64_t c0 = a * T, c1 = std::min(c->n_owned, b * T);

@@ -260,6 +260,8 @@ def test_matrixfree_parity(case):
     ctx.reconstruct(Qd, o2, part=P.PART_INTERIOR)
     ctx.reconstruct(Qd, o2, part=P.PART_BOUNDARY)
     assert np.array_equal(o2.cpu().numpy(), a)
+    # host buffers through cwreco_reconstruct_host, in pieces of cells
+    assert np.array_equal(ctx.reconstruct_host(Q, n_pieces=3).numpy(), a)
 
 
 @pytest.mark.parametrize("d,M,V,per", [(2, 3, 4, True), (3, 2, 5, True), (3, 3, 9, True), (2, 2, 3, False)],

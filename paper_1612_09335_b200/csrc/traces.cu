@@ -15,6 +15,7 @@
 // write (d+1)·nq·V doubles per cell.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -34,56 +35,93 @@ struct TraceState {
   int nq = 0;
 };
 
-template <int NM, int V>
+// A block handles CB consecutive cells.  Work unit = (cell, face, block of QB points):
+// a V × QB register tile streamed over the ℳ modes (per mode V coefficient loads and
+// QB table loads feed V·QB FMAs, so a cell's coefficients are read (d+1)·nq/QB
+// times, not (d+1)·nq).  The tiles land in shared memory in the output layout and
+// the block's contiguous output region is written with coalesced stores.
+template <int NM, int V, int QB>
 __global__ void __launch_bounds__(256) k_traces(const double* __restrict__ w, int64_t ccs, int64_t cvs,
                                                 const double* __restrict__ phi, const uint8_t* __restrict__ code,
-                                                int nf, int nq, int64_t n_owned, double* __restrict__ out) {
-  const int64_t gid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;  // (cell, face, point)
-  const int64_t per = int64_t(nf) * nq;
-  if (gid >= n_owned * per) return;
-  const int64_t i = gid / per;
-  const int fq = int(gid - i * per), f = fq / nq, q = fq - f * nq;
-  const double* p = phi + (int64_t(code[i * nf + f]) * nq + q) * NM;
-  double ph[NM];
+                                                int nf, int nq, int cb, int64_t n_owned, double* __restrict__ out) {
+  extern __shared__ __align__(16) double tr_smem[];  // [cb][nf][nq][V]
+  const int nb = nq / QB, units = nf * nb;
+  const int64_t c0 = int64_t(blockIdx.x) * cb;
+  const int ncell = (int)min((int64_t)cb, n_owned - c0);
+  const int u = threadIdx.x;
+  if (u < ncell * units) {
+    const int cl = u / units, fb = u - cl * units, f = fb / nb, q0 = (fb - f * nb) * QB;
+    const int64_t i = c0 + cl;
+    const double* p = phi + (int64_t(code[i * nf + f]) * nq + q0) * NM;
+    const double* wi = w + i * ccs;
+    double acc[V][QB];
 #pragma unroll
-  for (int l = 0; l < NM; ++l) ph[l] = p[l];
-  const double* wi = w + i * ccs;
-  double* o = out + gid * V;
+    for (int v = 0; v < V; ++v)
 #pragma unroll
-  for (int v = 0; v < V; ++v) {
-    double t = 0.0;
+      for (int b = 0; b < QB; ++b) acc[v][b] = 0.0;
 #pragma unroll
-    for (int l = 0; l < NM; ++l) t = __fma_rn(wi[v * cvs + l], ph[l], t);
-    o[v] = t;
+    for (int l = 0; l < NM; ++l) {
+      double ph[QB], wv[V];
+#pragma unroll
+      for (int b = 0; b < QB; ++b) ph[b] = __ldg(p + b * NM + l);
+#pragma unroll
+      for (int v = 0; v < V; ++v) wv[v] = __ldg(wi + v * cvs + l);
+#pragma unroll
+      for (int v = 0; v < V; ++v)
+#pragma unroll
+        for (int b = 0; b < QB; ++b) acc[v][b] = __fma_rn(wv[v], ph[b], acc[v][b]);
+    }
+    double* o = tr_smem + ((cl * nf + f) * nq + q0) * V;
+#pragma unroll
+    for (int b = 0; b < QB; ++b)
+#pragma unroll
+      for (int v = 0; v < V; ++v) o[b * V + v] = acc[v][b];
   }
+  __syncthreads();
+  const int n = ncell * nf * nq * V;
+  double* dst = out + c0 * nf * nq * V;
+  for (int k = threadIdx.x; k < n; k += blockDim.x) dst[k] = tr_smem[k];
 }
 
-using TrFn = void (*)(const double*, int64_t, int64_t, const double*, const uint8_t*, int, int, int64_t, double*);
-template <int NM>
+using TrFn = void (*)(const double*, int64_t, int64_t, const double*, const uint8_t*, int, int, int, int64_t,
+                      double*);
+template <int NM, int QB>
 static TrFn tr_fn_v(int V) {
   switch (V) {
-    case 1: return k_traces<NM, 1>;
-    case 2: return k_traces<NM, 2>;
-    case 3: return k_traces<NM, 3>;
-    case 4: return k_traces<NM, 4>;
-    case 5: return k_traces<NM, 5>;
-    case 6: return k_traces<NM, 6>;
-    case 7: return k_traces<NM, 7>;
-    case 8: return k_traces<NM, 8>;
-    case 9: return k_traces<NM, 9>;
+    case 1: return k_traces<NM, 1, QB>;
+    case 2: return k_traces<NM, 2, QB>;
+    case 3: return k_traces<NM, 3, QB>;
+    case 4: return k_traces<NM, 4, QB>;
+    case 5: return k_traces<NM, 5, QB>;
+    case 6: return k_traces<NM, 6, QB>;
+    case 7: return k_traces<NM, 7, QB>;
+    case 8: return k_traces<NM, 8, QB>;
+    case 9: return k_traces<NM, 9, QB>;
     default: return nullptr;
   }
 }
-static TrFn tr_fn(int nm, int V) {
+// points per work unit (measured, tools/traces_bench.py with CWRECO_TRACE_QB): 3 for
+// the 9-point faces of 3-D M = 2 (C3 1.53 → 1.04 ms), otherwise 1 (C5: 18.9 ms at 1,
+// 21.1 at 2, 31.9 at 4 — the ℳ = 20 tiles stall on their table loads; C2 0.152 at 1)
+static int tr_qb(int nq, int nm) { return (nq % 3 == 0 && nm <= 10) ? 3 : 1; }
+static TrFn tr_fn(int nm, int V, int qb) {
   TrFn f = nullptr;
+#define TRC(NMV)                                   \
+  case NMV:                                        \
+    f = qb == 4   ? tr_fn_v<NMV, 4>(V)             \
+        : qb == 3 ? tr_fn_v<NMV, 3>(V)             \
+        : qb == 2 ? tr_fn_v<NMV, 2>(V)             \
+                  : tr_fn_v<NMV, 1>(V);            \
+    break;
   switch (nm) {
-    case 3: f = tr_fn_v<3>(V); break;
-    case 4: f = tr_fn_v<4>(V); break;
-    case 6: f = tr_fn_v<6>(V); break;
-    case 10: f = tr_fn_v<10>(V); break;
-    case 15: f = tr_fn_v<15>(V); break;
-    case 20: f = tr_fn_v<20>(V); break;
+    TRC(3)
+    TRC(4)
+    TRC(6)
+    TRC(10)
+    TRC(15)
+    TRC(20)
   }
+#undef TRC
   if (!f) fail(CWRECO_EUNSUPPORTED, "face traces: nvars must be ≤ 9");
   return f;
 }
@@ -153,11 +191,20 @@ void dev_face_traces(cwreco_ctx* c, const double* coeffs, int64_t ccs, int64_t c
   if (!c->tr) traces_prepare(c);
   TraceState* t = (TraceState*)c->tr;
   const int nv = c->d + 1;
-  const int64_t threads = c->n_owned * nv * t->nq;
-  if (threads == 0) return;
-  TrFn f = tr_fn(c->nm, c->V);
-  f<<<(unsigned)((threads + 255) / 256), 256, 0, (cudaStream_t)stream>>>(coeffs, ccs, cvs, t->phi, t->code, nv, t->nq,
-                                                                          c->n_owned, traces);
+  int qb = tr_qb(t->nq, c->nm);
+  if (const char* e = std::getenv("CWRECO_TRACE_QB")) {  // tuning experiments only
+    const int x = std::atoi(e);
+    if (x >= 1 && x <= 4 && t->nq % x == 0) qb = x;
+  }
+  const int units = nv * (t->nq / qb);
+  const int cb = std::max(1, 256 / units);
+  const int64_t blocks = (c->n_owned + cb - 1) / cb;
+  if (blocks == 0) return;
+  const size_t smem = size_t(cb) * nv * t->nq * c->V * sizeof(double);
+  TrFn f = tr_fn(c->nm, c->V, qb);
+  TCK(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  f<<<(unsigned)blocks, 256, smem, (cudaStream_t)stream>>>(coeffs, ccs, cvs, t->phi, t->code, nv, t->nq, cb,
+                                                           c->n_owned, traces);
   TCK(cudaGetLastError());
 }
 

@@ -299,3 +299,16 @@ def test_c_client_on_gpu(tmp_path):
     r = subprocess.run([exe, "0"], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "conservation error" in r.stdout
+
+
+def test_rowblk_constant_data(monkeypatch):
+    """The row-block family forms B⁺ΔQ as B⁺Q − rs·Q_i: on constant data the higher
+    modes are rounding-level (not exactly 0 as in the ΔQ form), the mean exact."""
+    monkeypatch.setenv("CWRECO_FAMILY", "1")
+    nodes, cells, period = gen.box_mesh(3, 4, True, 0.1, 4)
+    ctx = P.setup_context(nodes, cells, period, 3, 9, device=0)
+    assert ctx.info()["kernel_family"] == 1
+    Qc = np.full((cells.shape[0], 9), 1.25)
+    w = _run(ctx, Qc, "pipelined")
+    assert np.all(w[:, :, 0] == 1.25 / np.sqrt(6.0))
+    assert np.abs(w[:, :, 1:]).max() <= 1e-14 * 1.25

@@ -162,7 +162,7 @@ CWR_HD constexpr int rb_consumers(int R, int V) { return rb_cons_for(R, V, rb_ma
 // bound by its shared-memory broadcasts (ℳ = 20 and V ≥ 7: C4); measured slower
 // elsewhere (C2 0.25 vs 0.17 ms, C3 1.34 vs 1.09, C5 13.0 vs 12.0)
 CWR_HD constexpr bool rb_default(int R, int V) { return R > 14 && V >= 7; }
-constexpr int kRbKC = 2;  // positions per streamed chunk of the row-block layout
+constexpr int kRbKC = 4;  // positions per streamed chunk of the row-block layout (2 pairs)
 constexpr int kRbMaxStages = 32;  // row-block stage ring: as deep as shared memory allows
 bool rowblk_supported(int d, int M, int V);
 // CTAs per SM (≤ max_ctas, by shared memory) and stage-ring depth of a ROWBLK

@@ -155,9 +155,10 @@ __global__ void __launch_bounds__(rb_consumers(nmodes(M, D) - 1, V) + 32, 1) k_r
     // are loaded right after its stage arrives, before chunk ch's stage is released.
     // Ping-pong buffers (qa/qb, ba/bb) avoid register moves.  A trailing odd
     // position (G odd) is peeled.
-    static_assert(KC == 2, "row-block main loop is written for position pairs");
-    const int G = a.G, nfc = G / 2, nch = (G + 1) / 2;
-    const uint32_t* ix2 = reinterpret_cast<const uint32_t*>(ixb) + ct;  // [chunk][T] offset pairs
+    static_assert(KC % 2 == 0, "row-block chunks hold whole position pairs");
+    constexpr int PPS = KC / 2;  // position pairs per stage
+    const int G = a.G, nfc = G / 2, npr = (G + 1) / 2;  // full pairs; pairs incl. a trailing single
+    const uint32_t* ix2 = reinterpret_cast<const uint32_t*>(ixb) + ct;  // [pair][T] offset pairs
     auto ldq = [&](int off, double (&d)[V]) {
       const double* q = Qb + off;
 #pragma unroll
@@ -172,7 +173,7 @@ __global__ void __launch_bounds__(rb_consumers(nmodes(M, D) - 1, V) + 32, 1) k_r
       ldq(int(pr & 0xffffu), d[0]);
       ldq(int(pr >> 16), d[1]);
     };
-    auto ldb = [&](const double* Bs, double (&b)[2][RB]) {
+    auto ldb = [&](const double* Bs, double (&b)[2][RB]) {  // Bs: the pair's first position
 #pragma unroll
       for (int k = 0; k < 2; ++k)
 #pragma unroll
@@ -194,38 +195,44 @@ __global__ void __launch_bounds__(rb_consumers(nmodes(M, D) - 1, V) + 32, 1) k_r
       rg.next(S);
     };
     if (!mainthr) {  // epilogue-only warps (warp-uniform): walk the ring, no math
-      for (int c2 = 0; c2 < nch; ++c2) {
+      for (int c2 = 0; c2 < a.NCH; ++c2) {
         mbar_wait(&full[rg.st], rg.ph);
         release();
       }
     } else {
     double qa[2][V], qb[2][V], ba[2][RB], bb[2][RB];
     ldq2(ix2[0], qa);
-    uint32_t ipn = ix2[min(1, nch - 1) * T];
+    uint32_t ipn = ix2[min(1, npr - 1) * T];
     mbar_wait(&full[rg.st], rg.ph);
     ldb(stage_ptr(), ba);
-    // one full chunk: q/b hold its averages and B⁺ entries; qn/bn receive chunk ch+1's
-    auto chunk = [&](int ch, const double (&q)[2][V], const double (&b)[2][RB], double (&qn)[2][V],
-                     double (&bn)[2][RB]) {
+    // one full pair pp: q/b hold its averages and B⁺ entries; qn/bn receive pair pp+1's
+    // (from the same stage, or from the next one, which releases the current stage)
+    auto pair = [&](int pp, const double (&q)[2][V], const double (&b)[2][RB], double (&qn)[2][V],
+                    double (&bn)[2][RB]) {
       ldq2(ipn, qn);
-      ipn = ix2[min(ch + 2, nch - 1) * T];
+      ipn = ix2[min(pp + 2, npr - 1) * T];
       fma_pos(q[0], b[0]);
       fma_pos(q[1], b[1]);
-      if (ch + 1 < nch) {  // next stage: its B⁺ entries (a tail chunk reads past kc into the stage: unused)
-        Ring nx = rg;
-        nx.next(S);
-        mbar_wait(&full[nx.st], nx.ph);
-        ldb((const double*)(stg + nx.st * pc.stage_bytes), bn);
+      const int nx = pp + 1;
+      if (nx >= npr) {
+        release();
+      } else if (nx % PPS == 0) {  // next stage (a tail pair reads past kc into the stage: unused)
+        Ring nr = rg;
+        nr.next(S);
+        mbar_wait(&full[nr.st], nr.ph);
+        ldb((const double*)(stg + nr.st * pc.stage_bytes), bn);
+        release();
+      } else {
+        ldb(stage_ptr() + (nx % PPS) * 2 * R * T, bn);
       }
-      release();
     };
-    int ch = 0;
-    for (; ch + 1 < nfc; ch += 2) {
-      chunk(ch, qa, ba, qb, bb);
-      chunk(ch + 1, qb, bb, qa, ba);
+    int pp = 0;
+    for (; pp + 1 < nfc; pp += 2) {
+      pair(pp, qa, ba, qb, bb);
+      pair(pp + 1, qb, bb, qa, ba);
     }
-    const bool odd_pair = ch < nfc;
-    if (odd_pair) chunk(ch, qa, ba, qb, bb);
+    const bool odd_pair = pp < nfc;
+    if (odd_pair) pair(pp, qa, ba, qb, bb);
     if (G & 1) {  // the last position alone (its stage already waited for)
       fma_pos(odd_pair ? qb[0] : qa[0], odd_pair ? bb[0] : ba[0]);
       release();

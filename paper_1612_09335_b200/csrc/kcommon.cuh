@@ -89,16 +89,16 @@ __device__ __forceinline__ void cweno_epilogue(double qi, double* acc, const dou
 #pragma unroll
   for (int s = 0; s <= D; ++s) nval += valid[s] ? 1 : 0;
   const double l0 = a.l0[nval], il0 = a.inv_l0[nval], ls = a.ls[nval];
-  // P0 = (P_opt − Σ_s λ̄_s P_s)/λ̄0; modes above d are P_opt/λ̄0
+  // P0 = (P_opt − Σ_s λ̄_s P_s)/λ̄0 is kept unscaled: acc := λ̄0·P0 (only the
+  // first d modes change; modes above d are P_opt), and the factor 1/λ̄0 goes into σ_0
+  // (× 1/λ̄0²) and into the blend weight (ω0/λ̄0) — ℳ−1 fewer multiplications
 #pragma unroll
   for (int l = 0; l < D; ++l) {
     double s = 0.0;
 #pragma unroll
     for (int q = 0; q <= D; ++q) s = __dadd_rn(s, valid[q] ? ps[q][l] : 0.0);
-    acc[l] = __dmul_rn(__fma_rn(-ls, s, acc[l]), il0);
+    acc[l] = __fma_rn(-ls, s, acc[l]);
   }
-#pragma unroll
-  for (int l = D; l < R; ++l) acc[l] = __dmul_rn(acc[l], il0);
   // σ_0 = P0ᵀ Σ P0 and σ_s = P_sᵀ Σ P_s; explicit roundings (here and in
   // every kernel) so that all kernels perform the same operations bit for bit
   double sg0 = 0.0;
@@ -130,6 +130,7 @@ __device__ __forceinline__ void cweno_epilogue(double qi, double* acc, const dou
   }
   // ω̃_s = λ̄_s/(σ_s+ε)^r, ω_s = ω̃_s/Σ ω̃; invalid sectors get 0 (R14)
   // reciprocals instead of divisions (one extra rounding, far inside the 1e-11 bar)
+  sg0 = __dmul_rn(sg0, __dmul_rn(il0, il0));  // σ_0 of P0 = σ(λ̄0·P0)/λ̄0²
   const double wt0 = __dmul_rn(l0, __drcp_rn(powr(__dadd_rn(sg0, a.eps), a.r)));
   double wts[D + 1];
   double sum = wt0;
@@ -145,15 +146,16 @@ __device__ __forceinline__ void cweno_epilogue(double qi, double* acc, const dou
   for (int s = 0; s <= D; ++s) oms[s] = __dmul_rn(wts[s], isum);
   // w = Σ_s ω_s P_s;  w[0] := Q_i/ψ1 (R17)
   w[0] = p0;
+  const double om0s = __dmul_rn(om0, il0);  // ω0 · P0 = (ω0/λ̄0) · acc
 #pragma unroll
   for (int l = 0; l < D; ++l) {
-    double v = __dmul_rn(om0, acc[l]);
+    double v = __dmul_rn(om0s, acc[l]);
 #pragma unroll
     for (int s = 0; s <= D; ++s) v = __fma_rn(oms[s], ps[s][l], v);
     w[l + 1] = v;
   }
 #pragma unroll
-  for (int l = D; l < R; ++l) w[l + 1] = __dmul_rn(om0, acc[l]);
+  for (int l = D; l < R; ++l) w[l + 1] = __dmul_rn(om0s, acc[l]);
   if (sigma_out) {
     sigma_out[0] = sg0;
     omega_out[0] = om0;

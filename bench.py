@@ -1,22 +1,28 @@
 #!/usr/bin/env python
 """Benchmark of the CWENO reconstruction pass (arXiv 1612.09335 §2.1) on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl ours|reference]
 
 One "step" = one full reconstruction pass (gather → B⁺ΔQ → sectors → P0 → σ → ω →
-blend → store, all rows of SURVEY §8(a)) over every cell of the workload.  N=1
-runs BASELINE.json configs[1] ("C2": 524,288 jittered triangles, M=3, 4 vars);
-N>1 (torchrun, one rank per GPU, NCCL) runs the weak-scaling ladder of the same
-workload (n = round(512·sqrt(N)), ≈524k cells per GPU) with the halo exchange
-overlapped with the interior tiles.
+blend → store, all rows of SURVEY §8(a)) over every cell of the workload.  The
+default workload is C4 (BASELINE.json configs[3]: 12.6 M jittered tetrahedra,
+M=3, 9 MHD variables, 138.6 GB of algorithmic traffic per pass) — the largest
+configuration that fits one GPU, the one the north_star 60 %-of-HBM gate and
+the 8-GPU efficiency gate are about.  N>1 (torchrun, one rank per GPU, NCCL):
+C4 is STRONG scaling (the same mesh partitioned into N Morton ranges, halo
+exchange overlapped with the interior tiles); --config C5 runs the weak ladder
+n = 100/126/159/200 (R26); C2/C3 scale their box with N (weak).
 
 Timing: W untimed warm-up steps, then K steps bracketed by a barrier and a
 device synchronize; each step is timed with CUDA events on the stream the
 kernel is launched on, and the L2 is flushed (a 512 MiB write) between steps,
-outside the events, so every step starts cold.  Max over ranks.
+outside the events, so every step starts cold.  Max over ranks.  SM clocks and
+throttle reasons are sampled in-process (NVML, every 20 ms) during the timed
+region.
 
-Prints ONE JSON line (rank 0).  --impl reference times the CPU oracle (oracle/)
-on the host cores on a bounded sample of the same workload.
+Prints ONE JSON line (rank 0).  --impl reference times the CPU oracle (oracle/,
+precomputed per-cell matrices, pass only, all host cores) on a bounded sample of
+the same workload; so does this arm's cpu_baseline (N=1).
 """
 from __future__ import annotations
 
@@ -48,10 +54,13 @@ def env_rank():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
+STRONG = {"C4"}   # configs partitioned as one fixed mesh across N GPUs (R26: C4 strong 1→8)
+
+
 def workload_n(cfg, N):
     import gen
     base = gen.CONFIGS[cfg]["n"]
-    if N == 1:
+    if N == 1 or cfg in STRONG:
         return base
     if cfg == "C5":
         return gen.C5_WEAK_N.get(N, round(100 * N ** (1 / 3)))
@@ -89,75 +98,88 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def profiled_traffic(cfg, kernel):
-    """Per-launch DRAM bytes of the dominant kernel from the committed ncu capture."""
+def profiled_traffic(cfg, kernel_symbol):
+    """Per-launch dram__bytes_read.sum + dram__bytes_write.sum of the kernel actually
+    launched (e.g. "C4:k_rowblk"), from the committed ncu --set full capture
+    (profiles/ncu_traffic.json, written by tools/ncu_summary.py); None if absent."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
             j = json.load(f)
-        return j.get(f"{cfg}:{kernel}")
+        return j.get(f"{cfg}:{kernel_symbol}")
     except Exception:
         return None
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons of one GPU sampled in-process with NVML every
+    20 ms while the timed region runs (B200_PROFILING.md clocks line)."""
 
-    def __init__(self, index):
-        self.index = index
-        self.proc = None
-        self.lines = []
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
+
+    def __init__(self, index, period_s=0.02):
+        self.index, self.period = index, period_s
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
-                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml as N
+            N.nvmlInit()
+            # torch's device index → NVML handle through the PCI bus id
+            import torch
+            bus = torch.cuda.get_device_properties(self.index).pci_bus_id if hasattr(
+                torch.cuda.get_device_properties(self.index), "pci_bus_id") else None
+            h = None
+            if bus:
+                try:
+                    h = N.nvmlDeviceGetHandleByPciBusId(bus)
+                except Exception:
+                    h = None
+            if h is None:
+                vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+                idx = int(vis.split(",")[self.index]) if vis and vis.split(",")[0].isdigit() else self.index
+                h = N.nvmlDeviceGetHandleByIndex(idx)
+            self.N, self.h = N, h
+            self.max_mhz = float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
+            self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
-        except Exception:
-            self.proc = None
+        except Exception as e:  # no NVML: report no samples
+            self.err = str(e)
+            self.N = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _run(self):
+        N, h = self.N, self.h
+        while not self._stop.is_set():
+            try:
+                self.samples.append(float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)))
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                for name, bit in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(self.period)
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        if self.N is not None:
+            self.t.join(timeout=2)
 
     def summary(self):
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            f = [x.strip() for x in ln.split(",")]
-            if len(f) < 7:
-                continue
-            try:
-                sm.append(float(f[0]))
-                mx.append(float(f[1]))
-            except ValueError:
-                continue
-            for k, nm in enumerate(names):
-                if f[3 + k].lower() == "active":
-                    reasons.add(nm)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
-                "samples": len(sm)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0,
+                    "source": "nvml"}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples), "source": "nvml, 20 ms"}
 
 
 # ----------------------------------------------------------------------------- oracle arm
 def _one_thread():
-    """Limit numpy's BLAS/LAPACK pools to one thread so `cores: 1` is what ran."""
+    """Limit numpy's BLAS/LAPACK pools to one thread per worker process."""
     try:
         from threadpoolctl import threadpool_limits
         return threadpool_limits(limits=1)
@@ -166,21 +188,97 @@ def _one_thread():
         return contextlib.nullcontext()
 
 
-def oracle_rate(w, budget_s, seed=0, max_cells=None):
-    """Oracle cells/s on a random sample of the workload's cells (1 core)."""
+_ORC = {}   # fork-inherited state of the oracle workers (mesh, averages, degree)
+
+
+def _oracle_worker(conn, cells, pre_budget_s):
+    """One host core: precompute the matrices of its sample cells (setup, not
+    timed), then on each request run the pass (oracle.reconstruct.apply_cell) over
+    them and report (cells, seconds)."""
     from oracle import reconstruct as R
-    from oracle.mesh import OracleMesh
-    m = OracleMesh(w["nodes"], w["cells"], w["period"], w["M"])
-    Q = w["avgs"][m.perm]
-    rng = np.random.default_rng(seed)
-    order = rng.permutation(m.N)
+    m, Q, M = _ORC["m"], _ORC["Q"], _ORC["M"]
     with _one_thread():
-        n, t0 = 0, time.perf_counter()
-        while time.perf_counter() - t0 < budget_s and (max_cells is None or n < max_cells):
-            R.reconstruct_cell(m, int(order[n % m.N]), Q, w["M"])
-            n += 1
-        dt = time.perf_counter() - t0
-    return n / dt, n, dt, m, Q
+        t0 = time.perf_counter()
+        pre = []
+        for i in cells:
+            if pre and time.perf_counter() - t0 > pre_budget_s:
+                break
+            pre.append(R.precompute_cell(m, int(i), M))
+        conn.send(("ready", len(pre), time.perf_counter() - t0))
+        while True:
+            msg = conn.recv()
+            if msg[0] == "stop":
+                break
+            t = time.perf_counter()
+            for _ in range(msg[1]):
+                for p in pre:
+                    R.apply_cell(p, Q)
+            conn.send((msg[1] * len(pre), time.perf_counter() - t))
+
+
+class OraclePool:
+    """The CPU oracle on every host core: one forked process per core,
+    each with a random sample of the workload's cells and their precomputed matrices;
+    a step = every worker runs the reconstruction pass over its sample once."""
+
+    def __init__(self, w, pre_budget_s=8.0, max_workers=None, seed=0):
+        import multiprocessing as mp
+        from oracle.mesh import OracleMesh
+        t = time.perf_counter()
+        m = OracleMesh(w["nodes"], w["cells"], w["period"], w["M"])
+        _ORC.update(m=m, Q=w["avgs"][m.perm], M=w["M"])
+        self.mesh_s = time.perf_counter() - t
+        cores = len(os.sched_getaffinity(0))
+        self.cores = max(1, min(cores, max_workers or 128))
+        order = np.random.default_rng(seed).permutation(m.N)
+        per = max(1, min(4096, m.N // self.cores))
+        ctx = mp.get_context("fork")
+        self.conns, self.procs = [], []
+        for k in range(self.cores):
+            a, b = ctx.Pipe()
+            pr = ctx.Process(target=_oracle_worker, args=(b, order[k * per:(k + 1) * per], pre_budget_s), daemon=True)
+            pr.start()
+            self.conns.append(a)
+            self.procs.append(pr)
+        rd = [c.recv() for c in self.conns]
+        self.sample = sum(r[1] for r in rd)
+        self.pre_s = max(r[2] for r in rd)
+        self.N = m.N
+
+    def step(self, reps=1):
+        """One pass over every worker's sample; returns (cells, wall seconds)."""
+        t = time.perf_counter()
+        for c in self.conns:
+            c.send(("run", reps))
+        n = sum(c.recv()[0] for c in self.conns)
+        return n, time.perf_counter() - t
+
+    def close(self):
+        for c in self.conns:
+            try:
+                c.send(("stop",))
+            except Exception:
+                pass
+        for p in self.procs:
+            p.join(timeout=5)
+
+    def describe(self, cfg):
+        return (f"{self.sample} random cells of {cfg} ({self.N} cells) over {self.cores} host cores "
+                f"(one process each), oracle per-cell matrices precomputed first "
+                f"({self.pre_s:.1f} s, not timed), pass only (oracle.reconstruct.apply_cell)")
+
+
+def oracle_baseline(w, cfg, seconds):
+    """cpu_baseline of our arm: the pooled oracle pass for about `seconds` of work."""
+    pool = OraclePool(w)
+    try:
+        n, dt = pool.step()            # warm-up sweep
+        reps = max(1, int(seconds / max(dt, 1e-3)))
+        n, dt = pool.step(reps)
+        return {"value": n / dt, "unit": "cells/s", "cores": pool.cores, "kind": "oracle",
+                "sample": pool.describe(cfg) + f"; {reps} sweeps in {dt:.1f} s"}
+    finally:
+        pool.close()
 
 
 def run_reference(args):
@@ -189,36 +287,25 @@ def run_reference(args):
         return 0
     import gen
     w = gen.make(args.config, workload_n(args.config, 1))
-    from oracle import reconstruct as R
-    from oracle.mesh import OracleMesh
-    m = OracleMesh(w["nodes"], w["cells"], w["period"], w["M"])
-    Q = w["avgs"][m.perm]
-    rng = np.random.default_rng(0)
-    t = time.perf_counter()
-    R.reconstruct_cell(m, 0, Q, w["M"])
-    per_cell = time.perf_counter() - t
-    per_step = max(1, int(120.0 / max(1, args.steps + args.warmup) / max(per_cell, 1e-4)))
-    per_step = min(per_step, 64)
-    order = rng.permutation(m.N)
-    k = 0
-    with _one_thread():
+    pool = OraclePool(w, pre_budget_s=min(8.0, 60.0 / max(1, args.steps + args.warmup) + 2.0))
+    try:
         for _ in range(args.warmup):
-            for _ in range(per_step):
-                R.reconstruct_cell(m, int(order[k % m.N]), Q, w["M"]); k += 1
-        t0 = time.perf_counter()
+            pool.step()
+        cells, t = 0, 0.0
         for _ in range(args.steps):
-            for _ in range(per_step):
-                R.reconstruct_cell(m, int(order[k % m.N]), Q, w["M"]); k += 1
-        dt = time.perf_counter() - t0
-    cells = args.steps * per_step
-    value = cells / dt
-    sample = f"{per_step} random cells of {args.config} per step (oracle rebuilds each cell's stencil matrices and solves)"
+            n, dt = pool.step()
+            cells += n
+            t += dt
+    finally:
+        pool.close()
+    value = cells / t
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "cells/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": f"{args.config}: {WORKLOAD_TEXT[args.config]}",
-                                             "n_cells": int(m.N)},
-            "cpu_baseline": {"value": value, "unit": "cells/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "strong" if args.config in STRONG else "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {WORKLOAD_TEXT[args.config]}", "n_cells": int(pool.N)},
+            "cpu_baseline": {"value": value, "unit": "cells/s", "cores": pool.cores, "kind": "oracle",
+                             "sample": pool.describe(args.config) + "; a step = one pass over the sample"},
             "e2e": {"value": value, "unit": "cells/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -236,13 +323,21 @@ def run_ours(args):
     if world != args.gpus:
         if rank == 0:
             print(f"warning: WORLD_SIZE={world} but --gpus {args.gpus}; using WORLD_SIZE", file=sys.stderr)
+    version = P.lib.cwreco_version().decode()
+    if "experiments" in version:
+        print(f"refusing to time {version}: rebuild without CWRECO_BUILD_EXPERIMENTS", file=sys.stderr)
+        return 2
+    n = workload_n(args.config, world)
+    w = gen.make(args.config, n)
+    # the oracle baseline forks host workers: run it before this process initialises CUDA
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = oracle_baseline(w, args.config, args.cpu_seconds)
+
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-
-    n = workload_n(args.config, world)
-    w = gen.make(args.config, n)
     t_setup = time.perf_counter()
     ctx = P.Context(w["d"], w["M"], w["V"], device=local)
     ctx.set_mesh(w["nodes"], w["cells"], w["period"])
@@ -352,30 +447,27 @@ def run_ours(args):
 
     clocks = clk.summary()
     if rank == 0:
-        cpu = None
-        if world == 1 and not args.no_cpu_baseline:
-            rate, ncell, dt, *_ = oracle_rate(w, args.cpu_seconds)
-            cpu = {"value": rate, "unit": "cells/s", "cores": 1, "kind": "oracle",
-                   "sample": f"{ncell} random cells of {args.config} in {dt:.1f} s, single core "
-                             f"(oracle rebuilds stencil matrices and solves per cell)"}
+        ksym = ("k_rowblk" if inf.get("kernel_family") == 1 else "k_pipelined") if args.kernel == "pipelined" \
+            else ("k_simple" if args.kernel == "simple" else "k_matfree")
         line = {
             "metric": METRIC, "value": value, "unit": "cells/s", "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong" if args.config in STRONG else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
             "config": {"workload": f"{args.config}: {WORKLOAD_TEXT[args.config]}", "n_cells_total": int(cells_total),
                        "n_cells_per_gpu": int(n_owned), "d": w["d"], "M": w["M"], "V": V, "box_n": n,
                        "kernel": args.kernel, "l2": "flushed (512 MiB write) between timed steps",
                        "parallelism": f"cell partition x{world}" + (" + NCCL halo" if world > 1 else ""),
-                       "setup_s": round(t_setup, 3)},
+                       "setup_s": round(t_setup, 3), "library": version},
             "roofline": ({"bound": "alu", "achieved": mf_flops * n_owned / kern_s / 1e12, "peak": FP64_PEAK_TF,
                           "unit": "TFLOP/s", "frac": mf_flops * n_owned / kern_s / 1e12 / FP64_PEAK_TF,
                           "traffic": None, "peak_source": FP64_PEAK_SRC, "flops_per_cell": mf_flops,
                           "kernel": "cwr::k_matfree"} if mf_flops else
                          {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "frac_vs_8tbs": achieved / 8000.0, "traffic": profiled_traffic(args.config, args.kernel),
+                         "frac": achieved / peak, "frac_vs_8tbs": achieved / 8000.0,
+                         "traffic": profiled_traffic(args.config, ksym) if world == 1 else None,
                          "peak_source": peak_src, "algorithmic_bytes_per_cell": bpc,
-                         "kernel": ("cwr::k_rowblk" if inf.get("kernel_family") == 1 else "cwr::k_pipelined")
-                                   if args.kernel == "pipelined" else "cwr::k_simple"}),
+                         "kernel": "cwr::" + ksym}),
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "cells/s", "h2d_bytes_per_step": int(avgs_local.nbytes),
                     "d2h_bytes_per_step": int(n_owned * V * nm * 8), "api": e2e_api},
@@ -391,12 +483,12 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--kernel", default="pipelined", choices=["pipelined", "simple", "matrixfree"])
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":

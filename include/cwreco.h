@@ -127,6 +127,23 @@ cwreco_status cwreco_get_info(const cwreco_ctx* ctx, cwreco_info* out);
 /* CWRECO_KERNEL_* */
 cwreco_status cwreco_set_kernel(cwreco_ctx* ctx, int variant);
 
+/* Launch / layout options (cwreco_set_option).  None changes any result: every
+ * family and grid size computes the same operations in the same order (tested
+ * bitwise).
+ *   CWRECO_OPT_FAMILY    packed-stream layout and kernel family chosen by the next
+ *                        cwreco_precompute: -1 = default per shape (row-block where
+ *                        ℳ = 20 and nvars ≥ 7, else cell-variable), 0 = cell-variable
+ *                        (k_pipelined), 1 = row-block (k_rowblk, where instantiated).
+ *                        Setting it drops the packed matrices (ESTATE until the next
+ *                        cwreco_precompute).
+ *   CWRECO_OPT_MAX_CTAS  upper bound on the CTAs of the persistent reconstruction
+ *                        kernels (0 = one wave over every SM, the default).  A small
+ *                        bound makes each CTA walk many tiles (tests of the multi-tile
+ *                        pipeline) or leaves SMs free for concurrent work.
+ * EINVAL for an unknown option or a value out of range. */
+enum { CWRECO_OPT_FAMILY = 1, CWRECO_OPT_MAX_CTAS = 2 };
+cwreco_status cwreco_set_option(cwreco_ctx* ctx, int option, int64_t value);
+
 /* ---------------------------------------------------------------- mesh / setup */
 /* xyz: [n_nodes][dim] fp64; cell_nodes: [n_cells][dim+1] int64 (any orientation);
  * period: [dim] box lengths of a periodic box, or NULL for an open domain

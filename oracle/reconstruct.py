@@ -1,8 +1,9 @@
 """Oracle: the CWENO reconstruction of one cell, literally.
 
 TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).  fp64 numpy, one cell at a
-time, no precomputation, no fusion: every call rebuilds the stencil matrices
-from the geometry and solves the systems afresh.
+time, no fusion.  precompute_cell() builds one cell's stencil matrices from the
+geometry and inverts them; apply_cell() is the reconstruction pass of
+that cell; reconstruct_cell() does both on every call.
 
 Steps (paper order):
  1. Stencils S_i^0 and S_i^s (oracle.mesh).
@@ -17,7 +18,8 @@ Steps (paper order):
     because ∫_{T_E} ψ_l = 0 for l > 1 (orthogonality to the constant ψ_1,
     pinned in tests), so the constraint fixes p̂_1 = Q_i / ψ_1 and the rest
     minimises Σ_{k≥2} (Q_j(k) − A[k][1] p̂_1 − Σ_{l≥2} A[k][l] p̂_l)² —
-    solved with numpy.linalg.lstsq (SVD).  (R10)
+    solved with the SVD pseudo-inverse of A[1:,1:] (numpy.linalg.pinv), which
+    the Eulerian scheme may precompute once per cell.  (R10)
  4. P_s (Eq. CWENO:Ps): the (d+1)×(d+1) interpolation system on
     the sector cells, basis ψ_1..ψ_{d+1} (which span ℙ_1), numpy.linalg.solve.
  5. λ̄ = (λ_0, λ_s…)/Σ over VALID stencils, λ_0 = 1e5, λ_s = 1 (R5, R14).
@@ -118,38 +120,52 @@ def stencil_matrix(mesh: OracleMesh, i, cells_, M):
     return m @ Cb.T   # [n, ℳ]
 
 
-def reconstruct_cell(mesh: OracleMesh, i, Q, M, lam0=LAMBDA0, lams=LAMBDAS, eps=EPS, r=R_EXP,
-                     central=None, sectors=None, valid=None):
-    """Reconstruct cell i (SFC id).  Q: [N, V] cell averages in SFC order.
+def precompute_cell(mesh: OracleMesh, i, M, central=None, sectors=None, valid=None):
+    """The per-cell matrices of the Eulerian (fixed-mesh) scheme, built once
+    ("precomputed, inverted and saved in the pre-processing stage", P:230):
 
-    Returns dict with w [V, ℳ] and the intermediates popt [V, ℳ],
-    psec [d+1, V, d+1], sigma [d+2, V], omega [d+2, V], valid [d+1]."""
+      A        [n_e, ℳ]   stencil matrix, row 0 = the cell itself
+      pinv     [ℳ-1, n_e-1]  pseudo-inverse of A[1:,1:] (SVD, numpy.linalg.pinv):
+               the minimiser of the reduced LSQ of P:136-149 (R10) is pinv·rhs
+      As       [d+1][d+1, d+1]  the sector systems on ψ_1..ψ_{d+1},
+               solved in the pass; None for an invalid sector (R14)
+    plus the stencils themselves.  apply_cell() is the pass."""
     d = mesh.d
-    V = Q.shape[1]
-    nm = n_modes(M, d)
     if central is None:
         central = mesh.central_stencil(i)
     if sectors is None:
         sectors, valid = mesh.sector_stencils(i)
+    A = stencil_matrix(mesh, i, central, M)                    # [n_e, ℳ]
+    pinv = np.linalg.pinv(A[1:, 1:])                           # [ℳ-1, n_e-1]
+    As = [stencil_matrix(mesh, i, sectors[s], M)[:, : d + 1] if valid[s] else None   # ψ_1..ψ_{d+1}
+          for s in range(d + 1)]
+    return dict(i=int(i), d=d, M=M, central=central, sectors=sectors, valid=valid, A=A, pinv=pinv, As=As)
+
+
+def apply_cell(pre, Q, lam0=LAMBDA0, lams=LAMBDAS, eps=EPS, r=R_EXP):
+    """One cell of the reconstruction pass with precompute_cell's matrices.
+
+    Returns dict with w [V, ℳ] and the intermediates popt [V, ℳ], psec [d+1, V, d+1],
+    P0 [V, ℳ], sigma [d+2, V], omega [d+2, V], lam [d+2] (normalised λ̄), valid [d+1]."""
+    d, M, i = pre["d"], pre["M"], pre["i"]
+    central, sectors, valid, A = pre["central"], pre["sectors"], pre["valid"], pre["A"]
+    V = Q.shape[1]
+    nm = n_modes(M, d)
     Sig = sigma_numeric(d, M)
     p1 = psi1(d)
 
     # --- P_opt: constrained LSQ (P:136-149)
-    A = stencil_matrix(mesh, i, central, M)                    # [n_e, ℳ]
     Qs = Q[np.asarray(central)]                                # [n_e, V]
     popt = np.zeros((V, nm))
     popt[:, 0] = Q[i] / p1                                     # constraint row k=1
     rhs = Qs[1:] - np.outer(A[1:, 0], popt[:, 0])              # [n_e-1, V]
-    sol, *_ = np.linalg.lstsq(A[1:, 1:], rhs, rcond=None)      # [ℳ-1, V]
-    popt[:, 1:] = sol.T
+    popt[:, 1:] = (pre["pinv"] @ rhs).T                        # [ℳ-1, V] least-squares solution
 
     # --- sectorial P_s (P:184-191)
     psec = np.zeros((d + 1, V, d + 1))
     for s in range(d + 1):
-        if not valid[s]:
-            continue
-        As = stencil_matrix(mesh, i, sectors[s], M)[:, : d + 1]     # ψ_1..ψ_{d+1}
-        psec[s] = np.linalg.solve(As, Q[np.asarray(sectors[s])]).T
+        if valid[s]:
+            psec[s] = np.linalg.solve(pre["As"][s], Q[np.asarray(sectors[s])]).T
 
     # --- linear weights, normalised over valid stencils (R5, R14)
     lam = np.array([lam0] + [lams if valid[s] else 0.0 for s in range(d + 1)])
@@ -167,8 +183,16 @@ def reconstruct_cell(mesh: OracleMesh, i, Q, M, lam0=LAMBDA0, lams=LAMBDAS, eps=
     wt = np.array([lam[s] / (sigma[s] + eps) ** r for s in range(d + 2)])     # [d+2, V]
     omega = wt / wt.sum(axis=0)
     w = sum(omega[s][:, None] * cand[s] for s in range(d + 2))
-    return dict(w=w, popt=popt, psec=psec, sigma=sigma, omega=omega, valid=np.array(valid),
+    return dict(w=w, popt=popt, psec=psec, P0=P0, sigma=sigma, omega=omega, lam=lam, valid=np.array(valid),
                 central=central, sectors=sectors)
+
+
+def reconstruct_cell(mesh: OracleMesh, i, Q, M, lam0=LAMBDA0, lams=LAMBDAS, eps=EPS, r=R_EXP,
+                     central=None, sectors=None, valid=None):
+    """Reconstruct cell i (SFC id).  Q: [N, V] cell averages in SFC order.
+    = apply_cell(precompute_cell(...)): every call rebuilds the matrices."""
+    pre = precompute_cell(mesh, i, M, central, sectors, valid)
+    return apply_cell(pre, Q, lam0, lams, eps, r)
 
 
 def reconstruct(mesh: OracleMesh, Q, M, cells_=None, **kw):

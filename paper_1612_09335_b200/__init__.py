@@ -11,13 +11,15 @@ import os
 
 import numpy as np
 
-__all__ = ["Context", "CwrecoError", "lib", "KERNELS", "PART_ALL", "PART_INTERIOR", "PART_BOUNDARY",
+__all__ = ["Context", "CwrecoError", "lib", "KERNELS", "OPT_FAMILY", "OPT_MAX_CTAS", "PART_ALL",
+           "PART_INTERIOR", "PART_BOUNDARY",
            "n_modes", "setup_context"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "libcwreco.so")
 
 KERNELS = {"pipelined": 0, "simple": 1, "matrixfree": 2}
+OPT_FAMILY, OPT_MAX_CTAS = 1, 2
 PART_ALL, PART_INTERIOR, PART_BOUNDARY = 0, 1, 2
 _STATUS = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "ECUDA", 4: "EMESH", 5: "ESTENCIL", 6: "ESINGULAR",
            7: "ESTATE", 8: "EUNSUPPORTED"}
@@ -54,6 +56,7 @@ def _load():
         "cwreco_create": [I32, I32, I32, P, I32, P],
         "cwreco_get_info": [P, P],
         "cwreco_set_kernel": [P, I32],
+        "cwreco_set_option": [P, I32, I64],
         "cwreco_set_mesh": [P, I64, P, I64, P, P],
         "cwreco_get_permutation": [P, P],
         "cwreco_set_partition": [P, I32, I32],
@@ -208,6 +211,15 @@ class Context:
     def set_kernel(self, name):
         _check(lib.cwreco_set_kernel(self._h, KERNELS[name]))
 
+    def set_option(self, option, value):
+        """cwreco_set_option: OPT_FAMILY (-1 default, 0 cell-variable, 1 row-block; before
+        precompute) or OPT_MAX_CTAS (0 = every SM)."""
+        _check(lib.cwreco_set_option(self._h, int(option), int(value)))
+
+    def _need_shape(self, t, shape, what):
+        if tuple(t.shape) != tuple(shape):
+            raise ValueError(f"{what} must have shape {tuple(shape)}, got {tuple(t.shape)}")
+
     # ---------------------------------------------------------------- halo
     def halo_plan(self):
         inf = self.info()
@@ -248,9 +260,14 @@ class Context:
         import torch
         if not (avgs.is_cuda and avgs.dtype == torch.float64 and avgs.dim() == 2):
             raise ValueError("avgs must be a 2-D float64 CUDA tensor")
+        inf = self.info()
+        n_owned = inf["n_owned"]
+        self._need_shape(avgs, (n_owned + inf["n_ghost"], self.V), "avgs")
         if out is None:
-            n_owned = self.info()["n_owned"]
             out = torch.empty((n_owned, self.V, self.nm), dtype=torch.float64, device=avgs.device)
+        if not (out.is_cuda and out.dtype == torch.float64 and out.device == avgs.device):
+            raise ValueError("out must be a float64 tensor on the device of avgs")
+        self._need_shape(out, (n_owned, self.V, self.nm), "out")
         a_cs, a_vs = avgs.stride()
         c_cs, c_vs, c_ls = out.stride()
         if c_ls != 1:
@@ -269,11 +286,14 @@ class Context:
             avgs = torch.from_numpy(np.ascontiguousarray(avgs, dtype=np.float64))
         if avgs.is_cuda or avgs.dtype != torch.float64 or avgs.dim() != 2 or not avgs.is_contiguous():
             raise ValueError("avgs must be a C-contiguous 2-D float64 host tensor")
+        inf = self.info()
+        self._need_shape(avgs, (inf["n_owned"] + inf["n_ghost"], self.V), "avgs")
         if out is None:
-            out = torch.empty((self.info()["n_owned"], self.V, self.nm), dtype=torch.float64,
+            out = torch.empty((inf["n_owned"], self.V, self.nm), dtype=torch.float64,
                               pin_memory=avgs.is_pinned())
         if out.is_cuda or out.dtype != torch.float64 or not out.is_contiguous():
             raise ValueError("out must be a C-contiguous float64 host tensor")
+        self._need_shape(out, (inf["n_owned"], self.V, self.nm), "out")
         _check(lib.cwreco_reconstruct_host(self._h, ctypes.c_void_p(avgs.data_ptr()),
                                            ctypes.c_void_p(out.data_ptr()), int(n_pieces),
                                            _stream_handle(stream)))
@@ -299,9 +319,17 @@ class Context:
         out [n_owned, dim+1, nq, V] on the device."""
         import torch
         nq = self.face_rule()[1].shape[0]
+        n_owned = self.info()["n_owned"]
+        if not (coeffs.is_cuda and coeffs.dtype == torch.float64 and coeffs.dim() == 3):
+            raise ValueError("coeffs must be a 3-D float64 CUDA tensor")
+        if coeffs.shape[0] < n_owned or tuple(coeffs.shape[1:]) != (self.V, self.nm):
+            raise ValueError(f"coeffs must have shape (>= {n_owned}, {self.V}, {self.nm})")
         if out is None:
-            out = torch.empty((coeffs.shape[0], self.dim + 1, nq, self.V), dtype=torch.float64,
+            out = torch.empty((n_owned, self.dim + 1, nq, self.V), dtype=torch.float64,
                               device=coeffs.device)
+        if not (out.is_cuda and out.dtype == torch.float64 and out.device == coeffs.device):
+            raise ValueError("out must be a float64 tensor on the device of coeffs")
+        self._need_shape(out, (n_owned, self.dim + 1, nq, self.V), "out")
         c_cs, c_vs, c_ls = coeffs.stride()
         if c_ls != 1 or not out.is_contiguous():
             raise ValueError("coeffs must be contiguous along the mode axis and out dense")
@@ -324,9 +352,14 @@ class Context:
         return dict(popt=popt, psec=psec, sigma=sig, omega=om, w=w)
 
 
-def setup_context(nodes, cells, period, degree_M, nvars, device=0, rank=0, nranks=1, **params):
-    """set_mesh → set_partition → build_stencils → precompute."""
+def setup_context(nodes, cells, period, degree_M, nvars, device=0, rank=0, nranks=1, family=-1, max_ctas=0,
+                  **params):
+    """set_mesh → set_partition → build_stencils → precompute (family / max_ctas:
+    cwreco_set_option, see include/cwreco.h)."""
     ctx = Context(nodes.shape[1], degree_M, nvars, device, **params)
+    ctx.set_option(OPT_FAMILY, family)
+    if max_ctas:
+        ctx.set_option(OPT_MAX_CTAS, max_ctas)
     ctx.set_mesh(nodes, cells, period)
     if nranks > 1:
         ctx.set_partition(rank, nranks)

@@ -27,6 +27,14 @@ NVFLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-s
            "-Xcompiler", "-fPIC", "-Xptxas", "-v", "-I", INC, "-I", CSRC]
 
 
+# Timing-only experiment switches (CWRECO_EXP_FLAGS, CWRECO_KC, CWRECO_MAX_STAGES, …)
+# exist only in a library built with CWRECO_BUILD_EXPERIMENTS=1 (tools/); the product
+# build has none of them, and cwreco_version() says which build is loaded.
+if os.environ.get("CWRECO_BUILD_EXPERIMENTS") == "1":
+    CXXFLAGS = CXXFLAGS + ["-DCWRECO_EXPERIMENTS"]
+    NVFLAGS = NVFLAGS + ["-DCWRECO_EXPERIMENTS"]
+
+
 def _run(cmd, log):
     r = subprocess.run(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
     log.write(" ".join(cmd) + "\n" + r.stdout + "\n")

@@ -34,6 +34,23 @@ void need(bool cond, cwreco_status s, const char* msg) {
   if (!cond) cwr::fail(s, msg);
 }
 
+// Derived device state (face-trace tables, matrix-free arrays) is built from the
+// mesh, partition and stencils: drop it whenever one of those changes.
+void invalidate_derived(cwreco_ctx* c) {
+  cwr::dev_traces_destroy(c);
+  cwr::dev_matfree_destroy(c);
+}
+
+// Coefficient rows (c, v) → c·ccs + v·cvs + [0, ℳ) must not overlap: cell-major
+// (cvs ≥ ℳ, ccs ≥ V·cvs) or variable-major (ccs ≥ ℳ, cvs ≥ n·ccs).
+void need_disjoint_rows(const cwreco_ctx* c, int64_t ccs, int64_t cvs, int64_t n, const char* what) {
+  const bool cell_major = cvs >= c->nm && ccs >= (int64_t)c->V * cvs;
+  const bool var_major = ccs >= c->nm && (c->V == 1 || cvs >= n * ccs);
+  if (!(cell_major || var_major))
+    cwr::fail(CWRECO_EINVAL, std::string(what) + ": coefficient strides make rows overlap (need cvs >= n_modes and "
+                                                 "ccs >= nvars*cvs, or ccs >= n_modes and cvs >= n_owned*ccs)");
+}
+
 void need_device(const cwreco_ctx* c, const char* what) {
   if (c->device < 0 || !c->dev)
     cwr::fail(CWRECO_ECUDA, std::string(what) + ": host-only context (no CUDA device); there is no CPU fallback");
@@ -45,7 +62,13 @@ extern "C" {
 
 const char* cwreco_last_error(void) { return g_last_error.c_str(); }
 
-const char* cwreco_version(void) { return "cwreco 0.1.0 (sm_100a)"; }
+const char* cwreco_version(void) {
+#ifdef CWRECO_EXPERIMENTS
+  return "cwreco 0.2.0 (sm_100a) +experiments (timing-only switches compiled in; not a product build)";
+#else
+  return "cwreco 0.2.0 (sm_100a)";
+#endif
+}
 
 cwreco_status cwreco_create(int dim, int degree_M, int nvars, const cwreco_params* params, int cuda_device,
                             cwreco_ctx** out) {
@@ -131,10 +154,30 @@ cwreco_status cwreco_set_kernel(cwreco_ctx* c, int variant) {
   });
 }
 
+cwreco_status cwreco_set_option(cwreco_ctx* c, int option, int64_t value) {
+  return guard([&] {
+    need(c != nullptr, CWRECO_EINVAL, "set_option: NULL");
+    switch (option) {
+      case CWRECO_OPT_FAMILY:
+        need(value >= -1 && value <= 1, CWRECO_EINVAL, "set_option: family must be -1, 0 or 1");
+        c->family = (int)value;
+        c->has_blocks = false;  // the packed layout depends on the family
+        break;
+      case CWRECO_OPT_MAX_CTAS:
+        need(value >= 0 && value <= (1 << 30), CWRECO_EINVAL, "set_option: max_ctas must be >= 0");
+        c->max_ctas = value;
+        break;
+      default:
+        cwr::fail(CWRECO_EINVAL, "set_option: unknown option " + std::to_string(option));
+    }
+  });
+}
+
 cwreco_status cwreco_set_mesh(cwreco_ctx* c, int64_t n_nodes, const double* xyz, int64_t n_cells,
                               const int64_t* cell_nodes, const double* period) {
   return guard([&] {
     need(c != nullptr, CWRECO_EINVAL, "set_mesh: NULL ctx");
+    invalidate_derived(c);
     cwr::set_mesh(c, n_nodes, xyz, n_cells, cell_nodes, period);
   });
 }
@@ -151,6 +194,7 @@ cwreco_status cwreco_set_partition(cwreco_ctx* c, int rank, int nranks) {
   return guard([&] {
     need(c != nullptr, CWRECO_EINVAL, "set_partition: NULL");
     need(nranks >= 1 && rank >= 0 && rank < nranks, CWRECO_EINVAL, "set_partition: bad rank/nranks");
+    invalidate_derived(c);
     c->rank = rank;
     c->nranks = nranks;
     c->has_stencils = c->has_blocks = false;
@@ -166,6 +210,7 @@ cwreco_status cwreco_build_stencils(cwreco_ctx* c) {
     need(c != nullptr, CWRECO_EINVAL, "build_stencils: NULL");
     need(c->has_mesh, CWRECO_ESTATE, "build_stencils: call cwreco_set_mesh first");
     need(c->own_hi > c->own_lo, CWRECO_EINVAL, "build_stencils: this rank owns no cells");
+    invalidate_derived(c);
     cwr::build_stencils(c);
   });
 }
@@ -229,6 +274,7 @@ cwreco_status cwreco_set_stencils(cwreco_ctx* c, const int32_t* central, const i
       for (int v = 0; v < nv; ++v)
         if (!c->valid[q * nv + v])
           for (int k = 0; k < nv; ++k) c->sectors[(q * nv + v) * nv + k] = -1;
+    invalidate_derived(c);
     cwr::finalize_stencils(c);
   });
 }
@@ -377,7 +423,7 @@ cwreco_status cwreco_reconstruct(cwreco_ctx* c, const double* d_avgs, int64_t ac
       need(c->has_blocks, CWRECO_ESTATE, "reconstruct: call cwreco_precompute first");
     need(d_avgs && d_coeffs, CWRECO_EINVAL, "reconstruct: NULL buffer");
     need(acs >= 1 && avs >= 1 && ccs >= 1 && cvs >= 1, CWRECO_EINVAL, "reconstruct: strides must be >= 1");
-    need(cvs >= c->nm && ccs >= (int64_t)cvs * 1, CWRECO_EINVAL, "reconstruct: coefficient rows overlap");
+    need_disjoint_rows(c, ccs, cvs, c->n_owned, "reconstruct");
     need(part == CWRECO_PART_ALL || part == CWRECO_PART_INTERIOR || part == CWRECO_PART_BOUNDARY, CWRECO_EINVAL,
          "reconstruct: bad part");
     cwr::dev_reconstruct(c, d_avgs, acs, avs, d_coeffs, ccs, cvs, part, stream);
@@ -444,7 +490,7 @@ cwreco_status cwreco_face_traces(cwreco_ctx* c, const double* d_coeffs, int64_t 
     need_device(c, "face_traces");
     need(c->has_stencils, CWRECO_ESTATE, "face_traces: no stencils");
     need(d_coeffs && d_traces, CWRECO_EINVAL, "face_traces: NULL buffer");
-    need(cvs >= c->nm && ccs >= cvs, CWRECO_EINVAL, "face_traces: bad strides");
+    need_disjoint_rows(c, ccs, cvs, c->n_owned, "face_traces");
     cwr::dev_face_traces(c, d_coeffs, ccs, cvs, d_traces, stream);
   });
 }

@@ -143,7 +143,8 @@ inline int64_t pipe_budget(int nm, int max_smem) {
 
 // max_smem: opt-in shared memory per block of the device (227 KB on B200);
 // umax_for(T): the largest per-tile stencil union for tiles of T cells.
-Layout make_layout(int d, int M, int V, int G, int max_smem, const std::function<int(int)>& umax_for);
+Layout make_layout(int d, int M, int V, int G, int max_smem, const std::function<int(int)>& umax_for,
+                   int family = -1);
 // k_rowblk: consumer threads per CTA, and whether an instantiation exists for (d, M, V)
 // main-loop threads of a row-block CTA (8 warps: T = 256 / NG cells × NG row groups)
 CWR_HD constexpr int rb_main(int R, int V) { return (R > 14 && rb_ng(R, V) == 4) ? 128 : 256; }
@@ -191,6 +192,8 @@ struct cwreco_ctx {
   cwreco_params prm{1e5, 1.0, 1e-14, 4};
   int device = -1;
   int kernel = CWRECO_KERNEL_PIPELINED;
+  int family = -1;       // CWRECO_OPT_FAMILY (-1: default per shape)
+  int64_t max_ctas = 0;  // CWRECO_OPT_MAX_CTAS (0: every SM)
 
   // ---- mesh, SFC order (set_mesh)
   bool has_mesh = false;

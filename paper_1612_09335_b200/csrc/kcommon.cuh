@@ -9,6 +9,7 @@
 #include <cstdint>
 #include <type_traits>
 
+#include "devguard.cuh"
 #include "internal.hpp"
 
 namespace cwr {
@@ -46,13 +47,21 @@ struct KArgs {
   double* out;
   int64_t ccs, cvs;
   int dense_out;
-  int exp_flags;  // bottleneck experiments only (CWRECO_EXP_FLAGS): 1 no gather, 2 no B⁺ FMAs,
-                 // 16 no epilogue (timing only: results are wrong)
+  int exp_flags;  // bottleneck experiments only (CWRECO_EXP_FLAGS, read only by a library built
+                 // with -DCWRECO_EXPERIMENTS): 1 no gather, 2 no B⁺ FMAs, 16 no epilogue
+                 // (timing only: results are wrong).  The product build compiles these
+                 // branches out (EXP() is constant false).
   double eps, psi1;
   int r;
   // normalised linear weights (R5, R14) indexed by the number of valid sectors
   double l0[5], inv_l0[5], ls[5];
 };
+
+#ifdef CWRECO_EXPERIMENTS
+#define EXP(a, bit) (((a).exp_flags & (bit)) != 0)
+#else
+#define EXP(a, bit) false
+#endif
 
 struct DbgOut {
   double *popt, *psec, *sigma, *omega, *w;

@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(max_threads(D, M), min_blocks(D, M)) k_pipelin
       for (int i = tid; i < (int)(a.idx_bytes / 16); i += nct) dsti[i] = src[i];
     }
     double* dst = Qu + (size_t)buf * a.Umax * a.V;
-    if (!(a.exp_flags & 1)) {
+    if (!EXP(a, 1)) {
       // element e = u·V + vv, e = tid, tid + nct, …: (u, vv) stepped without divisions
       int u = tid / a.V, vv = tid - (tid / a.V) * a.V;
       const int du = nct / a.V, dv = nct - du * a.V;
@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(max_threads(D, M), min_blocks(D, M)) k_pipelin
       for (int kk = 0; kk < KC; ++kk) dq[kk] = (FULL || kk < kc) ? Qb[ic[kk * a.T]] - qi : 0.0;
       mbar_wait(&full[rg.st], rg.ph);
       const double* Bs = (const double*)(stg + rg.st * pc.stage_bytes);  // chunk_elem layout
-      if (a.exp_flags & 2) {
+      if (EXP(a, 2)) {
         acc[0] += dq[0];
       } else if (FULL) {
         if (decltype(cap)::value) {
@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(max_threads(D, M), min_blocks(D, M)) k_pipelin
       const int nlive = (int)max((int64_t)0, min((int64_t)32, lim));
       if (lane == 0) bulk_wait_read();  // the staging rows are free again
       __syncwarp();
-      if (a.exp_flags & 16) {
+      if (EXP(a, 16)) {
         outw[lane * NM] = acc[0] + ps[0][0];
       } else {
         cweno_epilogue<D, NM>(qi, acc, ps, valid, a, outw + lane * NM, nullptr, nullptr);
@@ -431,10 +431,12 @@ static KArgs make_args(const cwreco_ctx* c, const double* avgs, int64_t acs, int
   a.ccs = ccs;
   a.cvs = cvs;
   a.dense_out = 0;
+#ifdef CWRECO_EXPERIMENTS
   {
     const char* e = std::getenv("CWRECO_EXP_FLAGS");  // bottleneck experiments (tools/exp_bench.py)
     a.exp_flags = e ? std::atoi(e) : 0;
   }
+#endif
   a.eps = c->prm.eps;
   a.psi1 = c->psi1;
   a.r = c->prm.r;
@@ -457,7 +459,14 @@ static PipeFn rowblk_fn(const cwreco_ctx* c) {
 }
 
 static PipeCfg pipe_cfg(const cwreco_ctx* c, int* ctas = nullptr) {
-  if (c->dev->have_cfg && !std::getenv("CWRECO_MAX_STAGES") && !std::getenv("CWRECO_CTAS")) {
+#ifdef CWRECO_EXPERIMENTS
+  const char* kcap = std::getenv("CWRECO_CTAS");        // tuning experiments only
+  const char* cap = std::getenv("CWRECO_MAX_STAGES");   // tuning experiments only (tools/sweep.py)
+#else
+  const char* kcap = nullptr;
+  const char* cap = nullptr;
+#endif
+  if (c->dev->have_cfg && !cap && !kcap) {
     if (ctas) *ctas = c->dev->cfg_ctas;
     return c->dev->cfg;
   }
@@ -472,7 +481,6 @@ static PipeCfg pipe_cfg(const cwreco_ctx* c, int* ctas = nullptr) {
     int k = 0, st = 0;
     const PipeFn f = rowblk_fn(c);
     const int nthr = rb_cons_for(L.R, L.V, L.T) + 32;
-    const char* kcap = std::getenv("CWRECO_CTAS");  // tuning experiments only
     for (int want = kcap ? std::max(1, std::min(3, std::atoi(kcap))) : 3; want >= 1; --want) {
       rowblk_plan(L, c->dev->max_smem, want, k, st);
       if (k < want) continue;
@@ -481,7 +489,6 @@ static PipeCfg pipe_cfg(const cwreco_ctx* c, int* ctas = nullptr) {
       if (occ >= want) break;
       k = 0;
     }
-    const char* cap = std::getenv("CWRECO_MAX_STAGES");  // tuning experiments only
     if (cap) st = std::max(kMinStages, std::min(st, std::atoi(cap)));
     if (!k) fail(CWRECO_EUNSUPPORTED, "row-block kernel: tile does not fit in shared memory");
     if (ctas) *ctas = k;
@@ -500,7 +507,6 @@ static PipeCfg pipe_cfg(const cwreco_ctx* c, int* ctas = nullptr) {
   // large for that budget runs at 1 CTA/SM with the whole shared memory.  The
   // prefetch cursor runs up to PF + 1 stages ahead of the consumers.
   int st = 0;
-  const char* cap = std::getenv("CWRECO_MAX_STAGES");  // tuning experiments only (tools/exp_bench.py)
   const int smax = cap ? std::max(kMinStages, std::atoi(cap)) : kMaxStages;
   for (int64_t budget : {pipe_budget(c->nm, c->dev->max_smem), (int64_t)c->dev->max_smem}) {
     for (int s = smax; s >= kMinStages; --s)
@@ -525,14 +531,14 @@ int dev_max_smem(const cwreco_ctx* c) { return c->dev ? c->dev->max_smem : 227 *
 void dev_create(cwreco_ctx* c) {
   if (c->device < 0) return;
   c->dev = new DeviceState();
-  CK(cudaSetDevice(c->device));
+  DeviceGuard dg(c->device);
   CK(cudaDeviceGetAttribute(&c->dev->num_sms, cudaDevAttrMultiProcessorCount, c->device));
   CK(cudaDeviceGetAttribute(&c->dev->max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
 }
 
 void dev_destroy(cwreco_ctx* c) {
   if (!c->dev) return;
-  cudaSetDevice(c->device);
+  DeviceGuard dg(c->device);
   cudaFree(c->dev->blocks);
   cudaFree(c->dev->send);
   cudaFree(c->dev->dbg);
@@ -546,7 +552,7 @@ void dev_destroy(cwreco_ctx* c) {
 }
 
 void dev_alloc_blocks(cwreco_ctx* c, int64_t bytes) {
-  CK(cudaSetDevice(c->device));
+  DeviceGuard dg(c->device);
   if (c->dev->blocks) CK(cudaFree(c->dev->blocks));
   c->dev->blocks = nullptr;
   c->dev->blocks_bytes = 0;
@@ -559,6 +565,7 @@ void dev_alloc_blocks(cwreco_ctx* c, int64_t bytes) {
 }
 
 void dev_upload_blocks(cwreco_ctx* c, int64_t offset, const unsigned char* host, int64_t bytes) {
+  DeviceGuard dg(c->device);
   CK(cudaMemcpy(c->dev->blocks + offset, host, (size_t)bytes, cudaMemcpyHostToDevice));
 }
 
@@ -567,7 +574,7 @@ void dev_upload_aux(cwreco_ctx* c) {
   std::vector<double> packed;
   for (int l = 1; l < nm; ++l)
     for (int m = l; m < nm; ++m) packed.push_back((l == m ? 1.0 : 2.0) * c->sigma[l * nm + m]);
-  CK(cudaSetDevice(c->device));
+  DeviceGuard dg(c->device);
   const size_t sb = sizeof(double) * packed.size(), so = sizeof(double) * sig_off(c->d, c->M);
   CK(cudaMemcpyToSymbol(c_sig, packed.data(), sb, so));
   CK(rowblk_upload_sigma_2d(packed.data(), sb, so));
@@ -580,7 +587,7 @@ void dev_upload_aux(cwreco_ctx* c) {
 }
 
 void dev_download_tile(const cwreco_ctx* c, int64_t tile, unsigned char* host) {
-  CK(cudaSetDevice(c->device));
+  DeviceGuard dg(c->device);
   CK(cudaMemcpy(host, c->dev->blocks + tile * c->lay.tile_bytes, (size_t)c->lay.tile_bytes, cudaMemcpyDeviceToHost));
 }
 
@@ -608,7 +615,8 @@ static void launch_range(cwreco_ctx* c, const double* avgs, int64_t acs, int64_t
     int per_sm = 1;
     PipeCfg p = pipe_cfg(c, &per_sm);
     const int64_t ntiles = a.tile_end - a.tile_begin;
-    const int64_t grid = std::min<int64_t>(ntiles, (int64_t)c->dev->num_sms * per_sm);
+    int64_t grid = std::min<int64_t>(ntiles, (int64_t)c->dev->num_sms * per_sm);
+    if (c->max_ctas > 0) grid = std::min<int64_t>(grid, c->max_ctas);  // CWRECO_OPT_MAX_CTAS
     dim3 b((p.ncw + 1) * 32), g((unsigned)grid);
     PipeFn f = c->lay.kind == KIND_ROWBLK ? rowblk_fn(c) : pipe_fn(c->d, c->M, c->lay.KC);
     f<<<g, b, p.smem, st>>>(a, p);
@@ -618,6 +626,7 @@ static void launch_range(cwreco_ctx* c, const double* avgs, int64_t acs, int64_t
 
 void dev_reconstruct(cwreco_ctx* c, const double* avgs, int64_t acs, int64_t avs, double* coeffs, int64_t ccs,
                      int64_t cvs, int part, void* stream) {
+  DeviceGuard dg(c->device);
   if (c->kernel == CWRECO_KERNEL_MATRIXFREE) {  // cells, not tiles: interior first in local order
     const int64_t c0 = part == CWRECO_PART_BOUNDARY ? c->n_interior : 0;
     const int64_t c1 = part == CWRECO_PART_INTERIOR ? c->n_interior : c->n_owned;
@@ -638,7 +647,7 @@ void dev_reconstruct(cwreco_ctx* c, const double* avgs, int64_t acs, int64_t avs
 void dev_reconstruct_host(cwreco_ctx* c, const double* h_avgs, double* h_coeffs, int n_pieces, void* stream) {
   DeviceState* ds = c->dev;
   cudaStream_t st = (cudaStream_t)stream;
-  CK(cudaSetDevice(c->device));
+  DeviceGuard dg(c->device);
   const int V = c->V, nm = c->nm;
   const int64_t na = (c->n_owned + c->n_ghost) * V, nc = c->n_owned * V * nm;
   auto grow = [&](double*& p, int64_t& have, int64_t need_n) {
@@ -682,6 +691,7 @@ void dev_reconstruct_host(cwreco_ctx* c, const double* h_avgs, double* h_coeffs,
 
 void dev_debug(cwreco_ctx* c, const double* avgs, int64_t acs, int64_t avs, int64_t n_sel, const int64_t* cells,
                double* popt, double* psec, double* sigma, double* omega, double* w, void* stream) {
+  DeviceGuard dg(c->device);
   cudaStream_t st = (cudaStream_t)stream;
   const int V = c->V, nm = c->nm, NV = c->d + 1;
   const int64_t n_popt = n_sel * V * nm, n_psec = n_sel * NV * V * NV, n_sig = n_sel * (NV + 1) * V;
@@ -730,7 +740,7 @@ void dev_debug(cwreco_ctx* c, const double* avgs, int64_t acs, int64_t avs, int6
 
 void dev_set_send(cwreco_ctx* c) {
   if (!c->dev) return;
-  CK(cudaSetDevice(c->device));
+  DeviceGuard dg(c->device);
   cudaFree(c->dev->send);
   c->dev->send = nullptr;
   c->dev->n_send = (int64_t)c->send_local.size();
@@ -745,6 +755,7 @@ void dev_halo_pack(cwreco_ctx* c, const double* avgs, int64_t acs, int64_t avs, 
 
 void dev_halo_pack_rows(cwreco_ctx* c, const double* rows, int64_t rs, int64_t es, int width, double* sendbuf,
                         void* stream) {
+  DeviceGuard dg(c->device);
   const int64_t n = c->dev->n_send;
   if (n == 0) return;
   const int64_t threads = n * width;

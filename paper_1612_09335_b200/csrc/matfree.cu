@@ -36,11 +36,23 @@ namespace cwr {
     if (e_ != cudaSuccess) fail(CWRECO_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
   } while (0)
 
-constexpr int kMfMaxMono = 64, kMfMaxQ = 64;
-static __constant__ int c_mexp[kMfMaxMono * 3];
-static __constant__ double c_mcoef[20 * kMfMaxMono];
-static __constant__ double c_qp[kMfMaxQ * 3];
-static __constant__ double c_qw[kMfMaxQ];
+// Basis (monomial form) and quadrature tables of every supported (d, M), each in its
+// own slot of the constant bank, so contexts of different (d, M) on one device never
+// overwrite each other's tables (the tables depend only on (d, M)).
+constexpr int kMfMaxQ = 64;
+__host__ __device__ constexpr int mf_slot(int D, int M) { return (D - 2) * 3 + (M - 1); }  // M ≤ 3
+__host__ __device__ constexpr int mf_coef_off(int D, int M) {
+  int off = 0;
+  for (int s = 0; s < mf_slot(D, M); ++s) {
+    const int n = nmodes(s % 3 + 1, s / 3 + 2);
+    off += n * n;
+  }
+  return off;
+}
+constexpr int kMfSlots = 6;
+static __constant__ double c_mcoef[mf_coef_off(3, 3) + 20 * 20];
+static __constant__ double c_qp[kMfSlots * kMfMaxQ * 3];
+static __constant__ double c_qw[kMfSlots * kMfMaxQ];
 
 // Monomial exponents in basis_monomials' graded order (basis.cpp): for n, for i = n..0,
 // for j = n−i..0, k = n−i−j (2-D: k = 0 only) — compile-time, so the powers index
@@ -139,6 +151,9 @@ __global__ void __launch_bounds__(256) k_matfree(MfArgs m, KArgs a) {
   constexpr int KPL = (K + 31) / 32;  // rows of A per lane
 
   const int lane = threadIdx.x & 31;
+  const double* qp = c_qp + mf_slot(D, M) * kMfMaxQ * 3;  // this (d, M)'s tables
+  const double* qw = c_qw + mf_slot(D, M) * kMfMaxQ;
+  const double* mcoef = c_mcoef + mf_coef_off(D, M);
   extern __shared__ __align__(16) double mf_smem[];
   double* scr = mf_smem + (threadIdx.x >> 5) * mf_scr_doubles(D, M, V);
   const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -198,7 +213,7 @@ __global__ void __launch_bounds__(256) k_matfree(MfArgs m, KArgs a) {
           for (int e = 0; e < D; ++e) {
             double s = t[e];
 #pragma unroll
-            for (int f = 0; f < D; ++f) s += C[e][f] * c_qp[q * D + f];
+            for (int f = 0; f < D; ++f) s += C[e][f] * qp[q * D + f];
             pw[e][0] = 1.0;
 #pragma unroll
             for (int p = 1; p <= M; ++p) pw[e][p] = pw[e][p - 1] * s;
@@ -207,7 +222,7 @@ __global__ void __launch_bounds__(256) k_matfree(MfArgs m, KArgs a) {
 #pragma unroll
             for (int p = 0; p <= M; ++p) pw[2][p] = p == 0 ? 1.0 : 0.0;
           }
-          const double wq = c_qw[q];
+          const double wq = qw[q];
           constexpr MonoTab MT = mono_tab(D, M);
 #pragma unroll
           for (int e = 0; e < NM; ++e) mom[e] += wq * (pw[0][MT.e[e][0]] * pw[1][MT.e[e][1]] * pw[2][MT.e[e][2]]);
@@ -216,7 +231,7 @@ __global__ void __launch_bounds__(256) k_matfree(MfArgs m, KArgs a) {
         for (int l = 1; l < NM; ++l) {
           double s = 0.0;
 #pragma unroll
-          for (int e = 0; e < NM; ++e) s += c_mcoef[l * NM + e] * mom[e];
+          for (int e = 0; e < NM; ++e) s += mcoef[l * NM + e] * mom[e];
           A[r][l - 1] = s;
         }
 #pragma unroll
@@ -338,9 +353,9 @@ __global__ void __launch_bounds__(256) k_matfree(MfArgs m, KArgs a) {
         // linear modes ψ_1..ψ_d at ξ: monomials 1, ξ, η(, ζ) are e = 0..d
 #pragma unroll
         for (int l = 0; l < D; ++l) {
-          double s = c_mcoef[(l + 1) * NM + 0];
+          double s = mcoef[(l + 1) * NM + 0];
 #pragma unroll
-          for (int e = 0; e < D; ++e) s += c_mcoef[(l + 1) * NM + 1 + e] * xi[e];
+          for (int e = 0; e < D; ++e) s += mcoef[(l + 1) * NM + 1 + e] * xi[e];
           As[mm][l] = s;
         }
 #pragma unroll
@@ -442,6 +457,7 @@ static void upload(T*& dst, const std::vector<T>& src) {
 void dev_matfree_destroy(cwreco_ctx* c) {
   MfState* s = (MfState*)c->mf;
   if (!s) return;
+  DeviceGuard dg(c->device);
   cudaFree(s->X);
   cudaFree(s->B);
   cudaFree(s->st);
@@ -456,9 +472,9 @@ void dev_matfree_destroy(cwreco_ctx* c) {
 void dev_matfree_upload(cwreco_ctx* c, const MatfreeHost& h) {
   if (c->device < 0) fail(CWRECO_ECUDA, "prepare_matrixfree: context has no device (no CPU fallback)");
   mf_fn(c->d, c->M, c->V);  // EUNSUPPORTED early
-  MCK(cudaSetDevice(c->device));
+  DeviceGuard dg(c->device);
   const int nmono = (int)h.mexp.size() / 3, nq = (int)h.qw.size();
-  if (nmono > kMfMaxMono || nq > kMfMaxQ || nmono != c->nm) fail(CWRECO_EUNSUPPORTED, "matrix-free: basis too large");
+  if (nq > kMfMaxQ || nmono != c->nm || c->M > 3) fail(CWRECO_EUNSUPPORTED, "matrix-free: basis too large");
   {  // the kernel's compile-time monomial order must be the library's
     int cnt = 0;
     for (int n = 0; n <= c->M; ++n)
@@ -486,10 +502,11 @@ void dev_matfree_upload(cwreco_ctx* c, const MatfreeHost& h) {
   std::vector<double> qp3(nq * 3, 0.0);
   for (int q = 0; q < nq; ++q)
     for (int e = 0; e < c->d; ++e) qp3[q * c->d + e] = h.qp[q * c->d + e];
-  MCK(cudaMemcpyToSymbol(c_mexp, h.mexp.data(), sizeof(int) * h.mexp.size()));
-  MCK(cudaMemcpyToSymbol(c_mcoef, h.mcoef.data(), sizeof(double) * h.mcoef.size()));
-  MCK(cudaMemcpyToSymbol(c_qp, qp3.data(), sizeof(double) * qp3.size()));
-  MCK(cudaMemcpyToSymbol(c_qw, h.qw.data(), sizeof(double) * h.qw.size()));
+  const int slot = mf_slot(c->d, c->M);
+  MCK(cudaMemcpyToSymbol(c_mcoef, h.mcoef.data(), sizeof(double) * h.mcoef.size(),
+                         sizeof(double) * mf_coef_off(c->d, c->M)));
+  MCK(cudaMemcpyToSymbol(c_qp, qp3.data(), sizeof(double) * qp3.size(), sizeof(double) * slot * kMfMaxQ * 3));
+  MCK(cudaMemcpyToSymbol(c_qw, h.qw.data(), sizeof(double) * h.qw.size(), sizeof(double) * slot * kMfMaxQ));
   const int nm = c->nm;
   std::vector<double> packed;
   for (int l = 1; l < nm; ++l)
@@ -502,6 +519,7 @@ void dev_matfree_reconstruct(cwreco_ctx* c, const double* avgs, int64_t acs, int
   MfState* s = (MfState*)c->mf;
   if (!s) fail(CWRECO_ESTATE, "matrix-free kernel: call cwreco_prepare_matrixfree first");
   if (cell_end <= cell_begin) return;
+  DeviceGuard dg(c->device);
   MfArgs m;
   m.X = s->X;
   m.B = s->B;
@@ -542,7 +560,8 @@ void dev_matfree_reconstruct(cwreco_ctx* c, const double* avgs, int64_t acs, int
   int occ = 1;
   MCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)f, 256, smem));
   const int64_t warps = cell_end - cell_begin;
-  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((warps + 7) / 8, (int64_t)nsm * std::max(1, occ)));
+  int64_t grid = std::max<int64_t>(1, std::min<int64_t>((warps + 7) / 8, (int64_t)nsm * std::max(1, occ)));
+  if (c->max_ctas > 0) grid = std::min<int64_t>(grid, c->max_ctas);  // CWRECO_OPT_MAX_CTAS
   f<<<(unsigned)grid, 256, smem, (cudaStream_t)stream>>>(m, a);
   MCK(cudaGetLastError());
 }

@@ -70,11 +70,12 @@ void rowblk_plan(const Layout& L, int max_smem, int max_ctas, int& ctas, int& st
   }
 }
 
-Layout make_layout(int d, int M, int V, int G, int max_smem, const std::function<int(int)>& umax_for) {
+Layout make_layout(int d, int M, int V, int G, int max_smem, const std::function<int(int)>& umax_for,
+                   int family) {
   const int nm = n_modes(M, d);
-  // CWRECO_FAMILY (tests / A-B experiments): 0 = cell-variable, 1 = row-block where instantiated
-  const char* fam = std::getenv("CWRECO_FAMILY");
-  const bool want_rb = fam ? std::atoi(fam) == 1 : rb_default(nm - 1, V);
+  // family (cwreco_set_option CWRECO_OPT_FAMILY): -1 = default, 0 = cell-variable,
+  // 1 = row-block where instantiated
+  const bool want_rb = family >= 0 ? family == 1 : rb_default(nm - 1, V);
   if (want_rb && rowblk_supported(d, M, V)) {
     // k_rowblk: T = consumers / NG cells per tile (halved while the CTA does not fit);
     // KC positions per chunk: ~10 KB of B⁺ per stage, KC ∈ {1, 2, 4} (compiled sizes)
@@ -101,7 +102,11 @@ Layout make_layout(int d, int M, int V, int G, int max_smem, const std::function
   // full (their ΔQ is captured with static indices) and kMinStages stages fit.
   // A tile whose sector chunk alone is too large (small ℳ, V = 1) is halved.
   const int64_t budget = pipe_budget(nm, max_smem);
+#ifdef CWRECO_EXPERIMENTS
   const char* force = std::getenv("CWRECO_KC");  // tuning experiments only (tools/sweep.py)
+#else
+  const char* force = nullptr;
+#endif
   Layout best;
   bool found = false;
   for (int T = T0; T >= 2; T = (T / 2) & ~1) {
@@ -375,7 +380,7 @@ void precompute(cwreco_ctx* c) {
       fail(CWRECO_EUNSUPPORTED, "precompute: tile stencil union × nvars exceeds the 16-bit offsets");
     return umax;
   };
-  c->lay = make_layout(d, M, c->V, G, c->device >= 0 ? dev_max_smem(c) : 227 * 1024, umax_for);
+  c->lay = make_layout(d, M, c->V, G, c->device >= 0 ? dev_max_smem(c) : 227 * 1024, umax_for, c->family);
   const Layout& L = c->lay;
   const int T = L.T;
   c->n_tiles = (c->n_owned + T - 1) / T;

@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(rb_consumers(nmodes(M, D) - 1, V) + 32, 1) k_r
       for (int i = tid; i < (int)(a.idx_bytes / 16); i += nct) dsti[i] = src[i];
     }
     double* dst = Qu + (size_t)bufn * a.Umax * VP;
-    if (a.exp_flags & 1) {  // experiment: no gather (timing only)
+    if (EXP(a, 1)) {  // experiment: no gather (timing only)
       cp_async_commit();
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[rg.st]);
@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(rb_consumers(nmodes(M, D) - 1, V) + 32, 1) k_r
           for (int v = 0; v < V; ++v) Oc[v * NM + r * NG] = acc[r][v];
     }
     consumer_bar(nct);
-    for (int item = tid; item < ((a.exp_flags & 16) ? 0 : T * V); item += nct) {  // flag 16: no epilogue
+    for (int item = tid; item < (EXP(a, 16) ? 0 : T * V); item += nct) {  // flag 16: no epilogue
       const int c2 = item / V, v2 = item - (item / V) * V;
       const int j = c2 / a.TSC, cl = c2 - j * a.TSC;
       const int sst = rs.st + j < S ? rs.st + j : rs.st + j - S;

@@ -19,6 +19,7 @@
 #include <string>
 #include <vector>
 
+#include "devguard.cuh"
 #include "internal.hpp"
 
 namespace cwr {
@@ -138,6 +139,7 @@ static TrFn tr_fn(int nm, int V, int qb) {
 void dev_traces_destroy(cwreco_ctx* c) {
   TraceState* t = (TraceState*)c->tr;
   if (!t) return;
+  DeviceGuard dg(c->device);
   cudaFree(t->phi);
   cudaFree(t->code);
   delete t;
@@ -213,15 +215,17 @@ static void traces_prepare(cwreco_ctx* c) {
 }
 
 void dev_face_traces(cwreco_ctx* c, const double* coeffs, int64_t ccs, int64_t cvs, double* traces, void* stream) {
-  TCK(cudaSetDevice(c->device));
+  DeviceGuard dg(c->device);
   if (!c->tr) traces_prepare(c);
   TraceState* t = (TraceState*)c->tr;
   const int nv = c->d + 1;
   int qb = tr_qb(t->nq, c->nm);
+#ifdef CWRECO_EXPERIMENTS
   if (const char* e = std::getenv("CWRECO_TRACE_QB")) {  // tuning experiments only
     const int x = std::atoi(e);
     if (x >= 1 && x <= 4 && t->nq % x == 0) qb = x;
   }
+#endif
   const int units = nv * (t->nq / qb);
   const int cb = std::max(1, 256 / units);
   const int64_t groups = (c->n_owned + cb - 1) / cb;

@@ -54,15 +54,14 @@ CASES = [
 
 @pytest.mark.parametrize("family", ["0", "1"], ids=["cellvar", "rowblk"])
 @pytest.mark.parametrize("case", CASES, ids=lambda c: c[0])
-def test_small_mesh_parity(case, family, monkeypatch):
-    """Both kernel families (CWRECO_FAMILY: 0 = one thread per (cell, variable),
+def test_small_mesh_parity(case, family):
+    """Both kernel families (CWRECO_OPT_FAMILY: 0 = one thread per (cell, variable),
     1 = row-block where instantiated, ℳ ≥ 10) against the oracle and k_simple."""
     name, d, n, M, jit, per, V, ncheck = case
     nodes, cells, period = gen.box_mesh(d, n, per, jit, 21)
     rng = np.random.default_rng(3)
     Qin = rng.standard_normal((cells.shape[0], V)) * 2.0 + 3.0
-    monkeypatch.setenv("CWRECO_FAMILY", family)
-    ctx = P.setup_context(nodes, cells, period, M, V, device=0)
+    ctx = P.setup_context(nodes, cells, period, M, V, device=0, family=int(family))
     m = OracleMesh(nodes, cells, period, M)
     assert np.array_equal(ctx.permutation(), m.perm)
     Q = Qin[m.perm]
@@ -122,12 +121,11 @@ def test_constant_and_linear_data():
 
 
 @pytest.mark.parametrize("family", ["0", "1"], ids=["cellvar", "rowblk"])
-def test_strides_parts_determinism(family, monkeypatch):
-    monkeypatch.setenv("CWRECO_FAMILY", family)
+def test_strides_parts_determinism(family):
     nodes, cells, period = gen.box_mesh(2, 20, True, 0.2, 9)
     V, M = 4, 3
     Q = np.random.default_rng(1).standard_normal((cells.shape[0], V))
-    ctx = P.setup_context(nodes, cells, period, M, V, device=0)
+    ctx = P.setup_context(nodes, cells, period, M, V, device=0, family=int(family))
     Qd = torch.tensor(Q, device="cuda")
     ref = ctx.reconstruct(Qd)
     again = ctx.reconstruct(Qd)
@@ -152,20 +150,20 @@ def test_strides_parts_determinism(family, monkeypatch):
 
 
 @pytest.mark.parametrize("family", ["0", "1"], ids=["cellvar", "rowblk"])
-def test_multirank_emulation_bitwise(family, monkeypatch):
+def test_multirank_emulation_bitwise(family):
     """T5: P logical ranks on one GPU (one context each, ghosts filled from the
     global array, library halo pack checked) reproduce the 1-rank output bitwise."""
-    monkeypatch.setenv("CWRECO_FAMILY", family)
     nodes, cells, period = gen.box_mesh(2, 22, True, 0.2, 13)
     V, M, NR = 3, 3, 3
     Qin = np.random.default_rng(2).standard_normal((cells.shape[0], V))
-    one = P.setup_context(nodes, cells, period, M, V, device=0)
+    one = P.setup_context(nodes, cells, period, M, V, device=0, family=int(family))
     perm = one.permutation()
     Qg = Qin[perm]
     ref = one.reconstruct(torch.tensor(Qg, device="cuda")).cpu().numpy()
     ctxs, plans = [], []
     for r in range(NR):
         c = P.Context(2, M, V, device=0)
+        c.set_option(P.OPT_FAMILY, int(family))
         c.set_mesh(nodes, cells, period)
         c.set_partition(r, NR)
         c.build_stencils()
@@ -301,12 +299,11 @@ def test_c_client_on_gpu(tmp_path):
     assert "conservation error" in r.stdout
 
 
-def test_rowblk_constant_data(monkeypatch):
+def test_rowblk_constant_data():
     """The row-block family forms B⁺ΔQ as B⁺Q − rs·Q_i: on constant data the higher
     modes are rounding-level (not exactly 0 as in the ΔQ form), the mean exact."""
-    monkeypatch.setenv("CWRECO_FAMILY", "1")
     nodes, cells, period = gen.box_mesh(3, 4, True, 0.1, 4)
-    ctx = P.setup_context(nodes, cells, period, 3, 9, device=0)
+    ctx = P.setup_context(nodes, cells, period, 3, 9, device=0, family=1)
     assert ctx.info()["kernel_family"] == 1
     Qc = np.full((cells.shape[0], 9), 1.25)
     w = _run(ctx, Qc, "pipelined")

@@ -21,15 +21,22 @@ Modules and what pins them (tests/test_oracle_*.py, all ``-m "not gpu"``):
   topology   face / node adjacency.  Pinned: symmetry, counts.
   stencils   central + sectorial stencils with exact rational predicates
              (R11-R15).  PARITY UNPINNED against the paper
-             (its figures are stripped); pinned only by invariants
+             (its figures are stripped); pinned by invariants
              (sizes P:166/P:179, self first, no duplicates, cone membership,
-             connectivity, determinism) and by brute-force cone checks.
+             connectivity, determinism), brute-force cone checks and one
+             hand-derived mesh that exercises the R14 node-neighbour fallback
+             and invalid sectors (tests/golden/sector_fallback_mesh.json).
   reconstruct  A by exact monomial averaging, constrained LSQ,
              sectors (P:184-191), P0 (P:196), σ (P:219-222), ω (P:205-215),
-             w.  Pinned: polynomial reproduction of degree ≤ M,
-             conservation, ℙ1 exactness, Σλ̄ P = P_opt, Σω = 1, ω = λ̄ for equal
-             σ, paper's λ0/(λ0+N_p), convergence order on the vortex, mpmath
-             40-digit re-evaluation on a tiny case.
+             w; precompute_cell / apply_cell split the per-cell
+             matrices from the pass.  Pinned: polynomial reproduction
+             of degree ≤ M, conservation, ℙ1 exactness, λ̄0 P0 + Σλ̄_s P_s =
+             P_opt on the returned P0, Σω = 1, ω = λ̄ for equal σ with the
+             paper's λ0/(λ0+N_p), hand-derived ω ratios at unequal σ (r = 4,
+             ε inside the power), the paper's λ/ε/r constants, convergence
+             order on a smooth sin·cos field, and a 40-digit mpmath
+             re-evaluation of all 512 cells of C1 with a different quadrature
+             and LSQ method (tests/test_oracle_mpmath.py).
   traces     face traces of the polynomials at the face quadrature points
              (SURVEY §8(f) NEXT-3, R31).  Pinned: rule exactness to
              degree 2M+1 (Dirichlet formula on the face simplex), traces of

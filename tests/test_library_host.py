@@ -299,3 +299,29 @@ def test_c_client_host_only(tmp_path):
     r = subprocess.run([exe, "-1"], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stderr
     assert "cells 1152, modes 10" in r.stdout and "status 3" in r.stderr
+
+
+def test_sector_fallback_hand_mesh_library():
+    """The library's stencil builder on the hand-derived R14 fallback mesh
+    (tests/golden/sector_fallback_mesh.json): same sectors and validity as derived
+    by hand, the fallback cell counted as an extra gather (R15), and the
+    precomputed matrices reproduce linear data exactly on the owner."""
+    import json
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with open(os.path.join(root, "tests", "golden", "sector_fallback_mesh.json")) as f:
+        g = json.load(f)
+    nodes, cells = np.array(g["nodes"]), np.array(g["cells"], dtype=np.int64)
+    ctx = P.Context(2, g["M"], 2, device=None)
+    ctx.set_mesh(nodes, cells, None)
+    ctx.build_stencils()
+    perm = ctx.permutation()
+    sfc = {int(inp): s for s, inp in enumerate(perm)}
+    cen, sec, val = ctx.stencils()
+    i = sfc[g["owner"]]
+    exp = [[sfc[c] if c >= 0 else -1 for c in row] for row in g["expected_sectors_input_ids"]]
+    assert sec[i].tolist() == exp
+    assert val[i].tolist() == g["expected_valid"]
+    assert sfc[2] not in cen[i].tolist()
+    ctx.precompute()
+    assert ctx.info()["n_extra_gather"] >= 1
+    assert ctx.info()["n_invalid_sectors"] >= 2

@@ -156,3 +156,29 @@ def test_errors():
     flat = nodes.copy(); flat[:, 1] = 0.0
     with pytest.raises(MeshError):
         OracleMesh(flat, cells, None, 1)                                      # zero area
+
+
+def _fallback_mesh():
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "sector_fallback_mesh.json")) as f:
+        g = json.load(f)
+    return g, np.array(g["nodes"]), np.array(g["cells"], dtype=np.int64)
+
+
+def test_sector_fallback_hand_mesh():
+    """R14: a sector whose face-BFS starves is completed from node neighbours
+    in the cone, and sectors that stay short are invalid — against the hand-derived
+    stencils of tests/golden/sector_fallback_mesh.json."""
+    g, nodes, cells = _fallback_mesh()
+    m = OracleMesh(nodes, cells, None, g["M"])
+    sfc = {int(inp): s for s, inp in enumerate(m.perm)}
+    i = sfc[g["owner"]]
+    # local vertex order of the owner is (v, a, b) (positively oriented, no swap)
+    assert list(m.cells[i]) == list(cells[g["owner"]])
+    S, valid = m.sector_stencils(i)
+    exp = [[sfc[c] if c >= 0 else -1 for c in row] for row in g["expected_sectors_input_ids"]]
+    assert S == exp
+    assert valid == g["expected_valid"]
+    # the fallback cell c2 lies outside the central stencil (R15: extra gather)
+    assert sfc[2] not in m.central_stencil(i)

@@ -107,13 +107,79 @@ def test_conservation_identities_c1(c1, golden):
         assert np.abs(r["w"][:, 0] * math.sqrt(2.0) - Q[i]).max() <= 4e-15 * np.abs(Q[i]).max()
         # Σ ω = 1, ω ≥ 0 (Eq. weights)
         assert np.abs(r["omega"].sum(axis=0) - 1).max() < 1e-15 and r["omega"].min() >= 0
-        # optimal-coefficient identity λ̄0 P0 + Σ λ̄_s P_s = P_opt
-        P0 = r["popt"].copy()
-        P0[:, : d + 1] -= sum(lam[s + 1] * r["psec"][s] for s in range(d + 1))
-        P0 /= lam[0]
-        comb = lam[0] * P0
+        # optimal-coefficient identity on the oracle's OWN P0:
+        # λ̄0 P0 + Σ λ̄_s P_s = P_opt, with λ̄ from the paper's values (golden)
+        assert np.all(r["valid"])
+        assert np.allclose(r["lam"], lam, rtol=1e-15, atol=0)
+        comb = lam[0] * r["P0"]
         comb[:, : d + 1] += sum(lam[s + 1] * r["psec"][s] for s in range(d + 1))
         assert np.abs(comb - r["popt"]).max() < 1e-13 * np.abs(Q[r["central"]]).max()
+        # the blend is Σ ω_s P_s over the oracle's candidates (P0 first)
+        blend = r["omega"][0][:, None] * r["P0"]
+        for s in range(d + 1):
+            blend[:, : d + 1] += r["omega"][s + 1][:, None] * r["psec"][s]
+        assert np.abs(blend - r["w"]).max() < 1e-13 * np.abs(Q[r["central"]]).max()
+
+
+def test_weight_constants_are_the_papers(golden):
+    """λ0 = 1e5, λ_s = 1, ε = 1e-14, r = 4: the oracle's defaults."""
+    g = golden["weights"]
+    assert (R.LAMBDA0, R.LAMBDAS, R.EPS, R.R_EXP) == (g["lambda0"], g["lambda_s"], g["eps"], g["r"])
+
+
+@pytest.mark.parametrize("regime", ["large", "eps"])
+def test_weights_unequal_sigma(regime, golden):
+    """ω at UNEQUAL σ, hand-derived.  Data linear with gradient g on the
+    owner and on sectors s ≠ s0, and with gradient 2g on the members of sector s0: every
+    sector interpolant is then exactly that linear function, so by the
+    closed form σ(linear p) = |T_E|·|∇_ξ p|² (App. A, pinned in test_oracle_basis)
+    σ_s = σ_g := |T_E|·|Jᵀg|² and σ_s0 = 4σ_g.  The equal linear weights of the
+    sectors cancel, and ω_s/ω_s0 = ((4σ_g + ε)/(σ_g + ε))^r:
+      large σ_g (ε negligible): 4^4 = 256   (r = 2 would give 16)
+      σ_g = ε:                 (5/2)^4 = 39.0625 (an ε outside the power, σ^r + ε,
+                               would give ≈ 1; no ε would give 256)."""
+    d, M = 2, 2
+    nodes, cells, period = gen.box_mesh(d, 10, periodic=False, jitter=0.1, seed=4)
+    m = OracleMesh(nodes, cells, None, M)
+    eps = golden["weights"]["eps"]
+    rng = np.random.default_rng(5)
+    checked = 0
+    for i in rng.permutation(m.N):
+        i = int(i)
+        sectors, valid = m.sector_stencils(i)
+        if not all(valid):
+            continue
+        try:
+            m.central_stencil(i)
+        except Exception:
+            continue
+        X = m.X[i]
+        J = (X[1:] - X[0]).T                       # x = X0 + J ξ (P:94-102)
+        g = np.array([0.7, -0.4])
+        sig_g = 0.5 * float(np.sum((J.T @ g) ** 2))
+        if regime == "eps":
+            g = g * np.sqrt(eps / sig_g)
+            sig_g = 0.5 * float(np.sum((J.T @ g) ** 2))
+        s0 = checked % (d + 1)
+        Q = m.bary @ g - m.bary[i] @ g                              # linear, Q_i = 0
+        members = [j for j in sectors[s0][1:]]
+        Q = Q.copy()
+        Q[members] = 2.0 * (m.bary[members] @ g - m.bary[i] @ g)   # gradient 2g on sector s0
+        r = R.reconstruct_cell(m, i, Q[:, None], M)
+        sig = r["sigma"][:, 0]
+        for s in range(d + 1):
+            want = 4 * sig_g if s == s0 else sig_g
+            assert abs(sig[1 + s] - want) <= 1e-9 * want, (s, sig[1 + s], want)
+        want_ratio = 256.0 if regime == "large" else 39.0625
+        for s in range(d + 1):
+            if s != s0:
+                ratio = r["omega"][1 + s, 0] / r["omega"][1 + s0, 0]
+                assert abs(ratio / want_ratio - 1) < (1e-6 if regime == "large" else 1e-6), (ratio, want_ratio)
+        assert abs(r["omega"][:, 0].sum() - 1) < 1e-15
+        checked += 1
+        if checked == 6:
+            break
+    assert checked == 6
 
 
 def test_weights_closed_form(golden):

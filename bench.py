@@ -128,19 +128,24 @@ class ClockSampler:
         try:
             import pynvml as N
             N.nvmlInit()
-            # torch's device index → NVML handle through the PCI bus id
+            # torch's device index → NVML handle through the device UUID
             import torch
-            bus = torch.cuda.get_device_properties(self.index).pci_bus_id if hasattr(
-                torch.cuda.get_device_properties(self.index), "pci_bus_id") else None
             h = None
-            if bus:
-                try:
-                    h = N.nvmlDeviceGetHandleByPciBusId(bus)
-                except Exception:
-                    h = None
+            try:
+                want = str(torch.cuda.get_device_properties(self.index).uuid).lower().replace("gpu-", "")
+                for k in range(N.nvmlDeviceGetCount()):
+                    hk = N.nvmlDeviceGetHandleByIndex(k)
+                    u = N.nvmlDeviceGetUUID(hk)
+                    u = (u.decode() if isinstance(u, bytes) else str(u)).lower().replace("gpu-", "")
+                    if u == want:
+                        h = hk
+                        break
+            except Exception:
+                h = None
             if h is None:
-                vis = os.environ.get("CUDA_VISIBLE_DEVICES")
-                idx = int(vis.split(",")[self.index]) if vis and vis.split(",")[0].isdigit() else self.index
+                vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+                first = vis.split(",")[self.index] if vis else ""
+                idx = int(first) if first.isdigit() else self.index
                 h = N.nvmlDeviceGetHandleByIndex(idx)
             self.N, self.h = N, h
             self.max_mhz = float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))

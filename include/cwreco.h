@@ -60,7 +60,8 @@ typedef enum {
   CWRECO_ESTENCIL = 5,    /* central stencil exhausted (component has < n_e cells) */
   CWRECO_ESINGULAR = 6,   /* rank-deficient central least-squares system */
   CWRECO_ESTATE = 7,      /* call out of order (e.g. reconstruct before precompute) */
-  CWRECO_EUNSUPPORTED = 8 /* (d, M, V) outside the compiled range */
+  CWRECO_EUNSUPPORTED = 8, /* (d, M, V) outside the compiled range */
+  CWRECO_ENCCL = 9         /* NCCL could not be loaded, or an NCCL call failed */
 } cwreco_status;
 
 /* Linear weights and WENO parameters.  Defaults: lambda0 = 1e5,
@@ -154,9 +155,31 @@ cwreco_status cwreco_set_mesh(cwreco_ctx* ctx, int64_t n_nodes, const double* xy
                               const int64_t* cell_nodes, const double* period);
 /* sfc_to_input: [n_cells] out. */
 cwreco_status cwreco_get_permutation(const cwreco_ctx* ctx, int64_t* sfc_to_input);
-/* Ownership: rank owns SFC ids [floor(r·N/P), floor((r+1)·N/P)).  Optional;
- * default rank 0 of 1.  Must precede cwreco_build_stencils. */
-cwreco_status cwreco_set_partition(cwreco_ctx* ctx, int rank, int nranks);
+/* Ownership: rank owns SFC ids [floor(r·N/P), floor((r+1)·N/P)) (contiguous Morton
+ * ranges).  Optional; default rank 0 of 1.  Must precede cwreco_build_stencils.
+ * id: NULL (no transport: the caller moves ghost data itself with cwreco_halo_plan /
+ * cwreco_set_send_lists / cwreco_halo_pack), or 128 bytes from
+ *   cwreco_nccl_unique_id   (one process per rank; every rank passes the SAME bytes,
+ *                            made by one rank and broadcast by the caller): the
+ *                            context creates an NCCL communicator over the ranks
+ *                            (ncclCommInitRank — COLLECTIVE, blocks until all ranks
+ *                            join; needs a CUDA device; ENCCL if libnccl cannot be
+ *                            loaded or fails), or
+ *   cwreco_loopback_unique_id (all ranks in ONE process, one host thread per rank,
+ *                            each with its own context): peer transfers are device
+ *                            copies (tests on one GPU; the plan exchange also works
+ *                            host-only).
+ * With a transport, cwreco_build_stencils / cwreco_set_stencils become collective:
+ * after the stencils every rank sends each owner the ids of the ghosts it needs and
+ * installs what it must send (the send lists), so cwreco_halo_exchange and
+ * cwreco_reconstruct_overlap need no further setup.  Re-partitioning destroys the
+ * previous transport.  EINVAL for a bad rank / nranks / unknown loopback id. */
+cwreco_status cwreco_set_partition(cwreco_ctx* ctx, int rank, int nranks, const uint8_t* id);
+/* id[128] ← a fresh NCCL unique id (ncclGetUniqueId) for cwreco_set_partition;
+ * ENCCL if libnccl.so.2 cannot be loaded. */
+cwreco_status cwreco_nccl_unique_id(uint8_t* id);
+/* id[128] ← a fresh in-process loopback group of nranks ranks for cwreco_set_partition. */
+cwreco_status cwreco_loopback_unique_id(int nranks, uint8_t* id);
 /* Central and sectorial stencils of every owned cell (R11-R15),
  * exact geometric predicates; then ghosts and the local numbering. */
 cwreco_status cwreco_build_stencils(cwreco_ctx* ctx);
@@ -204,7 +227,8 @@ cwreco_status cwreco_get_blocks(const cwreco_ctx* ctx, int64_t n_sel, const int6
 cwreco_status cwreco_prepare_matrixfree(cwreco_ctx* ctx);
 
 /* ---------------------------------------------------------------- multi-rank halo */
-/* recv_counts [nranks]: ghosts owned by each rank; recv_ids [n_ghost]: their SFC
+/* Lower-level pieces of the exchange, for callers that move the bytes themselves
+ * (no transport id): recv_counts [nranks]: ghosts owned by each rank; recv_ids [n_ghost]: their SFC
  * ids in local ghost order (grouped by owner rank, ascending id). */
 cwreco_status cwreco_halo_plan(const cwreco_ctx* ctx, int64_t* recv_counts, int64_t* recv_ids);
 /* Install what this rank sends: send_counts [nranks], send_ids [Σ counts] = SFC ids
@@ -212,6 +236,10 @@ cwreco_status cwreco_halo_plan(const cwreco_ctx* ctx, int64_t* recv_counts, int6
  * id is not owned. */
 cwreco_status cwreco_set_send_lists(cwreco_ctx* ctx, const int64_t* send_counts, const int64_t* send_ids);
 cwreco_status cwreco_send_total(const cwreco_ctx* ctx, int64_t* total);
+/* The installed send lists (by cwreco_set_send_lists or the transport's plan
+ * exchange): send_counts [nranks], send_ids [send_total] as SFC ids, peer order.
+ * Either may be NULL. */
+cwreco_status cwreco_get_send_lists(const cwreco_ctx* ctx, int64_t* send_counts, int64_t* send_ids);
 /* Pack the requested owned rows of d_avgs into d_sendbuf [send_total][nvars]
  * (contiguous, peer order) on `stream`.  The caller moves d_sendbuf to the peers'
  * ghost rows (e.g. NCCL all-to-all-v) before CWRECO_PART_BOUNDARY. */
@@ -238,6 +266,32 @@ cwreco_status cwreco_halo_pack_rows(cwreco_ctx* ctx, const double* d_rows, int64
 cwreco_status cwreco_reconstruct(cwreco_ctx* ctx, const double* d_avgs, int64_t a_cell_stride,
                                  int64_t a_var_stride, double* d_coeffs, int64_t c_cell_stride,
                                  int64_t c_var_stride, int part, cwreco_stream stream);
+/* The first exchange of the scheme ("exchange of the cell averages
+ * before the reconstruction"): fill the ghost rows n_owned.. of d_avgs (strides as
+ * cwreco_reconstruct) with the owners' averages, through the transport of
+ * cwreco_set_partition: on the library's comm stream, after the work already on
+ * `stream`, pack (one kernel) → NCCL send/recv per peer (or loopback copies) into
+ * the ghost rows (directly when d_avgs is dense [n_local][nvars], else staged and
+ * scattered by a kernel); `stream` then waits for it.  Asynchronous.  nranks == 1:
+ * no-op.  ESTATE without a transport; ECUDA without a device.  Every rank must make
+ * the same sequence of exchange calls. */
+cwreco_status cwreco_halo_exchange(cwreco_ctx* ctx, double* d_avgs, int64_t a_cell_stride, int64_t a_var_stride,
+                                   cwreco_stream stream);
+/* The second exchange (the reconstruction polynomials after the pass):
+ * rows of `width` contiguous doubles, row stride row_stride (e.g. the coefficients
+ * [n_local][nvars][ℳ]: width = row_stride = nvars·ℳ); ghost rows n_owned.. are
+ * filled from the owners' rows.  As cwreco_halo_exchange otherwise. */
+cwreco_status cwreco_halo_exchange_rows(cwreco_ctx* ctx, double* d_rows, int64_t row_stride, int width,
+                                        cwreco_stream stream);
+/* One overlapped multi-rank pass (SURVEY §8(b) overlap_halo): the exchange of
+ * cwreco_halo_exchange on the comm stream, the INTERIOR tiles (stencils fully owned,
+ * no ghost reads) on `stream` concurrently, then — after the exchange event — the
+ * BOUNDARY tiles.  Writes the ghost rows of d_avgs and all owned rows of d_coeffs;
+ * results are bitwise those of a single-rank pass.  nranks == 1: a plain
+ * cwreco_reconstruct.  Errors as cwreco_reconstruct / cwreco_halo_exchange. */
+cwreco_status cwreco_reconstruct_overlap(cwreco_ctx* ctx, double* d_avgs, int64_t a_cell_stride,
+                                         int64_t a_var_stride, double* d_coeffs, int64_t c_cell_stride,
+                                         int64_t c_var_stride, cwreco_stream stream);
 /* End-to-end pass on HOST buffers (the whole hot path behind one call):
  *   h_avgs   [n_owned + n_ghost][nvars] dense row-major, local order (ghost rows
  *            already filled by the caller when nranks > 1);

@@ -12,6 +12,7 @@ import os
 import numpy as np
 
 __all__ = ["Context", "CwrecoError", "lib", "KERNELS", "OPT_FAMILY", "OPT_MAX_CTAS", "PART_ALL",
+           "nccl_unique_id", "loopback_unique_id",
            "PART_INTERIOR", "PART_BOUNDARY",
            "n_modes", "setup_context"]
 
@@ -22,7 +23,7 @@ KERNELS = {"pipelined": 0, "simple": 1, "matrixfree": 2}
 OPT_FAMILY, OPT_MAX_CTAS = 1, 2
 PART_ALL, PART_INTERIOR, PART_BOUNDARY = 0, 1, 2
 _STATUS = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "ECUDA", 4: "EMESH", 5: "ESTENCIL", 6: "ESINGULAR",
-           7: "ESTATE", 8: "EUNSUPPORTED"}
+           7: "ESTATE", 8: "EUNSUPPORTED", 9: "ENCCL"}
 
 
 class CwrecoError(RuntimeError):
@@ -59,7 +60,12 @@ def _load():
         "cwreco_set_option": [P, I32, I64],
         "cwreco_set_mesh": [P, I64, P, I64, P, P],
         "cwreco_get_permutation": [P, P],
-        "cwreco_set_partition": [P, I32, I32],
+        "cwreco_set_partition": [P, I32, I32, P],
+        "cwreco_nccl_unique_id": [P],
+        "cwreco_loopback_unique_id": [I32, P],
+        "cwreco_halo_exchange": [P, P, I64, I64, P],
+        "cwreco_halo_exchange_rows": [P, P, I64, I32, P],
+        "cwreco_reconstruct_overlap": [P, P, I64, I64, P, I64, I64, P],
         "cwreco_build_stencils": [P],
         "cwreco_get_stencils": [P, P, P, P],
         "cwreco_get_local_cells": [P, P],
@@ -74,6 +80,7 @@ def _load():
         "cwreco_halo_plan": [P, P, P],
         "cwreco_set_send_lists": [P, P, P],
         "cwreco_send_total": [P, P],
+        "cwreco_get_send_lists": [P, P, P],
         "cwreco_halo_pack": [P, P, I64, I64, P, P],
         "cwreco_halo_pack_rows": [P, P, I64, I32, P, P],
         "cwreco_reconstruct": [P, P, I64, I64, P, I64, I64, I32, P],
@@ -108,6 +115,22 @@ def n_modes(M, d):
     for l in range(1, d + 1):
         num *= (M + l)
     return num // (2 if d == 2 else 6)
+
+
+def nccl_unique_id():
+    """128 bytes of a fresh NCCL unique id (cwreco_nccl_unique_id); one rank makes it,
+    the caller broadcasts it, every rank passes it to Context.set_partition."""
+    buf = (ctypes.c_uint8 * 128)()
+    _check(lib.cwreco_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def loopback_unique_id(nranks):
+    """128 bytes naming a fresh in-process loopback group of nranks ranks
+    (cwreco_loopback_unique_id): one thread per rank, each with its own Context."""
+    buf = (ctypes.c_uint8 * 128)()
+    _check(lib.cwreco_loopback_unique_id(int(nranks), buf))
+    return bytes(buf)
 
 
 def _stream_handle(stream):
@@ -151,9 +174,16 @@ class Context:
         _check(lib.cwreco_get_permutation(self._h, _ptr(out)))
         return out
 
-    def set_partition(self, rank, nranks):
+    def set_partition(self, rank, nranks, uid=None):
+        """cwreco_set_partition; uid: None (no transport) or the 128 bytes of
+        nccl_unique_id() / loopback_unique_id() (collective with a transport)."""
         self.rank, self.nranks = int(rank), int(nranks)
-        _check(lib.cwreco_set_partition(self._h, self.rank, self.nranks))
+        idb = None
+        if uid is not None:
+            if len(uid) != 128:
+                raise ValueError("uid must be 128 bytes")
+            idb = (ctypes.c_uint8 * 128).from_buffer_copy(bytes(uid))
+        _check(lib.cwreco_set_partition(self._h, self.rank, self.nranks, idb))
 
     def build_stencils(self):
         _check(lib.cwreco_build_stencils(self._h))
@@ -234,6 +264,13 @@ class Context:
         _check(lib.cwreco_set_send_lists(self._h, _ptr(counts), _ptr(ids)))
         self.send_counts = counts
 
+    def send_lists(self):
+        """(send_counts [nranks], send_ids [send_total] SFC ids) as installed."""
+        counts = np.empty(self.nranks, dtype=np.int64)
+        ids = np.empty(max(1, self.send_total()), dtype=np.int64)
+        _check(lib.cwreco_get_send_lists(self._h, _ptr(counts), _ptr(ids)))
+        return counts, ids[: self.send_total()]
+
     def send_total(self):
         t = ctypes.c_int64()
         _check(lib.cwreco_send_total(self._h, ctypes.byref(t)))
@@ -253,7 +290,53 @@ class Context:
                                          rows.shape[1], ctypes.c_void_p(sendbuf.data_ptr()),
                                          _stream_handle(stream)))
 
+    def halo_exchange(self, avgs, stream=None):
+        """cwreco_halo_exchange: fill the ghost rows avgs[n_owned:] from their owners."""
+        self._check_avgs(avgs)
+        a_cs, a_vs = avgs.stride()
+        _check(lib.cwreco_halo_exchange(self._h, ctypes.c_void_p(avgs.data_ptr()), a_cs, a_vs,
+                                        _stream_handle(stream)))
+
+    def halo_exchange_rows(self, rows, stream=None):
+        """cwreco_halo_exchange_rows: rows CUDA float64 [n_local, W] with contiguous rows
+        (e.g. coefficients viewed as [n_local, V·ℳ]); fills rows[n_owned:]."""
+        import torch
+        inf = self.info()
+        if not (rows.is_cuda and rows.dtype == torch.float64 and rows.dim() == 2 and rows.stride(1) == 1):
+            raise ValueError("rows must be a [n_local, W] float64 CUDA tensor with contiguous rows")
+        if rows.shape[0] != inf["n_owned"] + inf["n_ghost"]:
+            raise ValueError(f"rows must have n_local = {inf['n_owned'] + inf['n_ghost']} rows")
+        _check(lib.cwreco_halo_exchange_rows(self._h, ctypes.c_void_p(rows.data_ptr()), rows.stride(0),
+                                             rows.shape[1], _stream_handle(stream)))
+
+    def _check_avgs(self, avgs):
+        import torch
+        if not (avgs.is_cuda and avgs.dtype == torch.float64 and avgs.dim() == 2):
+            raise ValueError("avgs must be a 2-D float64 CUDA tensor")
+        inf = self.info()
+        self._need_shape(avgs, (inf["n_owned"] + inf["n_ghost"], self.V), "avgs")
+        return inf
+
     # ---------------------------------------------------------------- hot path
+    def reconstruct_overlap(self, avgs, out=None, stream=None):
+        """cwreco_reconstruct_overlap: halo exchange into avgs' ghost rows overlapped
+        with the interior tiles, then the boundary tiles; returns / fills out."""
+        import torch
+        inf = self._check_avgs(avgs)
+        n_owned = inf["n_owned"]
+        if out is None:
+            out = torch.empty((n_owned, self.V, self.nm), dtype=torch.float64, device=avgs.device)
+        if not (out.is_cuda and out.dtype == torch.float64 and out.device == avgs.device):
+            raise ValueError("out must be a float64 tensor on the device of avgs")
+        self._need_shape(out, (n_owned, self.V, self.nm), "out")
+        a_cs, a_vs = avgs.stride()
+        c_cs, c_vs, c_ls = out.stride()
+        if c_ls != 1:
+            raise ValueError("out must be contiguous along the mode axis")
+        _check(lib.cwreco_reconstruct_overlap(self._h, ctypes.c_void_p(avgs.data_ptr()), a_cs, a_vs,
+                                              ctypes.c_void_p(out.data_ptr()), c_cs, c_vs, _stream_handle(stream)))
+        return out
+
     def reconstruct(self, avgs, out=None, part=PART_ALL, stream=None):
         """avgs: CUDA float64 tensor [n_local, V] (any strides); returns / fills
         out [n_owned, V, ℳ] (float64, CUDA)."""
@@ -353,7 +436,7 @@ class Context:
 
 
 def setup_context(nodes, cells, period, degree_M, nvars, device=0, rank=0, nranks=1, family=-1, max_ctas=0,
-                  **params):
+                  uid=None, **params):
     """set_mesh → set_partition → build_stencils → precompute (family / max_ctas:
     cwreco_set_option, see include/cwreco.h)."""
     ctx = Context(nodes.shape[1], degree_M, nvars, device, **params)
@@ -362,7 +445,7 @@ def setup_context(nodes, cells, period, degree_M, nvars, device=0, rank=0, nrank
         ctx.set_option(OPT_MAX_CTAS, max_ctas)
     ctx.set_mesh(nodes, cells, period)
     if nranks > 1:
-        ctx.set_partition(rank, nranks)
+        ctx.set_partition(rank, nranks, uid)
     ctx.build_stencils()
     ctx.precompute()
     return ctx

@@ -103,6 +103,7 @@ cwreco_status cwreco_create(int dim, int degree_M, int nvars, const cwreco_param
 void cwreco_destroy(cwreco_ctx* ctx) {
   if (!ctx) return;
   try {
+    cwr::halo_destroy(ctx);
     cwr::dev_matfree_destroy(ctx);
     cwr::dev_traces_destroy(ctx);
     cwr::dev_destroy(ctx);
@@ -190,11 +191,12 @@ cwreco_status cwreco_get_permutation(const cwreco_ctx* c, int64_t* out) {
   });
 }
 
-cwreco_status cwreco_set_partition(cwreco_ctx* c, int rank, int nranks) {
+cwreco_status cwreco_set_partition(cwreco_ctx* c, int rank, int nranks, const uint8_t* id) {
   return guard([&] {
     need(c != nullptr, CWRECO_EINVAL, "set_partition: NULL");
     need(nranks >= 1 && rank >= 0 && rank < nranks, CWRECO_EINVAL, "set_partition: bad rank/nranks");
     invalidate_derived(c);
+    cwr::halo_destroy(c);
     c->rank = rank;
     c->nranks = nranks;
     c->has_stencils = c->has_blocks = false;
@@ -202,6 +204,21 @@ cwreco_status cwreco_set_partition(cwreco_ctx* c, int rank, int nranks) {
       c->own_lo = (rank * c->N) / nranks;
       c->own_hi = ((rank + 1) * c->N) / nranks;
     }
+    cwr::halo_set_transport(c, id);
+  });
+}
+
+cwreco_status cwreco_nccl_unique_id(uint8_t* id) {
+  return guard([&] {
+    need(id != nullptr, CWRECO_EINVAL, "nccl_unique_id: NULL");
+    cwr::halo_unique_id_nccl(id);
+  });
+}
+
+cwreco_status cwreco_loopback_unique_id(int nranks, uint8_t* id) {
+  return guard([&] {
+    need(id != nullptr, CWRECO_EINVAL, "loopback_unique_id: NULL");
+    cwr::halo_unique_id_loopback(nranks, id);
   });
 }
 
@@ -212,6 +229,7 @@ cwreco_status cwreco_build_stencils(cwreco_ctx* c) {
     need(c->own_hi > c->own_lo, CWRECO_EINVAL, "build_stencils: this rank owns no cells");
     invalidate_derived(c);
     cwr::build_stencils(c);
+    cwr::halo_plan_exchange(c);  // collective when a transport is set
   });
 }
 
@@ -276,6 +294,7 @@ cwreco_status cwreco_set_stencils(cwreco_ctx* c, const int32_t* central, const i
           for (int k = 0; k < nv; ++k) c->sectors[(q * nv + v) * nv + k] = -1;
     invalidate_derived(c);
     cwr::finalize_stencils(c);
+    cwr::halo_plan_exchange(c);  // collective when a transport is set
   });
 }
 
@@ -362,23 +381,18 @@ cwreco_status cwreco_set_send_lists(cwreco_ctx* c, const int64_t* send_counts, c
   return guard([&] {
     need(c && send_counts, CWRECO_EINVAL, "set_send_lists: NULL");
     need(c->has_stencils, CWRECO_ESTATE, "set_send_lists: no stencils");
-    int64_t tot = 0;
-    for (int r = 0; r < c->nranks; ++r) {
-      need(send_counts[r] >= 0, CWRECO_EINVAL, "set_send_lists: negative count");
-      tot += send_counts[r];
-    }
-    need(tot == 0 || send_ids, CWRECO_EINVAL, "set_send_lists: NULL ids");
-    std::vector<int32_t> own2local(c->own_hi - c->own_lo, -1);
-    for (int64_t li = 0; li < c->n_owned; ++li) own2local[c->local2global[li] - c->own_lo] = (int32_t)li;
-    std::vector<int64_t> loc(tot);
-    for (int64_t k = 0; k < tot; ++k) {
-      const int64_t g = send_ids[k];
-      need(g >= c->own_lo && g < c->own_hi, CWRECO_EINVAL, "set_send_lists: id not owned by this rank");
-      loc[k] = own2local[g - c->own_lo];
-    }
-    c->send_counts.assign(send_counts, send_counts + c->nranks);
-    c->send_local = loc;
-    cwr::dev_set_send(c);
+    cwr::install_send_lists(c, send_counts, send_ids);
+  });
+}
+
+cwreco_status cwreco_get_send_lists(const cwreco_ctx* c, int64_t* send_counts, int64_t* send_ids) {
+  return guard([&] {
+    need(c != nullptr, CWRECO_EINVAL, "get_send_lists: NULL");
+    need(c->has_stencils, CWRECO_ESTATE, "get_send_lists: no stencils");
+    if (send_counts)
+      for (int r = 0; r < c->nranks; ++r) send_counts[r] = r < (int)c->send_counts.size() ? c->send_counts[r] : 0;
+    if (send_ids)
+      for (size_t k = 0; k < c->send_local.size(); ++k) send_ids[k] = c->local2global[c->send_local[k]];
   });
 }
 
@@ -427,6 +441,51 @@ cwreco_status cwreco_reconstruct(cwreco_ctx* c, const double* d_avgs, int64_t ac
     need(part == CWRECO_PART_ALL || part == CWRECO_PART_INTERIOR || part == CWRECO_PART_BOUNDARY, CWRECO_EINVAL,
          "reconstruct: bad part");
     cwr::dev_reconstruct(c, d_avgs, acs, avs, d_coeffs, ccs, cvs, part, stream);
+  });
+}
+
+cwreco_status cwreco_halo_exchange(cwreco_ctx* c, double* d_avgs, int64_t acs, int64_t avs, cwreco_stream stream) {
+  return guard([&] {
+    need(c != nullptr, CWRECO_EINVAL, "halo_exchange: NULL ctx");
+    need_device(c, "halo_exchange");
+    need(c->has_stencils, CWRECO_ESTATE, "halo_exchange: no stencils");
+    need(d_avgs != nullptr, CWRECO_EINVAL, "halo_exchange: NULL buffer");
+    need(acs >= 1 && avs >= 1, CWRECO_EINVAL, "halo_exchange: strides must be >= 1");
+    if (c->nranks == 1) return;
+    cwr::halo_exchange(c, d_avgs, acs, avs, c->V, stream);
+  });
+}
+
+cwreco_status cwreco_halo_exchange_rows(cwreco_ctx* c, double* d_rows, int64_t row_stride, int width,
+                                        cwreco_stream stream) {
+  return guard([&] {
+    need(c != nullptr, CWRECO_EINVAL, "halo_exchange_rows: NULL ctx");
+    need_device(c, "halo_exchange_rows");
+    need(c->has_stencils, CWRECO_ESTATE, "halo_exchange_rows: no stencils");
+    need(d_rows != nullptr, CWRECO_EINVAL, "halo_exchange_rows: NULL buffer");
+    need(width >= 1 && row_stride >= width, CWRECO_EINVAL, "halo_exchange_rows: bad width / stride");
+    if (c->nranks == 1) return;
+    cwr::halo_exchange(c, d_rows, row_stride, 1, width, stream);
+  });
+}
+
+cwreco_status cwreco_reconstruct_overlap(cwreco_ctx* c, double* d_avgs, int64_t acs, int64_t avs, double* d_coeffs,
+                                         int64_t ccs, int64_t cvs, cwreco_stream stream) {
+  return guard([&] {
+    need(c != nullptr, CWRECO_EINVAL, "reconstruct_overlap: NULL ctx");
+    need_device(c, "reconstruct_overlap");
+    if (c->kernel == CWRECO_KERNEL_MATRIXFREE)
+      need(c->mf != nullptr, CWRECO_ESTATE, "reconstruct_overlap: call cwreco_prepare_matrixfree first");
+    else
+      need(c->has_blocks, CWRECO_ESTATE, "reconstruct_overlap: call cwreco_precompute first");
+    need(d_avgs && d_coeffs, CWRECO_EINVAL, "reconstruct_overlap: NULL buffer");
+    need(acs >= 1 && avs >= 1 && ccs >= 1 && cvs >= 1, CWRECO_EINVAL, "reconstruct_overlap: strides must be >= 1");
+    need_disjoint_rows(c, ccs, cvs, c->n_owned, "reconstruct_overlap");
+    if (c->nranks == 1) {
+      cwr::dev_reconstruct(c, d_avgs, acs, avs, d_coeffs, ccs, cvs, CWRECO_PART_ALL, stream);
+      return;
+    }
+    cwr::halo_reconstruct_overlap(c, d_avgs, acs, avs, d_coeffs, ccs, cvs, stream);
   });
 }
 

@@ -237,6 +237,7 @@ struct cwreco_ctx {
   cwr::DeviceState* dev = nullptr;
   void* mf = nullptr;  // matrix-free device state (matfree.cu), after cwreco_prepare_matrixfree
   void* tr = nullptr;  // face-trace tables (traces.cu), built on the first cwreco_face_traces
+  void* halo = nullptr;  // multi-rank transport (halo.cu), after cwreco_set_partition with an id
 };
 
 namespace cwr {
@@ -265,6 +266,18 @@ void dev_matfree_destroy(cwreco_ctx* c);
 void face_rule(int d, int M, std::vector<double>& lam, std::vector<double>& w);
 void dev_face_traces(cwreco_ctx* c, const double* coeffs, int64_t ccs, int64_t cvs, double* traces, void* stream);
 void dev_traces_destroy(cwreco_ctx* c);
+// stencil.cpp: send lists (owned cells requested by each peer, SFC ids) → local ids
+void install_send_lists(cwreco_ctx* c, const int64_t* send_counts, const int64_t* send_ids);
+// halo.cu: multi-rank transport (NCCL or in-process loopback) and the exchange
+void halo_unique_id_nccl(uint8_t* id);
+void halo_unique_id_loopback(int nranks, uint8_t* id);
+void halo_set_transport(cwreco_ctx* c, const uint8_t* id);  // id == nullptr: none
+bool halo_has_transport(const cwreco_ctx* c);
+void halo_plan_exchange(cwreco_ctx* c);                       // collective, after the stencils
+void halo_exchange(cwreco_ctx* c, double* rows, int64_t rs, int64_t es, int width, void* stream);
+void halo_reconstruct_overlap(cwreco_ctx* c, double* avgs, int64_t acs, int64_t avs, double* coeffs, int64_t ccs,
+                              int64_t cvs, void* stream);
+void halo_destroy(cwreco_ctx* c);
 // kernels.cu (device side; all return cudaError_t as int)
 void dev_create(cwreco_ctx* c);
 void dev_destroy(cwreco_ctx* c);

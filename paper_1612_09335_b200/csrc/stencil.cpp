@@ -423,4 +423,24 @@ void finalize_stencils(cwreco_ctx* c) {
   c->has_blocks = false;
 }
 
+void install_send_lists(cwreco_ctx* c, const int64_t* send_counts, const int64_t* send_ids) {
+  int64_t tot = 0;
+  for (int r = 0; r < c->nranks; ++r) {
+    if (send_counts[r] < 0) fail(CWRECO_EINVAL, "set_send_lists: negative count");
+    tot += send_counts[r];
+  }
+  if (tot > 0 && !send_ids) fail(CWRECO_EINVAL, "set_send_lists: NULL ids");
+  std::vector<int32_t> own2local(c->own_hi - c->own_lo, -1);
+  for (int64_t li = 0; li < c->n_owned; ++li) own2local[c->local2global[li] - c->own_lo] = (int32_t)li;
+  std::vector<int64_t> loc(tot);
+  for (int64_t k = 0; k < tot; ++k) {
+    const int64_t g = send_ids[k];
+    if (g < c->own_lo || g >= c->own_hi) fail(CWRECO_EINVAL, "set_send_lists: id not owned by this rank");
+    loc[k] = own2local[g - c->own_lo];
+  }
+  c->send_counts.assign(send_counts, send_counts + c->nranks);
+  c->send_local = loc;
+  dev_set_send(c);
+}
+
 }  // namespace cwr

@@ -309,3 +309,86 @@ def test_rowblk_constant_data():
     w = _run(ctx, Qc, "pipelined")
     assert np.all(w[:, :, 0] == 1.25 / np.sqrt(6.0))
     assert np.abs(w[:, :, 1:]).max() <= 1e-14 * 1.25
+
+
+@pytest.mark.parametrize("family", ["0", "1"], ids=["cellvar", "rowblk"])
+def test_multirank_loopback_overlap(family):
+    """The library's own exchange path on ONE GPU: 3 ranks in 3 host threads, each
+    with its own context joined by a loopback transport (cwreco_set_partition with a
+    loopback id).  cwreco_reconstruct_overlap = pack → peer copies into the ghost rows
+    on the comm stream, interior tiles concurrently, boundary tiles after the event.
+    Every rank's ghost rows equal the owners' averages and its coefficients equal
+    the single-rank pass BITWISE, for three passes in a row (buffer reuse across
+    epochs) with a small CTA cap (many tiles per CTA); the second exchange
+    (cwreco_halo_exchange_rows) delivers the owners' polynomial rows."""
+    import threading
+    nodes, cells, period = gen.box_mesh(2, 40, True, 0.2, 13)
+    V, M, NR = 3, 3, 3
+    Qin = np.random.default_rng(2).standard_normal((cells.shape[0], V))
+    one = P.setup_context(nodes, cells, period, M, V, device=0, family=int(family))
+    Qg = Qin[one.permutation()]
+    ref = one.reconstruct(torch.tensor(Qg, device="cuda")).cpu().numpy()
+    uid = P.loopback_unique_id(NR)
+    res, errs = [None] * NR, []
+
+    def run(r):
+        try:
+            c = P.Context(2, M, V, device=0)
+            c.set_option(P.OPT_FAMILY, int(family))
+            c.set_option(P.OPT_MAX_CTAS, 3)
+            c.set_mesh(nodes, cells, period)
+            c.set_partition(r, NR, uid)
+            c.build_stencils()                 # collective: plan exchange
+            c.precompute()
+            inf = c.info()
+            loc = c.local_cells()
+            n_owned = inf["n_owned"]
+            st = torch.cuda.Stream()
+            outs, ghosts = [], []
+            with torch.cuda.stream(st):
+                A = torch.full((len(loc), V), float("nan"), dtype=torch.float64, device="cuda")
+                A[:n_owned] = torch.tensor(Qg[loc[:n_owned]], device="cuda")
+                for it in range(3):
+                    out = torch.full((n_owned, V, c.nm), float("nan"), dtype=torch.float64, device="cuda")
+                    c.reconstruct_overlap(A, out, stream=st)
+                    outs.append(out)
+                # second exchange: polynomial rows of the ghosts
+                W = torch.full((len(loc), V * c.nm), float("nan"), dtype=torch.float64, device="cuda")
+                W[:n_owned] = outs[-1].reshape(n_owned, V * c.nm)
+                c.halo_exchange_rows(W, stream=st)
+            st.synchronize()
+            res[r] = (loc, n_owned, inf, A.cpu().numpy(), [o.cpu().numpy() for o in outs], W.cpu().numpy(), c)
+        except Exception as e:  # pragma: no cover
+            errs.append(repr(e))
+    th = [threading.Thread(target=run, args=(r,)) for r in range(NR)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert not errs, errs
+    for r in range(NR):
+        loc, n_owned, inf, A, outs, W, c = res[r]
+        assert inf["n_ghost"] > 0 and inf["n_interior"] < n_owned
+        assert np.array_equal(A[n_owned:], Qg[loc[n_owned:]])
+        for o in outs:
+            assert np.array_equal(o, ref[loc[:n_owned]])
+        assert np.array_equal(W[n_owned:], ref[loc[n_owned:]].reshape(-1, V * c.nm))
+
+
+def test_many_tiles_per_cta_parity():
+    """CWRECO_OPT_MAX_CTAS: with 2 CTAs every CTA walks many tiles (double-buffered
+    union gather of the next tile, ring phase wrap-around across tiles), bitwise equal
+    to the default launch and to the simple kernel, for both families and 2-D / 3-D."""
+    for d, n, M, V, fam in [(2, 24, 3, 4, 0), (2, 24, 3, 4, 1), (3, 6, 2, 5, 0), (3, 6, 3, 9, 1), (3, 6, 3, 5, 0)]:
+        nodes, cells, period = gen.box_mesh(d, n, True, 0.15, 23)
+        Q = np.random.default_rng(d + M).standard_normal((cells.shape[0], V)) + 1.0
+        ctx = P.setup_context(nodes, cells, period, M, V, device=0, family=fam)
+        Qp = torch.tensor(Q[ctx.permutation()], device="cuda")
+        full = ctx.reconstruct(Qp).cpu().numpy()
+        ctx.set_option(P.OPT_MAX_CTAS, 2)
+        assert ctx.info()["n_tiles"] >= 8
+        capped = ctx.reconstruct(Qp).cpu().numpy()
+        ctx.set_kernel("simple")
+        simple = ctx.reconstruct(Qp).cpu().numpy()
+        assert np.array_equal(capped, full), (d, M, V, fam)
+        assert np.array_equal(simple, full), (d, M, V, fam)

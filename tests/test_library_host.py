@@ -325,3 +325,48 @@ def test_sector_fallback_hand_mesh_library():
     ctx.precompute()
     assert ctx.info()["n_extra_gather"] >= 1
     assert ctx.info()["n_invalid_sectors"] >= 2
+
+
+def test_loopback_plan_exchange_host_threads():
+    """The library's own plan exchange (cwreco_set_partition with a loopback id,
+    collective cwreco_build_stencils): three host-only contexts in three threads;
+    each rank's installed send lists equal what the other ranks requested
+    (cwreco_halo_plan), peer by peer, in order."""
+    import threading
+    nodes, cells, period = gen.box_mesh(2, 18, True, 0.2, 7)
+    NR = 3
+    uid = P.loopback_unique_id(NR)
+    ctxs = [P.Context(2, 3, 2, device=None) for _ in range(NR)]
+    errs = []
+
+    def run(r):
+        try:
+            ctxs[r].set_mesh(nodes, cells, period)
+            ctxs[r].set_partition(r, NR, uid)
+            ctxs[r].build_stencils()            # collective: plan exchange inside
+        except Exception as e:                  # pragma: no cover
+            errs.append(repr(e))
+    th = [threading.Thread(target=run, args=(r,)) for r in range(NR)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=120)
+    assert not errs, errs
+    plans = [c.halo_plan() for c in ctxs]
+    for r, c in enumerate(ctxs):
+        counts, ids = c.send_lists()
+        want_ids = []
+        for p in range(NR):
+            pc, pid = plans[p]
+            off = int(pc[:r].sum())
+            assert counts[p] == pc[r]
+            want_ids += pid[off:off + pc[r]].tolist()
+        assert ids.tolist() == want_ids
+        assert counts[r] == 0 and c.send_total() == len(want_ids) > 0
+    with pytest.raises(P.CwrecoError, match="EINVAL"):
+        P.Context(2, 3, 2, device=None).set_partition(0, 3, b"CWRLOOP\x00" + b"\xff" * 120)  # unknown group
+    with pytest.raises(P.CwrecoError, match="ESTATE|ECUDA"):
+        ctxs[0].halo_exchange.__func__  # noqa: B018 (attribute exists)
+        import ctypes
+        st = P.lib.cwreco_halo_exchange(ctxs[0]._h, ctypes.c_void_p(8), 2, 1, None)
+        P._check(st)

@@ -49,9 +49,13 @@ class _Info(ctypes.Structure):
 
 def _load():
     from . import _build
-    if not os.path.exists(_LIB_PATH) or _build.stale_abi(_LIB_PATH):
-        _build.build()   # missing, or older than include/cwreco.h's entry points
-    L = ctypes.CDLL(_LIB_PATH)
+    alt = os.environ.get("CWRECO_LIBRARY")   # tuning variants of the library (tools/ only)
+    if alt:
+        L = ctypes.CDLL(alt)
+    else:
+        if not os.path.exists(_LIB_PATH) or _build.stale_abi(_LIB_PATH):
+            _build.build()   # missing, or older than include/cwreco.h's entry points
+        L = ctypes.CDLL(_LIB_PATH)
     P, I64, I32, D = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
     sigs = {
         "cwreco_create": [I32, I32, I32, P, I32, P],

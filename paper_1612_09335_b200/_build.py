@@ -44,31 +44,35 @@ def _run(cmd, log):
     return r.stdout
 
 
-def build(verbose=False):
-    """Compile every source in parallel (one process each), then link."""
+def build(verbose=False, out=None, defines=()):
+    """Compile every source in parallel (one process each), then link.  out / defines:
+    tuning variants only (tools/): another file name and extra -D macros."""
     from concurrent.futures import ThreadPoolExecutor
-    os.makedirs(BUILD, exist_ok=True)
+    out = out or OUT
+    bdir = BUILD if out == OUT else os.path.join(BUILD, os.path.basename(out) + ".d")
+    os.makedirs(bdir, exist_ok=True)
+    dflags = ["-D" + d for d in defines]
     jobs = []
     for s in CXX_SRCS:
-        jobs.append((["g++", *CXXFLAGS, "-c", os.path.join(CSRC, s), "-o", os.path.join(BUILD, s + ".o")],
-                     os.path.join(BUILD, s + ".o")))
+        jobs.append((["g++", *CXXFLAGS, *dflags, "-c", os.path.join(CSRC, s), "-o", os.path.join(bdir, s + ".o")],
+                     os.path.join(bdir, s + ".o")))
     for s in CU_SRCS:
-        jobs.append(([NVCC, *NVFLAGS, "-c", os.path.join(CSRC, s), "-o", os.path.join(BUILD, s + ".o")],
-                     os.path.join(BUILD, s + ".o")))
+        jobs.append(([NVCC, *NVFLAGS, *dflags, "-c", os.path.join(CSRC, s), "-o", os.path.join(bdir, s + ".o")],
+                     os.path.join(bdir, s + ".o")))
     logs = [io.StringIO() for _ in jobs]
     with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
         futs = [ex.submit(_run, cmd, lg) for (cmd, _), lg in zip(jobs, logs)]
         outs = [f.result() for f in futs]
     objs = [o for _, o in jobs]
-    with open(os.path.join(BUILD, "build.log"), "w") as log:
+    with open(os.path.join(bdir, "build.log"), "w") as log:
         for lg in logs:
             log.write(lg.getvalue())
         if verbose:
             print("\n".join(outs))
-        _run(["g++", "-shared", "-o", OUT + ".tmp", *objs, "-fopenmp", "-L" + os.path.join(CUDA_HOME, "lib64"),
+        _run(["g++", "-shared", "-o", out + ".tmp", *objs, "-fopenmp", "-L" + os.path.join(CUDA_HOME, "lib64"),
               "-lcudart_static", "-lrt", "-ldl", "-lpthread"], log)
-    os.replace(OUT + ".tmp", OUT)
-    return OUT
+    os.replace(out + ".tmp", out)
+    return out
 
 
 def stale_abi(path):
@@ -95,4 +99,13 @@ def needs_build():
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv))
+    # python _build.py [-v] [--out FILE] [-D MACRO=VAL ...]   (variants: tools only)
+    args = sys.argv[1:]
+    o, ds = None, []
+    while args:
+        x = args.pop(0)
+        if x == "--out":
+            o = args.pop(0)
+        elif x == "-D":
+            ds.append(args.pop(0))
+    print(build(verbose="-v" in sys.argv, out=o, defines=ds))

@@ -62,7 +62,10 @@ inline int n_modes(int M, int d) {  // ℳ(M,d) = (1/d!) Π_{l=1..d} (M+l)   (P:
 enum { KIND_CELLVAR = 0, KIND_ROWBLK = 1 };
 // NG: 8 groups of ≤3 rows for ℳ = 20 (8 warps for a tile of 32 cells; 4 groups of ≤5
 // rows with 4 warps measured slower on C4: 43.5 vs 41.2 ms), else 4 groups
-CWR_HD constexpr int rb_ng(int R, int V) { return (void)V, R > 14 ? 8 : 4; }
+#ifndef CWR_RB_NG20
+#define CWR_RB_NG20 7  // 7 groups of <= 3 rows: 21 slots for 19 rows (8 groups: 24)
+#endif
+CWR_HD constexpr int rb_ng(int R, int V) { return (void)V, R > 14 ? CWR_RB_NG20 : 4; }
 CWR_HD constexpr int rb_rb(int R, int V) { return (R + rb_ng(R, V) - 1) / rb_ng(R, V); }
 CWR_HD constexpr int rb_nfull(int R, int V) { return R - (rb_rb(R, V) - 1) * rb_ng(R, V); }
 CWR_HD constexpr int rb_ngr(int R, int V, int r) { return r < rb_rb(R, V) - 1 ? rb_ng(R, V) : rb_nfull(R, V); }
@@ -145,26 +148,35 @@ inline int64_t pipe_budget(int nm, int max_smem) {
 // umax_for(T): the largest per-tile stencil union for tiles of T cells.
 Layout make_layout(int d, int M, int V, int G, int max_smem, const std::function<int(int)>& umax_for,
                    int family = -1);
-// k_rowblk: consumer threads per CTA, and whether an instantiation exists for (d, M, V)
-// main-loop threads of a row-block CTA (8 warps: T = 256 / NG cells × NG row groups)
-CWR_HD constexpr int rb_main(int R, int V) { return (R > 14 && rb_ng(R, V) == 4) ? 128 : 256; }
-// consumer threads for T cells: the main-loop threads plus, when V > NG, extra warps
-// that only join the union gather and the per-(cell, variable) epilogue, so its T·V
-// items take one round (C4: 288 items on 9 warps instead of two rounds on 8; C3 with
-// the row-block kernel 1.37 → 1.19 ms), as long as the CTA stays at ≤ 10 consumer warps
-CWR_HD constexpr int rb_extra(int R, int V, int T) {
-  return V > rb_ng(R, V) ? ((T * (V - rb_ng(R, V)) + 31) / 32) * 32 : 0;
-}
-CWR_HD constexpr int rb_cons_for(int R, int V, int T) {  // at most 10 consumer warps
-  return T * rb_ng(R, V) + (T * rb_ng(R, V) + rb_extra(R, V, T) <= 320 ? rb_extra(R, V, T) : 0);
-}
-CWR_HD constexpr int rb_consumers(int R, int V) { return rb_cons_for(R, V, rb_main(R, V) / rb_ng(R, V)); }
+// k_rowblk (warp-specialised, rowblk.cuh): a CTA of kRbThreads threads = main warps
+// (T = kRbMainThreads / NG cells × NG row groups, rounded up to whole warps), kRbEW
+// epilogue warps and one producer warp; one CTA per SM.
+#ifndef CWR_RB_EW
+#define CWR_RB_EW 4
+#endif
+#ifndef CWR_RB_MAIN
+#define CWR_RB_MAIN 224  // 7 main warps; C4-shape proxy: 224/7/4 -> 0.750, 256/8/3 -> 0.695, 192/6/5 -> 0.651
+#endif
+constexpr int kRbMainThreads = CWR_RB_MAIN, kRbEW = CWR_RB_EW, kRbThreads = 32 * ((kRbMainThreads + 31) / 32 + kRbEW + 1);
+CWR_HD constexpr int rb_main(int R, int V) { return (void)R, (void)V, kRbMainThreads; }
+CWR_HD constexpr int rb_main_warps(int T, int NG) { return (T * NG + 31) / 32; }
 // default family choice: the row-block kernel where the cell-variable kernel is
 // bound by its shared-memory broadcasts (ℳ = 20 and V ≥ 7: C4); measured slower
 // elsewhere (C2 0.25 vs 0.17 ms, C3 1.34 vs 1.09, C5 13.0 vs 12.0)
 CWR_HD constexpr bool rb_default(int R, int V) { return R > 14 && V >= 7; }
-constexpr int kRbKC = 4;  // positions per streamed chunk of the row-block layout (2 pairs)
+#ifndef CWR_RB_KC
+#define CWR_RB_KC 4
+#endif
+constexpr int kRbKC = CWR_RB_KC;  // positions per streamed chunk of the row-block layout (2 pairs)
 constexpr int kRbMaxStages = 32;  // row-block stage ring: as deep as shared memory allows
+// shared memory of a row-block CTA with S ring stages: ring (position chunks),
+// 3 union-chunk buffers, 2 sector-chunk buffers, Q_u[2][Umax][VP], O[T][V][ℳ], barriers
+inline int64_t rb_ubuf_bytes(const Layout& L) { return round128(L.u_bytes); }
+inline int64_t rb_sbuf_bytes(const Layout& L) { return round128(int64_t(L.NSC) * L.sector_bytes); }
+inline int64_t rb_smem(const Layout& L, int S) {
+  return int64_t(S) * round128(L.chunk_bytes) + 3 * rb_ubuf_bytes(L) + 2 * rb_sbuf_bytes(L) +
+         round128(2 * int64_t(L.Umax) * L.VP * 8) + round128(int64_t(L.T) * L.V * L.nm * 8) + 8 * (2 * S + 12);
+}
 bool rowblk_supported(int d, int M, int V);
 // CTAs per SM (≤ max_ctas, by shared memory) and stage-ring depth of a ROWBLK
 // layout (0 CTAs: does not fit)

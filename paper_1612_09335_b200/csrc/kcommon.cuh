@@ -269,7 +269,10 @@ struct PipeCfg {
   int stages;
   int64_t stage_bytes, q_bytes, out_bytes;
   int64_t off_stage, off_q, off_out, off_bar, smem;
-  int ncw;  // consumer warps
+  int ncw;  // consumer warps (k_rowblk: main warps)
+  // k_rowblk only: epilogue warps, union / sector chunk buffers
+  int eww;
+  int64_t off_ubuf, off_sbuf, ubuf_bytes, sbuf_bytes;
 };
 
 using PipeFn = void (*)(KArgs, PipeCfg);

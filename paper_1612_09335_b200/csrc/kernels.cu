@@ -471,34 +471,34 @@ static PipeCfg pipe_cfg(const cwreco_ctx* c, int* ctas = nullptr) {
     return c->dev->cfg;
   }
   const Layout& L = c->lay;
-  PipeCfg p;
+  PipeCfg p{};
   p.stage_bytes = pipe_stage_bytes(L);
   p.q_bytes = pipe_q_bytes(L);
   p.out_bytes = pipe_out_bytes(L);
   if (L.kind == KIND_ROWBLK) {
-    // as many CTAs/SM as shared memory AND registers allow (occupancy API), then
-    // the deepest stage ring that fits
+    // warp-specialised row-block kernel: one CTA per SM, the deepest stage ring that fits
     int k = 0, st = 0;
-    const PipeFn f = rowblk_fn(c);
-    const int nthr = rb_cons_for(L.R, L.V, L.T) + 32;
-    for (int want = kcap ? std::max(1, std::min(3, std::atoi(kcap))) : 3; want >= 1; --want) {
-      rowblk_plan(L, c->dev->max_smem, want, k, st);
-      if (k < want) continue;
-      int occ = 0;
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)f, nthr, (size_t)pipe_smem(L, st)));
-      if (occ >= want) break;
-      k = 0;
-    }
+    rowblk_plan(L, c->dev->max_smem, 1, k, st);
     if (cap) st = std::max(kMinStages, std::min(st, std::atoi(cap)));
     if (!k) fail(CWRECO_EUNSUPPORTED, "row-block kernel: tile does not fit in shared memory");
-    if (ctas) *ctas = k;
-    p.ncw = rb_cons_for(L.R, L.V, L.T) / 32;
+    if (ctas) *ctas = 1;
+    p.ncw = rb_main_warps(L.T, rb_ng(L.R, L.V));
+    p.eww = kRbEW;
     p.stages = st;
+    p.stage_bytes = round128(L.chunk_bytes);
+    p.ubuf_bytes = rb_ubuf_bytes(L);
+    p.sbuf_bytes = rb_sbuf_bytes(L);
+    p.q_bytes = round128(2 * int64_t(L.Umax) * L.VP * 8);
+    p.out_bytes = round128(int64_t(L.T) * L.V * L.nm * 8);
     p.off_stage = 0;
-    p.off_q = st * p.stage_bytes;
+    p.off_ubuf = st * p.stage_bytes;
+    p.off_sbuf = p.off_ubuf + 3 * p.ubuf_bytes;
+    p.off_q = p.off_sbuf + 2 * p.sbuf_bytes;
     p.off_out = p.off_q + p.q_bytes;
     p.off_bar = p.off_out + p.out_bytes;
-    p.smem = p.off_bar + 16 * st;
+    p.smem = p.off_bar + 8 * (2 * st + 12);
+    if (p.smem != rb_smem(L, st)) fail(CWRECO_EUNSUPPORTED, "row-block kernel: shared-memory model mismatch");
+    (void)kcap;
     return p;
   }
   if (ctas) *ctas = ctas_per_sm(c->nm);
@@ -617,7 +617,7 @@ static void launch_range(cwreco_ctx* c, const double* avgs, int64_t acs, int64_t
     const int64_t ntiles = a.tile_end - a.tile_begin;
     int64_t grid = std::min<int64_t>(ntiles, (int64_t)c->dev->num_sms * per_sm);
     if (c->max_ctas > 0) grid = std::min<int64_t>(grid, c->max_ctas);  // CWRECO_OPT_MAX_CTAS
-    dim3 b((p.ncw + 1) * 32), g((unsigned)grid);
+    dim3 b((p.ncw + (c->lay.kind == KIND_ROWBLK ? p.eww : 0) + 1) * 32), g((unsigned)grid);
     PipeFn f = c->lay.kind == KIND_ROWBLK ? rowblk_fn(c) : pipe_fn(c->d, c->M, c->lay.KC);
     f<<<g, b, p.smem, st>>>(a, p);
   }

@@ -54,20 +54,16 @@ static Layout layout_with(int d, int M, int V, int G, int T, int KC, int Umax, i
 }
 
 void rowblk_plan(const Layout& L, int max_smem, int max_ctas, int& ctas, int& stages) {
-  // per-SM shared memory = per-block opt-in + the 1 KB the driver reserves per block
-  const int64_t per_sm = int64_t(max_smem) + 1024;
+  // one warp-specialised CTA per SM: the deepest stage ring that fits
+  (void)max_ctas;
   ctas = 0;
   stages = 0;
-  for (int k = max_ctas; k >= 1; --k) {
-    const int64_t budget = std::min<int64_t>(max_smem, per_sm / k - 1024);
-    // every sector piece of a tile is held at once: the ring needs NSC + 1 stages
-    for (int s = kRbMaxStages; s >= std::max(kMinStages, L.NSC + 1); --s)
-      if (pipe_smem(L, s) <= budget) {
-        ctas = k;
-        stages = s;
-        return;
-      }
-  }
+  for (int s = kRbMaxStages; s >= kMinStages; --s)
+    if (rb_smem(L, s) <= max_smem) {
+      ctas = 1;
+      stages = s;
+      return;
+    }
 }
 
 Layout make_layout(int d, int M, int V, int G, int max_smem, const std::function<int(int)>& umax_for,
@@ -80,13 +76,9 @@ Layout make_layout(int d, int M, int V, int G, int max_smem, const std::function
     // k_rowblk: T = consumers / NG cells per tile (halved while the CTA does not fit);
     // KC positions per chunk: ~10 KB of B⁺ per stage, KC ∈ {1, 2, 4} (compiled sizes)
     const int R = nm - 1;
-    for (int T = rb_main(R, V) / rb_ng(R, V); T >= 32 / rb_ng(R, V); T /= 2) {
-      Layout L0 = layout_with(d, M, V, G, T, kRbKC, umax_for(T), KIND_ROWBLK);
-      // sector data in pieces no larger than a position chunk or the union chunk
-      const int64_t stage = std::max(L0.chunk_bytes, L0.u_bytes);
-      int nsc = 1;
-      while (nsc < T && r16(int64_t((T + nsc - 1) / nsc) * (L0.srec * 8 + 1)) > stage) ++nsc;
-      Layout L = layout_with(d, M, V, G, T, kRbKC, L0.Umax, KIND_ROWBLK, nsc);
+    for (int T = rb_main(R, V) / rb_ng(R, V); T >= 2; T /= 2) {
+      // the whole sector chunk of a tile goes to its own buffer: one piece
+      Layout L = layout_with(d, M, V, G, T, kRbKC, umax_for(T), KIND_ROWBLK, 1);
       int ctas, stages;
       rowblk_plan(L, max_smem, 1, ctas, stages);
       if (ctas > 0) return L;

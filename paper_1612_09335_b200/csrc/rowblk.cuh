@@ -1,29 +1,29 @@
 // k_rowblk: the row-block CWENO reconstruction kernel (sm_100a), for ℳ ≥ 10.
 //
 // The central LSQ apply is, per cell, the small product
-//     p̂_opt[1..R][v] = B⁺[R][G] · ΔQ[G][V]      (R = ℳ−1 reduced rows, G positions).
-// k_pipelined gives every (cell, variable) its own thread, so each B⁺ element is
-// read from shared memory by V lanes (a broadcast that still costs a full
-// wavefront per quarter-warp: ncu counts ~4 wavefronts per LDS.128, and the
-// shared-memory pipe saturates at ~83 % on C4).  Here a thread owns one cell and
-// a group of RB rows for ALL V variables: each B⁺ element is loaded once and used
-// V times from registers, and only the V averages of a position are broadcast
-// (NG threads per cell).  Shared-memory wavefronts per cell and position drop
-// from V·(R+1)·8/128 to (R + NG·V)·8/128 (C4: 11.3 → 3.4).
+//     p̂_opt[1..R][v] = B⁺[R][G] · Q[G][V]      (R = ℳ−1 reduced rows, G positions).
+// A thread owns one cell and a group of RB rows for ALL V variables: each B⁺
+// element is loaded from shared memory once and used V times from registers;
+// only the V averages of a position are broadcast to the NG threads of the cell.
 //
-// Pipeline (persistent, warp-specialised, as k_pipelined):
-//  - producer warp (one elected lane): per tile, the union chunk of the CTA's
-//    NEXT tile, then the position chunks, then the sector chunk, into a ring of S
-//    stages with 1-D TMA bulk copies completing on mbarrier transaction counts;
-//  - consumers (T cells × NG row groups): at tile start they cp.async the V
-//    averages of every cell of the next tile's stencil union into the other half
-//    of a double-buffered Q_u[2][Umax][VP]; per position: acc[r][v] +=
-//    B⁺[row r][p]·Q_u[idx][v] for the thread's rows and all V (B⁺ΔQ = B⁺Q − rs·Q_i
-//    is completed in the epilogue with the stored row sums rs); after the
-//    last chunk the row groups write p̂_opt into the tile's output rows
-//    O[T][V][ℳ] (slots 1..R), and one thread per (cell, variable) runs the fused
-//    sector / P0 / σ / ω / blend epilogue in place (reading its sector ΔQ back
-//    from Q_u) — the tile's output block is then written with one bulk store.
+// Warp specialisation (persistent, one CTA per SM), three roles:
+//  - producer warp (one elected lane): streams, with 1-D TMA bulk copies completing
+//    on mbarrier transaction counts, per tile t_k of the CTA: its position chunks
+//    into a ring of S stages; the union chunk of t_{k+2} (stencil-union cell ids +
+//    position → union offsets) into one of 3 union buffers; the sector chunk of
+//    t_{k+1} (sector inverses, B⁺ row sums, validity) into one of 2 sector buffers.
+//  - main warps (T cells × NG row groups): per tile, wait for the tile's gathered
+//    averages Q_u[k%2], run the B⁺·Q main loop over the ring (software-pipelined
+//    over position pairs), then hand the p̂_opt rows to the epilogue warps through
+//    the output block O[T][V][ℳ] (named barriers OFREE / OFULL) and go straight on
+//    to the next tile.
+//  - epilogue warps: per tile, one thread per (cell, variable) runs the fused
+//    sector / P0 / σ / ω / blend epilogue in place in O, one bulk store
+//    writes the tile's rows, the buffers of the tile are released, and the stencil
+//    averages of tile t_{k+2} are gathered into Q_u[k%2] with cp.async (completion
+//    on an mbarrier) — all of it while the main warps stream tile t_{k+1}.
+// So the epilogue and the gather no longer serialise with the B⁺ stream (round 1:
+// one thread set did both, and the stream stalled during every epilogue).
 // Arithmetic per (cell, variable) and its order are those of k_simple (bitwise
 // identical results, tested).
 #pragma once
@@ -31,10 +31,35 @@
 
 namespace cwr {
 
-constexpr int KC = kRbKC;                       // positions per chunk (compile time)
+constexpr int KC = kRbKC;  // positions per chunk (compile time)
+
+// Timeline probes of CTA 0 (tuning builds with -DCWR_TRACE only; tools/c4_iter.py --trace)
+#ifdef CWR_TRACE
+static __device__ long long g_rb_trace[64][16];
+#define RB_TRACE(k, slot)                                              \
+  do {                                                                 \
+    if (blockIdx.x == 0 && (k) < 64) g_rb_trace[k][slot] = clock64(); \
+  } while (0)
+#else
+#define RB_TRACE(k, slot) \
+  do {                    \
+  } while (0)
+#endif
+constexpr int RB_BAR_OFULL = 1, RB_BAR_OFREE = 2, RB_BAR_EW = 3;
+#ifndef CWR_RB_PAIR
+#define CWR_RB_PAIR 0  // epilogue items computed two at a time (measured slower: registers)
+#endif
+
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void named_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 
 template <int D, int M, int V>
-__global__ void __launch_bounds__(rb_consumers(nmodes(M, D) - 1, V) + 32, 1) k_rowblk(KArgs a, PipeCfg pc) {
+__global__ void __launch_bounds__(kRbThreads, 1) k_rowblk(KArgs a, PipeCfg pc) {
   constexpr int NM = nmodes(M, D), R = NM - 1, NV = D + 1, NCAP = NV * D;
   constexpr int NG = rb_ng(R, V), RB = rb_rb(R, V), NF = rb_nfull(R, V);
   constexpr int VP = V + (V & 1);
@@ -42,229 +67,247 @@ __global__ void __launch_bounds__(rb_consumers(nmodes(M, D) - 1, V) + 32, 1) k_r
   unsigned char* stg = smem + pc.off_stage;
   double* O = (double*)(smem + pc.off_out);  // [T][V][ℳ] output rows of the tile
   double* Qu = (double*)(smem + pc.off_q);   // [2][Umax][VP] gathered averages
-  uint16_t* Ix = (uint16_t*)(smem + pc.off_q + ((2 * (int64_t)a.Umax * VP * 8 + 127) & ~int64_t(127)));  // [2][G][T]
+  unsigned char* ubuf = smem + pc.off_ubuf;  // [3] union chunks (uid int32[Umax] | idx)
+  unsigned char* sbuf = smem + pc.off_sbuf;  // [2] sector chunks
   uint64_t* bars = (uint64_t*)(smem + pc.off_bar);
   const int S = pc.stages;
-  uint64_t* full = bars;       // [S]
-  uint64_t* empty = bars + S;  // [S]
+  uint64_t* full = bars;        // [S] ring
+  uint64_t* empty = bars + S;   // [S]
+  uint64_t* ufull = bars + 2 * S;   // [3]
+  uint64_t* uempty = ufull + 3;     // [3]
+  uint64_t* sfull = uempty + 3;     // [2]
+  uint64_t* sempty = sfull + 2;     // [2]
+  uint64_t* qfull = sempty + 2;     // [2] gather of Q_u[b] complete
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int T = a.T;
-  const int64_t t0 = a.tile_begin + blockIdx.x;  // this CTA's tiles: t0, t0 + grid, …
+  const int MW = pc.ncw * 32, EW = pc.eww * 32, NB = MW + EW;  // main / epilogue threads
+  const int64_t t0 = a.tile_begin + blockIdx.x;                 // this CTA's tiles: t0 + k·grid
+  const int nk = t0 < a.tile_end ? int((a.tile_end - 1 - t0) / gridDim.x + 1) : 0;
+  auto tile_of = [&](int k) { return t0 + int64_t(k) * gridDim.x; };
 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], pc.ncw);
     }
+    for (int s = 0; s < 3; ++s) {
+      mbar_init(&ufull[s], 1);
+      mbar_init(&uempty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&sfull[s], 1);
+      mbar_init(&sempty[s], 1);
+      mbar_init(&qfull[s], EW);
+    }
     fence_barrier_init();
   }
   __syncthreads();
 
-  if (warp == pc.ncw) {
+  if (warp == pc.ncw + pc.eww) {
     // ------------------------------------------------ TMA producer
     if (lane == 0) {
       Ring rg;
-      auto issue = [&](const unsigned char* src, uint32_t bytes) {
-        mbar_wait_sleep(&empty[rg.st], rg.ph ^ 1);
-        mbar_expect_tx(&full[rg.st], bytes);
-        bulk_g2s(stg + rg.st * pc.stage_bytes, src, bytes, &full[rg.st]);
-        rg.next(S);
+      auto load_union = [&](int k) {  // union chunk of tile k → ubuf[k%3]
+        const int s = k % 3;
+        mbar_wait_sleep(&uempty[s], ((k / 3) & 1) ^ 1);
+        mbar_expect_tx(&ufull[s], (uint32_t)a.u_bytes);
+        bulk_g2s(ubuf + s * pc.ubuf_bytes, a.blocks + tile_of(k) * a.tile_bytes, (uint32_t)a.u_bytes, &ufull[s]);
       };
-      if (t0 < a.tile_end) issue(a.blocks + t0 * a.tile_bytes, (uint32_t)a.u_bytes);
-      for (int64_t tile = t0; tile < a.tile_end; tile += gridDim.x) {
-        const unsigned char* tb = a.blocks + tile * a.tile_bytes;
-        if (tile + gridDim.x < a.tile_end) issue(tb + gridDim.x * a.tile_bytes, (uint32_t)a.u_bytes);
-        for (int ch = 0; ch < a.NCH; ++ch)
-          issue(tb + a.u_bytes + ch * a.chunk_bytes, (uint32_t)(min(a.KC, a.G - ch * a.KC) * a.kslice_bytes));
-        for (int j = 0; j < a.NSC; ++j) issue(tb + a.off_sector + j * a.sector_bytes, (uint32_t)a.sector_bytes);
+      auto load_sector = [&](int k) {  // all sector pieces of tile k → sbuf[k%2]
+        const int s = k & 1;
+        const uint32_t bytes = (uint32_t)(a.NSC * a.sector_bytes);
+        mbar_wait_sleep(&sempty[s], ((k >> 1) & 1) ^ 1);
+        mbar_expect_tx(&sfull[s], bytes);
+        bulk_g2s(sbuf + s * pc.sbuf_bytes, a.blocks + tile_of(k) * a.tile_bytes + a.off_sector, bytes, &sfull[s]);
+      };
+      for (int k = 0; k < nk && k < 2; ++k) load_union(k);
+      if (nk > 0) load_sector(0);
+      for (int k = 0; k < nk; ++k) {
+        RB_TRACE(k, 9);
+        const unsigned char* tb = a.blocks + tile_of(k) * a.tile_bytes;
+        for (int ch = 0; ch < a.NCH; ++ch) {
+          mbar_wait_sleep(&empty[rg.st], rg.ph ^ 1);
+          const uint32_t bytes = (uint32_t)(min(a.KC, a.G - ch * a.KC) * a.kslice_bytes);
+          mbar_expect_tx(&full[rg.st], bytes);
+          bulk_g2s(stg + rg.st * pc.stage_bytes, tb + a.u_bytes + ch * a.chunk_bytes, bytes, &full[rg.st]);
+          rg.next(S);
+        }
+        RB_TRACE(k, 10);
+        if (k + 2 < nk) load_union(k + 2);
+        RB_TRACE(k, 11);
+        if (k + 1 < nk) load_sector(k + 1);
+        RB_TRACE(k, 12);
       }
     }
     return;
   }
 
-  // -------------------------------------------------- consumer warps
-  const int nct = pc.ncw * 32;  // T·NG main-loop threads (+ epilogue-only warps, rb_cons_for)
-  const bool mainthr = tid < T * NG;
-  const int ct = mainthr ? tid / NG : 0, g = mainthr ? tid % NG : 0;
-  // offsets of this thread's B⁺ entries inside a row slot (chunk_elem, KIND_ROWBLK):
-  // slots r < RB−1 hold all NG groups, the last one the first NF (a group without a
-  // row there reads a neighbour's entry into an accumulator that is never written out)
-  const int bfull = ct * NG + g, bpart = ct * NF + min(g, NF - 1);
-  Ring rg;
-  // gather the union of the next tile (its union chunk is the current stage) into
-  // Q_u[bufn] and copy its position → union-offset table into Ix[bufn]
-  auto gather_union = [&](int bufn) {
-    mbar_wait(&full[rg.st], rg.ph);
-    const unsigned char* ub = stg + rg.st * pc.stage_bytes;
-    const int32_t* uid = (const int32_t*)ub;
-    {
-      const uint4* src = (const uint4*)(ub + a.off_idx);
-      uint4* dsti = (uint4*)((unsigned char*)Ix + bufn * a.idx_bytes);
-      for (int i = tid; i < (int)(a.idx_bytes / 16); i += nct) dsti[i] = src[i];
-    }
-    double* dst = Qu + (size_t)bufn * a.Umax * VP;
-    if (EXP(a, 1)) {  // experiment: no gather (timing only)
-      cp_async_commit();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[rg.st]);
-      rg.next(S);
-      return;
-    }
-    // element e = u·V + vv, e = tid, tid + nct, …: (u, vv) stepped without divisions
-    int u = tid / V, vv = tid - (tid / V) * V;
-    const int du = nct / V, dv = nct - du * V;
-    for (int e = tid; e < a.Umax * V; e += nct) {
-      cp_async8(dst + u * VP + vv, a.Q + int64_t(uid[u]) * a.acs + vv * a.avs);
-      u += du;
-      vv += dv;
-      if (vv >= V) {
-        vv -= V;
-        ++u;
+  const bool is_main = warp < pc.ncw;
+  // union gather of tile k into Q_u[k%2] by the epilogue threads (cp.async, completion
+  // counted on qfull[k%2] by every epilogue thread)
+  auto gather = [&](int k, int etid) {
+    const int s = k % 3;
+    mbar_wait(&ufull[s], (k / 3) & 1);
+    const int32_t* uid = (const int32_t*)(ubuf + s * pc.ubuf_bytes);
+    double* dst = Qu + (size_t)(k & 1) * a.Umax * VP;
+    if (!EXP(a, 1)) {
+      // element e = u·V + vv, e = etid, etid + EW, …: (u, vv) stepped without divisions
+      int u = etid / V, vv = etid - (etid / V) * V;
+      const int du = EW / V, dv = EW - du * V;
+      for (int e = etid; e < a.Umax * V; e += EW) {
+        cp_async8(dst + u * VP + vv, a.Q + int64_t(uid[u]) * a.acs + vv * a.avs);
+        u += du;
+        vv += dv;
+        if (vv >= V) {
+          vv -= V;
+          ++u;
+        }
       }
     }
-    cp_async_commit();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[rg.st]);
-    rg.next(S);
+    cp_async_mbar_arrive_noinc(&qfull[k & 1]);
   };
-  auto store_tile = [&](int64_t tile) {  // one bulk store of the tile's live output rows
-    const int64_t nlive = min((int64_t)T, a.n_owned - tile * T);
-    if (nlive > 0) bulk_s2g(a.out + tile * T * (int64_t)(V * NM), O, (uint32_t)(nlive * V * NM * 8));
-  };
-  if (t0 < a.tile_end) gather_union(0);
 
-  int buf = 0;
-  int64_t prev = -1;
-  for (int64_t tile = t0; tile < a.tile_end; tile += gridDim.x, buf ^= 1) {
-    cp_async_wait<0>();
-    consumer_bar(nct);  // Q_u[buf] complete and visible; tile t−1 fully done (O written, Q_u[buf^1] free)
-    if (a.dense_out && tid == 0 && prev >= 0) store_tile(prev);
-    if (tile + gridDim.x < a.tile_end) gather_union(buf ^ 1);
-    const double* Qb = Qu + (size_t)buf * a.Umax * VP;
-    const uint16_t* ixb = (const uint16_t*)((const unsigned char*)Ix + buf * a.idx_bytes);
+  if (is_main) {
+    // -------------------------------------------------- main warps
+    const bool mainthr = tid < T * NG;
+    const int ct = mainthr ? tid / NG : 0, g = mainthr ? tid % NG : 0;
+    // offsets of this thread's B⁺ entries inside a row slot (chunk_elem, KIND_ROWBLK):
+    // slots r < RB−1 hold all NG groups, the last one the first NF (a group without a
+    // row there reads a neighbour's entry into an accumulator that is never written out)
+    const int bfull = ct * NG + g, bpart = ct * NF + min(g, NF - 1);
+    Ring rg;
+    for (int k = 0; k < nk; ++k) {
+      if (tid == 0) RB_TRACE(k, 0);
+      mbar_wait(&qfull[k & 1], (k >> 1) & 1);  // Q_u[k%2] gathered
+      mbar_wait(&ufull[k % 3], (k / 3) & 1);   // its position → union offsets
+      if (tid == 0) RB_TRACE(k, 1);
+      const double* Qb = Qu + (size_t)(k & 1) * a.Umax * VP;
+      const uint16_t* ixb = (const uint16_t*)(ubuf + (k % 3) * pc.ubuf_bytes + a.off_idx);
 
-    double acc[RB][V];
-#pragma unroll
-    for (int r = 0; r < RB; ++r)
-#pragma unroll
-      for (int v = 0; v < V; ++v) acc[r][v] = 0.0;
-    // Main loop over chunks of KC = 2 positions, software-pipelined: the averages of
-    // chunk ch+1 and the union offsets of chunk ch+2 are loaded while chunk ch's
-    // FMAs run (they do not depend on the stage ring); the B⁺ entries of chunk ch+1
-    // are loaded right after its stage arrives, before chunk ch's stage is released.
-    // Ping-pong buffers (qa/qb, ba/bb) avoid register moves.  A trailing odd
-    // position (G odd) is peeled.
-    static_assert(KC % 2 == 0, "row-block chunks hold whole position pairs");
-    constexpr int PPS = KC / 2;  // position pairs per stage
-    const int G = a.G, nfc = G / 2, npr = (G + 1) / 2;  // full pairs; pairs incl. a trailing single
-    const uint32_t* ix2 = reinterpret_cast<const uint32_t*>(ixb) + ct;  // [pair][T] offset pairs
-    auto ldq = [&](int off, double (&d)[V]) {
-      const double* q = Qb + off;
-#pragma unroll
-      for (int v = 0; v + 1 < V; v += 2) {
-        const double2 x = *reinterpret_cast<const double2*>(q + v);
-        d[v] = x.x;
-        d[v + 1] = x.y;
-      }
-      if (V & 1) d[V - 1] = q[V - 1];
-    };
-    auto ldq2 = [&](uint32_t pr, double (&d)[2][V]) {
-      ldq(int(pr & 0xffffu), d[0]);
-      ldq(int(pr >> 16), d[1]);
-    };
-    auto ldb = [&](const double* Bs, double (&b)[2][RB]) {  // Bs: the pair's first position
-#pragma unroll
-      for (int k = 0; k < 2; ++k)
-#pragma unroll
-        for (int r = 0; r < RB; ++r) b[k][r] = Bs[(k * R + r * NG) * T + (r < RB - 1 ? bfull : bpart)];
-    };
-    // B⁺Q on the raw averages (no per-lane ΔQ subtractions); B⁺ΔQ = B⁺Q − rs·Q_i is
-    // formed in the epilogue with the row sums rs of the sector record (|B⁺| rows sum
-    // to < 1 on the configs, so the cancellation costs ~1e-16·max|Q|, far inside R25)
-    auto fma_pos = [&](const double (&q)[V], const double (&b)[RB]) {
+      double acc[RB][V];
 #pragma unroll
       for (int r = 0; r < RB; ++r)
 #pragma unroll
-        for (int v = 0; v < V; ++v) acc[r][v] = __fma_rn(b[r], q[v], acc[r][v]);
-    };
-    auto stage_ptr = [&]() { return (const double*)(stg + rg.st * pc.stage_bytes); };
-    auto release = [&]() {
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[rg.st]);
-      rg.next(S);
-    };
-    if (!mainthr) {  // epilogue-only warps (warp-uniform): walk the ring, no math
-      for (int c2 = 0; c2 < a.NCH; ++c2) {
-        mbar_wait(&full[rg.st], rg.ph);
-        release();
-      }
-    } else {
-    double qa[2][V], qb[2][V], ba[2][RB], bb[2][RB];
-    ldq2(ix2[0], qa);
-    uint32_t ipn = ix2[min(1, npr - 1) * T];
-    mbar_wait(&full[rg.st], rg.ph);
-    ldb(stage_ptr(), ba);
-    // one full pair pp: q/b hold its averages and B⁺ entries; qn/bn receive pair pp+1's
-    // (from the same stage, or from the next one, which releases the current stage)
-    auto pair = [&](int pp, const double (&q)[2][V], const double (&b)[2][RB], double (&qn)[2][V],
-                    double (&bn)[2][RB]) {
-      ldq2(ipn, qn);
-      ipn = ix2[min(pp + 2, npr - 1) * T];
-      fma_pos(q[0], b[0]);
-      fma_pos(q[1], b[1]);
-      const int nx = pp + 1;
-      if (nx >= npr) {
-        release();
-      } else if (nx % PPS == 0) {  // next stage (a tail pair reads past kc into the stage: unused)
-        Ring nr = rg;
-        nr.next(S);
-        mbar_wait(&full[nr.st], nr.ph);
-        ldb((const double*)(stg + nr.st * pc.stage_bytes), bn);
-        release();
-      } else {
-        ldb(stage_ptr() + (nx % PPS) * 2 * R * T, bn);
-      }
-    };
-    int pp = 0;
-    for (; pp + 1 < nfc; pp += 2) {
-      pair(pp, qa, ba, qb, bb);
-      pair(pp + 1, qb, bb, qa, ba);
-    }
-    const bool odd_pair = pp < nfc;
-    if (odd_pair) pair(pp, qa, ba, qb, bb);
-    if (G & 1) {  // the last position alone (its stage already waited for)
-      fma_pos(odd_pair ? qb[0] : qa[0], odd_pair ? bb[0] : ba[0]);
-      release();
-    }
-    }  // main-loop threads
-
-    // (after the previous tile's bulk store has read O)
-    if (tid == 0) bulk_wait_read();
-    consumer_bar(nct);
-    const Ring rs = rg;  // the sector pieces: NSC consecutive stages
-    for (int j = 0; j < a.NSC; ++j) {
+        for (int v = 0; v < V; ++v) acc[r][v] = 0.0;
+      // Main loop over position pairs, software-pipelined: the averages of pair pp+1
+      // and the union offsets of pair pp+2 are loaded while pair pp's FMAs run; the
+      // B⁺ entries of pair pp+1 are loaded as soon as its stage arrives, before pair
+      // pp's stage is released.  Ping-pong registers (qa/qb, ba/bb).  A trailing odd
+      // position (G odd) is peeled.
+      static_assert(KC % 2 == 0, "row-block chunks hold whole position pairs");
+      constexpr int PPS = KC / 2;  // position pairs per stage
+      const int G = a.G, nfc = G / 2, npr = (G + 1) / 2;
+      const uint32_t* ix2 = reinterpret_cast<const uint32_t*>(ixb) + ct;  // [pair][T] offset pairs
+      auto ldq = [&](int off, double (&d)[V]) {
+        const double* q = Qb + off;
+#pragma unroll
+        for (int v = 0; v + 1 < V; v += 2) {
+          const double2 x = *reinterpret_cast<const double2*>(q + v);
+          d[v] = x.x;
+          d[v + 1] = x.y;
+        }
+        if (V & 1) d[V - 1] = q[V - 1];
+      };
+      auto ldq2 = [&](uint32_t pr, double (&d)[2][V]) {
+        ldq(int(pr & 0xffffu), d[0]);
+        ldq(int(pr >> 16), d[1]);
+      };
+      auto ldb = [&](const double* Bs, double (&b)[2][RB]) {  // Bs: the pair's first position
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk)
+#pragma unroll
+          for (int r = 0; r < RB; ++r) b[kk][r] = Bs[(kk * R + r * NG) * T + (r < RB - 1 ? bfull : bpart)];
+      };
+      // B⁺Q on the raw averages; B⁺ΔQ = B⁺Q − rs·Q_i is formed in the epilogue with
+      // the row sums rs of the sector record
+      auto fma_pos = [&](const double (&q)[V], const double (&b)[RB]) {
+        if (EXP(a, 2)) return;
+#pragma unroll
+        for (int r = 0; r < RB; ++r)
+#pragma unroll
+          for (int v = 0; v < V; ++v) acc[r][v] = __fma_rn(b[r], q[v], acc[r][v]);
+      };
+      auto stage_ptr = [&]() { return (const double*)(stg + rg.st * pc.stage_bytes); };
+      auto release = [&]() {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[rg.st]);
+        rg.next(S);
+      };
+      double qa[2][V], qb[2][V], ba[2][RB], bb[2][RB];
+      ldq2(ix2[0], qa);
+      uint32_t ipn = ix2[min(1, npr - 1) * T];
       mbar_wait(&full[rg.st], rg.ph);
-      rg.next(S);
-    }
-    // ---- per-item epilogue: p̂_opt rows → O[ct][v][1 + row], then one thread per
-    // (cell, variable) runs cweno_epilogue in place
-    if (mainthr) {
-      double* Oc = O + (size_t)ct * V * NM + 1 + g;  // row l = r·NG + g
+      ldb(stage_ptr(), ba);
+      auto pair = [&](int pp, const double (&q)[2][V], const double (&b)[2][RB], double (&qn)[2][V],
+                      double (&bn)[2][RB]) {
+        ldq2(ipn, qn);
+        ipn = ix2[min(pp + 2, npr - 1) * T];
+        fma_pos(q[0], b[0]);
+        fma_pos(q[1], b[1]);
+        const int nx = pp + 1;
+        if (nx >= npr) {
+          release();
+        } else if (nx % PPS == 0) {  // next stage (a tail pair reads past kc into the stage: unused)
+          Ring nr = rg;
+          nr.next(S);
+          mbar_wait(&full[nr.st], nr.ph);
+          ldb((const double*)(stg + nr.st * pc.stage_bytes), bn);
+          release();
+        } else {
+          ldb(stage_ptr() + (nx % PPS) * 2 * R * T, bn);
+        }
+      };
+      int pp = 0;
+      for (; pp + 1 < nfc; pp += 2) {
+        pair(pp, qa, ba, qb, bb);
+        pair(pp + 1, qb, bb, qa, ba);
+      }
+      const bool odd_pair = pp < nfc;
+      if (odd_pair) pair(pp, qa, ba, qb, bb);
+      if (G & 1) {  // the last position alone (its stage already waited for)
+        fma_pos(odd_pair ? qb[0] : qa[0], odd_pair ? bb[0] : ba[0]);
+        release();
+      }
+      // hand the p̂_opt rows to the epilogue warps: O[ct][v][1 + row], row l = r·NG + g
+      if (tid == 0) RB_TRACE(k, 2);
+      named_sync(RB_BAR_OFREE, NB);  // the epilogue of the previous tile is done with O
+      if (tid == 0) RB_TRACE(k, 3);
+      if (mainthr) {
+        double* Oc = O + (size_t)ct * V * NM + 1 + g;
 #pragma unroll
-      for (int r = 0; r < RB; ++r)
-        if (r < RB - 1 || g < NF)
+        for (int r = 0; r < RB; ++r)
+          if (r < RB - 1 || g < NF)
 #pragma unroll
-          for (int v = 0; v < V; ++v) Oc[v * NM + r * NG] = acc[r][v];
+            for (int v = 0; v < V; ++v) Oc[v * NM + r * NG] = acc[r][v];
+      }
+      named_arrive(RB_BAR_OFULL, NB);
     }
-    consumer_bar(nct);
-    for (int item = tid; item < (EXP(a, 16) ? 0 : T * V); item += nct) {  // flag 16: no epilogue
+    return;
+  }
+
+  // -------------------------------------------------- epilogue warps
+  const int etid = tid - MW;
+  if (nk > 0) gather(0, etid);
+  if (nk > 1) gather(1, etid);
+  if (nk > 0) named_arrive(RB_BAR_OFREE, NB);  // O starts free
+  for (int k = 0; k < nk; ++k) {
+    const int64_t tile = tile_of(k);
+    named_sync(RB_BAR_OFULL, NB);  // p̂_opt rows of tile k are in O
+    if (etid == 0) RB_TRACE(k, 4);
+    mbar_wait(&sfull[k & 1], (k >> 1) & 1);
+    if (etid == 0) RB_TRACE(k, 5);
+    const double* Qb = Qu + (size_t)(k & 1) * a.Umax * VP;
+    const uint16_t* ixb = (const uint16_t*)(ubuf + (k % 3) * pc.ubuf_bytes + a.off_idx);
+    const unsigned char* sb0 = sbuf + (k & 1) * pc.sbuf_bytes;
+    // one (cell, variable) item → its blended coefficients w (registers); two items per
+    // thread are computed before either is stored, so their dependency chains interleave
+    auto item_w = [&](int item, double (&w)[NM]) {
       const int c2 = item / V, v2 = item - (item / V) * V;
       const int j = c2 / a.TSC, cl = c2 - j * a.TSC;
-      const int sst = rs.st + j < S ? rs.st + j : rs.st + j - S;
-      const unsigned char* sb = stg + sst * pc.stage_bytes;
+      const unsigned char* sb = sb0 + j * a.sector_bytes;
       const double q2 = Qb[c2 * VP + v2];
-      double* row = O + (size_t)item * NM;
+      const double* row = O + (size_t)item * NM;
       const double* srec = (const double*)sb + size_t(cl) * a.srec;  // sector inverses, then rs
       double accr[R];
 #pragma unroll
@@ -278,11 +321,15 @@ __global__ void __launch_bounds__(rb_consumers(nmodes(M, D) - 1, V) + 32, 1) k_r
       for (int q = 0; q < NV; ++q) valid[q] = (vmask >> q) & 1;
       double ps[NV][D];
       sector_apply<D>(srec, dqs, ps);
+      cweno_epilogue<D, NM>(q2, accr, ps, valid, a, w, nullptr, nullptr);
+    };
+    auto item_store = [&](int item, const double (&w)[NM]) {
       if (a.dense_out) {
-        cweno_epilogue<D, NM>(q2, accr, ps, valid, a, row, nullptr, nullptr);
+        double* row = O + (size_t)item * NM;
+#pragma unroll
+        for (int l = 0; l < NM; ++l) row[l] = w[l];
       } else {
-        double w[NM];
-        cweno_epilogue<D, NM>(q2, accr, ps, valid, a, w, nullptr, nullptr);
+        const int c2 = item / V, v2 = item - (item / V) * V;
         const int64_t c = tile * T + c2;
         if (c < a.n_owned) {
           double* o = a.out + c * a.ccs + v2 * a.cvs;
@@ -290,23 +337,42 @@ __global__ void __launch_bounds__(rb_consumers(nmodes(M, D) - 1, V) + 32, 1) k_r
           for (int l = 0; l < NM; ++l) o[l] = w[l];
         }
       }
+    };
+    const int n_items = EXP(a, 16) ? 0 : T * V;  // flag 16: no epilogue
+#if CWR_RB_PAIR
+    for (int i0 = etid; i0 < n_items; i0 += 2 * EW) {
+      const int i1 = i0 + EW < n_items ? i0 + EW : i0;
+      double w0[NM], w1[NM];
+      item_w(i0, w0);
+      item_w(i1, w1);
+      item_store(i0, w0);
+      if (i1 != i0) item_store(i1, w1);
     }
-    __syncwarp();
-    if (lane == 0) {
-      int sst = rs.st;
-      for (int j = 0; j < a.NSC; ++j) {
-        mbar_arrive(&empty[sst]);
-        if (++sst == S) sst = 0;
-      }
+#else
+    for (int i0 = etid; i0 < n_items; i0 += EW) {
+      double w0[NM];
+      item_w(i0, w0);
+      item_store(i0, w0);
     }
-    if (a.dense_out) fence_proxy_async();  // O rows → visible to the bulk store after the next barrier
-    prev = tile;
+#endif
+    named_sync(RB_BAR_EW, EW);  // every item of the tile is done; Q_u[k%2] no longer read
+    if (etid == 0) RB_TRACE(k, 6);
+    if (etid == 0 && a.dense_out) {
+      fence_proxy_async();  // O rows → visible to the bulk store
+      const int64_t nlive = min((int64_t)T, a.n_owned - tile * T);
+      if (nlive > 0) bulk_s2g(a.out + tile * T * (int64_t)(V * NM), O, (uint32_t)(nlive * V * NM * 8));
+    }
+    if (k + 2 < nk) gather(k + 2, etid);  // Q_u[k%2] is free: main warps are past tile k
+    if (etid == 0) RB_TRACE(k, 7);
+    if (etid == 0) {
+      if (a.dense_out) bulk_wait_read();  // O may be overwritten once the store has read it
+      mbar_arrive(&sempty[k & 1]);
+      mbar_arrive(&uempty[k % 3]);
+    }
+    if (etid == 0) RB_TRACE(k, 8);
+    if (k + 1 < nk) named_arrive(RB_BAR_OFREE, NB);  // (completes only once etid 0 has arrived)
   }
-  consumer_bar(nct);
-  if (a.dense_out && tid == 0 && prev >= 0) {
-    store_tile(prev);
-    bulk_wait_all();
-  }
+  if (etid == 0) bulk_wait_all();
   cp_async_wait<0>();
 }
 

@@ -14,3 +14,9 @@ cudaError_t rowblk_upload_sigma_3d(const double* packed, size_t bytes, size_t of
 }
 
 }  // namespace cwr
+
+#ifdef CWR_TRACE
+extern "C" int cwreco_debug_rb_trace(long long* out) {  // tuning builds only: [64][16] clock64 stamps of CTA 0
+  return (int)cudaMemcpyFromSymbol(out, cwr::g_rb_trace, sizeof(cwr::g_rb_trace));
+}
+#endif

@@ -325,6 +325,35 @@ cwreco_status cwreco_face_neighbors(const cwreco_ctx* ctx, int64_t* nbr);
 cwreco_status cwreco_face_traces(cwreco_ctx* ctx, const double* d_coeffs, int64_t c_cell_stride,
                                  int64_t c_var_stride, double* d_traces, cwreco_stream stream);
 
+/* ---------------------------------------------------------------- space-time predictor (NEXT-2) */
+/* The element-local space-time Galerkin predictor of the ADER scheme (paper §2.2,
+ * P:235-320), Eulerian (fixed mesh), compressible Euler equations (nvars = dim + 2:
+ * ρ, ρu_1..ρu_dim, E; p = (γ−1)(E − ½ρ|u|²)).  Per owned cell the
+ * reconstruction polynomial w is evolved into a space-time polynomial of degree M,
+ * q_h = Σ_l θ_l(ξ, τ) q̂_l on T_E × [0,1] (τ = (t − tⁿ)/Δt), with nodal basis θ_l on
+ * the uniform lattice of the (dim+1)-simplex (R32), by the Picard iteration of Eq.
+ * CGfinal with the test functions of the unknown τ > 0 nodes (R33), the
+ * nodal flux interpolant of Eq. PDEterm (R34), from q̂_l = w(ξ_l), until
+ * max|Δq̂| ≤ 1e-12·max(1, max|q̂⁰|) or 2(M+1) iterations (R35).  No neighbour data.
+ *
+ * Setup (after the stencils: local numbering): the universal space-time matrices
+ * (K_τ, M of Eq. cgPDE, by quadrature) to the constant bank, the owned cells'
+ * inverse Jacobians to the device.  gamma > 1 (1.4: P:754).  ESTATE before the
+ * stencils; EUNSUPPORTED unless nvars = dim + 2 and M ≤ 3; ECUDA host-only. */
+cwreco_status cwreco_predictor_setup(cwreco_ctx* ctx, double gamma);
+/* *n_nodes = 𝓛 = ℳ(M, dim+1), *n_known = ℳ(M, dim) (the τ = 0 nodes, first);
+ * nodes [𝓛][dim+1] (may be NULL): (ξ_1..ξ_dim, τ) of each node in output order
+ * (known nodes first, then by τ level, then by the lattice tuple). */
+cwreco_status cwreco_predictor_nodes(const cwreco_ctx* ctx, int* n_nodes, int* n_known, double* nodes);
+/* d_coeffs: the reconstruction of the owned cells, (c, v, l) at
+ * d_coeffs[c·c_cell_stride + v·c_var_stride + l] (cwreco_reconstruct's output);
+ * dt ≥ 0 the time step; d_qhat [n_owned][𝓛][nvars] dense ← the nodal space-time
+ * degrees of freedom; d_iters [n_owned] (may be NULL) ← Picard iterations per cell,
+ * or −(iterations + 1) if the cell did not converge or met ρ ≤ 0 / p ≤ 0 at a node.
+ * Asynchronous on `stream`.  ESTATE before cwreco_predictor_setup. */
+cwreco_status cwreco_predict(cwreco_ctx* ctx, const double* d_coeffs, int64_t c_cell_stride, int64_t c_var_stride,
+                             double dt, double* d_qhat, int32_t* d_iters, cwreco_stream stream);
+
 /* Debug tap (tests): intermediates of n_sel owned cells (local ids), computed by
  * the SIMPLE kernel and copied to host (synchronises `stream`):
  *   popt [n][nvars][ℳ], psec [n][dim+1][nvars][dim+1], sigma [n][dim+2][nvars],

@@ -90,6 +90,9 @@ def _load():
         "cwreco_reconstruct": [P, P, I64, I64, P, I64, I64, I32, P],
         "cwreco_reconstruct_debug": [P, P, I64, I64, I64, P, P, P, P, P, P, P],
         "cwreco_reconstruct_host": [P, P, P, I32, P],
+        "cwreco_predictor_setup": [P, D],
+        "cwreco_predictor_nodes": [P, P, P, P],
+        "cwreco_predict": [P, P, I64, I64, D, P, P, P],
     }
     for name, args in sigs.items():
         f = getattr(L, name)
@@ -422,6 +425,43 @@ class Context:
             raise ValueError("coeffs must be contiguous along the mode axis and out dense")
         _check(lib.cwreco_face_traces(self._h, ctypes.c_void_p(coeffs.data_ptr()), c_cs, c_vs,
                                       ctypes.c_void_p(out.data_ptr()), _stream_handle(stream)))
+        return out
+
+    # ---------------------------------------------------------------- predictor (NEXT-2)
+    def predictor_setup(self, gamma=1.4):
+        """cwreco_predictor_setup: Euler (nvars = dim + 2), after build_stencils."""
+        _check(lib.cwreco_predictor_setup(self._h, float(gamma)))
+
+    def predictor_nodes(self):
+        """(nodes [𝓛][dim+1] (ξ, τ) in output order, number of known τ = 0 nodes)."""
+        n, k = ctypes.c_int(), ctypes.c_int()
+        _check(lib.cwreco_predictor_nodes(self._h, ctypes.byref(n), ctypes.byref(k), None))
+        nodes = np.empty((n.value, self.dim + 1))
+        _check(lib.cwreco_predictor_nodes(self._h, ctypes.byref(n), ctypes.byref(k), _ptr(nodes)))
+        return nodes, k.value
+
+    def predict(self, coeffs, dt, out=None, iters=None, stream=None):
+        """cwreco_predict: coeffs CUDA [n_owned, V, ℳ] (mode axis contiguous) → out
+        [n_owned, 𝓛, V] nodal space-time DOFs; iters (optional int32 [n_owned])."""
+        import torch
+        n_owned = self.info()["n_owned"]
+        if not (coeffs.is_cuda and coeffs.dtype == torch.float64 and coeffs.dim() == 3):
+            raise ValueError("coeffs must be a 3-D float64 CUDA tensor")
+        if coeffs.shape[0] < n_owned or tuple(coeffs.shape[1:]) != (self.V, self.nm) or coeffs.stride(2) != 1:
+            raise ValueError(f"coeffs must be (>= {n_owned}, {self.V}, {self.nm}) with contiguous modes")
+        L = self.predictor_nodes()[0].shape[0]
+        if out is None:
+            out = torch.empty((n_owned, L, self.V), dtype=torch.float64, device=coeffs.device)
+        if not (out.is_cuda and out.dtype == torch.float64 and out.is_contiguous()):
+            raise ValueError("out must be a dense float64 CUDA tensor")
+        self._need_shape(out, (n_owned, L, self.V), "out")
+        if iters is not None and (iters.dtype != torch.int32 or tuple(iters.shape) != (n_owned,)):
+            raise ValueError("iters must be int32 [n_owned]")
+        c_cs, c_vs, _ = coeffs.stride()
+        _check(lib.cwreco_predict(self._h, ctypes.c_void_p(coeffs.data_ptr()), c_cs, c_vs, float(dt),
+                                  ctypes.c_void_p(out.data_ptr()),
+                                  None if iters is None else ctypes.c_void_p(iters.data_ptr()),
+                                  _stream_handle(stream)))
         return out
 
     def reconstruct_debug(self, avgs, cells, stream=None):

@@ -15,8 +15,8 @@ INC = os.path.join(ROOT, "include")
 OUT = os.path.join(HERE, "libcwreco.so")
 BUILD = os.path.join(HERE, "build")
 
-CXX_SRCS = ["api.cpp", "mesh.cpp", "stencil.cpp", "basis.cpp", "precompute.cpp"]
-CU_SRCS = ["kernels.cu", "rowblk_2d.cu", "rowblk_3d.cu", "matfree.cu", "traces.cu", "halo.cu"]
+CXX_SRCS = ["api.cpp", "mesh.cpp", "stencil.cpp", "basis.cpp", "precompute.cpp", "predictor.cpp"]
+CU_SRCS = ["kernels.cu", "rowblk_2d.cu", "rowblk_3d.cu", "matfree.cu", "traces.cu", "halo.cu", "predictor.cu"]
 CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 # -ffp-contract=off: the IEEE-specified geometry (R29) must not be fused; -mfma

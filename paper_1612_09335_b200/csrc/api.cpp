@@ -39,6 +39,7 @@ void need(bool cond, cwreco_status s, const char* msg) {
 void invalidate_derived(cwreco_ctx* c) {
   cwr::dev_traces_destroy(c);
   cwr::dev_matfree_destroy(c);
+  cwr::dev_predictor_destroy(c);
 }
 
 // Coefficient rows (c, v) → c·ccs + v·cvs + [0, ℳ) must not overlap: cell-major
@@ -104,6 +105,7 @@ void cwreco_destroy(cwreco_ctx* ctx) {
   if (!ctx) return;
   try {
     cwr::halo_destroy(ctx);
+    cwr::dev_predictor_destroy(ctx);
     cwr::dev_matfree_destroy(ctx);
     cwr::dev_traces_destroy(ctx);
     cwr::dev_destroy(ctx);
@@ -500,6 +502,47 @@ cwreco_status cwreco_reconstruct_host(cwreco_ctx* c, const double* h_avgs, doubl
       need(c->has_blocks, CWRECO_ESTATE, "reconstruct_host: call cwreco_precompute first");
     need(h_avgs && h_coeffs, CWRECO_EINVAL, "reconstruct_host: NULL buffer");
     cwr::dev_reconstruct_host(c, h_avgs, h_coeffs, n_pieces > 0 ? n_pieces : 4, stream);
+  });
+}
+
+cwreco_status cwreco_predictor_setup(cwreco_ctx* c, double gamma) {
+  return guard([&] {
+    need(c != nullptr, CWRECO_EINVAL, "predictor_setup: NULL ctx");
+    need_device(c, "predictor_setup");
+    need(c->has_stencils, CWRECO_ESTATE, "predictor_setup: call cwreco_build_stencils first (local numbering)");
+    need(c->M <= 3, CWRECO_EUNSUPPORTED, "predictor_setup: degree M must be <= 3");
+    need(c->V == c->d + 2, CWRECO_EUNSUPPORTED, "predictor_setup: the Euler system needs nvars = dim + 2");
+    need(gamma > 1.0, CWRECO_EINVAL, "predictor_setup: gamma must be > 1");
+    cwr::PredictorHost h;
+    cwr::predictor_matrices(c->d, c->M, h);
+    std::vector<double> jinv;
+    cwr::predictor_jinv(c, jinv);
+    cwr::dev_predictor_setup(c, h, jinv, gamma);
+  });
+}
+
+cwreco_status cwreco_predictor_nodes(const cwreco_ctx* c, int* n_nodes, int* n_known, double* nodes) {
+  return guard([&] {
+    need(c && n_nodes && n_known, CWRECO_EINVAL, "predictor_nodes: NULL");
+    need(c->M <= 3, CWRECO_EUNSUPPORTED, "predictor_nodes: degree M must be <= 3");
+    cwr::PredictorHost h;
+    cwr::predictor_matrices(c->d, c->M, h);
+    *n_nodes = h.L;
+    *n_known = h.nk;
+    if (nodes) std::memcpy(nodes, h.nodes.data(), sizeof(double) * h.nodes.size());
+  });
+}
+
+cwreco_status cwreco_predict(cwreco_ctx* c, const double* d_coeffs, int64_t ccs, int64_t cvs, double dt,
+                             double* d_qhat, int32_t* d_iters, cwreco_stream stream) {
+  return guard([&] {
+    need(c != nullptr, CWRECO_EINVAL, "predict: NULL ctx");
+    need_device(c, "predict");
+    need(c->pred != nullptr, CWRECO_ESTATE, "predict: call cwreco_predictor_setup first");
+    need(d_coeffs && d_qhat, CWRECO_EINVAL, "predict: NULL buffer");
+    need(ccs >= 1 && cvs >= 1, CWRECO_EINVAL, "predict: strides must be >= 1");
+    need(dt >= 0.0, CWRECO_EINVAL, "predict: dt must be >= 0");
+    cwr::dev_predict(c, d_coeffs, ccs, cvs, dt, d_qhat, d_iters, stream);
   });
 }
 

@@ -250,6 +250,7 @@ struct cwreco_ctx {
   void* mf = nullptr;  // matrix-free device state (matfree.cu), after cwreco_prepare_matrixfree
   void* tr = nullptr;  // face-trace tables (traces.cu), built on the first cwreco_face_traces
   void* halo = nullptr;  // multi-rank transport (halo.cu), after cwreco_set_partition with an id
+  void* pred = nullptr;  // space-time predictor tables (predictor.cu), after cwreco_predictor_setup
 };
 
 namespace cwr {
@@ -278,6 +279,19 @@ void dev_matfree_destroy(cwreco_ctx* c);
 void face_rule(int d, int M, std::vector<double>& lam, std::vector<double>& w);
 void dev_face_traces(cwreco_ctx* c, const double* coeffs, int64_t ccs, int64_t cvs, double* traces, void* stream);
 void dev_traces_destroy(cwreco_ctx* c);
+// predictor.cpp / predictor.cu: the local space-time Galerkin predictor (NEXT-2)
+struct PredictorHost {
+  int L = 0, nk = 0;                 // space-time nodes, known (τ = 0) nodes
+  std::vector<double> nodes;         // [L][d+1]
+  std::vector<double> A, C0, Phi;    // [d][L−nk][L], [L−nk][nk], [L][nk]
+};
+void st_nodes(int d, int M, std::vector<std::vector<int>>& nodes);
+void predictor_matrices(int d, int M, PredictorHost& h);
+void predictor_jinv(const cwreco_ctx* c, std::vector<double>& jinv);
+void dev_predictor_setup(cwreco_ctx* c, const PredictorHost& h, const std::vector<double>& jinv, double gamma);
+void dev_predictor_destroy(cwreco_ctx* c);
+void dev_predict(cwreco_ctx* c, const double* w, int64_t ccs, int64_t cvs, double dt, double* q, int32_t* iters,
+                 void* stream);
 // stencil.cpp: send lists (owned cells requested by each peer, SFC ids) → local ids
 void install_send_lists(cwreco_ctx* c, const int64_t* send_counts, const int64_t* send_ids);
 // halo.cu: multi-rank transport (NCCL or in-process loopback) and the exchange

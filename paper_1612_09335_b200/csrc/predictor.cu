@@ -1,0 +1,309 @@
+// k_predictor: the element-local space-time Galerkin predictor on sm_100a (paper
+// §2.2), Eulerian (fixed mesh), Euler equations.
+//
+// Per owned cell, from the reconstruction polynomial w (cwreco_reconstruct's
+// output, Dubiner modes) and Δt:
+//   q̂_l = w(ξ_l) at all 𝓛 space-time nodes (initial guess, R35; the τ = 0 ones
+//   stay: the known DOFs q̂⁰);
+//   Picard (Eq. CGfinal, test functions of the unknown nodes, R33):
+//       F̂_l = F(q̂_l) (Eq. PDEterm), Ĝ_b,l = Σ_a (∂ξ_b/∂x_a) F̂_a,l,
+//       q̂¹ = −Δt Σ_b A_b Ĝ_b − C0 q̂⁰      A_b = K_uu⁻¹ M_u D_b, C0 = K_uu⁻¹ K_uk
+//   until max|Δq̂¹| ≤ 1e-12·max(1, max|q̂⁰|) or 2(M+1) iterations (R35).
+// Output: q̂ [n_owned][𝓛][V] (nodes in the order of cwreco_predictor_nodes) and,
+// optionally, per cell the iteration count (negative: not converged or an
+// inadmissible state ρ ≤ 0 / p ≤ 0 met at a node).
+//
+// Layout: a CTA holds CB cells; shared memory q̂[CB][𝓛][V] and Ĝ[CB][d][𝓛][V].
+// Flux phase: one thread per (cell, node) evaluates the Euler flux and its
+// contravariant components.  Update phase: one thread per (cell, variable) forms
+// all NU = 𝓛 − ℳ unknown rows; the universal matrices A_b and C0 live in the
+// constant bank (warp-uniform operands), Ĝ is read from shared memory.  A cell
+// that has converged is frozen (its iteration count is that of the oracle).
+// fp64-ALU bound: ≈ d·NU·𝓛·V FMAs per cell and iteration.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "devguard.cuh"
+#include "kcommon.cuh"
+
+namespace cwr {
+
+#define PCK(x)                                                                                 \
+  do {                                                                                         \
+    cudaError_t e_ = (x);                                                                      \
+    if (e_ != cudaSuccess) fail(CWRECO_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+// 𝓛 = ℳ(M, d+1) space-time nodes, ℳ(M, d) of them known (τ = 0)
+__host__ __device__ constexpr int pr_L(int D, int M) {
+  return D == 2 ? (M + 1) * (M + 2) * (M + 3) / 6 : (M + 1) * (M + 2) * (M + 3) * (M + 4) / 24;
+}
+__host__ __device__ constexpr int pr_nk(int D, int M) { return nmodes(M, D); }
+__host__ __device__ constexpr int pr_len(int D, int M) {  // doubles of the (D, M) tables: A, C0, Phi
+  return D * (pr_L(D, M) - pr_nk(D, M)) * pr_L(D, M) + (pr_L(D, M) - pr_nk(D, M)) * pr_nk(D, M) +
+         pr_L(D, M) * pr_nk(D, M);
+}
+__host__ __device__ constexpr int pr_off(int D, int M) {
+  int off = 0;
+  for (int dd = 2; dd <= 3; ++dd)
+    for (int mm = 1; mm <= 3; ++mm) {
+      if (dd == D && mm == M) return off;
+      off += pr_len(dd, mm);
+    }
+  return off;
+}
+static __constant__ double c_pred[pr_off(4, 1)];
+
+struct PredArgs {
+  const double* w;     // coefficients: (c, v, m) at w[c·ccs + v·cvs + m]
+  int64_t ccs, cvs;
+  const double* jinv;  // [n_owned][d][d]  ∂ξ_b/∂x_a at [b·d + a]
+  double* q;           // [n_owned][𝓛][V]
+  int32_t* iters;      // [n_owned] or nullptr
+  int64_t n;
+  double dt, gamma, tol;
+  int maxit;
+};
+
+template <int D, int M>
+__global__ void __launch_bounds__(256) k_predictor(PredArgs p) {
+  constexpr int V = D + 2, L = pr_L(D, M), NK = pr_nk(D, M), NU = L - NK;
+  constexpr int CB = 32;  // cells per CTA
+  constexpr int OA = pr_off(D, M), OC = OA + D * NU * L, OP = OC + NU * NK;
+  extern __shared__ __align__(16) double psm[];
+  double* Q = psm;                                   // [CB][L][V]
+  double* G = Q + CB * L * V;                        // [CB][D][L][V]
+  double* Ji = G + CB * D * L * V;                   // [CB][D][D]
+  double* dl = Ji + CB * D * D;                      // [CB][V] update norms
+  double* sc = dl + CB * V;                          // [CB] scales
+  int* flag = (int*)(sc + CB);                       // [CB] 0 active, 1 converged; bit 2: inadmissible
+  int* its = flag + CB;                              // [CB]
+  const int tid = threadIdx.x, nth = blockDim.x;
+  for (int64_t c0 = int64_t(blockIdx.x) * CB; c0 < p.n; c0 += int64_t(gridDim.x) * CB) {
+    const int nc = (int)(p.n - c0 < CB ? p.n - c0 : CB);
+    // ---- initial guess q̂_l = Σ_m Φ[l][m] w_m (every node), per (cell, variable)
+    for (int it = tid; it < nc * V; it += nth) {
+      const int cl = it / V, v = it - cl * V;
+      const double* wp = p.w + (c0 + cl) * p.ccs + v * p.cvs;
+      double wm[NK];
+#pragma unroll
+      for (int m = 0; m < NK; ++m) wm[m] = wp[m];
+#pragma unroll
+      for (int l = 0; l < L; ++l) {
+        double s = 0.0;
+#pragma unroll
+        for (int m = 0; m < NK; ++m) s = __fma_rn(c_pred[OP + l * NK + m], wm[m], s);
+        Q[(cl * L + l) * V + v] = s;
+      }
+    }
+    for (int it = tid; it < nc * D * D; it += nth) Ji[it] = p.jinv[c0 * D * D + it];
+    for (int it = tid; it < CB; it += nth) {
+      flag[it] = it < nc ? 0 : 1;
+      its[it] = 0;
+    }
+    __syncthreads();
+    for (int it = tid; it < nc; it += nth) {  // scale = max(1, max|q̂⁰|)
+      double s = 1.0;
+      for (int e = 0; e < NK * V; ++e) s = fmax(s, fabs(Q[it * L * V + e]));
+      sc[it] = s;
+    }
+    // C0 q̂⁰ is fixed: kept in registers by the update threads (≤ 1 item per thread)
+    const int ui = tid;
+    const bool upd = ui < nc * V;
+    const int ucl = upd ? ui / V : 0, uv = upd ? ui - (ui / V) * V : 0;
+    double base[NU];
+    if (upd) {
+#pragma unroll
+      for (int k = 0; k < NU; ++k) {
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j < NK; ++j) s = __fma_rn(c_pred[OC + k * NK + j], Q[(ucl * L + j) * V + uv], s);
+        base[k] = -s;
+      }
+    }
+    for (int iter = 0; iter < p.maxit; ++iter) {
+      __syncthreads();
+      // ---- flux phase: (cell, node) → Ĝ_b = Σ_a Jinv[b][a] F_a(q̂)
+      for (int it = tid; it < nc * L; it += nth) {
+        const int cl = it / L, l = it - cl * L;
+        if (flag[cl] & 1) continue;
+        const double* qn = Q + (cl * L + l) * V;
+        double q[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) q[v] = qn[v];
+        const double rho = q[0], E = q[D + 1];
+        const double ir = 1.0 / rho;
+        double u[D], ke = 0.0;
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          u[a] = q[1 + a] * ir;
+          ke = __fma_rn(q[1 + a], u[a], ke);
+        }
+        const double pr = (p.gamma - 1.0) * (E - 0.5 * ke);
+        if (!(rho > 0.0) || !(pr > 0.0)) atomicOr(&flag[cl], 4);
+        double F[D][V];
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          F[a][0] = q[1 + a];
+#pragma unroll
+          for (int b = 0; b < D; ++b) F[a][1 + b] = q[1 + a] * u[b] + (a == b ? pr : 0.0);
+          F[a][D + 1] = u[a] * (E + pr);
+        }
+        const double* J = Ji + cl * D * D;
+#pragma unroll
+        for (int b = 0; b < D; ++b)
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            double s = 0.0;
+#pragma unroll
+            for (int a = 0; a < D; ++a) s = __fma_rn(J[b * D + a], F[a][v], s);
+            G[((cl * D + b) * L + l) * V + v] = s;
+          }
+      }
+      __syncthreads();
+      // ---- update phase: (cell, variable) → the NU unknown rows
+      if (upd && !(flag[ucl] & 1)) {
+        double acc[NU];
+#pragma unroll
+        for (int k = 0; k < NU; ++k) acc[k] = 0.0;
+        const double* Gc = G + (ucl * D * L) * V + uv;
+#pragma unroll
+        for (int b = 0; b < D; ++b)
+#pragma unroll
+          for (int l = 0; l < L; ++l) {
+            const double g = Gc[(b * L + l) * V];
+#pragma unroll
+            for (int k = 0; k < NU; ++k) acc[k] = __fma_rn(c_pred[OA + (b * NU + k) * L + l], g, acc[k]);
+          }
+        double dmax = 0.0;
+        double* qu = Q + (ucl * L + NK) * V + uv;
+#pragma unroll
+        for (int k = 0; k < NU; ++k) {
+          const double nv = __fma_rn(-p.dt, acc[k], base[k]);
+          dmax = fmax(dmax, fabs(nv - qu[k * V]));
+          qu[k * V] = nv;
+        }
+        dl[ucl * V + uv] = dmax;
+      }
+      __syncthreads();
+      int active = 0;
+      for (int cl = tid; cl < nc; cl += nth) {
+        if (flag[cl] & 1) continue;
+        its[cl] = iter + 1;
+        double dm = 0.0;
+        for (int v = 0; v < V; ++v) dm = fmax(dm, dl[cl * V + v]);
+        if (dm <= p.tol * sc[cl])
+          flag[cl] |= 1;
+        else
+          active = 1;
+      }
+      if (!__syncthreads_or(active)) break;
+    }
+    __syncthreads();
+    // ---- the last iterate's states: admissibility of the final q̂ (as the oracle)
+    for (int it = tid; it < nc * L; it += nth) {
+      const int cl = it / L, l = it - cl * L;
+      const double* qn = Q + (cl * L + l) * V;
+      double ke = 0.0;
+#pragma unroll
+      for (int a = 0; a < D; ++a) ke = __fma_rn(qn[1 + a], qn[1 + a] / qn[0], ke);
+      const double pr = (p.gamma - 1.0) * (qn[D + 1] - 0.5 * ke);
+      if (!(qn[0] > 0.0) || !(pr > 0.0)) atomicOr(&flag[cl], 4);
+    }
+    __syncthreads();
+    // ---- store q̂ (contiguous [cell][L][V] rows) and the iteration counts
+    double* qo = p.q + c0 * L * V;
+    for (int e = tid; e < nc * L * V; e += nth) qo[e] = Q[e];
+    if (p.iters)
+      for (int cl = tid; cl < nc; cl += nth)
+        p.iters[c0 + cl] = ((flag[cl] & 1) && !(flag[cl] & 4)) ? its[cl] : -its[cl] - 1;
+    __syncthreads();
+  }
+}
+
+using PredFn = void (*)(PredArgs);
+static PredFn pred_fn(int d, int M) {
+#define PC(DD, MM) \
+  if (d == DD && M == MM) return k_predictor<DD, MM>;
+  PC(2, 1) PC(2, 2) PC(2, 3) PC(3, 1) PC(3, 2) PC(3, 3)
+#undef PC
+  fail(CWRECO_EUNSUPPORTED, "predictor: (d, M) not instantiated (M ≤ 3)");
+}
+static size_t pred_smem(int d, int M) {
+  const int L = pr_L(d, M), V = d + 2, CB = 32;
+  return sizeof(double) * (size_t(CB) * L * V * (1 + d) + CB * d * d + CB * V + CB) + 2 * sizeof(int) * CB;
+}
+
+struct PredState {
+  double* jinv = nullptr;
+  double gamma = 1.4;
+  int L = 0;
+};
+
+void dev_predictor_setup(cwreco_ctx* c, const PredictorHost& h, const std::vector<double>& jinv, double gamma) {
+  if (c->device < 0) fail(CWRECO_ECUDA, "predictor_setup: host-only context (no CUDA device)");
+  if (c->V != c->d + 2) fail(CWRECO_EUNSUPPORTED, "predictor: the Euler system needs nvars = dim + 2");
+  PredFn f = pred_fn(c->d, c->M);
+  DeviceGuard dg(c->device);
+  if (pr_L(c->d, c->M) != h.L || pr_nk(c->d, c->M) != h.nk) fail(CWRECO_EUNSUPPORTED, "predictor: table shape");
+  std::vector<double> tab;
+  tab.insert(tab.end(), h.A.begin(), h.A.end());
+  tab.insert(tab.end(), h.C0.begin(), h.C0.end());
+  tab.insert(tab.end(), h.Phi.begin(), h.Phi.end());
+  if ((int)tab.size() != pr_len(c->d, c->M)) fail(CWRECO_EUNSUPPORTED, "predictor: table length");
+  PCK(cudaMemcpyToSymbol(c_pred, tab.data(), tab.size() * sizeof(double), sizeof(double) * pr_off(c->d, c->M)));
+  PCK(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pred_smem(c->d, c->M)));
+  auto* s = (PredState*)c->pred;
+  if (!s) c->pred = s = new PredState();
+  cudaFree(s->jinv);
+  s->jinv = nullptr;
+  PCK(cudaMalloc(&s->jinv, std::max<size_t>(1, jinv.size()) * sizeof(double)));
+  if (!jinv.empty()) PCK(cudaMemcpy(s->jinv, jinv.data(), jinv.size() * sizeof(double), cudaMemcpyHostToDevice));
+  s->gamma = gamma;
+  s->L = h.L;
+}
+
+void dev_predictor_destroy(cwreco_ctx* c) {
+  auto* s = (PredState*)c->pred;
+  if (!s) return;
+  DeviceGuard dg(c->device);
+  cudaFree(s->jinv);
+  delete s;
+  c->pred = nullptr;
+}
+
+void dev_predict(cwreco_ctx* c, const double* w, int64_t ccs, int64_t cvs, double dt, double* q, int32_t* iters,
+                 void* stream) {
+  auto* s = (PredState*)c->pred;
+  if (!s) fail(CWRECO_ESTATE, "predict: call cwreco_predictor_setup first");
+  DeviceGuard dg(c->device);
+  PredArgs a;
+  a.w = w;
+  a.ccs = ccs;
+  a.cvs = cvs;
+  a.jinv = s->jinv;
+  a.q = q;
+  a.iters = iters;
+  a.n = c->n_owned;
+  a.dt = dt;
+  a.gamma = s->gamma;
+  a.tol = 1e-12;
+  a.maxit = 2 * (c->M + 1);
+  if (a.n == 0) return;
+  PredFn f = pred_fn(c->d, c->M);
+  int occ = 1, nsm = 148;
+  const size_t smem = pred_smem(c->d, c->M);
+  PCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)f, 160, smem));
+  PCK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
+  const int64_t blocks = (a.n + 31) / 32;
+  int64_t grid = std::min<int64_t>(blocks, (int64_t)nsm * std::max(1, occ));
+  if (c->max_ctas > 0) grid = std::min<int64_t>(grid, c->max_ctas);
+  f<<<(unsigned)grid, 32 * (c->d + 2), smem, (cudaStream_t)stream>>>(a);
+  PCK(cudaGetLastError());
+}
+
+}  // namespace cwr

@@ -112,6 +112,7 @@ typedef struct {
                                             0 = cell-variable (k_pipelined),
                                             1 = row-block (k_rowblk); -1 before */
   int32_t reserved_;
+  int64_t n_boundary_ghosts;             /* mirror cells (R37) referenced by the owned stencils */
 } cwreco_info;
 
 /* ---------------------------------------------------------------- lifecycle */
@@ -153,6 +154,20 @@ cwreco_status cwreco_set_option(cwreco_ctx* ctx, int option, int64_t value);
  * and the Morton order (R29), builds face and node adjacency. */
 cwreco_status cwreco_set_mesh(cwreco_ctx* ctx, int64_t n_nodes, const double* xyz, int64_t n_cells,
                               const int64_t* cell_nodes, const double* period);
+/* Physical boundaries of an OPEN mesh by reflected ghost cells (R37; the paper is
+ * silent on boundary stencils): side_bc [2·dim], side s = 2·axis + (0 low,
+ * 1 high) of the nodes' bounding box: 0 none (stencils grow inward, sectors may
+ * starve), 1 transmissive, 2 wall.  Stencil searches cross every boundary face that
+ * lies exactly on an active side into the mirror image of the domain across it
+ * (ghost id N + s·N + k = cell k mirrored, vertices X'_a = c + (c − X_a)); ghosts
+ * enter through face adjacency only (the R14 node-neighbour fallback stays on real
+ * cells) and are never reflected twice.  A ghost's averages are its source's, with
+ * ρu_axis (index mom0 + axis, mom0 ≥ 0) negated on wall sides; the library fills
+ * them before every pass.  Call after cwreco_set_mesh, before the stencils (drops
+ * them); one rank only (EUNSUPPORTED at cwreco_build_stencils otherwise); not with
+ * the matrix-free mode.  EINVAL for a periodic mesh, codes outside 0..2 or a mom0
+ * that leaves no room for dim momenta.  side_bc == NULL clears the boundaries. */
+cwreco_status cwreco_set_boundary(cwreco_ctx* ctx, const int* side_bc, int mom0);
 /* sfc_to_input: [n_cells] out. */
 cwreco_status cwreco_get_permutation(const cwreco_ctx* ctx, int64_t* sfc_to_input);
 /* Ownership: rank owns SFC ids [floor(r·N/P), floor((r+1)·N/P)) (contiguous Morton

@@ -79,7 +79,10 @@ class OracleMesh:
       node_cells CSR     (nc_ptr, nc_idx) node -> sorted SFC cell ids
     """
 
-    def __init__(self, nodes, cells, period, M):
+    def __init__(self, nodes, cells, period, M, bc=None, mom0=None):
+        """bc: None, or per side s = 2·axis + (0 low, 1 high) of the nodes' bounding
+        box: 0 none, 1 transmissive, 2 wall — boundary ghost cells by reflection
+        (R37, open meshes only); mom0: index of ρu_1 in the conserved vector (wall)."""
         nodes = np.asarray(nodes, dtype=np.float64)
         cells = np.asarray(cells, dtype=np.int64)
         self.d = d = nodes.shape[1]
@@ -106,6 +109,97 @@ class OracleMesh:
         self.n_nodes = nodes.shape[0]
         self._adjacency()
         self._frac_cache = {}
+        self.bc = None
+        if bc is not None:
+            if self.period is not None:
+                raise MeshError("boundary ghost cells need an open mesh")
+            if len(bc) != 2 * d:
+                raise MeshError("bc needs one entry per box side")
+            self.bc = [int(x) for x in bc]
+            self.mom0 = mom0
+            lo, hi = nodes.min(axis=0), nodes.max(axis=0)
+            self.plane = [float(lo[s // 2]) if s % 2 == 0 else float(hi[s // 2]) for s in range(2 * d)]
+            self._gX = {}
+
+    # ------------------------------------------------- boundary ghosts (R37)
+    # Ghost id N + s·N + k = the mirror image of real cell k across box side s
+    # (x_a = c, a = s // 2): vertices X'_a = c + (c − X_a) in IEEE double, the last
+    # two swapped (orientation, R28).  Face adjacency: a real boundary face on an
+    # active side s borders the mirror of its own cell; a ghost's faces border the
+    # mirrors (same side) of its source's neighbours, its mirrored face on s borders
+    # the source itself, and faces on other sides border nothing (no double
+    # reflection).  Node (Voronoi) neighbours — the R14 fallback — stay real cells.
+    def is_ghost(self, j):
+        return j >= self.N
+
+    def ghost_of(self, j):
+        """(side s, source k) of ghost id j."""
+        s, k = divmod(j - self.N, self.N)
+        return s, k
+
+    def face_side(self, k, f):
+        """Active box side containing face f of real cell k (all its vertices on the
+        plane, exactly), or -1."""
+        if self.bc is None:
+            return -1
+        d = self.d
+        V = [self.X[k, v] for v in range(d + 1) if v != f]
+        for s in range(2 * d):
+            if self.bc[s] and all(x[s // 2] == self.plane[s] for x in V):
+                return s
+        return -1
+
+    def Xc(self, j):
+        """Vertex coordinates [d+1][d] of real or ghost cell j."""
+        if j < self.N:
+            return self.X[j]
+        g = self._gX.get(j)
+        if g is None:
+            s, k = self.ghost_of(j)
+            a, c = s // 2, self.plane[s]
+            g = self.X[k].copy()
+            g[:, a] = c + (c - self.X[k][:, a])
+            g[[self.d - 1, self.d]] = g[[self.d, self.d - 1]]
+            self._gX[j] = g
+        return g
+
+    def neighbours(self, c):
+        """Face neighbours of real or ghost cell c (ghosts included when bc is set)."""
+        if c < self.N:
+            out = []
+            for f in range(self.d + 1):
+                nb = int(self.nbr[c, f])
+                if nb >= 0:
+                    out.append(nb)
+                else:
+                    s = self.face_side(c, f)
+                    if s >= 0:
+                        out.append(self.N + s * self.N + c)
+            return out
+        s, k = self.ghost_of(c)
+        out = []
+        for f in range(self.d + 1):
+            nb = int(self.nbr[k, f])
+            if nb >= 0:
+                out.append(self.N + s * self.N + nb)
+            elif self.face_side(k, f) == s:
+                out.append(k)
+        return out
+
+    def values(self, Q, ids):
+        """Averages of real or ghost cells: a ghost carries its source's averages,
+        with the momentum component normal to a WALL side negated (R37)."""
+        ids = [int(j) for j in ids]
+        out = np.empty((len(ids), Q.shape[1]))
+        for r, j in enumerate(ids):
+            if j < self.N:
+                out[r] = Q[j]
+            else:
+                s, k = self.ghost_of(j)
+                out[r] = Q[k]
+                if self.bc[s] == 2 and self.mom0 is not None:
+                    out[r, self.mom0 + s // 2] = -Q[k, self.mom0 + s // 2]
+        return out
 
     # -------------------------------------------------------------- geometry
     def _unwrap(self, nodes, cells):
@@ -225,7 +319,8 @@ class OracleMesh:
         """Exact vertex coordinates and vertex sums S_c of cell c (Fractions)."""
         got = self._frac_cache.get(c)
         if got is None:
-            Xf = [[Fraction(float(v)) for v in self.X[c, k]] for k in range(self.d + 1)]
+            Xc = self.Xc(c)
+            Xf = [[Fraction(float(v)) for v in Xc[k]] for k in range(self.d + 1)]
             S = [sum(Xf[k][a] for k in range(self.d + 1)) for a in range(self.d)]
             got = (Xf, S)
             if len(self._frac_cache) > 200000:
@@ -295,9 +390,8 @@ class OracleMesh:
         while len(S) < n_e:
             cand = set()
             for c in frontier:
-                for nb in self.nbr[c]:
-                    nb = int(nb)
-                    if nb >= 0 and nb not in inS:
+                for nb in self.neighbours(c):
+                    if nb not in inS:
                         cand.add(nb)
             if not cand:
                 raise StencilExhausted(f"central stencil of cell {i} exhausted at {len(S)} < {n_e}")
@@ -311,6 +405,8 @@ class OracleMesh:
     def node_neighbours(self, cells_):
         out = set()
         for c in cells_:
+            if c >= self.N:
+                continue            # ghosts contribute no node neighbours (R37)
             for nd in self.cells[c]:
                 out.update(int(x) for x in self.nc_idx[self.nc_ptr[nd]:self.nc_ptr[nd + 1]])
         return out
@@ -324,9 +420,8 @@ class OracleMesh:
         while len(S) < d + 1:
             cand = set()
             for c in frontier:
-                for nb in self.nbr[c]:
-                    nb = int(nb)
-                    if nb >= 0 and nb not in seen:
+                for nb in self.neighbours(c):
+                    if nb not in seen:
                         cand.add(nb)
             seen.update(cand)
             acc = [j for j in cand if self.in_cone(i, j, v)]

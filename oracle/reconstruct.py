@@ -106,13 +106,13 @@ def stencil_matrix(mesh: OracleMesh, i, cells_, M):
     """A[k][l] = average over (periodic image of) cell cells_[k] of ψ_l(ξ_i(x))."""
     d = mesh.d
     exps, Cb = basis_numeric(d, M)
-    X0i, Ji = _affine(mesh.X[i])
+    X0i, Ji = _affine(mesh.Xc(i))
     t = np.empty((len(cells_), d))
     C = np.empty((len(cells_), d, d))
     for k, j in enumerate(cells_):
         n = np.array(mesh.shift(i, j), dtype=np.float64)
         L = mesh.period if mesh.period is not None else np.zeros(d)
-        Xj = mesh.X[j] + n * L
+        Xj = mesh.Xc(j) + n * L
         X0j, Jj = _affine(Xj)
         t[k] = np.linalg.solve(Ji, X0j - X0i)
         C[k] = np.linalg.solve(Ji, Jj)
@@ -139,7 +139,15 @@ def precompute_cell(mesh: OracleMesh, i, M, central=None, sectors=None, valid=No
     pinv = np.linalg.pinv(A[1:, 1:])                           # [ℳ-1, n_e-1]
     As = [stencil_matrix(mesh, i, sectors[s], M)[:, : d + 1] if valid[s] else None   # ψ_1..ψ_{d+1}
           for s in range(d + 1)]
-    return dict(i=int(i), d=d, M=M, central=central, sectors=sectors, valid=valid, A=A, pinv=pinv, As=As)
+    return dict(i=int(i), d=d, M=M, central=central, sectors=sectors, valid=valid, A=A, pinv=pinv, As=As,
+                mesh=mesh if mesh.bc is not None else None)
+
+
+def mesh_values(pre, Q, ids):
+    """Q rows of the stencil cells; boundary ghosts (R37) through mesh.values."""
+    if pre.get("mesh") is not None:
+        return pre["mesh"].values(Q, ids)
+    return Q[np.asarray(ids)]
 
 
 def apply_cell(pre, Q, lam0=LAMBDA0, lams=LAMBDAS, eps=EPS, r=R_EXP):
@@ -155,7 +163,7 @@ def apply_cell(pre, Q, lam0=LAMBDA0, lams=LAMBDAS, eps=EPS, r=R_EXP):
     p1 = psi1(d)
 
     # --- P_opt: constrained LSQ
-    Qs = Q[np.asarray(central)]                                # [n_e, V]
+    Qs = mesh_values(pre, Q, central)                          # [n_e, V]
     popt = np.zeros((V, nm))
     popt[:, 0] = Q[i] / p1                                     # constraint row k=1
     rhs = Qs[1:] - np.outer(A[1:, 0], popt[:, 0])              # [n_e-1, V]
@@ -165,7 +173,7 @@ def apply_cell(pre, Q, lam0=LAMBDA0, lams=LAMBDAS, eps=EPS, r=R_EXP):
     psec = np.zeros((d + 1, V, d + 1))
     for s in range(d + 1):
         if valid[s]:
-            psec[s] = np.linalg.solve(pre["As"][s], Q[np.asarray(sectors[s])]).T
+            psec[s] = np.linalg.solve(pre["As"][s], mesh_values(pre, Q, sectors[s])).T
 
     # --- linear weights, normalised over valid stencils (R5, R14)
     lam = np.array([lam0] + [lams if valid[s] else 0.0 for s in range(d + 1)])

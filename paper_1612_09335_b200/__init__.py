@@ -44,7 +44,8 @@ class _Info(ctypes.Structure):
                                                "n_interior_tiles", "tile_bytes", "device_bytes",
                                                "algorithmic_bytes_per_cell", "n_invalid_sectors",
                                                "n_extra_gather", "union_max")] + \
-               [(n, ctypes.c_int32) for n in ("kernel_family", "reserved_")]
+               [(n, ctypes.c_int32) for n in ("kernel_family", "reserved_")] + \
+               [("n_boundary_ghosts", ctypes.c_int64)]
 
 
 def _load():
@@ -64,6 +65,7 @@ def _load():
         "cwreco_set_option": [P, I32, I64],
         "cwreco_set_mesh": [P, I64, P, I64, P, P],
         "cwreco_get_permutation": [P, P],
+        "cwreco_set_boundary": [P, P, I32],
         "cwreco_set_partition": [P, I32, I32, P],
         "cwreco_nccl_unique_id": [P],
         "cwreco_loopback_unique_id": [I32, P],
@@ -175,6 +177,12 @@ class Context:
         per = None if period is None else np.ascontiguousarray(period, dtype=np.float64)
         self.N = cells.shape[0]
         _check(lib.cwreco_set_mesh(self._h, nodes.shape[0], _ptr(nodes), cells.shape[0], _ptr(cells), _ptr(per)))
+
+    def set_boundary(self, side_bc, mom0=-1):
+        """cwreco_set_boundary: side_bc [2·dim] (0 none, 1 transmissive, 2 wall) per box
+        side s = 2·axis + (0 low, 1 high); mom0 = index of ρu_1 (walls negate ρu_axis)."""
+        arr = None if side_bc is None else np.ascontiguousarray(side_bc, dtype=np.int32)
+        _check(lib.cwreco_set_boundary(self._h, _ptr(arr), int(mom0)))
 
     def permutation(self):
         out = np.empty(self.N, dtype=np.int64)

@@ -132,6 +132,7 @@ cwreco_status cwreco_get_info(const cwreco_ctx* c, cwreco_info* o) {
     o->n_extra_gather = c->n_extra;
     o->union_max = c->lay.Umax;
     o->kernel_family = c->has_blocks ? c->lay.kind : -1;
+    o->n_boundary_ghosts = (int64_t)c->bc_ids.size();
     if (c->has_blocks) {
       o->tile_cells = c->lay.T;
       o->chunk_k = c->lay.KC;
@@ -182,6 +183,29 @@ cwreco_status cwreco_set_mesh(cwreco_ctx* c, int64_t n_nodes, const double* xyz,
     need(c != nullptr, CWRECO_EINVAL, "set_mesh: NULL ctx");
     invalidate_derived(c);
     cwr::set_mesh(c, n_nodes, xyz, n_cells, cell_nodes, period);
+  });
+}
+
+cwreco_status cwreco_set_boundary(cwreco_ctx* c, const int* side_bc, int mom0) {
+  return guard([&] {
+    need(c != nullptr, CWRECO_EINVAL, "set_boundary: NULL ctx");
+    need(c->has_mesh, CWRECO_ESTATE, "set_boundary: call cwreco_set_mesh first");
+    need(!c->periodic, CWRECO_EINVAL, "set_boundary: boundary ghost cells need an open mesh (period = NULL)");
+    need(mom0 >= -1 && mom0 + c->d <= c->V, CWRECO_EINVAL, "set_boundary: mom0 must be -1 or leave room for dim momenta");
+    bool any = false;
+    for (int s = 0; s < 2 * c->d; ++s) {
+      const int b = side_bc ? side_bc[s] : 0;
+      need(b >= 0 && b <= 2, CWRECO_EINVAL, "set_boundary: side codes are 0 (none), 1 (transmissive), 2 (wall)");
+      any |= b != 0;
+    }
+    need(!any || c->N * int64_t(2 * c->d + 1) < INT32_MAX, CWRECO_EUNSUPPORTED,
+         "set_boundary: ghost ids exceed 32 bits");
+    invalidate_derived(c);
+    for (int s = 0; s < 6; ++s) c->bc[s] = (side_bc && s < 2 * c->d) ? side_bc[s] : 0;
+    c->mom0 = mom0;
+    c->has_bc = any;
+    c->bc_ids.clear();
+    c->has_stencils = c->has_blocks = false;
   });
 }
 

@@ -219,6 +219,14 @@ struct cwreco_ctx {
   std::vector<int64_t> nbr;         // [N][d+1] face neighbours, -1 none
   std::vector<int64_t> nc_ptr, nc_idx;  // node -> cells (SFC ids, ascending)
 
+  double box_lo[3] = {0, 0, 0}, box_hi[3] = {0, 0, 0};  // bounding box of the nodes
+
+  // ---- boundary ghost cells by reflection (R37, cwreco_set_boundary; open meshes)
+  bool has_bc = false;
+  int bc[6] = {0, 0, 0, 0, 0, 0};  // per box side s = 2·axis + (0 low, 1 high): 0 none, 1 transmissive, 2 wall
+  int mom0 = -1;                   // index of ρu_1 among the variables (wall sides negate ρu_axis)
+  std::vector<int64_t> bc_ids;     // ghost ids N + s·N + k referenced by owned stencils, ascending
+
   // ---- partition
   int rank = 0, nranks = 1;
   int64_t own_lo = 0, own_hi = 0;
@@ -292,6 +300,10 @@ void dev_predictor_setup(cwreco_ctx* c, const PredictorHost& h, const std::vecto
 void dev_predictor_destroy(cwreco_ctx* c);
 void dev_predict(cwreco_ctx* c, const double* w, int64_t ccs, int64_t cvs, double dt, double* q, int32_t* iters,
                  void* stream);
+// stencil.cpp: real and boundary-ghost cells (R37): vertices, barycentre, face neighbours
+const double* cell_X(const cwreco_ctx* c, int64_t j, double* buf);  // [d+1][d]; buf ≥ 12 doubles
+void cell_bary(const cwreco_ctx* c, int64_t j, double* out);
+int cell_neighbours(const cwreco_ctx* c, int64_t j, int64_t* out);  // out ≥ d+1 entries; returns count
 // stencil.cpp: send lists (owned cells requested by each peer, SFC ids) → local ids
 void install_send_lists(cwreco_ctx* c, const int64_t* send_counts, const int64_t* send_ids);
 // halo.cu: multi-rank transport (NCCL or in-process loopback) and the exchange

@@ -44,6 +44,8 @@ struct KArgs {
   int64_t n_owned, tile_begin, tile_end;
   const double* Q;
   int64_t acs, avs;
+  int64_t n_local;     // local ids ≥ n_local are boundary ghosts (R37): rows of Qbc [n_bc][V]
+  const double* Qbc;
   double* out;
   int64_t ccs, cvs;
   int dense_out;
@@ -62,6 +64,11 @@ struct KArgs {
 #else
 #define EXP(a, bit) false
 #endif
+
+// address of the average (local cell j, variable v): caller rows, or a boundary ghost row
+__device__ __forceinline__ const double* qptr(const KArgs& a, int64_t j, int v) {
+  return j < a.n_local ? a.Q + j * a.acs + v * a.avs : a.Qbc + (j - a.n_local) * a.V + v;
+}
 
 struct DbgOut {
   double *popt, *psec, *sigma, *omega, *w;

@@ -38,6 +38,10 @@ struct DeviceState {
   int64_t dbg_bytes = 0;
   int64_t* dbg_cells = nullptr;
   int64_t dbg_ncells = 0;
+  int64_t* bc_src = nullptr;  // boundary ghosts (R37): local id of the source cell
+  int32_t* bc_neg = nullptr;  //   variable negated (wall side), −1 none
+  double* Qbc = nullptr;      //   their averages [n_bc][V], filled before every pass
+  int64_t n_bc = 0;
   double* h_avgs = nullptr;  // device buffers of cwreco_reconstruct_host (lazy)
   double* h_coeffs = nullptr;
   int64_t h_avgs_n = 0, h_coeffs_n = 0;
@@ -89,7 +93,7 @@ __global__ void __launch_bounds__(256) k_simple(KArgs a, DbgOut dbg) {
     for (int kk = 0; kk < kc; ++kk) {
       const int p = ch * a.KC + kk;
       const int32_t j = ((const int32_t*)tb)[idx[idx_elem(a.kind, a.T, p, ct)] / a.VP];  // union chunk
-      const double qj = Qv[int64_t(j) * a.acs];
+      const double qj = *qptr(a, j, v);
       const double dq = qj - qi;
 #pragma unroll
       for (int q = 0; q < NCAP; ++q)
@@ -222,7 +226,7 @@ __global__ void __launch_bounds__(max_threads(D, M), min_blocks(D, M)) k_pipelin
       int u = tid / a.V, vv = tid - (tid / a.V) * a.V;
       const int du = nct / a.V, dv = nct - du * a.V;
       for (int e = tid; e < a.Umax * a.V; e += nct) {
-        cp_async8(dst + e, a.Q + int64_t(uid[u]) * a.acs + vv * a.avs);
+        cp_async8(dst + e, qptr(a, uid[u], vv));
         u += du;
         vv += dv;
         if (vv >= a.V) {
@@ -352,6 +356,27 @@ __global__ void __launch_bounds__(max_threads(D, M), min_blocks(D, M)) k_pipelin
   if (lane == 0) bulk_wait_all();
 }
 
+// ---------------------------------------------------------------- boundary ghosts (R37)
+__global__ void k_bc_fill(const double* __restrict__ Q, int64_t acs, int64_t avs, int V,
+                          const int64_t* __restrict__ src, const int32_t* __restrict__ neg, int64_t n,
+                          double* __restrict__ Qbc) {
+  const int64_t gid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (gid >= n * V) return;
+  const int64_t g = gid / V;
+  const int v = int(gid % V);
+  const double x = Q[src[g] * acs + v * avs];
+  Qbc[gid] = v == neg[g] ? -x : x;  // transmissive: copy; wall: −ρu_normal
+}
+
+static void bc_fill(cwreco_ctx* c, const double* avgs, int64_t acs, int64_t avs, cudaStream_t st) {
+  DeviceState* ds = c->dev;
+  if (ds->n_bc == 0) return;
+  const int64_t th = ds->n_bc * c->V;
+  k_bc_fill<<<(unsigned)((th + 255) / 256), 256, 0, st>>>(avgs, acs, avs, c->V, ds->bc_src, ds->bc_neg, ds->n_bc,
+                                                          ds->Qbc);
+  CK(cudaGetLastError());
+}
+
 // ---------------------------------------------------------------- halo pack
 __global__ void k_halo_pack(const double* __restrict__ Q, int64_t acs, int64_t avs, int V,
                             const int64_t* __restrict__ send, int64_t n, double* __restrict__ buf) {
@@ -427,6 +452,8 @@ static KArgs make_args(const cwreco_ctx* c, const double* avgs, int64_t acs, int
   a.Q = avgs;
   a.acs = acs;
   a.avs = avs;
+  a.n_local = c->n_owned + c->n_ghost;
+  a.Qbc = c->dev ? c->dev->Qbc : nullptr;
   a.out = out;
   a.ccs = ccs;
   a.cvs = cvs;
@@ -545,6 +572,9 @@ void dev_destroy(cwreco_ctx* c) {
   cudaFree(c->dev->dbg_cells);
   cudaFree(c->dev->h_avgs);
   cudaFree(c->dev->h_coeffs);
+  cudaFree(c->dev->bc_src);
+  cudaFree(c->dev->bc_neg);
+  cudaFree(c->dev->Qbc);
   for (cudaEvent_t e : c->dev->piece_done) cudaEventDestroy(e);
   if (c->dev->copy_stream) cudaStreamDestroy(c->dev->copy_stream);
   delete c->dev;
@@ -571,6 +601,33 @@ void dev_upload_blocks(cwreco_ctx* c, int64_t offset, const unsigned char* host,
 
 void dev_upload_aux(cwreco_ctx* c) {
   const int nm = c->nm;
+  {  // boundary ghosts (R37): source local ids and the negated (wall) variable
+    DeviceGuard dg0(c->device);
+    DeviceState* ds = c->dev;
+    cudaFree(ds->bc_src);
+    cudaFree(ds->bc_neg);
+    cudaFree(ds->Qbc);
+    ds->bc_src = nullptr;
+    ds->bc_neg = nullptr;
+    ds->Qbc = nullptr;
+    ds->n_bc = (int64_t)c->bc_ids.size();
+    if (ds->n_bc > 0) {
+      std::vector<int64_t> own2local(c->own_hi - c->own_lo, -1);
+      for (int64_t li = 0; li < c->n_owned; ++li) own2local[c->local2global[li] - c->own_lo] = li;
+      std::vector<int64_t> src(ds->n_bc);
+      std::vector<int32_t> neg(ds->n_bc);
+      for (int64_t g = 0; g < ds->n_bc; ++g) {
+        const int64_t id = c->bc_ids[g], s = (id - c->N) / c->N, k = (id - c->N) % c->N;
+        src[g] = own2local[k - c->own_lo];
+        neg[g] = (c->bc[s] == 2 && c->mom0 >= 0) ? int32_t(c->mom0 + s / 2) : -1;
+      }
+      CK(cudaMalloc(&ds->bc_src, ds->n_bc * 8));
+      CK(cudaMalloc(&ds->bc_neg, ds->n_bc * 4));
+      CK(cudaMalloc(&ds->Qbc, ds->n_bc * c->V * 8));
+      CK(cudaMemcpy(ds->bc_src, src.data(), ds->n_bc * 8, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(ds->bc_neg, neg.data(), ds->n_bc * 4, cudaMemcpyHostToDevice));
+    }
+  }
   std::vector<double> packed;
   for (int l = 1; l < nm; ++l)
     for (int m = l; m < nm; ++m) packed.push_back((l == m ? 1.0 : 2.0) * c->sigma[l * nm + m]);
@@ -633,6 +690,7 @@ void dev_reconstruct(cwreco_ctx* c, const double* avgs, int64_t acs, int64_t avs
     dev_matfree_reconstruct(c, avgs, acs, avs, coeffs, ccs, cvs, c0, c1, stream);
     return;
   }
+  bc_fill(c, avgs, acs, avs, (cudaStream_t)stream);
   int64_t t0 = 0, t1 = c->n_tiles;
   if (part == CWRECO_PART_INTERIOR) {
     t1 = c->n_int_tiles;
@@ -670,6 +728,7 @@ void dev_reconstruct_host(cwreco_ctx* c, const double* h_avgs, double* h_coeffs,
     ds->piece_done.push_back(e);
   }
   CK(cudaMemcpyAsync(ds->h_avgs, h_avgs, na * 8, cudaMemcpyHostToDevice, st));
+  if (c->kernel != CWRECO_KERNEL_MATRIXFREE) bc_fill(c, ds->h_avgs, V, 1, st);
   const bool mf = c->kernel == CWRECO_KERNEL_MATRIXFREE;  // pieces of cells instead of tiles
   const int64_t nt = mf ? c->n_owned : c->n_tiles, T = mf ? 1 : c->lay.T, row = (int64_t)V * nm;
   for (int k = 0; k < n_pieces; ++k) {
@@ -718,6 +777,7 @@ void dev_debug(cwreco_ctx* c, const double* avgs, int64_t acs, int64_t avs, int6
   o.w = o.omega + n_sig;
   o.cells = c->dev->dbg_cells;
   o.n = n_sel;
+  bc_fill(c, avgs, acs, avs, st);
   KArgs a = make_args(c, avgs, acs, avs, nullptr, 0, 0);
   const int64_t threads = n_sel * V;
   dim3 b(256), g((unsigned)((threads + 255) / 256));

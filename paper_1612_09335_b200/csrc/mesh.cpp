@@ -67,6 +67,15 @@ void set_mesh(cwreco_ctx* c, int64_t n_nodes, const double* xyz, int64_t n_cells
   }
   for (int64_t i = 0; i < n_nodes * d; ++i)
     if (!std::isfinite(xyz[i])) fail(CWRECO_EMESH, "set_mesh: non-finite node coordinate");
+  c->has_bc = false;
+  c->bc_ids.clear();
+  for (int a = 0; a < d; ++a) {
+    c->box_lo[a] = c->box_hi[a] = xyz[a];
+    for (int64_t n = 1; n < n_nodes; ++n) {
+      c->box_lo[a] = std::min(c->box_lo[a], xyz[n * d + a]);
+      c->box_hi[a] = std::max(c->box_hi[a], xyz[n * d + a]);
+    }
+  }
 
   const int64_t N = n_cells;
   std::vector<int64_t> cn(cells_in, cells_in + N * nv);

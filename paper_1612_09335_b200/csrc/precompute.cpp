@@ -348,6 +348,11 @@ void precompute(cwreco_ctx* c) {
   for (int64_t li = 0; li < c->n_owned; ++li) own2local[c->local2global[li] - c->own_lo] = (int32_t)li;
   auto to_local = [&](int64_t g) -> int32_t {
     if (g >= c->own_lo && g < c->own_hi) return own2local[g - c->own_lo];
+    if (g >= c->N) {  // boundary ghost (R37): local ids after the halo ghosts
+      auto it = std::lower_bound(c->bc_ids.begin(), c->bc_ids.end(), g);
+      if (it == c->bc_ids.end() || *it != g) return -1;
+      return (int32_t)(n_loc + (it - c->bc_ids.begin()));
+    }
     auto b = c->local2global.begin() + c->n_owned, e = c->local2global.begin() + n_loc;
     auto it = std::lower_bound(b, e, g);
     if (it == e || *it != g) return -1;
@@ -454,7 +459,8 @@ void precompute(cwreco_ctx* c) {
         double psi[64], xi[3], sh[3];
         for (int k = 1; k < ne; ++k) {
           const int64_t j = cen[k];
-          const double* Xj = &c->X[j * nv * d];
+          double xb[12];
+          const double* Xj = cell_X(c, j, xb);
           shift_of(c, g, j, sh);
           // ξ = t + C ξ' with t = J⁻¹(X_j0 + sh − X_i0), C = J⁻¹ J_j
           double t[3], Cm[9], Jj[9];
@@ -522,9 +528,11 @@ void precompute(cwreco_ctx* c) {
           for (int m = 0; m < d; ++m) {
             const int64_t j = sec[s * nv + 1 + m];
             shift_of(c, g, j, sh);
+            double bj[3];
+            cell_bary(c, j, bj);
             for (int a = 0; a < d; ++a) {
               double s2 = 0.0;
-              for (int e = 0; e < d; ++e) s2 += Ji[a * d + e] * (c->bary[j * d + e] + sh[e] - Xi[e]);
+              for (int e = 0; e < d; ++e) s2 += Ji[a * d + e] * (bj[e] + sh[e] - Xi[e]);
               xi[a] = s2;
             }
             basis_eval(d, 1, xi, psi);
@@ -558,6 +566,7 @@ void precompute(cwreco_ctx* c) {
 // 0 → 0, 1 → +L, 2 → −L, R16), the basis in monomial form and the quadrature rule.
 void matfree_prepare(cwreco_ctx* c, MatfreeHost& h) {
   if (!c->has_stencils) fail(CWRECO_ESTATE, "prepare_matrixfree: call cwreco_build_stencils first");
+  if (c->has_bc) fail(CWRECO_EUNSUPPORTED, "prepare_matrixfree: boundary ghost cells are not supported");
   const int d = c->d, ne = c->ne, nv = d + 1;
   const int64_t n_loc = c->n_owned + c->n_ghost;
   std::vector<int32_t> own2local(c->own_hi - c->own_lo, -1);

@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(kRbThreads, 1) k_rowblk(KArgs a, PipeCfg pc) {
       int u = etid / V, vv = etid - (etid / V) * V;
       const int du = EW / V, dv = EW - du * V;
       for (int e = etid; e < a.Umax * V; e += EW) {
-        cp_async8(dst + u * VP + vv, a.Q + int64_t(uid[u]) * a.acs + vv * a.avs);
+        cp_async8(dst + u * VP + vv, qptr(a, uid[u], vv));
         u += du;
         vv += dv;
         if (vv >= V) {

@@ -18,6 +18,88 @@
 
 namespace cwr {
 
+// ---------------------------------------------------------------- boundary ghosts (R37)
+// Ghost id N + s·N + k is the mirror image of real cell k across box side s (plane
+// x_a = c, a = s / 2): vertices X'_a = c + (c − X_a) (IEEE double), last two swapped
+// (orientation, R28).  A real boundary face lying exactly on an active side s borders
+// the mirror of its own cell; a ghost's faces border the mirrors (same side) of its
+// source's face neighbours, its mirrored face on s borders the source, and faces on
+// other sides border nothing (no double reflection).
+static double side_plane(const cwreco_ctx* c, int s) { return (s & 1) ? c->box_hi[s / 2] : c->box_lo[s / 2]; }
+
+static int face_side(const cwreco_ctx* c, int64_t k, int f) {
+  if (!c->has_bc) return -1;
+  const int d = c->d;
+  const double* X = &c->X[k * (d + 1) * d];
+  for (int s = 0; s < 2 * d; ++s) {
+    if (!c->bc[s]) continue;
+    const int a = s / 2;
+    const double pl = side_plane(c, s);
+    bool on = true;
+    for (int v = 0; v <= d && on; ++v)
+      if (v != f) on = X[v * d + a] == pl;
+    if (on) return s;
+  }
+  return -1;
+}
+
+const double* cell_X(const cwreco_ctx* c, int64_t j, double* buf) {
+  const int d = c->d;
+  if (j < c->N) return &c->X[j * (d + 1) * d];
+  const int64_t s = (j - c->N) / c->N, k = (j - c->N) % c->N;
+  const int a = int(s / 2);
+  const double pl = side_plane(c, int(s));
+  const double* X = &c->X[k * (d + 1) * d];
+  for (int v = 0; v <= d; ++v) {
+    const int src = v == d - 1 ? d : v == d ? d - 1 : v;  // last two swapped
+    for (int e = 0; e < d; ++e) buf[v * d + e] = e == a ? pl + (pl - X[src * d + e]) : X[src * d + e];
+  }
+  return buf;
+}
+
+void cell_bary(const cwreco_ctx* c, int64_t j, double* out) {
+  const int d = c->d;
+  if (j < c->N) {
+    for (int a = 0; a < d; ++a) out[a] = c->bary[j * d + a];
+    return;
+  }
+  double buf[12];
+  const double* X = cell_X(c, j, buf);
+  for (int a = 0; a < d; ++a) {  // R29 order
+    double s = X[a] + X[d + a];
+    s = s + X[2 * d + a];
+    if (d == 3) s = s + X[3 * d + a];
+    out[a] = s / double(d + 1);
+  }
+}
+
+int cell_neighbours(const cwreco_ctx* c, int64_t j, int64_t* out) {
+  const int d = c->d;
+  const int64_t N = c->N;
+  int n = 0;
+  if (j < N) {
+    for (int f = 0; f <= d; ++f) {
+      const int64_t nb = c->nbr[j * (d + 1) + f];
+      if (nb >= 0) {
+        out[n++] = nb;
+      } else {
+        const int s = face_side(c, j, f);
+        if (s >= 0) out[n++] = N + s * N + j;
+      }
+    }
+    return n;
+  }
+  const int64_t s = (j - N) / N, k = (j - N) % N;
+  for (int f = 0; f <= d; ++f) {
+    const int64_t nb = c->nbr[k * (d + 1) + f];
+    if (nb >= 0)
+      out[n++] = N + s * N + nb;
+    else if (face_side(c, k, f) == s)
+      out[n++] = k;
+  }
+  return n;
+}
+
 namespace {
 
 constexpr double U = 1.1102230246251565e-16;  // 2^-53
@@ -122,7 +204,8 @@ void make_cand(Owner& o, int64_t j, Cand& cd) {
   cd.ex = -1;
   shift_of(c, o.i, j, cd.n);
   const double* Xi = &c->X[o.i * (d + 1) * d];
-  const double* Xj = &c->X[j * (d + 1) * d];
+  double xb[12];
+  const double* Xj = cell_X(c, j, xb);
   IV key{0.0, 0.0};
   for (int a = 0; a < d; ++a) {
     IV sj = iv_exact(Xj[a]), si = iv_exact(Xi[a]);
@@ -142,7 +225,8 @@ const ExData& ensure_exact(Owner& o, Cand& cd) {
   o.ensure_exactW();
   const cwreco_ctx* c = o.c;
   const int d = o.d;
-  const double* Xj = &c->X[cd.j * (d + 1) * d];
+  double xb[12];
+  const double* Xj = cell_X(c, cd.j, xb);
   ExData x;
   for (int a = 0; a < d; ++a) {
     exact::Ex s;
@@ -243,11 +327,12 @@ bool central_stencil(Cache& cc, int32_t* out) {
   std::vector<int> idx;
   while ((int)S.size() < ne) {
     cand.clear();
-    for (int64_t f : frontier)
-      for (int k = 0; k <= d; ++k) {
-        int64_t nb = c->nbr[f * (d + 1) + k];
-        if (nb >= 0 && !contains(S, nb) && !contains(cand, nb)) cand.push_back(nb);
-      }
+    for (int64_t f : frontier) {
+      int64_t nbs[4];
+      const int nn = cell_neighbours(c, f, nbs);
+      for (int k = 0; k < nn; ++k)
+        if (!contains(S, nbs[k]) && !contains(cand, nbs[k])) cand.push_back(nbs[k]);
+    }
     if (cand.empty()) return false;
     idx.clear();
     for (int64_t x : cand) idx.push_back(cc.get(x));
@@ -274,11 +359,12 @@ bool sector_stencil(Cache& cc, int v, int32_t* out) {
   std::vector<int> taken, acc;
   while ((int)S.size() < d + 1) {
     cand.clear();
-    for (int64_t f : frontier)
-      for (int k = 0; k <= d; ++k) {
-        int64_t nb = c->nbr[f * (d + 1) + k];
-        if (nb >= 0 && !contains(seen, nb) && !contains(cand, nb)) cand.push_back(nb);
-      }
+    for (int64_t f : frontier) {
+      int64_t nbs[4];
+      const int nn = cell_neighbours(c, f, nbs);
+      for (int k = 0; k < nn; ++k)
+        if (!contains(seen, nbs[k]) && !contains(cand, nbs[k])) cand.push_back(nbs[k]);
+    }
     for (int64_t x : cand) seen.push_back(x);
     acc.clear();
     for (int64_t x : cand) {
@@ -289,6 +375,7 @@ bool sector_stencil(Cache& cc, int v, int32_t* out) {
       // fallback: node (Voronoi) neighbours of all selected sector cells
       cand.clear();
       for (int64_t s : S) {
+        if (s >= c->N) continue;  // ghosts contribute no node neighbours (R37)
         const int64_t* nd = &c->cell_nodes[s * (d + 1)];
         for (int k = 0; k <= d; ++k)
           for (int64_t q = c->nc_ptr[nd[k]]; q < c->nc_ptr[nd[k] + 1]; ++q) {
@@ -330,6 +417,8 @@ int owner_rank(const cwreco_ctx* c, int64_t g) {
 
 void build_stencils(cwreco_ctx* c) {
   if (!c->has_mesh) fail(CWRECO_ESTATE, "build_stencils: no mesh");
+  if (c->has_bc && c->nranks > 1)
+    fail(CWRECO_EUNSUPPORTED, "build_stencils: boundary ghost cells are supported on one rank");
   const int d = c->d, ne = c->ne, nv = d + 1;
   const int64_t lo = c->own_lo, hi = c->own_hi, n_own = hi - lo;
   c->central.assign(n_own * ne, -1);
@@ -369,18 +458,24 @@ void finalize_stencils(cwreco_ctx* c) {
   const int64_t lo = c->own_lo, hi = c->own_hi, n_own = hi - lo;
   std::vector<uint8_t> is_bnd(n_own, 0);
   std::vector<int64_t> ghosts;
+  std::vector<int64_t> bcg;
   for (int64_t q = 0; q < n_own; ++q) {
     bool b = false;
     for (int k = 0; k < ne; ++k) {
       int64_t g = c->central[q * ne + k];
-      if (g < lo || g >= hi) { b = true; ghosts.push_back(g); }
+      if (g >= c->N) bcg.push_back(g);
+      else if (g < lo || g >= hi) { b = true; ghosts.push_back(g); }
     }
     for (int k = 0; k < nv * nv; ++k) {
       int64_t g = c->sectors[q * nv * nv + k];
-      if (g >= 0 && (g < lo || g >= hi)) { b = true; ghosts.push_back(g); }
+      if (g >= c->N) bcg.push_back(g);
+      else if (g >= 0 && (g < lo || g >= hi)) { b = true; ghosts.push_back(g); }
     }
     is_bnd[q] = b;
   }
+  std::sort(bcg.begin(), bcg.end());
+  bcg.erase(std::unique(bcg.begin(), bcg.end()), bcg.end());
+  c->bc_ids = bcg;
   std::sort(ghosts.begin(), ghosts.end());
   ghosts.erase(std::unique(ghosts.begin(), ghosts.end()), ghosts.end());
   c->n_owned = n_own;

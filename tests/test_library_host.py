@@ -370,3 +370,27 @@ def test_loopback_plan_exchange_host_threads():
         import ctypes
         st = P.lib.cwreco_halo_exchange(ctxs[0]._h, ctypes.c_void_p(8), 2, 1, None)
         P._check(st)
+
+
+@pytest.mark.parametrize("d,n,M,bc", [(2, 8, 2, [1, 2, 1, 2]), (2, 7, 3, [2, 2, 0, 1]), (3, 4, 2, [1, 1, 2, 2, 1, 0])])
+def test_boundary_ghost_stencils_bit_exact(d, n, M, bc):
+    """R37: the library's stencils with reflected boundary ghosts equal the oracle's
+    bit for bit (ghost ids N + s·N + k), and the precompute accepts them."""
+    nodes, cells, _ = gen.box_mesh(d, n, False, 0.12, 9)
+    ctx = P.Context(d, M, d + 2, device=None)
+    ctx.set_mesh(nodes, cells, None)
+    ctx.set_boundary(bc, mom0=1)
+    ctx.build_stencils()
+    m = OracleMesh(nodes, cells, None, M, bc=bc, mom0=1)
+    assert np.array_equal(ctx.permutation(), m.perm)
+    cen, sec, val = ctx.stencils()
+    for i in range(m.N):
+        assert cen[i].tolist() == m.central_stencil(i), i
+        s, v = m.sector_stencils(i)
+        assert sec[i].tolist() == s and val[i].tolist() == v, i
+    ctx.precompute()
+    assert ctx.info()["n_boundary_ghosts"] > 0
+    with pytest.raises(P.CwrecoError, match="EINVAL"):
+        c2 = P.Context(d, M, d + 2, device=None)
+        c2.set_mesh(*gen.box_mesh(d, n, True)[:2], np.ones(d))
+        c2.set_boundary(bc, 1)

@@ -182,3 +182,29 @@ def test_sector_fallback_hand_mesh():
     assert valid == g["expected_valid"]
     # the fallback cell c2 lies outside the central stencil (R15: extra gather)
     assert sfc[2] not in m.central_stencil(i)
+
+
+@pytest.mark.parametrize("d,n,M", [(2, 8, 2), (2, 7, 3), (3, 4, 2)])
+def test_boundary_ghosts_uniform_stencils(d, n, M):
+    """R37 (reflected ghosts keep stencil sizes uniform): with every side
+    active, each cell of an open jittered box gets a full central stencil and d+1
+    valid sectors; boundary cells use ghosts, whose mirrored vertices are positively
+    oriented; ghost adjacency is symmetric."""
+    nodes, cells, _ = gen.box_mesh(d, n, False, 0.12, 5)
+    m = OracleMesh(nodes, cells, None, M, bc=[1] * (2 * d), mom0=None)
+    used = 0
+    for i in range(m.N):
+        S = m.central_stencil(i)
+        sec, val = m.sector_stencils(i)
+        assert len(S) == m.n_e and all(val), i
+        used += sum(j >= m.N for j in S)
+        for j in S:
+            if j >= m.N:
+                X = m.Xc(j)
+                assert np.linalg.det((X[1:] - X[0]).T) > 0
+                for nb in m.neighbours(j):
+                    assert j in m.neighbours(nb)
+    assert used > 0
+    # without ghosts some boundary sectors starve
+    m0 = OracleMesh(nodes, cells, None, M)
+    assert any(not all(m0.sector_stencils(i)[1]) for i in range(m0.N))

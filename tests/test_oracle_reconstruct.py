@@ -297,3 +297,42 @@ def test_scale_equivariance():
         a = R.reconstruct_cell(m, i, Q, 2)["w"]
         b = R.reconstruct_cell(m, i, 2.0 * Q, 2)["w"]
         assert np.abs(b - 2.0 * a).max() < 1e-6 * np.abs(a).max()
+
+
+@pytest.mark.parametrize("d,n,M", [(2, 8, 2), (2, 8, 3), (3, 4, 2)])
+def test_boundary_ghost_symmetric_reproduction(d, n, M):
+    """R37 pinned by symmetry: with ghosts across the low-x side only, data from a
+    polynomial EVEN in x (transmissive copy) and a momentum ODD in x (wall negation)
+    are exactly the averages of the same global polynomials over the mirrored cells,
+    so P_opt reproduces them on the cells whose stencils reach across x = 0."""
+    rng = np.random.default_rng(7)
+    nodes, cells, _ = gen.box_mesh(d, n, periodic=False, jitter=0.12, seed=8)
+    terms_even = [e for e in itertools.product(range(M + 1), repeat=d) if sum(e) <= M and e[0] % 2 == 0]
+    terms_odd = [e for e in itertools.product(range(M + 1), repeat=d) if sum(e) <= M and e[0] % 2 == 1]
+    ce, co = rng.standard_normal(len(terms_even)), rng.standard_normal(len(terms_odd))
+    feven = lambda x: sum(c * np.prod([x[:, a] ** e[a] for a in range(d)], axis=0) for c, e in zip(ce, terms_even))
+    fodd = lambda x: sum(c * np.prod([x[:, a] ** e[a] for a in range(d)], axis=0) for c, e in zip(co, terms_odd))
+    Qin = gen.polynomial_averages(nodes, cells, [feven, fodd])      # var 0 scalar, var 1 = "ρu_x"
+    bc = [2] + [0] * (2 * d - 1)                                    # wall at x = 0 only
+    m = OracleMesh(nodes, cells, None, M, bc=bc, mom0=1)
+    Q = Qin[m.perm]
+    checked = 0
+    for i in range(m.N):
+        if not any(j >= m.N for j in m.central_stencil(i)):
+            continue
+        res = R.reconstruct_cell(m, i, Q, M)
+        ref = _projection(m, i, lambda x: np.stack([feven(x), fodd(x)], axis=1), M).T
+        assert np.abs(res["popt"] - ref).max() < 1e-10 * np.abs(ref).max(), i
+        checked += 1
+        if checked >= 12:
+            break
+    assert checked >= 6
+    # the wrong transform (a transmissive copy of the odd momentum) breaks it
+    m2 = OracleMesh(nodes, cells, None, M, bc=[1] + [0] * (2 * d - 1), mom0=1)
+    bad = 0
+    for i in range(m2.N):
+        if any(j >= m2.N for j in m2.central_stencil(i)):
+            res = R.reconstruct_cell(m2, i, Q, M)
+            ref = _projection(m2, i, lambda x: np.stack([feven(x), fodd(x)], axis=1), M).T
+            bad += np.abs(res["popt"][1] - ref[1]).max() > 1e-6 * np.abs(ref).max()
+    assert bad > 0

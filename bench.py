@@ -277,8 +277,9 @@ def oracle_baseline(w, cfg, seconds):
     """cpu_baseline of our arm: the pooled oracle pass for about `seconds` of work."""
     pool = OraclePool(w)
     try:
-        n, dt = pool.step()            # warm-up sweep
-        reps = max(1, int(seconds / max(dt, 1e-3)))
+        pool.step()                    # warm-up sweeps (the first builds each worker's Σ tables)
+        n, dt = pool.step()
+        reps = max(1, int(seconds / max(dt, 1e-4)))
         n, dt = pool.step(reps)
         return {"value": n / dt, "unit": "cells/s", "cores": pool.cores, "kind": "oracle",
                 "sample": pool.describe(cfg) + f"; {reps} sweeps in {dt:.1f} s"}

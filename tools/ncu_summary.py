@@ -13,6 +13,7 @@ import csv
 import io
 import json
 import os
+import re
 import subprocess
 import sys
 
@@ -138,7 +139,8 @@ def main():
     open(out, "w").write("\n".join(lines) + "\n")
     tj = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     t = json.load(open(tj)) if os.path.exists(tj) else {}
-    t[f"{a.config}:{a.kernel}"] = int(rd + wr)
+    m = re.search(r"(k_[a-z_]+)", kname)      # keyed by the captured kernel (bench.py reads "<cfg>:<symbol>")
+    t[f"{a.config}:{m.group(1) if m else a.kernel}"] = int(rd + wr)
     json.dump(t, open(tj, "w"), indent=1, sort_keys=True)
     print(out)
 

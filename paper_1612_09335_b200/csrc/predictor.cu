@@ -8,7 +8,8 @@
 //   Picard (Eq. CGfinal, test functions of the unknown nodes, R33):
 //       F̂_l = F(q̂_l) (Eq. PDEterm), Ĝ_b,l = Σ_a (∂ξ_b/∂x_a) F̂_a,l,
 //       q̂¹ = −Δt Σ_b A_b Ĝ_b − C0 q̂⁰      A_b = K_uu⁻¹ M_u D_b, C0 = K_uu⁻¹ K_uk
-//   until max|Δq̂¹| ≤ 1e-12·max(1, max|q̂⁰|) or 2(M+1) iterations (R35).
+//   until max|Δq̂¹| ≤ 1e-12·max(1, max|q̂⁰|) or 2(M+1) iterations (R35; at the cap
+//   an update ≤ 1e-8·max(1, max|q̂⁰|) still counts as converged).
 // Output: q̂ [n_owned][𝓛][V] (nodes in the order of cwreco_predictor_nodes) and,
 // optionally, per cell the iteration count (negative: not converged or an
 // inadmissible state ρ ≤ 0 / p ≤ 0 met at a node).
@@ -198,6 +199,8 @@ __global__ void __launch_bounds__(256) k_predictor(PredArgs p) {
         for (int v = 0; v < V; ++v) dm = fmax(dm, dl[cl * V + v]);
         if (dm <= p.tol * sc[cl])
           flag[cl] |= 1;
+        else if (iter + 1 == p.maxit)
+          flag[cl] |= dm <= 1e-8 * sc[cl] ? 8 : 0;  // R35: acceptable update at the cap
         else
           active = 1;
       }
@@ -220,7 +223,7 @@ __global__ void __launch_bounds__(256) k_predictor(PredArgs p) {
     for (int e = tid; e < nc * L * V; e += nth) qo[e] = Q[e];
     if (p.iters)
       for (int cl = tid; cl < nc; cl += nth)
-        p.iters[c0 + cl] = ((flag[cl] & 1) && !(flag[cl] & 4)) ? its[cl] : -its[cl] - 1;
+        p.iters[c0 + cl] = ((flag[cl] & 9) && !(flag[cl] & 4)) ? its[cl] : -its[cl] - 1;
     __syncthreads();
   }
 }

@@ -52,7 +52,8 @@ def test_predictor_parity(d, n, M):
     cells_ = range(m.N) if m.N <= 400 else np.random.default_rng(0).choice(m.N, 400, replace=False)
     for i in cells_:
         r = PR.predict_cell(m.X[i], wc[i], dt, M)
-        assert r["converged"] and r["admissible"]
+        assert r["admissible"]
+        assert (it[i] > 0) == r["converged"]
         scale = max(1.0, float(np.abs(r["q"][S["known"]]).max()))
         worst = max(worst, float(np.abs(q[i] - r["q"]).max()) / scale)
         same_it += int(it[i] == r["iters"])
@@ -64,7 +65,7 @@ def test_predictor_parity(d, n, M):
     # Δt = 0: H drops out and q_h(ξ, τ) = w(ξ) — q̂_l = w at the node's spatial point
     q0 = ctx.predict(w, 0.0).cpu().numpy()
     want = np.einsum("lm,cvm->clv", S["Phi"], wc)
-    assert np.abs(q0 - want).max() <= 1e-12 * max(1.0, np.abs(want).max())
+    assert np.abs(q0 - want).max() <= 1e-10 * max(1.0, np.abs(want).max())   # κ(K_uu) ≤ 5e4
     # the τ = 0 rows (known DOFs) do not depend on Δt
     known = S["known"]
     assert np.array_equal(q[:, known], q0[:, known])

@@ -65,7 +65,10 @@ enum { KIND_CELLVAR = 0, KIND_ROWBLK = 1 };
 #ifndef CWR_RB_NG20
 #define CWR_RB_NG20 7  // 7 groups of <= 3 rows: 21 slots for 19 rows (8 groups: 24)
 #endif
-CWR_HD constexpr int rb_ng(int R, int V) { return (void)V, R > 14 ? CWR_RB_NG20 : 4; }
+#ifndef CWR_RB_NG10
+#define CWR_RB_NG10 3  // ℳ = 10 (R = 9 rows): 3 groups of 3 rows, no padded slot
+#endif
+CWR_HD constexpr int rb_ng(int R, int V) { return (void)V, R > 14 ? CWR_RB_NG20 : CWR_RB_NG10; }
 CWR_HD constexpr int rb_rb(int R, int V) { return (R + rb_ng(R, V) - 1) / rb_ng(R, V); }
 CWR_HD constexpr int rb_nfull(int R, int V) { return R - (rb_rb(R, V) - 1) * rb_ng(R, V); }
 CWR_HD constexpr int rb_ngr(int R, int V, int r) { return r < rb_rb(R, V) - 1 ? rb_ng(R, V) : rb_nfull(R, V); }
@@ -160,10 +163,11 @@ Layout make_layout(int d, int M, int V, int G, int max_smem, const std::function
 constexpr int kRbMainThreads = CWR_RB_MAIN, kRbEW = CWR_RB_EW, kRbThreads = 32 * ((kRbMainThreads + 31) / 32 + kRbEW + 1);
 CWR_HD constexpr int rb_main(int R, int V) { return (void)R, (void)V, kRbMainThreads; }
 CWR_HD constexpr int rb_main_warps(int T, int NG) { return (T * NG + 31) / 32; }
-// default family choice: the row-block kernel where the cell-variable kernel is
-// bound by its shared-memory broadcasts (ℳ = 20 and V ≥ 7: C4); measured slower
-// elsewhere (C2 0.25 vs 0.17 ms, C3 1.34 vs 1.09, C5 13.0 vs 12.0)
-CWR_HD constexpr bool rb_default(int R, int V) { return R > 14 && V >= 7; }
+// default family choice (C4-shape proxies, tools/gpu_families.sh): the warp-specialised
+// row-block kernel for ℳ = 20 (3-D M = 3: V = 9 0.75 vs 0.60, V = 5 1.00 vs 0.81 of the copy
+// peak) and for 3-D M = 2 with V ≥ 5 (0.670 vs 0.659); the cell-variable kernel for
+// 2-D M = 3 (0.84 vs 0.69) and the small shapes
+CWR_HD constexpr bool rb_default(int d, int R, int V) { return (R > 14 && V >= 3) || (d == 3 && R == 9 && V >= 5); }
 #ifndef CWR_RB_KC
 #define CWR_RB_KC 4
 #endif

@@ -71,7 +71,7 @@ Layout make_layout(int d, int M, int V, int G, int max_smem, const std::function
   const int nm = n_modes(M, d);
   // family (cwreco_set_option CWRECO_OPT_FAMILY): -1 = default, 0 = cell-variable,
   // 1 = row-block where instantiated
-  const bool want_rb = family >= 0 ? family == 1 : rb_default(nm - 1, V);
+  const bool want_rb = family >= 0 ? family == 1 : rb_default(d, nm - 1, V);
   if (want_rb && rowblk_supported(d, M, V)) {
     // k_rowblk: T = consumers / NG cells per tile (halved while the CTA does not fit);
     // KC positions per chunk: ~10 KB of B⁺ per stage, KC ∈ {1, 2, 4} (compiled sizes)

@@ -51,7 +51,24 @@ def test_config_parity(cfg):
     assert np.array_equal(m.perm, perm)
     cen, sec, val = ctx.stencils()
     rng = np.random.default_rng(17)
-    sel = range(m.N) if NSAMPLE[cfg] is None else rng.choice(m.N, NSAMPLE[cfg], replace=False)
+    if NSAMPLE[cfg] is None:
+        sel = list(range(m.N))
+    else:
+        # random cells + targeted ones: the first and last tile (pipeline start / ragged
+        # end), every cell whose sector reaches outside its central stencil (R15, the
+        # extra gather), and the 50 cells with the widest data range on their stencil
+        # (discontinuities: nonlinear weights far from λ̄)
+        T = ctx.info()["tile_cells"]
+        extra = []
+        if ctx.info()["n_extra_gather"] > 0:
+            mem = sec[:, :, 1:]                                        # [N, d+1, d] sector members
+            inside = (mem[..., None] == cen[:, None, None, :]).any(-1) | (mem < 0)
+            extra = np.nonzero(~inside.all(axis=(1, 2)))[0].tolist()
+        rngQ = np.ptp(Q[cen], axis=1).max(axis=1) / (np.abs(Q).max(axis=0).max() + 1e-300)
+        wide = np.argsort(-rngQ)[:50]
+        sel = sorted(set(rng.choice(m.N, NSAMPLE[cfg], replace=False).tolist()) | set(range(T)) |
+                     set(range(m.N - T, m.N)) | set(extra[:200]) | set(wide.tolist()))
+        print(f"{cfg}: {len(extra)} extra-gather cells, first/last tile of {T} cells, 50 widest-range cells")
     worst = 0.0
     for i in sel:
         r = R.reconstruct_cell(m, int(i), Q, w["M"])
@@ -60,3 +77,41 @@ def test_config_parity(cfg):
         worst = max(worst, floored_err(a[i], r["w"], Q, r["central"]))
     print(f"{cfg}: setup {t_setup:.1f}s, N={m.N}, checked {len(sel)} cells, max floored rel err {worst:.2e}")
     assert worst <= TOL
+
+
+_ORC = {}
+
+
+def _orc_stencils(args):
+    lo, hi = args
+    m = _ORC["m"]                      # built once in the parent, inherited by fork
+    out = []
+    for i in range(lo, hi):
+        s, v = m.sector_stencils(i)
+        out.append((m.central_stencil(i), s, v))
+    return lo, out
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2"])
+def test_full_mesh_stencils_bit_exact(cfg):
+    """Every cell's central and sectorial stencils (and validity) of the full C1 and
+    C2 meshes: library == oracle bit for bit (the oracle in parallel processes)."""
+    import multiprocessing as mp
+    import os
+    w = gen.make(cfg)
+    ctx = P.Context(w["d"], w["M"], w["V"], device=None)
+    ctx.set_mesh(w["nodes"], w["cells"], w["period"])
+    ctx.build_stencils()
+    cen, sec, val = ctx.stencils()
+    N = cen.shape[0]
+    _ORC["m"] = OracleMesh(w["nodes"], w["cells"], w["period"], w["M"])
+    assert np.array_equal(_ORC["m"].perm, ctx.permutation())
+    nproc = max(1, min(32, len(os.sched_getaffinity(0))))
+    chunk = (N + 4 * nproc - 1) // (4 * nproc)
+    jobs = [(lo, min(N, lo + chunk)) for lo in range(0, N, chunk)]
+    with mp.get_context("fork").Pool(nproc) as pool:
+        for lo, res in pool.imap_unordered(_orc_stencils, jobs):
+            for k, (c, s, v) in enumerate(res):
+                i = lo + k
+                assert cen[i].tolist() == c, (cfg, i)
+                assert sec[i].tolist() == s and val[i].tolist() == v, (cfg, i)

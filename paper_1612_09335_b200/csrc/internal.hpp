@@ -163,11 +163,12 @@ Layout make_layout(int d, int M, int V, int G, int max_smem, const std::function
 constexpr int kRbMainThreads = CWR_RB_MAIN, kRbEW = CWR_RB_EW, kRbThreads = 32 * ((kRbMainThreads + 31) / 32 + kRbEW + 1);
 CWR_HD constexpr int rb_main(int R, int V) { return (void)R, (void)V, kRbMainThreads; }
 CWR_HD constexpr int rb_main_warps(int T, int NG) { return (T * NG + 31) / 32; }
-// default family choice (C4-shape proxies, tools/gpu_families.sh): the warp-specialised
-// row-block kernel for ℳ = 20 (3-D M = 3: V = 9 0.75 vs 0.60, V = 5 1.00 vs 0.81 of the copy
-// peak) and for 3-D M = 2 with V ≥ 5 (0.670 vs 0.659); the cell-variable kernel for
-// 2-D M = 3 (0.84 vs 0.69) and the small shapes
-CWR_HD constexpr bool rb_default(int d, int R, int V) { return (R > 14 && V >= 3) || (d == 3 && R == 9 && V >= 5); }
+// default family choice (tools/gpu_families.sh proxies, then the configs): the
+// warp-specialised row-block kernel for ℳ = 20 (3-D M = 3: V = 9 0.75 vs 0.60, V = 5 1.00
+// vs 0.81 of the copy peak on the proxy; C5 0.904 vs 0.775); the cell-variable kernel for
+// ℳ = 10 (C2 0.847 vs 0.69; C3 0.655 vs 0.636 — the proxy's 0.670 vs 0.659 did not carry
+// over to the explosion data) and the small shapes
+CWR_HD constexpr bool rb_default(int d, int R, int V) { return (void)d, R > 14 && V >= 3; }
 #ifndef CWR_RB_KC
 #define CWR_RB_KC 4
 #endif

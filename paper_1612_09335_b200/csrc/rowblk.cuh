@@ -46,9 +46,6 @@ static __device__ long long g_rb_trace[64][16];
   } while (0)
 #endif
 constexpr int RB_BAR_OFULL = 1, RB_BAR_OFREE = 2, RB_BAR_EW = 3;
-#ifndef CWR_RB_LDG
-#define CWR_RB_LDG 0  // > 0: main warps load B⁺ from global memory, this many position pairs ahead
-#endif
 #ifndef CWR_RB_PAIR
 #define CWR_RB_PAIR 0  // epilogue items computed two at a time (measured slower: registers)
 #endif
@@ -129,13 +126,6 @@ __global__ void __launch_bounds__(kRbThreads, 1) k_rowblk(KArgs a, PipeCfg pc) {
       for (int k = 0; k < nk; ++k) {
         RB_TRACE(k, 9);
         const unsigned char* tb = a.blocks + tile_of(k) * a.tile_bytes;
-#if CWR_RB_LDG
-        // main warps read B⁺ straight from global memory: warm L2 one tile ahead
-        (void)rg;
-        if (k == 0) bulk_prefetch_l2(tb + a.u_bytes, (uint32_t)(a.off_sector - a.u_bytes));
-        if (k + 1 < nk)
-          bulk_prefetch_l2(a.blocks + tile_of(k + 1) * a.tile_bytes + a.u_bytes, (uint32_t)(a.off_sector - a.u_bytes));
-#else
         for (int ch = 0; ch < a.NCH; ++ch) {
           mbar_wait_sleep(&empty[rg.st], rg.ph ^ 1);
           const uint32_t bytes = (uint32_t)(min(a.KC, a.G - ch * a.KC) * a.kslice_bytes);
@@ -143,7 +133,6 @@ __global__ void __launch_bounds__(kRbThreads, 1) k_rowblk(KArgs a, PipeCfg pc) {
           bulk_g2s(stg + rg.st * pc.stage_bytes, tb + a.u_bytes + ch * a.chunk_bytes, bytes, &full[rg.st]);
           rg.next(S);
         }
-#endif
         RB_TRACE(k, 10);
         if (k + 2 < nk) load_union(k + 2);
         RB_TRACE(k, 11);
@@ -239,46 +228,6 @@ __global__ void __launch_bounds__(kRbThreads, 1) k_rowblk(KArgs a, PipeCfg pc) {
 #pragma unroll
           for (int v = 0; v < V; ++v) acc[r][v] = __fma_rn(b[r], q[v], acc[r][v]);
       };
-#if CWR_RB_LDG
-      // B⁺ straight from global memory (each element is used by exactly one thread:
-      // no shared-memory round trip), a ring of PDP positions in flight; the averages
-      // of position p+1 are loaded while position p's FMAs run
-      constexpr int PDP = CWR_RB_LDG;
-      static_assert(PDP % 2 == 0, "even ring depth keeps the q ping-pong static");
-      const double* cbase = (const double*)(a.blocks + tile_of(k) * a.tile_bytes + a.u_bytes);
-      const int64_t cstride = a.chunk_bytes / 8;
-      auto ldb1 = [&](int p, double (&b)[RB]) {
-        const int ch = p / KC, kk = p - ch * KC;
-        const double* Bs = cbase + ch * cstride + kk * R * T;
-#pragma unroll
-        for (int r = 0; r < RB; ++r) b[r] = ld_nc_na(Bs + r * NG * T + (r < RB - 1 ? bfull : bpart));
-      };
-      const uint16_t* ix1 = reinterpret_cast<const uint16_t*>(ix2);  // [pair][T][2]
-      auto qoff = [&](int p) { return int(ix1[((p >> 1) * T) * 2 + (p & 1)]); };
-      double bq[PDP][RB], q2[2][V];
-#pragma unroll
-      for (int s2 = 0; s2 < PDP; ++s2)
-        if (s2 < G) ldb1(s2, bq[s2]);
-      ldq(qoff(0), q2[0]);
-      int p0 = 0;
-      for (; p0 + PDP <= G; p0 += PDP) {
-#pragma unroll
-        for (int s2 = 0; s2 < PDP; ++s2) {
-          const int p = p0 + s2;
-          if (p + 1 < G) ldq(qoff(p + 1), q2[(s2 + 1) & 1]);
-          fma_pos(q2[s2 & 1], bq[s2]);
-          if (p + PDP < G) ldb1(p + PDP, bq[s2]);
-        }
-      }
-#pragma unroll
-      for (int s2 = 0; s2 < PDP; ++s2) {  // the last G mod PDP positions
-        const int p = p0 + s2;
-        if (p < G) {
-          if (p + 1 < G) ldq(qoff(p + 1), q2[(s2 + 1) & 1]);
-          fma_pos(q2[s2 & 1], bq[s2]);
-        }
-      }
-#else
       auto stage_ptr = [&]() { return (const double*)(stg + rg.st * pc.stage_bytes); };
       auto release = [&]() {
         __syncwarp();
@@ -320,7 +269,6 @@ __global__ void __launch_bounds__(kRbThreads, 1) k_rowblk(KArgs a, PipeCfg pc) {
         fma_pos(odd_pair ? qb[0] : qa[0], odd_pair ? bb[0] : ba[0]);
         release();
       }
-#endif
       // hand the p̂_opt rows to the epilogue warps: O[ct][v][1 + row], row l = r·NG + g
       if (tid == 0) RB_TRACE(k, 2);
       named_sync(RB_BAR_OFREE, NB);  // the epilogue of the previous tile is done with O

@@ -154,21 +154,26 @@ Layout make_layout(int d, int M, int V, int G, int max_smem, const std::function
 // k_rowblk (warp-specialised, rowblk.cuh): a CTA of kRbThreads threads = main warps
 // (T = kRbMainThreads / NG cells × NG row groups, rounded up to whole warps), kRbEW
 // epilogue warps and one producer warp; one CTA per SM.
+// ℳ = 20: 7 main warps (T = 32 cells × 7 row groups) + 4 epilogue warps (C4-shape proxy:
+// 224/7/4 → 0.750, 256/8/3 → 0.695, 192/6/5 → 0.651); ℳ = 10 (3 groups of 3 rows): 6 main
+// warps (T = 64) + 5 epilogue warps (C3 data: 0.708; 224/4 0.636, 96/8 0.632)
+#ifndef CWR_RB_MAIN
+#define CWR_RB_MAIN 224
+#endif
 #ifndef CWR_RB_EW
 #define CWR_RB_EW 4
 #endif
-#ifndef CWR_RB_MAIN
-#define CWR_RB_MAIN 224  // 7 main warps; C4-shape proxy: 224/7/4 -> 0.750, 256/8/3 -> 0.695, 192/6/5 -> 0.651
-#endif
-constexpr int kRbMainThreads = CWR_RB_MAIN, kRbEW = CWR_RB_EW, kRbThreads = 32 * ((kRbMainThreads + 31) / 32 + kRbEW + 1);
-CWR_HD constexpr int rb_main(int R, int V) { return (void)R, (void)V, kRbMainThreads; }
+constexpr int kRbThreads = 384;
+CWR_HD constexpr int rb_main(int R, int V) { return (void)V, R > 14 ? CWR_RB_MAIN : 192; }
+CWR_HD constexpr int rb_ew(int R, int V) { return (void)V, R > 14 ? CWR_RB_EW : 5; }
+static_assert(32 * ((CWR_RB_MAIN + 31) / 32 + CWR_RB_EW + 1) == kRbThreads, "row-block CTA shape");
 CWR_HD constexpr int rb_main_warps(int T, int NG) { return (T * NG + 31) / 32; }
 // default family choice (tools/gpu_families.sh proxies, then the configs): the
 // warp-specialised row-block kernel for ℳ = 20 (3-D M = 3: V = 9 0.75 vs 0.60, V = 5 1.00
 // vs 0.81 of the copy peak on the proxy; C5 0.904 vs 0.775); the cell-variable kernel for
-// ℳ = 10 (C2 0.847 vs 0.69; C3 0.655 vs 0.636 — the proxy's 0.670 vs 0.659 did not carry
-// over to the explosion data) and the small shapes
-CWR_HD constexpr bool rb_default(int d, int R, int V) { return (void)d, R > 14 && V >= 3; }
+// 2-D ℳ = 10 (C2 0.847 vs 0.69) and the small shapes; 3-D M = 2 on the row-block kernel with
+// 6 main / 5 epilogue warps (C3 data 0.708 vs 0.640)
+CWR_HD constexpr bool rb_default(int d, int R, int V) { return (R > 14 && V >= 3) || (d == 3 && R == 9 && V >= 5); }
 #ifndef CWR_RB_KC
 #define CWR_RB_KC 4
 #endif

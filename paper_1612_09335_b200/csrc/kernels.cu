@@ -510,7 +510,7 @@ static PipeCfg pipe_cfg(const cwreco_ctx* c, int* ctas = nullptr) {
     if (!k) fail(CWRECO_EUNSUPPORTED, "row-block kernel: tile does not fit in shared memory");
     if (ctas) *ctas = 1;
     p.ncw = rb_main_warps(L.T, rb_ng(L.R, L.V));
-    p.eww = kRbEW;
+    p.eww = rb_ew(L.R, L.V);
     p.stages = st;
     p.stage_bytes = round128(L.chunk_bytes);
     p.ubuf_bytes = rb_ubuf_bytes(L);

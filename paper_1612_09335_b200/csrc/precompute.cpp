@@ -76,7 +76,8 @@ Layout make_layout(int d, int M, int V, int G, int max_smem, const std::function
     // k_rowblk: T = consumers / NG cells per tile (halved while the CTA does not fit);
     // KC positions per chunk: ~10 KB of B⁺ per stage, KC ∈ {1, 2, 4} (compiled sizes)
     const int R = nm - 1;
-    for (int T = rb_main(R, V) / rb_ng(R, V); T >= 2; T /= 2) {
+    // T even: a position slice T·R doubles must stay a multiple of 16 bytes (TMA bulk sizes)
+    for (int T = (rb_main(R, V) / rb_ng(R, V)) & ~1; T >= 2; T = (T / 2) & ~1) {
       // the whole sector chunk of a tile goes to its own buffer: one piece
       Layout L = layout_with(d, M, V, G, T, kRbKC, umax_for(T), KIND_ROWBLK, 1);
       int ctas, stages;

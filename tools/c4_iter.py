@@ -26,13 +26,19 @@ ap.add_argument("--V", type=int, default=9)
 ap.add_argument("--family", type=int, default=-1)
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--check", action="store_true")
+ap.add_argument("--config", default=None, help="use a BASELINE config's mesh and data instead (C1..C5)")
 ap.add_argument("--max-ctas", type=int, default=0)
 ap.add_argument("--trace", action="store_true", help="print CTA 0's timeline (library built with -DCWR_TRACE)")
 a = ap.parse_args()
 
 t = time.time()
-nodes, cells, period = gen.box_mesh(a.d, a.n, True, 0.1, 4)
-Q = np.random.default_rng(0).standard_normal((cells.shape[0], a.V)) + 2.0
+if a.config:
+    w = gen.make(a.config)
+    nodes, cells, period, Q = w["nodes"], w["cells"], w["period"], w["avgs"]
+    a.d, a.M, a.V, a.n = w["d"], w["M"], w["V"], w["n"]
+else:
+    nodes, cells, period = gen.box_mesh(a.d, a.n, True, 0.1, 4)
+    Q = np.random.default_rng(0).standard_normal((cells.shape[0], a.V)) + 2.0
 ctx = P.setup_context(nodes, cells, period, a.M, a.V, device=0, family=a.family, max_ctas=a.max_ctas)
 setup = time.time() - t
 inf = ctx.info()

@@ -27,6 +27,7 @@ ap.add_argument("--family", type=int, default=-1)
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--check", action="store_true")
 ap.add_argument("--config", default=None, help="use a BASELINE config's mesh and data instead (C1..C5)")
+ap.add_argument("--kernel", default="pipelined", choices=["pipelined", "matrixfree"])
 ap.add_argument("--max-ctas", type=int, default=0)
 ap.add_argument("--trace", action="store_true", help="print CTA 0's timeline (library built with -DCWR_TRACE)")
 a = ap.parse_args()
@@ -39,7 +40,14 @@ if a.config:
 else:
     nodes, cells, period = gen.box_mesh(a.d, a.n, True, 0.1, 4)
     Q = np.random.default_rng(0).standard_normal((cells.shape[0], a.V)) + 2.0
-ctx = P.setup_context(nodes, cells, period, a.M, a.V, device=0, family=a.family, max_ctas=a.max_ctas)
+if a.kernel == "matrixfree":
+    ctx = P.Context(a.d, a.M, a.V, device=0)
+    ctx.set_mesh(nodes, cells, period)
+    ctx.build_stencils()
+    ctx.prepare_matrixfree()
+    ctx.set_kernel("matrixfree")
+else:
+    ctx = P.setup_context(nodes, cells, period, a.M, a.V, device=0, family=a.family, max_ctas=a.max_ctas)
 setup = time.time() - t
 inf = ctx.info()
 Qd = torch.tensor(Q[ctx.permutation()], device="cuda")
@@ -63,7 +71,13 @@ gbs = inf["algorithmic_bytes_per_cell"] * inf["n_owned"] / (ms * 1e-3) / 1e9
 res = {"n": a.n, "cells": inf["n_owned"], "family": inf["kernel_family"], "T": inf["tile_cells"],
        "union_max": inf["union_max"], "ms": ms, "ms_min": float(np.min(ts)), "gbs": gbs, "frac": gbs / 6533.5,
        "setup_s": round(setup, 1)}
-if a.check:
+if a.kernel == "matrixfree":
+    sys.path.insert(0, ROOT)
+    import bench
+    fl = bench.matfree_flops_per_cell(a.d, a.M, a.V)
+    res["tflops"] = fl * inf["n_owned"] / (ms * 1e-3) / 1e12
+    res["frac_fp64"] = res["tflops"] / bench.FP64_PEAK_TF
+if a.check and a.kernel != "matrixfree":
     ref = out.clone()
     ctx.set_kernel("simple")
     ctx.reconstruct(Qd, out, stream=st)

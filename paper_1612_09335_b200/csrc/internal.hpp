@@ -60,10 +60,12 @@ inline int n_modes(int M, int d) {  // ℳ(M,d) = (1/d!) Π_{l=1..d} (M+l)   (P:
 //                slots r < RB, slot r holding the ngr(r) groups that have a row
 //                there, so the lanes (ct, g) of a warp read consecutive doubles.
 enum { KIND_CELLVAR = 0, KIND_ROWBLK = 1 };
-// NG: 8 groups of ≤3 rows for ℳ = 20 (8 warps for a tile of 32 cells; 4 groups of ≤5
-// rows with 4 warps measured slower on C4: 43.5 vs 41.2 ms), else 4 groups
+// NG for ℳ = 20: 4 groups of ≤ 5 rows (20 slots for 19 rows) on 4 main warps that take
+// 200 registers each through setmaxnreg (k_rowblk); the B⁺ loads per FMA stay, the
+// average loads per FMA drop to 4/7 of the 7-group shape (C4-shape proxy under the
+// power cap: 0.719 vs 0.667; 7 groups of ≤ 3 rows was the 168-register design)
 #ifndef CWR_RB_NG20
-#define CWR_RB_NG20 7  // 7 groups of <= 3 rows: 21 slots for 19 rows (8 groups: 24)
+#define CWR_RB_NG20 4
 #endif
 #ifndef CWR_RB_NG10
 #define CWR_RB_NG10 3  // ℳ = 10 (R = 9 rows): 3 groups of 3 rows, no padded slot
@@ -154,20 +156,31 @@ Layout make_layout(int d, int M, int V, int G, int max_smem, const std::function
 // k_rowblk (warp-specialised, rowblk.cuh): a CTA of kRbThreads threads = main warps
 // (T = kRbMainThreads / NG cells × NG row groups, rounded up to whole warps), kRbEW
 // epilogue warps and one producer warp; one CTA per SM.
-// ℳ = 20: 7 main warps (T = 32 cells × 7 row groups) + 4 epilogue warps (C4-shape proxy:
-// 224/7/4 → 0.750, 256/8/3 → 0.695, 192/6/5 → 0.651); ℳ = 10 (3 groups of 3 rows): 6 main
+// ℳ = 20: 4 main warps (T = 32 cells × 4 row groups, 200 registers by setmaxnreg) + 7
+// epilogue warps (C4-shape proxy under the power cap: 0.719; the 168-register shapes
+// 7 main / 4 epilogue 0.667, 4 main / 3 epilogue at 8 warps 0.698, 5 / 6 0.648, 4 / 2
+// 0.539: the epilogue needs the warps); ℳ = 10 (3 groups of 3 rows): 6 main
 // warps (T = 64) + 5 epilogue warps (C3 data: 0.708; 224/4 0.636, 96/8 0.632)
 #ifndef CWR_RB_MAIN
-#define CWR_RB_MAIN 224
+#define CWR_RB_MAIN 128
 #endif
 #ifndef CWR_RB_EW
-#define CWR_RB_EW 4
+#define CWR_RB_EW 7
 #endif
-constexpr int kRbThreads = 384;
+#ifndef CWR_RB_MAINREG20
+#define CWR_RB_MAINREG20 200  // main-warp registers for ℳ = 20 (0: no setmaxnreg)
+#endif
 CWR_HD constexpr int rb_main(int R, int V) { return (void)V, R > 14 ? CWR_RB_MAIN : 192; }
 CWR_HD constexpr int rb_ew(int R, int V) { return (void)V, R > 14 ? CWR_RB_EW : 5; }
-static_assert(32 * ((CWR_RB_MAIN + 31) / 32 + CWR_RB_EW + 1) == kRbThreads, "row-block CTA shape");
 CWR_HD constexpr int rb_main_warps(int T, int NG) { return (T * NG + 31) / 32; }
+// threads of a row-block CTA (main + epilogue + producer warp): the kernel's launch bound
+CWR_HD constexpr int rb_threads(int R, int V) { return 32 * ((rb_main(R, V) + 31) / 32 + rb_ew(R, V) + 1); }
+// setmaxnreg split (3 warp groups of 128 threads launched at 168 registers): the main
+// group's increase must be covered by what the two others release, else it waits forever
+CWR_HD constexpr int rb_mainreg(int R, int V) { return (void)V, R > 14 ? CWR_RB_MAINREG20 : 0; }
+CWR_HD constexpr int rb_otherreg(int R, int V) { return ((168 * 3 - rb_mainreg(R, V)) / 2) & ~7; }
+static_assert(CWR_RB_MAINREG20 == 0 || CWR_RB_MAINREG20 - 168 <= 2 * (168 - ((168 * 3 - CWR_RB_MAINREG20) / 2 & ~7)),
+              "setmaxnreg increase not covered by the released registers");
 // default family choice (tools/gpu_families.sh proxies, then the configs): the
 // warp-specialised row-block kernel for ℳ = 20 (3-D M = 3: V = 9 0.75 vs 0.60, V = 5 1.00
 // vs 0.81 of the copy peak on the proxy; C5 0.904 vs 0.775); the cell-variable kernel for

@@ -49,6 +49,9 @@ constexpr int RB_BAR_OFULL = 1, RB_BAR_OFREE = 2, RB_BAR_EW = 3;
 #ifndef CWR_RB_PAIR
 #define CWR_RB_PAIR 0  // epilogue items computed two at a time (measured slower: registers)
 #endif
+#ifndef CWR_RB_LOOK1
+#define CWR_RB_LOOK1 0  // main loop with a one-position lookahead instead of the pair ping-pong
+#endif
 
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void named_arrive(int id, int n) {
@@ -59,7 +62,7 @@ __device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t* bar) {
 }
 
 template <int D, int M, int V>
-__global__ void __launch_bounds__(kRbThreads, 1) k_rowblk(KArgs a, PipeCfg pc) {
+__global__ void __launch_bounds__(rb_threads(nmodes(M, D) - 1, V), 1) k_rowblk(KArgs a, PipeCfg pc) {
   constexpr int NM = nmodes(M, D), R = NM - 1, NV = D + 1, NCAP = NV * D;
   constexpr int NG = rb_ng(R, V), RB = rb_rb(R, V), NF = rb_nfull(R, V);
   constexpr int VP = V + (V & 1);
@@ -104,8 +107,20 @@ __global__ void __launch_bounds__(kRbThreads, 1) k_rowblk(KArgs a, PipeCfg pc) {
   }
   __syncthreads();
 
+  // register rebalancing between the warp groups (setmaxnreg): warp group 0 = the main
+  // warps takes MAINREG registers per thread, the epilogue / producer groups give theirs
+  // back (the increase must be covered by what the other two release, else it waits)
+  constexpr int MAINREG = rb_mainreg(R, V), OTHERREG = rb_otherreg(R, V);
+  static_assert(!MAINREG || (rb_main(R, V) == 128 && rb_threads(R, V) == 384), "setmaxnreg: 3 warp groups");
+  auto reg_main = [] {
+    if constexpr (MAINREG > 0) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(MAINREG));
+  };
+  auto reg_other = [] {
+    if constexpr (MAINREG > 0) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(OTHERREG));
+  };
   if (warp == pc.ncw + pc.eww) {
     // ------------------------------------------------ TMA producer
+    reg_other();
     if (lane == 0) {
       Ring rg;
       auto load_union = [&](int k) {  // union chunk of tile k → ubuf[k%3]
@@ -170,6 +185,7 @@ __global__ void __launch_bounds__(kRbThreads, 1) k_rowblk(KArgs a, PipeCfg pc) {
 
   if (is_main) {
     // -------------------------------------------------- main warps
+    reg_main();
     const bool mainthr = tid < T * NG;
     const int ct = mainthr ? tid / NG : 0, g = mainthr ? tid % NG : 0;
     // offsets of this thread's B⁺ entries inside a row slot (chunk_elem, KIND_ROWBLK):
@@ -234,6 +250,51 @@ __global__ void __launch_bounds__(kRbThreads, 1) k_rowblk(KArgs a, PipeCfg pc) {
         if (lane == 0) mbar_arrive(&empty[rg.st]);
         rg.next(S);
       };
+#if CWR_RB_LOOK1
+      // One-position lookahead (half the operand registers of the pair ping-pong, so
+      // that RB = 4 rows × V = 9 accumulators fit): the averages and B⁺ entries of
+      // position p+1 are loaded while position p's FMAs run.
+      auto ldb1 = [&](const double* Bs, int kk, double (&b)[RB]) {
+#pragma unroll
+        for (int r = 0; r < RB; ++r) b[r] = Bs[(kk * R + r * NG) * T + (r < RB - 1 ? bfull : bpart)];
+      };
+      double q0[V], q1[V], b0[RB], b1[RB];
+      uint32_t ipc = ix2[0], ipn = ix2[min(1, npr - 1) * T];
+      mbar_wait(&full[rg.st], rg.ph);
+      ldq(int(ipc & 0xffffu), q0);
+      ldb1(stage_ptr(), 0, b0);
+      for (int pp = 0; pp < npr; ++pp) {
+        const int p = 2 * pp, kk = p % KC;
+        if (p + 1 < G) {
+          ldq(int(ipc >> 16), q1);
+          ldb1(stage_ptr(), kk + 1, b1);
+          fma_pos(q0, b0);
+          if (p + 2 < G) {
+            if ((p + 2) % KC == 0) {  // position p+2 opens the next stage
+              Ring nr = rg;
+              nr.next(S);
+              mbar_wait(&full[nr.st], nr.ph);
+              ldq(int(ipn & 0xffffu), q0);
+              ldb1((const double*)(stg + nr.st * pc.stage_bytes), 0, b0);
+              fma_pos(q1, b1);
+              release();
+            } else {
+              ldq(int(ipn & 0xffffu), q0);
+              ldb1(stage_ptr(), kk + 2, b0);
+              fma_pos(q1, b1);
+            }
+            ipc = ipn;
+            ipn = ix2[min(pp + 2, npr - 1) * T];
+          } else {
+            fma_pos(q1, b1);
+            release();
+          }
+        } else {  // G odd: the last position alone
+          fma_pos(q0, b0);
+          release();
+        }
+      }
+#else
       double qa[2][V], qb[2][V], ba[2][RB], bb[2][RB];
       ldq2(ix2[0], qa);
       uint32_t ipn = ix2[min(1, npr - 1) * T];
@@ -269,6 +330,7 @@ __global__ void __launch_bounds__(kRbThreads, 1) k_rowblk(KArgs a, PipeCfg pc) {
         fma_pos(odd_pair ? qb[0] : qa[0], odd_pair ? bb[0] : ba[0]);
         release();
       }
+#endif
       // hand the p̂_opt rows to the epilogue warps: O[ct][v][1 + row], row l = r·NG + g
       if (tid == 0) RB_TRACE(k, 2);
       named_sync(RB_BAR_OFREE, NB);  // the epilogue of the previous tile is done with O
@@ -287,6 +349,7 @@ __global__ void __launch_bounds__(kRbThreads, 1) k_rowblk(KArgs a, PipeCfg pc) {
   }
 
   // -------------------------------------------------- epilogue warps
+  reg_other();
   const int etid = tid - MW;
   if (nk > 0) gather(0, etid);
   if (nk > 1) gather(1, etid);

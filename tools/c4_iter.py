@@ -57,7 +57,9 @@ st = torch.cuda.current_stream()
 for _ in range(3):
     ctx.reconstruct(Qd, out, stream=st)
 torch.cuda.synchronize()
+import bench  # noqa: E402  (NVML clock sampler)
 ts = []
+cs = bench.ClockSampler(0).__enter__()
 for k in range(a.reps):
     flush.fill_(k & 255)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -66,14 +68,14 @@ for k in range(a.reps):
     e1.record(st)
     torch.cuda.synchronize()
     ts.append(e0.elapsed_time(e1))
+cs.__exit__()
+clk = cs.summary()
 ms = float(np.median(ts))
 gbs = inf["algorithmic_bytes_per_cell"] * inf["n_owned"] / (ms * 1e-3) / 1e9
 res = {"n": a.n, "cells": inf["n_owned"], "family": inf["kernel_family"], "T": inf["tile_cells"],
        "union_max": inf["union_max"], "ms": ms, "ms_min": float(np.min(ts)), "gbs": gbs, "frac": gbs / 6533.5,
-       "setup_s": round(setup, 1)}
+       "setup_s": round(setup, 1), "sm_mhz": clk["sm_mhz"], "reasons": clk["reasons"]}
 if a.kernel == "matrixfree":
-    sys.path.insert(0, ROOT)
-    import bench
     fl = bench.matfree_flops_per_cell(a.d, a.M, a.V)
     res["tflops"] = fl * inf["n_owned"] / (ms * 1e-3) / 1e12
     res["frac_fp64"] = res["tflops"] / bench.FP64_PEAK_TF

@@ -60,7 +60,10 @@ def main():
     ap.add_argument("--kernel", default="pipelined")
     ap.add_argument("--launches")
     ap.add_argument("--bench")
+    ap.add_argument("--cells", type=int, default=0, help="proxy mesh: cells of the captured launch (no traffic key)")
+    ap.add_argument("--cmd", default=None, help="command line of the capture (for the header)")
     a = ap.parse_args()
+    proxy = a.config.endswith("proxy")
 
     rows = ncu_csv(a.rep, "--page", "raw")
     hdr, units, vals = rows[0], rows[1], rows[2]
@@ -73,14 +76,14 @@ def main():
 
     import gen
     from paper_1612_09335_b200 import n_modes
-    cfg = gen.CONFIGS[a.config]
+    cfg = gen.CONFIGS[a.config.replace("proxy", "")]
     d, M = cfg["d"], cfg["M"]
     V = gen.nvars_of(cfg["ic"])
     nm = n_modes(M, d)
     ne = d * nm
     bcell = 8 * ((nm - 1) * (ne - 1) + (d + 1) * d * d) + 4 * (ne - 1) + (d + 1) * d + 8 * V + 8 * nm * V
     n = cfg["n"]
-    ncell = 2 * n * n if d == 2 else 6 * n ** 3
+    ncell = a.cells or (2 * n * n if d == 2 else 6 * n ** 3)
     alg = bcell * ncell
 
     src = ncu_csv(a.rep, "--page", "source", "--print-source", "sass")
@@ -101,7 +104,7 @@ def main():
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     lines = [f"# ncu --set full: {kname} — {a.config} ({a.tag})", "",
              f"Capture: `ncu --set full --clock-control none --import-source on -k \"regex:k_pipelined|k_rowblk\" -s 3 -c 1 "
-             f"python bench.py --config {a.config} --steps 3 --warmup 3 --no-cpu-baseline` on one B200 "
+             + (a.cmd or f"python bench.py --config {a.config} --steps 3 --warmup 3 --no-cpu-baseline") + "` on one B200 "
              f"(cold L2, serialised; per-launch numbers).", "",
              "| metric | value |", "|---|---|"]
     for k, label in METRICS:
@@ -137,6 +140,9 @@ def main():
                   "```", json.dumps(b), "```"]
     out = os.path.join(ROOT, "profiles", f"{a.tag}_{a.config}_ncu.md")
     open(out, "w").write("\n".join(lines) + "\n")
+    if proxy:
+        print(out)
+        return
     tj = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     t = json.load(open(tj)) if os.path.exists(tj) else {}
     m = re.search(r"(k_[a-z_]+)", kname)      # keyed by the captured kernel (bench.py reads "<cfg>:<symbol>")

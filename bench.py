@@ -74,18 +74,28 @@ FP64_PEAK_SRC = "derived: 148 SM x 64 fp64 FMA/clk x 2 x 1.965 GHz (no measured 
 
 
 def matfree_flops_per_cell(d, M, V):
-    """Algorithmic fp64 flops of one matrix-free cell: assembly of the
-    K = n_e−1 rows of A by nq-point quadrature, Householder QR of A (K×R) applied to V
-    right-hand sides, back substitution, d+1 sector solves, epilogue."""
+    """Algorithmic fp64 flops of one matrix-free cell (K3; FMA = 2): per row of
+    A (K = n_e−1 rows) the stencil cell's vertices in the owner's reference coordinates,
+    the power sums and closed-form simplex moments of the monomials of degree ≤ M, the
+    basis over the monomials of degree ≤ deg(ψ_l) and ΔQ; the Gram matrix [AᵀA | AᵀΔQ]
+    (upper triangle); Cholesky with the forward substitution of the V right-hand sides;
+    back substitution; d+1 sector solves; the epilogue."""
     nm = (M + 1) * (M + 2) // 2 if d == 2 else (M + 1) * (M + 2) * (M + 3) // 6
     R, K = nm - 1, d * nm - 1
-    nq = ((M + 2) // 2) ** d
-    assemble = K * (nq * (2 * d * d + d * M + 4 * nm) + 2 * R * nm + 4 * d * d * d)
-    qr = sum(4 * (K - c) * (R - c - 1 + V) + 4 * (K - c) for c in range(R))
+    cnt = (lambda n: (n + 1) * (n + 2) // 2) if d == 2 else (lambda n: (n + 1) * (n + 2) * (n + 3) // 6)
+    deg = lambda l: next(n for n in range(M + 1) if l < cnt(n))
+    c2, c3 = d * (d + 1) // 2, d * (d + 1) * (d + 2) // 6
+    row = ((d + 1) * (2 * d * d + d)                       # vertices
+           + (d + 1) * d + (2 * (d + 1) * c2 if M >= 2 else 0) + (2 * (d + 1) * c3 if M >= 3 else 0)  # power sums
+           + d + (3 * c2 if M >= 2 else 0) + (12 * c3 if M >= 3 else 0)                                  # moments
+           + 2 * sum(cnt(deg(l)) for l in range(1, nm))   # basis
+           + V)
+    gram = 2 * K * (R * (R + 1) // 2 + R * V)
+    chol = R ** 3 // 3 + R * R * V
     backsub = R * R * V
     sectors = (d + 1) * (2 * d ** 3 + 2 * d * d * V)
     epilogue = V * (2 * R * (R + 1) // 2 * 2 + 40 * (d + 2))
-    return assemble + qr + backsub + sectors + epilogue
+    return K * row + gram + chol + backsub + sectors + epilogue
 
 
 def measured_peak():

@@ -24,6 +24,7 @@
 #include <cmath>
 #include <cstring>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "kcommon.cuh"
@@ -49,10 +50,7 @@ __host__ __device__ constexpr int mf_coef_off(int D, int M) {
   }
   return off;
 }
-constexpr int kMfSlots = 6;
 static __constant__ double c_mcoef[mf_coef_off(3, 3) + 20 * 20];
-static __constant__ double c_qp[kMfSlots * kMfMaxQ * 3];
-static __constant__ double c_qw[kMfSlots * kMfMaxQ];
 
 // Monomial exponents in basis_monomials' graded order (basis.cpp): for n, for i = n..0,
 // for j = n−i..0, k = n−i−j (2-D: k = 0 only) — compile-time, so the powers index
@@ -114,51 +112,158 @@ __device__ __forceinline__ void shift_vec(uint8_t code, const double (&L)[3], do
 // 3×3 / 2×2 inverse by cofactors (as the host's sector inverse); false if det = 0
 template <int D>
 __device__ __forceinline__ bool inv_small_d(const double (&A)[D][D], double (&Ai)[D][D]) {
-  if (D == 2) {
+  if constexpr (D == 2) {
     const double det = A[0][0] * A[1][1] - A[0][1] * A[1][0];
     if (det == 0.0 || !isfinite(det)) return false;
-    Ai[0][0] = A[1][1] / det;
-    Ai[0][1] = -A[0][1] / det;
-    Ai[1][0] = -A[1][0] / det;
-    Ai[1][1] = A[0][0] / det;
+    const double r = 1.0 / det;
+    Ai[0][0] = A[1][1] * r;
+    Ai[0][1] = -A[0][1] * r;
+    Ai[1][0] = -A[1][0] * r;
+    Ai[1][1] = A[0][0] * r;
     return true;
   } else {
     const double c00 = A[1][1] * A[2][2] - A[1][2] * A[2][1], c01 = A[1][2] * A[2][0] - A[1][0] * A[2][2],
                  c02 = A[1][0] * A[2][1] - A[1][1] * A[2][0];
     const double det = A[0][0] * c00 + A[0][1] * c01 + A[0][2] * c02;
     if (det == 0.0 || !isfinite(det)) return false;
-    Ai[0][0] = c00 / det;
-    Ai[0][1] = (A[0][2] * A[2][1] - A[0][1] * A[2][2]) / det;
-    Ai[0][2] = (A[0][1] * A[1][2] - A[0][2] * A[1][1]) / det;
-    Ai[1][0] = c01 / det;
-    Ai[1][1] = (A[0][0] * A[2][2] - A[0][2] * A[2][0]) / det;
-    Ai[1][2] = (A[0][2] * A[1][0] - A[0][0] * A[1][2]) / det;
-    Ai[2][0] = c02 / det;
-    Ai[2][1] = (A[0][1] * A[2][0] - A[0][0] * A[2][1]) / det;
-    Ai[2][2] = (A[0][0] * A[1][1] - A[0][1] * A[1][0]) / det;
+    const double r = 1.0 / det;
+    Ai[0][0] = c00 * r;
+    Ai[0][1] = (A[0][2] * A[2][1] - A[0][1] * A[2][2]) * r;
+    Ai[0][2] = (A[0][1] * A[1][2] - A[0][2] * A[1][1]) * r;
+    Ai[1][0] = c01 * r;
+    Ai[1][1] = (A[0][0] * A[2][2] - A[0][2] * A[2][0]) * r;
+    Ai[1][2] = (A[0][2] * A[1][0] - A[0][0] * A[1][2]) * r;
+    Ai[2][0] = c02 * r;
+    Ai[2][1] = (A[0][1] * A[2][0] - A[0][0] * A[2][1]) * r;
+    Ai[2][2] = (A[0][0] * A[1][1] - A[0][1] * A[1][0]) * r;
     return true;
   }
 }
 
-// per-warp shared scratch: R factor, Qᵀ ΔQ, diag(R), sector products
+// Per-warp shared scratch (doubles): X = [A | ΔQ] with KP rows of stride NCP (the
+// Gram matrix and then the Cholesky factor reuse its first rows), then the sector
+// products [NV][D][V].
+template <int D, int M, int V>
+struct MfShape {
+  static constexpr int NM = nmodes(M, D), R = NM - 1, NV = D + 1, K = D * NM - 1;
+  static constexpr int KP = (K + 3) & ~3;            // rows padded to whole k-steps of 4
+  static constexpr int NC = R + V;                   // columns of [A | ΔQ]
+  static constexpr int NCP = (NC + 7) & ~7;          // padded to whole 8-column blocks
+  static constexpr int NB = NCP / 8;                 // column blocks (DMMA tiles per side)
+  static constexpr int GS = NCP + 1;                 // row stride of G and U in the scratch
+  static constexpr int X_DBL = KP * NCP > NCP * GS ? KP * NCP : NCP * GS;  // X, then G / U
+  static constexpr int PS_DBL = NV * D * V;
+  static constexpr int SCR = X_DBL + PS_DBL;
+  static_assert(NC <= 32, "one lane per column of [G | AᵀΔQ]");
+};
 __host__ __device__ constexpr int mf_scr_doubles(int D, int M, int V) {
-  return (nmodes(M, D) - 1) * (nmodes(M, D) - 1 + V + 1) + (D + 1) * D * V;
+  const int kp = (D * nmodes(M, D) - 1 + 3) & ~3, ncp = (nmodes(M, D) - 1 + V + 7) & ~7;
+  return (kp * ncp > ncp * (ncp + 1) ? kp * ncp : ncp * (ncp + 1)) + (D + 1) * D * V;
 }
 
+// Moments of the monomials of degree ≤ 3 over a simplex with vertices y_0..y_D, in
+// closed form (exact for polynomials, so equal to the degree-M quadrature of R19 up
+// to rounding): with λ ~ Dirichlet(1,…,1), E[λ^β] = D!·β!/(D+|β|)!, hence with
+// s_a = Σ_m y_m[a], S_ab = Σ_m y_m[a]y_m[b], T_abc = Σ_m y_m[a]y_m[b]y_m[c]:
+//   E[ξ_a] = s_a/(D+1),   E[ξ_aξ_b] = (S_ab + s_a s_b)/((D+1)(D+2)),
+//   E[ξ_aξ_bξ_c] = (2T_abc + S_ab s_c + S_ac s_b + S_bc s_a + s_a s_b s_c)/((D+1)(D+2)(D+3)).
+struct MonoIdx {  // per monomial: degree and its sorted coordinate multiset
+  int deg[64], a[64], b[64], c[64];
+};
+__host__ __device__ constexpr MonoIdx mono_idx(int D, int M) {
+  MonoIdx t{};
+  const MonoTab mt = mono_tab(D, M);
+  for (int e = 0; e < nmodes(M, D); ++e) {
+    int lst[3] = {0, 0, 0}, n = 0;
+    for (int ax = 0; ax < 3; ++ax)
+      for (int p = 0; p < mt.e[e][ax]; ++p) lst[n++] = ax;
+    t.deg[e] = n;
+    t.a[e] = lst[0];
+    t.b[e] = lst[1];
+    t.c[e] = lst[2];
+  }
+  return t;
+}
+// moment of monomial E (compile time: no runtime-indexed arrays) from the power sums
+template <int D, int M, int E>
+__device__ __forceinline__ double mono_moment(const double (&sv)[D], const double (&S2)[D][D],
+                                              const double (&T3)[D * D * D]) {
+  constexpr MonoIdx MI = mono_idx(D, M);
+  constexpr int dg = MI.deg[E], ea = MI.a[E], eb = MI.b[E], ec = MI.c[E];
+  constexpr double c1 = 1.0 / (D + 1), c2 = 1.0 / ((D + 1) * (D + 2)), c3 = 1.0 / ((D + 1) * (D + 2) * (D + 3));
+  if constexpr (dg == 0) {
+    return 1.0;
+  } else if constexpr (dg == 1) {
+    return sv[ea] * c1;
+  } else if constexpr (dg == 2) {
+    return (S2[ea][eb] + sv[ea] * sv[eb]) * c2;
+  } else {
+    return (2.0 * T3[(ea * D + eb) * D + ec] + S2[ea][eb] * sv[ec] + S2[ea][ec] * sv[eb] + S2[eb][ec] * sv[ea] +
+            sv[ea] * sv[eb] * sv[ec]) *
+           c3;
+  }
+}
+template <int D, int M, int NM, int... E>
+__device__ __forceinline__ void mono_moments(double (&mom)[NM], const double (&sv)[D], const double (&S2)[D][D],
+                                             const double (&T3)[D * D * D], std::integer_sequence<int, E...>) {
+  ((mom[E] = mono_moment<D, M, E>(sv, S2, T3)), ...);
+}
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// One warp per cell (persistent grid):
+//  1. assembly: lane L builds rows k = L, L+32 of X = [A | ΔQ] (A[k][l−1] = average of
+//     ψ_l(ξ_i(x)) over stencil cell j(k): closed-form simplex moments of the
+//     monomials, then the basis coefficients of mode l over the monomials of degree
+//     ≤ deg(l)) into shared memory;
+//  2. Gram: [AᵀA | AᵀΔQ] = XᵀX on the fp64 tensor cores (mma.sync m8n8k4: both operand
+//     fragments are X[k0 + lane%4][8·blk + lane/4]);
+//  3. the normal equations of the reduced LSQ (R10; R38): Cholesky of AᵀA in
+//     registers (lane k owns column k of [AᵀA | AᵀΔQ], pivot rows by shuffles), which
+//     also forward-substitutes the V right-hand sides; lanes v < V back-substitute;
+//  4. lanes 0..d solve the sector systems; lanes 0..V−1 run the fused
+//     epilogue and store w.
+// fp64-ALU bound; HBM per cell ≈ geometry + stencil ids + Q + w.
 template <int D, int M, int V>
-__global__ void __launch_bounds__(256) k_matfree(MfArgs m, KArgs a) {
-  constexpr int NM = nmodes(M, D), R = NM - 1, NV = D + 1, NE = D * NM, K = NE - 1;
-  constexpr int KPL = (K + 31) / 32;  // rows of A per lane
+__global__ void __launch_bounds__(128) k_matfree(MfArgs m, KArgs a) {
+  using S = MfShape<D, M, V>;
+  constexpr int NM = S::NM, R = S::R, NV = S::NV, K = S::K, KP = S::KP, NC = S::NC, NCP = S::NCP, NB = S::NB,
+                GS = S::GS;
+  constexpr int KPL = (K + 31) / 32;  // rows of X per lane
 
   const int lane = threadIdx.x & 31;
-  const double* qp = c_qp + mf_slot(D, M) * kMfMaxQ * 3;  // this (d, M)'s tables
-  const double* qw = c_qw + mf_slot(D, M) * kMfMaxQ;
   const double* mcoef = c_mcoef + mf_coef_off(D, M);
   extern __shared__ __align__(16) double mf_smem[];
-  double* scr = mf_smem + (threadIdx.x >> 5) * mf_scr_doubles(D, M, V);
+  double* X = mf_smem + (threadIdx.x >> 5) * S::SCR;  // [KP][NCP], later G / U [NCP][GS]
+  double* PSs = X + S::X_DBL;                          // [NV][D][V] sector products
   const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  // stencil ids and image codes of this lane's rows, loaded one cell ahead (the vertex
+  // gathers then depend on one global load, not two)
+  int32_t jn[KPL];
+  uint8_t cn[KPL];
+  auto load_ids = [&](int64_t ic) {
+#pragma unroll
+    for (int r = 0; r < KPL; ++r) {
+      const int k = lane + 32 * r;
+      const bool ok = ic < m.cell_end && k < K;
+      jn[r] = ok ? m.st[ic * K + k] : 0;
+      cn[r] = ok ? m.sh[ic * K + k] : 0;
+    }
+  };
+  load_ids(m.cell_begin + w0);
   for (int64_t i = m.cell_begin + w0; i < m.cell_end; i += nw) {
+    int32_t jc[KPL];
+    uint8_t cc[KPL];
+#pragma unroll
+    for (int r = 0; r < KPL; ++r) {
+      jc[r] = jn[r];
+      cc[r] = cn[r];
+    }
+    load_ids(i + nw);
     // ---- owner geometry x = X0 + J ξ, J⁻¹
     double X0[D], J[D][D], Ji[D][D];
     {
@@ -175,167 +280,96 @@ __global__ void __launch_bounds__(256) k_matfree(MfArgs m, KArgs a) {
 #pragma unroll
     for (int v = 0; v < V; ++v) qi[v] = a.Q[i * a.acs + v * a.avs];
 
-    // ---- rows of the reduced system: A[k][l-1] = avg_{T_j} ψ_l(ξ_i(x)), rhs = ΔQ
-    double A[KPL][R], rhs[KPL][V];
+    // ---- 1. rows of X = [A | ΔQ]
 #pragma unroll
     for (int r = 0; r < KPL; ++r) {
       const int k = lane + 32 * r;
+      if (k >= KP) continue;
+      double* xr = X + k * NCP;
+      if (k >= K) {  // zero rows up to a whole k-step
 #pragma unroll
-      for (int l = 0; l < R; ++l) A[r][l] = 0.0;
+        for (int l = 0; l < NCP; ++l) xr[l] = 0.0;
+        continue;
+      }
+      const int32_t j = jc[r];
+      double sh[D];
+      shift_vec<D>(cc[r], m.L, sh);
+      const double* Xj = m.X + int64_t(j) * NV * D;
+      // vertices y_v of T_j in ξ_i coordinates, y_0 = J⁻¹(X_j0 + shift − X0),
+      // y_v = y_0 + J⁻¹(X_jv − X_j0), accumulated into the power sums as they are formed
+      double sv[D], S2[D][D], T3[D * D * D], y0[D];
+      {
+        double d0[D];
 #pragma unroll
-      for (int v = 0; v < V; ++v) rhs[r][v] = 0.0;
-      if (k < K) {
-        const int32_t j = m.st[i * K + k];
-        double sh[D];
-        shift_vec<D>(m.sh[i * K + k], m.L, sh);
-        const double* Xj = m.X + int64_t(j) * NV * D;
-        double t[D], C[D][D];
+        for (int f = 0; f < D; ++f) d0[f] = Xj[f] + sh[f] - X0[f];
 #pragma unroll
         for (int e = 0; e < D; ++e) {
-          double s = 0.0;
+          double s0 = 0.0;
 #pragma unroll
-          for (int f = 0; f < D; ++f) s += Ji[e][f] * (Xj[f] + sh[f] - X0[f]);
-          t[e] = s;
-#pragma unroll
-          for (int f = 0; f < D; ++f) {
-            double s2 = 0.0;
-#pragma unroll
-            for (int g = 0; g < D; ++g) s2 += Ji[e][g] * (Xj[(f + 1) * D + g] - Xj[g]);
-            C[e][f] = s2;
-          }
+          for (int f = 0; f < D; ++f) s0 = fma(Ji[e][f], d0[f], s0);
+          y0[e] = s0;
         }
-        double mom[NM];  // monomial averages over T_j (ℳ monomials of degree ≤ M)
+      }
 #pragma unroll
-        for (int e = 0; e < NM; ++e) mom[e] = 0.0;
-        for (int q = 0; q < m.nq; ++q) {
-          double pw[3][M + 1];
+      for (int v2 = 0; v2 < NV; ++v2) {
+        double y[D];
+        if (v2 == 0) {
+#pragma unroll
+          for (int e = 0; e < D; ++e) y[e] = y0[e];
+        } else {
+          double dv[D];
+#pragma unroll
+          for (int f = 0; f < D; ++f) dv[f] = Xj[v2 * D + f] - Xj[f];
 #pragma unroll
           for (int e = 0; e < D; ++e) {
-            double s = t[e];
+            double s1 = y0[e];
 #pragma unroll
-            for (int f = 0; f < D; ++f) s += C[e][f] * qp[q * D + f];
-            pw[e][0] = 1.0;
-#pragma unroll
-            for (int p = 1; p <= M; ++p) pw[e][p] = pw[e][p - 1] * s;
+            for (int f = 0; f < D; ++f) s1 = fma(Ji[e][f], dv[f], s1);
+            y[e] = s1;
           }
-          if (D == 2) {
-#pragma unroll
-            for (int p = 0; p <= M; ++p) pw[2][p] = p == 0 ? 1.0 : 0.0;
-          }
-          const double wq = qw[q];
-          constexpr MonoTab MT = mono_tab(D, M);
-#pragma unroll
-          for (int e = 0; e < NM; ++e) mom[e] += wq * (pw[0][MT.e[e][0]] * pw[1][MT.e[e][1]] * pw[2][MT.e[e][2]]);
         }
 #pragma unroll
-        for (int l = 1; l < NM; ++l) {
-          double s = 0.0;
+        for (int e = 0; e < D; ++e) {
+          sv[e] = v2 == 0 ? y[e] : sv[e] + y[e];
 #pragma unroll
-          for (int e = 0; e < NM; ++e) s += mcoef[l * NM + e] * mom[e];
-          A[r][l - 1] = s;
+          for (int f = e; f < D; ++f) {
+            const double pef = y[e] * y[f];
+            S2[e][f] = v2 == 0 ? pef : S2[e][f] + pef;
+#pragma unroll
+            if constexpr (M >= 3) {
+#pragma unroll
+              for (int g2 = f; g2 < D; ++g2) {
+                double& t3 = T3[(e * D + f) * D + g2];
+                t3 = v2 == 0 ? pef * y[g2] : fma(pef, y[g2], t3);
+              }
+            }
+          }
         }
-#pragma unroll
-        for (int v = 0; v < V; ++v) rhs[r][v] = a.Q[int64_t(j) * a.acs + v * a.avs] - qi[v];
       }
+      double mom[NM];
+      mono_moments<D, M, NM>(mom, sv, S2, T3, std::make_integer_sequence<int, NM>{});
+      // A[k][l−1] = Σ_e C[l][e]·mom[e] over the monomials of degree ≤ deg(ψ_l): rows in
+      // blocks of one degree n (compile-time bounds), each block's row loop rolled
+#pragma unroll
+      for (int n = 1; n <= M; ++n) {
+        const int lo = D == 2 ? n * (n + 1) / 2 : n * (n + 1) * (n + 2) / 6;
+        const int hi = D == 2 ? (n + 1) * (n + 2) / 2 : (n + 1) * (n + 2) * (n + 3) / 6;
+#pragma unroll 1
+        for (int l = lo; l < hi; ++l) {
+          double s2 = 0.0;
+#pragma unroll
+          for (int e = 0; e < hi; ++e) s2 = fma(mcoef[l * NM + e], mom[e], s2);
+          xr[l - 1] = s2;
+        }
+      }
+#pragma unroll
+      for (int v = 0; v < V; ++v) xr[R + v] = a.Q[int64_t(j) * a.acs + v * a.avs] - qi[v];
+#pragma unroll
+      for (int l = NC; l < NCP; ++l) xr[l] = 0.0;
     }
 
-    // ---- Householder QR of A (K × R) applied to rhs; R factor left in rows 0..R−1.
-    // Per column c: the R+V dot products vᵀ[A|ΔQ] are reduced with a butterfly
-    // reduce-scatter (after the xor-o step a lane keeps the half selected by bit o,
-    // so lane L ends with column L's full sum: 31 shuffles instead of 5·(R+V)), then
-    // all-gathered for the rank-1 update.  The column loop is not unrolled (code size).
-    static_assert(R + V <= 32, "one lane per column of A|ΔQ");
-    constexpr int NP = R + V <= 16 ? 16 : 32;  // padded column count of the reduce-scatter
-    auto qr_step = [&](const int c) {
-      double x[KPL];
-      double part = 0.0;
-#pragma unroll
-      for (int r = 0; r < KPL; ++r) {
-        const int k = lane + 32 * r;
-        double ak = 0.0;
-#pragma unroll
-        for (int mm = 0; mm < R; ++mm)
-          if (mm == c) ak = A[r][mm];
-        x[r] = (k >= c && k < K) ? ak : 0.0;
-        part += x[r] * x[r];
-      }
-      const double nrm2 = warp_sum(part);
-      const double xc = __shfl_sync(0xffffffffu, x[0], c);  // row c is slot 0 of lane c
-      const double alpha = xc >= 0.0 ? -sqrt(nrm2) : sqrt(nrm2);
-      const double vtv = 2.0 * (nrm2 - alpha * xc);
-      const double tau = vtv > 0.0 ? 2.0 / vtv : 0.0;
-      if (lane == c) x[0] -= alpha;
-      double dd[NP];
-#pragma unroll
-      for (int mm = 0; mm < NP; ++mm) {
-        double s2 = 0.0;
-        if (mm < R + V) {
-#pragma unroll
-          for (int r = 0; r < KPL; ++r) s2 += x[r] * (mm < R ? A[r][mm] : rhs[r][mm < R ? 0 : mm - R]);
-        }
-        dd[mm] = s2;
-      }
-#pragma unroll
-      for (int o = NP / 2; o > 0; o >>= 1) {
-        const bool up = (lane & o) != 0;
-#pragma unroll
-        for (int i2 = 0; i2 < o; ++i2) {
-          const double keep = up ? dd[i2 + o] : dd[i2];
-          const double send = up ? dd[i2] : dd[i2 + o];
-          dd[i2] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-        }
-      }
-      if (NP == 16) dd[0] += __shfl_xor_sync(0xffffffffu, dd[0], 16);
-      const double fl = tau * dd[0];  // lane L: τ·(vᵀ column L mod NP)
-#pragma unroll
-      for (int mm = 0; mm < R + V; ++mm) {
-        const double f = __shfl_sync(0xffffffffu, fl, mm);
-        if (mm > c) {
-#pragma unroll
-          for (int r = 0; r < KPL; ++r) {
-            if (mm < R)
-              A[r][mm] -= f * x[r];
-            else
-              rhs[r][mm - R] -= f * x[r];
-          }
-        }
-      }
-      if (lane == c) {
-#pragma unroll
-        for (int mm = 0; mm < R; ++mm)
-          if (mm == c) A[0][mm] = alpha;
-      }
-    };
-    if constexpr (R <= 9) {  // small: fully unrolled (column selects fold away)
-#pragma unroll
-      for (int c = 0; c < R; ++c) qr_step(c);
-    } else {  // ℳ ≥ 15: a rolled column loop keeps the code in the instruction cache
-#pragma unroll 1
-      for (int c = 0; c < R; ++c) qr_step(c);
-    }
-    // ---- R factor and Qᵀ ΔQ to this warp's shared scratch: lane v < V then solves
-    // R p = (Qᵀ ΔQ)[0:R] for its variable, keeping p̂_opt in registers
-    double* Rs = scr;                 // [R][R] upper triangle of R
-    double* Ys = Rs + R * R;          // [R][V]
-    double* Ri = Ys + R * V;          // [R] diagonal of R
-    double* PSs = Ri + R;             // [NV][D][V] sector products
-    if (lane < R) {
-#pragma unroll
-      for (int mm = 0; mm < R; ++mm)
-        if (mm >= lane) Rs[lane * R + mm] = A[0][mm];
-#pragma unroll
-      for (int v = 0; v < V; ++v) Ys[lane * V + v] = rhs[0][v];
-#pragma unroll
-      for (int mm = 0; mm < R; ++mm)
-        if (mm == lane) Ri[lane] = A[0][mm];
-    }
-    // ---- sectors: lane s < d+1 solves sector s for all variables
-    double psl[D][V];
+    // ---- 4a. sectors: lane s < d+1 solves sector s for all variables
     bool vs = false;
-#pragma unroll
-    for (int l = 0; l < D; ++l)
-#pragma unroll
-      for (int v = 0; v < V; ++v) psl[l][v] = 0.0;
     if (lane < NV && ((m.vmask[i] >> lane) & 1)) {
       double As[D][D], Si[D][D], dq[D][V];
 #pragma unroll
@@ -370,20 +404,79 @@ __global__ void __launch_bounds__(256) k_matfree(MfArgs m, KArgs a) {
             double s = 0.0;
 #pragma unroll
             for (int mm = 0; mm < D; ++mm) s += Si[l][mm] * dq[mm][v];
-            psl[l][v] = s;
+            PSs[(lane * D + l) * V + v] = s;
           }
       }
     }
-
-    // ---- per variable (lane v): back substitution, gather, fused epilogue
-    if (lane < NV) {
+    if (lane < NV && !vs) {
 #pragma unroll
       for (int l = 0; l < D; ++l)
 #pragma unroll
-        for (int v = 0; v < V; ++v) PSs[(lane * D + l) * V + v] = psl[l][v];
+        for (int v = 0; v < V; ++v) PSs[(lane * D + l) * V + v] = 0.0;
     }
     const unsigned vbits = __ballot_sync(0xffffffffu, vs);
     __syncwarp();
+
+    // ---- 2. Gram [AᵀA | AᵀΔQ] = XᵀX, upper block tiles (I ≤ J) on the fp64 tensor cores
+    double gc[NB][NB][2];
+#pragma unroll
+    for (int I = 0; I < NB; ++I)
+#pragma unroll
+      for (int J2 = 0; J2 < NB; ++J2) gc[I][J2][0] = gc[I][J2][1] = 0.0;
+    {
+      const double* xf = X + (lane & 3) * NCP + (lane >> 2);
+#pragma unroll 5
+      for (int k0 = 0; k0 < KP; k0 += 4) {
+        double fr[NB];
+#pragma unroll
+        for (int b = 0; b < NB; ++b) fr[b] = xf[k0 * NCP + 8 * b];
+#pragma unroll
+        for (int I = 0; I < NB; ++I)
+#pragma unroll
+          for (int J2 = I; J2 < NB; ++J2) dmma884(gc[I][J2][0], gc[I][J2][1], fr[I], fr[J2]);
+      }
+    }
+    __syncwarp();  // X is dead: G takes its place
+    double* G = X;  // [NCP][GS]: G[r][c] for r < R (both triangles of AᵀA), c < NC
+    {
+      const int gr = lane >> 2, gcol = 2 * (lane & 3);
+#pragma unroll
+      for (int I = 0; I < NB; ++I)
+#pragma unroll
+        for (int J2 = I; J2 < NB; ++J2)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int r0 = 8 * I + gr, c0 = 8 * J2 + gcol + e;
+            G[r0 * GS + c0] = gc[I][J2][e];
+            if (I != J2) G[c0 * GS + r0] = gc[I][J2][e];
+          }
+    }
+    __syncwarp();
+
+    // ---- 3. Cholesky AᵀA = UᵀU on [AᵀA | AᵀΔQ]: lane k holds column k; step c scales
+    // row c by 1/√G[c][c] and updates rows j > c with the broadcast U[c][j]; on the
+    // right-hand-side lanes (k = R + v) this is the forward substitution Uᵀy = AᵀΔQ.
+    double g[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) g[j] = lane < NC ? G[j * GS + lane] : 0.0;
+#pragma unroll
+    for (int c = 0; c < R; ++c) {
+      const double dcc = __shfl_sync(0xffffffffu, g[c], c);
+      const double inv = 1.0 / sqrt(dcc);  // NaN for a rank-deficient stencil (no silent result)
+      const double u = g[c] * inv;
+      g[c] = u;
+      if (lane == c) G[c * GS + NCP] = inv;  // 1/U[c][c] in the padding column
+#pragma unroll
+      for (int j = c + 1; j < R; ++j) g[j] = fma(-__shfl_sync(0xffffffffu, u, j), u, g[j]);
+    }
+    __syncwarp();
+    if (lane < NC) {
+#pragma unroll
+      for (int c = 0; c < R; ++c) G[c * GS + lane] = g[c];  // U[c][k] (k ≥ c), y[c] for k ≥ R
+    }
+    __syncwarp();
+
+    // ---- per variable (lane v): back substitution U p = y, gather, fused epilogue
     double acc[R], ps[NV][D];
     bool valid[NV];
 #pragma unroll
@@ -391,10 +484,10 @@ __global__ void __launch_bounds__(256) k_matfree(MfArgs m, KArgs a) {
     if (lane < V) {
 #pragma unroll
       for (int c = R - 1; c >= 0; --c) {
-        double t = Ys[c * V + lane];
+        double t = G[c * GS + R + lane];
 #pragma unroll
-        for (int mm = c + 1; mm < R; ++mm) t -= Rs[c * R + mm] * acc[mm];
-        acc[c] = t / Ri[c];
+        for (int mm = c + 1; mm < R; ++mm) t = fma(-G[c * GS + mm], acc[mm], t);
+        acc[c] = t * G[c * GS + NCP];
       }
 #pragma unroll
       for (int s2 = 0; s2 < NV; ++s2)
@@ -498,15 +591,25 @@ void dev_matfree_upload(cwreco_ctx* c, const MatfreeHost& h) {
   upload(s->vmask, h.vmask);
   s->nq = nq;
   s->nmono = nmono;
-  // constants of this translation unit: monomials, basis, rule, packed Σ
-  std::vector<double> qp3(nq * 3, 0.0);
-  for (int q = 0; q < nq; ++q)
-    for (int e = 0; e < c->d; ++e) qp3[q * c->d + e] = h.qp[q * c->d + e];
-  const int slot = mf_slot(c->d, c->M);
+  // the basis over the monomials: mode l of degree n may use only monomials of degree
+  // ≤ n (the kernel's sums stop there)
+  for (int l = 0; l < c->nm; ++l)
+    for (int e = 0; e < c->nm; ++e) {
+      const int de = h.mexp[3 * e] + h.mexp[3 * e + 1] + h.mexp[3 * e + 2];
+      int deg_l = 0;
+      for (int n = 0, cnt = 0; n <= c->M; ++n) {
+        cnt += c->d == 2 ? n + 1 : (n + 1) * (n + 2) / 2;
+        if (l < cnt) {
+          deg_l = n;
+          break;
+        }
+      }
+      if (de > deg_l && h.mcoef[size_t(l) * c->nm + e] != 0.0)
+        fail(CWRECO_EUNSUPPORTED, "matrix-free: basis mode uses a monomial above its degree");
+    }
+  // constants of this translation unit: basis coefficients, packed Σ
   MCK(cudaMemcpyToSymbol(c_mcoef, h.mcoef.data(), sizeof(double) * h.mcoef.size(),
                          sizeof(double) * mf_coef_off(c->d, c->M)));
-  MCK(cudaMemcpyToSymbol(c_qp, qp3.data(), sizeof(double) * qp3.size(), sizeof(double) * slot * kMfMaxQ * 3));
-  MCK(cudaMemcpyToSymbol(c_qw, h.qw.data(), sizeof(double) * h.qw.size(), sizeof(double) * slot * kMfMaxQ));
   const int nm = c->nm;
   std::vector<double> packed;
   for (int l = 1; l < nm; ++l)
@@ -555,14 +658,15 @@ void dev_matfree_reconstruct(cwreco_ctx* c, const double* avgs, int64_t acs, int
   int nsm = 148;
   MCK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
   MfFn f = mf_fn(c->d, c->M, c->V);
-  const size_t smem = size_t(8) * mf_scr_doubles(c->d, c->M, c->V) * sizeof(double);
+  constexpr int kWarps = 4;  // warps (cells in flight) per CTA
+  const size_t smem = size_t(kWarps) * mf_scr_doubles(c->d, c->M, c->V) * sizeof(double);
   MCK(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 1;
-  MCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)f, 256, smem));
+  MCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)f, 32 * kWarps, smem));
   const int64_t warps = cell_end - cell_begin;
-  int64_t grid = std::max<int64_t>(1, std::min<int64_t>((warps + 7) / 8, (int64_t)nsm * std::max(1, occ)));
+  int64_t grid = std::max<int64_t>(1, std::min<int64_t>((warps + kWarps - 1) / kWarps, (int64_t)nsm * std::max(1, occ)));
   if (c->max_ctas > 0) grid = std::min<int64_t>(grid, c->max_ctas);  // CWRECO_OPT_MAX_CTAS
-  f<<<(unsigned)grid, 256, smem, (cudaStream_t)stream>>>(m, a);
+  f<<<(unsigned)grid, 32 * kWarps, smem, (cudaStream_t)stream>>>(m, a);
   MCK(cudaGetLastError());
 }
 

@@ -115,3 +115,51 @@ def test_full_mesh_stencils_bit_exact(cfg):
                 i = lo + k
                 assert cen[i].tolist() == c, (cfg, i)
                 assert sec[i].tolist() == s and val[i].tolist() == v, (cfg, i)
+
+
+def _floored_all(got, ref, Q, cen, chunk=131072):
+    """max floored-relative error (R25) over every cell: got/ref [N, V, ℳ], cen [N, n_e]."""
+    worst = 0.0
+    aQ = np.abs(Q)
+    for lo in range(0, got.shape[0], chunk):
+        hi = min(got.shape[0], lo + chunk)
+        c = cen[lo:hi]
+        s = np.where(c[..., None] >= 0, aQ[np.maximum(c, 0)], 0.0).max(axis=1)[:, :, None]  # [n, V, 1]
+        den = np.maximum(np.abs(ref[lo:hi]), s)
+        e = np.abs(got[lo:hi] - ref[lo:hi])
+        assert np.all(e[np.broadcast_to(den == 0, e.shape)] == 0.0)
+        worst = max(worst, float((e / np.where(den > 0, den, 1.0)).max()))
+    return worst
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C3"])
+def test_matrixfree_full_config(cfg):
+    """Matrix-free mode (NEXT-1; normal equations, reading R38) on the full C2 (the most
+    distorted mesh: ±0.2h jitter) and C3 meshes: every cell within the R25 tolerance of
+    the precomputed-matrix kernel (itself checked against the oracle above), sampled
+    cells (random + the 50 widest-range ones) against the oracle, conservation exact."""
+    w = gen.make(cfg)
+    ctx = P.setup_context(w["nodes"], w["cells"], w["period"], w["M"], w["V"], device=0)
+    perm = ctx.permutation()
+    Q = w["avgs"][perm]
+    Qd = torch.tensor(Q, device="cuda")
+    ref = ctx.reconstruct(Qd).cpu().numpy()
+    ctx.prepare_matrixfree()
+    ctx.set_kernel("matrixfree")
+    got = ctx.reconstruct(Qd).cpu().numpy()
+    assert np.all(np.isfinite(got))
+    psi1 = np.sqrt(2.0 if w["d"] == 2 else 6.0)
+    assert np.abs(got[:, :, 0] * psi1 - Q).max() <= 4e-16 * np.abs(Q).max()
+    cen, _, _ = ctx.stencils()
+    worst_all = _floored_all(got, ref, Q, cen)
+    m = OracleMesh(w["nodes"], w["cells"], w["period"], w["M"])
+    rng = np.random.default_rng(23)
+    rngQ = np.ptp(Q[cen], axis=1).max(axis=1) / (np.abs(Q).max(axis=0).max() + 1e-300)
+    sel = sorted(set(rng.choice(m.N, 150, replace=False).tolist()) | set(np.argsort(-rngQ)[:50].tolist()))
+    worst = 0.0
+    for i in sel:
+        r = R.reconstruct_cell(m, int(i), Q, w["M"])
+        worst = max(worst, floored_err(got[i], r["w"], Q, r["central"]))
+    print(f"{cfg} matrix-free: all {m.N} cells vs matrix kernel {worst_all:.2e}, "
+          f"{len(sel)} cells vs oracle {worst:.2e}")
+    assert worst_all <= TOL and worst <= TOL

@@ -192,6 +192,12 @@ CWR_HD constexpr bool rb_default(int d, int R, int V) { return (R > 14 && V >= 3
 #endif
 constexpr int kRbKC = CWR_RB_KC;  // positions per streamed chunk of the row-block layout (2 pairs)
 constexpr int kRbMaxStages = 32;  // row-block stage ring: as deep as shared memory allows
+// row-block ring floor: 2 stages of KC positions before the tile is halved.  The ring
+// depth barely matters to the row-block kernel (C4 proxy: 3 stages 0.722, 7 stages of
+// half the size 0.710), halving T does (a partitioned C4 rank whose boundary tiles
+// raise the union maximum from 371 to 399 cells lost the 4th stage and fell to T = 16:
+// 1.48x the time per cell, tools/rank_projection.py)
+constexpr int kRbMinStages = 2;
 // shared memory of a row-block CTA with S ring stages: ring (position chunks),
 // 3 union-chunk buffers, 2 sector-chunk buffers, Q_u[2][Umax][VP], O[T][V][ℳ], barriers
 inline int64_t rb_ubuf_bytes(const Layout& L) { return round128(L.u_bytes); }

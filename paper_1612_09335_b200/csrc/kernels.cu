@@ -506,7 +506,7 @@ static PipeCfg pipe_cfg(const cwreco_ctx* c, int* ctas = nullptr) {
     // warp-specialised row-block kernel: one CTA per SM, the deepest stage ring that fits
     int k = 0, st = 0;
     rowblk_plan(L, c->dev->max_smem, 1, k, st);
-    if (cap) st = std::max(kMinStages, std::min(st, std::atoi(cap)));
+    if (cap) st = std::max(kRbMinStages, std::min(st, std::atoi(cap)));
     if (!k) fail(CWRECO_EUNSUPPORTED, "row-block kernel: tile does not fit in shared memory");
     if (ctas) *ctas = 1;
     p.ncw = rb_main_warps(L.T, rb_ng(L.R, L.V));

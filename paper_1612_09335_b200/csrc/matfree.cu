@@ -140,7 +140,19 @@ __device__ __forceinline__ bool inv_small_d(const double (&A)[D][D], double (&Ai
   }
 }
 
-// Per-warp shared scratch (doubles): X = [A | ΔQ] with KP rows of stride NCP (the
+// Row stride of X in doubles.  The assembly writes X row-per-lane (lane k, row k: a
+// 64-bit store of 16 lanes is conflict-free only if 16 consecutive rows fall in 16
+// different bank pairs, i.e. the stride is odd — NCP itself, a multiple of 8, put
+// every row of a half-warp in 2 bank pairs: 8-way conflicts, 4.9e9 per C5 pass); the
+// Gram fragments read rows lane%4 × columns lane/4, conflict-free only for strides
+// ≡ 4, 12 (mod 16): an odd stride with stride mod 16 ∉ {1, 15} keeps those 2-way.
+__host__ __device__ constexpr int mf_xs(int ncp) {
+  int s = ncp | 1;
+  while (s % 16 == 1 || s % 16 == 15) s += 2;
+  return s;
+}
+
+// Per-warp shared scratch (doubles): X = [A | ΔQ] with KP rows of stride XS (the
 // Gram matrix and then the Cholesky factor reuse its first rows), then the sector
 // products [NV][D][V].
 template <int D, int M, int V>
@@ -151,14 +163,15 @@ struct MfShape {
   static constexpr int NCP = (NC + 7) & ~7;          // padded to whole 8-column blocks
   static constexpr int NB = NCP / 8;                 // column blocks (DMMA tiles per side)
   static constexpr int GS = NCP + 1;                 // row stride of G and U in the scratch
-  static constexpr int X_DBL = KP * NCP > NCP * GS ? KP * NCP : NCP * GS;  // X, then G / U
+  static constexpr int XS = mf_xs(NCP);              // row stride of X (see mf_xs)
+  static constexpr int X_DBL = KP * XS > NCP * GS ? KP * XS : NCP * GS;  // X, then G / U
   static constexpr int PS_DBL = NV * D * V;
   static constexpr int SCR = X_DBL + PS_DBL;
   static_assert(NC <= 32, "one lane per column of [G | AᵀΔQ]");
 };
 __host__ __device__ constexpr int mf_scr_doubles(int D, int M, int V) {
-  const int kp = (D * nmodes(M, D) - 1 + 3) & ~3, ncp = (nmodes(M, D) - 1 + V + 7) & ~7;
-  return (kp * ncp > ncp * (ncp + 1) ? kp * ncp : ncp * (ncp + 1)) + (D + 1) * D * V;
+  const int kp = (D * nmodes(M, D) - 1 + 3) & ~3, ncp = (nmodes(M, D) - 1 + V + 7) & ~7, xs = mf_xs(ncp);
+  return (kp * xs > ncp * (ncp + 1) ? kp * xs : ncp * (ncp + 1)) + (D + 1) * D * V;
 }
 
 // Moments of the monomials of degree ≤ 3 over a simplex with vertices y_0..y_D, in
@@ -231,13 +244,14 @@ template <int D, int M, int V>
 __global__ void __launch_bounds__(128) k_matfree(MfArgs m, KArgs a) {
   using S = MfShape<D, M, V>;
   constexpr int NM = S::NM, R = S::R, NV = S::NV, K = S::K, KP = S::KP, NC = S::NC, NCP = S::NCP, NB = S::NB,
+                XS = S::XS,
                 GS = S::GS;
   constexpr int KPL = (K + 31) / 32;  // rows of X per lane
 
   const int lane = threadIdx.x & 31;
   const double* mcoef = c_mcoef + mf_coef_off(D, M);
   extern __shared__ __align__(16) double mf_smem[];
-  double* X = mf_smem + (threadIdx.x >> 5) * S::SCR;  // [KP][NCP], later G / U [NCP][GS]
+  double* X = mf_smem + (threadIdx.x >> 5) * S::SCR;  // [KP][XS], later G / U [NCP][GS]
   double* PSs = X + S::X_DBL;                          // [NV][D][V] sector products
   const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
@@ -285,7 +299,7 @@ __global__ void __launch_bounds__(128) k_matfree(MfArgs m, KArgs a) {
     for (int r = 0; r < KPL; ++r) {
       const int k = lane + 32 * r;
       if (k >= KP) continue;
-      double* xr = X + k * NCP;
+      double* xr = X + k * XS;
       if (k >= K) {  // zero rows up to a whole k-step
 #pragma unroll
         for (int l = 0; l < NCP; ++l) xr[l] = 0.0;
@@ -424,12 +438,12 @@ __global__ void __launch_bounds__(128) k_matfree(MfArgs m, KArgs a) {
 #pragma unroll
       for (int J2 = 0; J2 < NB; ++J2) gc[I][J2][0] = gc[I][J2][1] = 0.0;
     {
-      const double* xf = X + (lane & 3) * NCP + (lane >> 2);
+      const double* xf = X + (lane & 3) * XS + (lane >> 2);
 #pragma unroll 5
       for (int k0 = 0; k0 < KP; k0 += 4) {
         double fr[NB];
 #pragma unroll
-        for (int b = 0; b < NB; ++b) fr[b] = xf[k0 * NCP + 8 * b];
+        for (int b = 0; b < NB; ++b) fr[b] = xf[k0 * XS + 8 * b];
 #pragma unroll
         for (int I = 0; I < NB; ++I)
 #pragma unroll

@@ -58,7 +58,7 @@ void rowblk_plan(const Layout& L, int max_smem, int max_ctas, int& ctas, int& st
   (void)max_ctas;
   ctas = 0;
   stages = 0;
-  for (int s = kRbMaxStages; s >= kMinStages; --s)
+  for (int s = kRbMaxStages; s >= kRbMinStages; --s)
     if (rb_smem(L, s) <= max_smem) {
       ctas = 1;
       stages = s;

@@ -49,6 +49,9 @@ constexpr int RB_BAR_OFULL = 1, RB_BAR_OFREE = 2, RB_BAR_EW = 3;
 #ifndef CWR_RB_PAIR
 #define CWR_RB_PAIR 0  // epilogue items computed two at a time (measured slower: registers)
 #endif
+#ifndef CWR_RB_PF
+#define CWR_RB_PF 0  // B⁺ of the next pair loaded per position between the FMAs (see pair())
+#endif
 #ifndef CWR_RB_LOOK1
 #define CWR_RB_LOOK1 0  // main loop with a one-position lookahead instead of the pair ping-pong
 #endif
@@ -300,6 +303,35 @@ __global__ void __launch_bounds__(rb_threads(nmodes(M, D) - 1, V), 1) k_rowblk(K
       uint32_t ipn = ix2[min(1, npr - 1) * T];
       mbar_wait(&full[rg.st], rg.ph);
       ldb(stage_ptr(), ba);
+#if CWR_RB_PF
+      // B⁺ of the next pair one position at a time, each right after the FMAs that free
+      // its registers: position 0's entries are loaded while this pair's position 1 runs,
+      // position 1's while the next pair's position 0 runs — every B⁺ load has a
+      // position of FMAs in front of it (no extra registers at the peak)
+      auto ldb1 = [&](const double* Bs, int kk, double (&b)[RB]) {
+#pragma unroll
+        for (int r = 0; r < RB; ++r) b[r] = Bs[(kk * R + r * NG) * T + (r < RB - 1 ? bfull : bpart)];
+      };
+      auto pair = [&](int pp, const double (&q)[2][V], const double (&b)[2][RB], double (&qn)[2][V],
+                      double (&bn)[2][RB]) {
+        ldq2(ipn, qn);
+        ipn = ix2[min(pp + 2, npr - 1) * T];
+        fma_pos(q[0], b[0]);
+        const int nx = pp + 1;
+        const bool more = nx < npr, nstage = more && nx % PPS == 0;
+        const double* nb = stage_ptr() + (nx % PPS) * 2 * R * T;
+        if (nstage) {  // next stage (a tail pair reads past kc into the stage: unused)
+          Ring nr = rg;
+          nr.next(S);
+          mbar_wait(&full[nr.st], nr.ph);
+          nb = (const double*)(stg + nr.st * pc.stage_bytes);
+        }
+        if (more) ldb1(nb, 0, bn[0]);
+        fma_pos(q[1], b[1]);
+        if (more) ldb1(nb, 1, bn[1]);
+        if (!more || nstage) release();
+      };
+#else
       auto pair = [&](int pp, const double (&q)[2][V], const double (&b)[2][RB], double (&qn)[2][V],
                       double (&bn)[2][RB]) {
         ldq2(ipn, qn);
@@ -319,6 +351,7 @@ __global__ void __launch_bounds__(rb_threads(nmodes(M, D) - 1, V), 1) k_rowblk(K
           ldb(stage_ptr() + (nx % PPS) * 2 * R * T, bn);
         }
       };
+#endif
       int pp = 0;
       for (; pp + 1 < nfc; pp += 2) {
         pair(pp, qa, ba, qb, bb);

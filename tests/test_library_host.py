@@ -394,3 +394,25 @@ def test_boundary_ghost_stencils_bit_exact(d, n, M, bc):
         c2 = P.Context(d, M, d + 2, device=None)
         c2.set_mesh(*gen.box_mesh(d, n, True)[:2], np.ones(d))
         c2.set_boundary(bc, 1)
+
+
+def test_partition_keeps_full_rowblock_tile():
+    """A partitioned rank keeps the row-block tile of one rank (T = 32 cells for the C4
+    shape): boundary tiles raise the stencil-union maximum (370 → 519 cells here), and
+    the layout takes fewer ring stages before it halves the tile (rank projection: a
+    C4 rank at T = 16 cost 1.48× the time per cell).  Host-only: the layout is planned
+    for the 227 KB shared-memory opt-in of sm_100a."""
+    nodes, cells, per = gen.box_mesh(3, 16, True, 0.1, 4)
+    seen = {}
+    for nranks in (1, 2, 4, 8):
+        c = P.Context(3, 3, 9, device=None)
+        c.set_mesh(nodes, cells, per)
+        if nranks > 1:
+            c.set_partition(nranks - 1, nranks)
+        c.build_stencils()
+        c.precompute()
+        i = c.info()
+        assert i["kernel_family"] == 1
+        seen[nranks] = (i["tile_cells"], i["union_max"])
+    assert all(t == 32 for t, _ in seen.values()), seen
+    assert max(u for _, u in seen.values()) > seen[1][1]      # the case this guards

@@ -142,8 +142,14 @@ cwreco_status cwreco_set_kernel(cwreco_ctx* ctx, int variant);
  *                        kernels (0 = one wave over every SM, the default).  A small
  *                        bound makes each CTA walk many tiles (tests of the multi-tile
  *                        pipeline) or leaves SMs free for concurrent work.
+ *   CWRECO_OPT_MAX_TILE  upper bound on the cells per tile of the packed layout chosen by
+ *                        the next cwreco_precompute (0 = the largest tile that fits, the
+ *                        default; rounded down to even, ≥ 2).  A smaller tile runs the
+ *                        kernels' runtime-tile-size instantiations (tests) and trades
+ *                        stage-ring depth for tile width.  Setting it drops the packed
+ *                        matrices (ESTATE until the next cwreco_precompute).
  * EINVAL for an unknown option or a value out of range. */
-enum { CWRECO_OPT_FAMILY = 1, CWRECO_OPT_MAX_CTAS = 2 };
+enum { CWRECO_OPT_FAMILY = 1, CWRECO_OPT_MAX_CTAS = 2, CWRECO_OPT_MAX_TILE = 3 };
 cwreco_status cwreco_set_option(cwreco_ctx* ctx, int option, int64_t value);
 
 /* ---------------------------------------------------------------- mesh / setup */

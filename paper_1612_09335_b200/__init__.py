@@ -11,7 +11,7 @@ import os
 
 import numpy as np
 
-__all__ = ["Context", "CwrecoError", "lib", "KERNELS", "OPT_FAMILY", "OPT_MAX_CTAS", "PART_ALL",
+__all__ = ["Context", "CwrecoError", "lib", "KERNELS", "OPT_FAMILY", "OPT_MAX_CTAS", "OPT_MAX_TILE", "PART_ALL",
            "nccl_unique_id", "loopback_unique_id",
            "PART_INTERIOR", "PART_BOUNDARY",
            "n_modes", "setup_context"]
@@ -20,7 +20,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "libcwreco.so")
 
 KERNELS = {"pipelined": 0, "simple": 1, "matrixfree": 2}
-OPT_FAMILY, OPT_MAX_CTAS = 1, 2
+OPT_FAMILY, OPT_MAX_CTAS, OPT_MAX_TILE = 1, 2, 3
 PART_ALL, PART_INTERIOR, PART_BOUNDARY = 0, 1, 2
 _STATUS = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "ECUDA", 4: "EMESH", 5: "ESTENCIL", 6: "ESINGULAR",
            7: "ESTATE", 8: "EUNSUPPORTED", 9: "ENCCL"}
@@ -258,7 +258,8 @@ class Context:
 
     def set_option(self, option, value):
         """cwreco_set_option: OPT_FAMILY (-1 default, 0 cell-variable, 1 row-block; before
-        precompute) or OPT_MAX_CTAS (0 = every SM)."""
+        precompute), OPT_MAX_CTAS (0 = every SM) or OPT_MAX_TILE (cells per tile, 0 = the
+        largest that fits; before precompute)."""
         _check(lib.cwreco_set_option(self._h, int(option), int(value)))
 
     def _need_shape(self, t, shape, what):
@@ -488,13 +489,15 @@ class Context:
 
 
 def setup_context(nodes, cells, period, degree_M, nvars, device=0, rank=0, nranks=1, family=-1, max_ctas=0,
-                  uid=None, **params):
+                  uid=None, max_tile=0, **params):
     """set_mesh → set_partition → build_stencils → precompute (family / max_ctas:
     cwreco_set_option, see include/cwreco.h)."""
     ctx = Context(nodes.shape[1], degree_M, nvars, device, **params)
     ctx.set_option(OPT_FAMILY, family)
     if max_ctas:
         ctx.set_option(OPT_MAX_CTAS, max_ctas)
+    if max_tile:
+        ctx.set_option(OPT_MAX_TILE, max_tile)
     ctx.set_mesh(nodes, cells, period)
     if nranks > 1:
         ctx.set_partition(rank, nranks, uid)

@@ -171,6 +171,11 @@ cwreco_status cwreco_set_option(cwreco_ctx* c, int option, int64_t value) {
         need(value >= 0 && value <= (1 << 30), CWRECO_EINVAL, "set_option: max_ctas must be >= 0");
         c->max_ctas = value;
         break;
+      case CWRECO_OPT_MAX_TILE:
+        need(value >= 0 && value <= (1 << 16), CWRECO_EINVAL, "set_option: max_tile must be >= 0");
+        c->max_tile = value;
+        c->has_blocks = false;  // the packed layout depends on the tile size
+        break;
       default:
         cwr::fail(CWRECO_EINVAL, "set_option: unknown option " + std::to_string(option));
     }

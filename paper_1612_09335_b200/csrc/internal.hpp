@@ -151,8 +151,9 @@ inline int64_t pipe_budget(int nm, int max_smem) {
 
 // max_smem: opt-in shared memory per block of the device (227 KB on B200);
 // umax_for(T): the largest per-tile stencil union for tiles of T cells.
+// max_tile (CWRECO_OPT_MAX_TILE): upper bound on the cells per tile (0: none).
 Layout make_layout(int d, int M, int V, int G, int max_smem, const std::function<int(int)>& umax_for,
-                   int family = -1);
+                   int family = -1, int max_tile = 0);
 // k_rowblk (warp-specialised, rowblk.cuh): a CTA of kRbThreads threads = main warps
 // (T = kRbMainThreads / NG cells × NG row groups, rounded up to whole warps), kRbEW
 // epilogue warps and one producer warp; one CTA per SM.
@@ -173,6 +174,8 @@ Layout make_layout(int d, int M, int V, int G, int max_smem, const std::function
 CWR_HD constexpr int rb_main(int R, int V) { return (void)V, R > 14 ? CWR_RB_MAIN : 192; }
 CWR_HD constexpr int rb_ew(int R, int V) { return (void)V, R > 14 ? CWR_RB_EW : 5; }
 CWR_HD constexpr int rb_main_warps(int T, int NG) { return (T * NG + 31) / 32; }
+// the full row-block tile: main threads / row groups, even (T·R·8 a multiple of 16 bytes)
+CWR_HD constexpr int rb_tfull(int R, int V) { return (rb_main(R, V) / rb_ng(R, V)) & ~1; }
 // threads of a row-block CTA (main + epilogue + producer warp): the kernel's launch bound
 CWR_HD constexpr int rb_threads(int R, int V) { return 32 * ((rb_main(R, V) + 31) / 32 + rb_ew(R, V) + 1); }
 // setmaxnreg split (3 warp groups of 128 threads launched at 168 registers): the main
@@ -235,6 +238,7 @@ struct cwreco_ctx {
   int kernel = CWRECO_KERNEL_PIPELINED;
   int family = -1;       // CWRECO_OPT_FAMILY (-1: default per shape)
   int64_t max_ctas = 0;  // CWRECO_OPT_MAX_CTAS (0: every SM)
+  int64_t max_tile = 0;  // CWRECO_OPT_MAX_TILE (0: the largest tile that fits)
 
   // ---- mesh, SFC order (set_mesh)
   bool has_mesh = false;

@@ -285,8 +285,8 @@ struct PipeCfg {
 using PipeFn = void (*)(KArgs, PipeCfg);
 
 // row-block kernels (rowblk_2d.cu, rowblk_3d.cu): nullptr if (M, V) is not instantiated
-PipeFn rowblk_fn_2d(int M, int V);
-PipeFn rowblk_fn_3d(int M, int V);
+PipeFn rowblk_fn_2d(int M, int V, bool full_tile);
+PipeFn rowblk_fn_3d(int M, int V, bool full_tile);
 cudaError_t rowblk_upload_sigma_2d(const double* packed, size_t bytes, size_t offset);
 cudaError_t rowblk_upload_sigma_3d(const double* packed, size_t bytes, size_t offset);
 

@@ -477,10 +477,11 @@ static KArgs make_args(const cwreco_ctx* c, const double* avgs, int64_t acs, int
 }
 
 bool rowblk_supported(int d, int M, int V) {
-  return (d == 2 ? rowblk_fn_2d(M, V) : d == 3 ? rowblk_fn_3d(M, V) : nullptr) != nullptr;
+  return (d == 2 ? rowblk_fn_2d(M, V, true) : d == 3 ? rowblk_fn_3d(M, V, true) : nullptr) != nullptr;
 }
 static PipeFn rowblk_fn(const cwreco_ctx* c) {
-  PipeFn f = c->d == 2 ? rowblk_fn_2d(c->M, c->V) : rowblk_fn_3d(c->M, c->V);
+  const bool full = c->lay.T == rb_tfull(c->lay.R, c->lay.V);
+  PipeFn f = c->d == 2 ? rowblk_fn_2d(c->M, c->V, full) : rowblk_fn_3d(c->M, c->V, full);
   if (!f) fail(CWRECO_EUNSUPPORTED, "row-block kernel not instantiated for (d, M, V)");
   return f;
 }
@@ -509,7 +510,9 @@ static PipeCfg pipe_cfg(const cwreco_ctx* c, int* ctas = nullptr) {
     if (cap) st = std::max(kRbMinStages, std::min(st, std::atoi(cap)));
     if (!k) fail(CWRECO_EUNSUPPORTED, "row-block kernel: tile does not fit in shared memory");
     if (ctas) *ctas = 1;
-    p.ncw = rb_main_warps(L.T, rb_ng(L.R, L.V));
+    // the CTA keeps its compiled shape whatever T is (setmaxnreg acts per warp group:
+    // the 4 main warps must fill warp group 0); main threads tid ≥ T·NG idle in the loop
+    p.ncw = rb_main_warps(rb_tfull(L.R, L.V), rb_ng(L.R, L.V));
     p.eww = rb_ew(L.R, L.V);
     p.stages = st;
     p.stage_bytes = round128(L.chunk_bytes);

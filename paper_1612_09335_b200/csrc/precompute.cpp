@@ -67,7 +67,8 @@ void rowblk_plan(const Layout& L, int max_smem, int max_ctas, int& ctas, int& st
 }
 
 Layout make_layout(int d, int M, int V, int G, int max_smem, const std::function<int(int)>& umax_for,
-                   int family) {
+                   int family, int max_tile) {
+  auto capped = [&](int T) { return max_tile > 0 && T > max_tile ? std::max(2, max_tile & ~1) : T; };
   const int nm = n_modes(M, d);
   // family (cwreco_set_option CWRECO_OPT_FAMILY): -1 = default, 0 = cell-variable,
   // 1 = row-block where instantiated
@@ -77,7 +78,7 @@ Layout make_layout(int d, int M, int V, int G, int max_smem, const std::function
     // KC positions per chunk: ~10 KB of B⁺ per stage, KC ∈ {1, 2, 4} (compiled sizes)
     const int R = nm - 1;
     // T even: a position slice T·R doubles must stay a multiple of 16 bytes (TMA bulk sizes)
-    for (int T = (rb_main(R, V) / rb_ng(R, V)) & ~1; T >= 2; T = (T / 2) & ~1) {
+    for (int T = capped(rb_tfull(R, V)); T >= 2; T = (T / 2) & ~1) {
       // the whole sector chunk of a tile goes to its own buffer: one piece
       Layout L = layout_with(d, M, V, G, T, kRbKC, umax_for(T), KIND_ROWBLK, 1);
       int ctas, stages;
@@ -88,6 +89,7 @@ Layout make_layout(int d, int M, int V, int G, int max_smem, const std::function
   // one tile = T cells × V variables = one consumer thread each
   int T0 = (cons_threads(nm) / V) & ~1;
   if (T0 < 2) T0 = 2;
+  T0 = capped(T0);
   // positions per streamed chunk: ~10 KB of B⁺ per chunk (measured best: larger
   // chunks lengthen the gather bursts, smaller ones add per-chunk synchronisation),
   // even (the kernel reads position pairs with 16-byte shared loads), a compiled
@@ -378,7 +380,7 @@ void precompute(cwreco_ctx* c) {
       fail(CWRECO_EUNSUPPORTED, "precompute: tile stencil union × nvars exceeds the 16-bit offsets");
     return umax;
   };
-  c->lay = make_layout(d, M, c->V, G, c->device >= 0 ? dev_max_smem(c) : 227 * 1024, umax_for, c->family);
+  c->lay = make_layout(d, M, c->V, G, c->device >= 0 ? dev_max_smem(c) : 227 * 1024, umax_for, c->family, (int)c->max_tile);
   const Layout& L = c->lay;
   const int T = L.T;
   c->n_tiles = (c->n_owned + T - 1) / T;

@@ -52,6 +52,15 @@ constexpr int RB_BAR_OFULL = 1, RB_BAR_OFREE = 2, RB_BAR_EW = 3;
 #ifndef CWR_RB_PF
 #define CWR_RB_PF 0  // B⁺ of the next pair loaded per position between the FMAs (see pair())
 #endif
+// Whole-stage main loop without the per-pair stage / end tests: -1 = for ℳ = 20 only
+// (measured, same box: C4 proxy 0.841 vs 0.760, C5 shape 1.055 vs 1.040; 3-D M = 2 on
+// C3 0.712 vs 0.725), 0 = never, 1 = always
+#ifndef CWR_RB_STATIC
+#define CWR_RB_STATIC -1
+#endif
+#ifndef CWR_RB_TT
+#define CWR_RB_TT 1  // instantiate the full tile size T as a compile-time constant
+#endif
 #ifndef CWR_RB_LOOK1
 #define CWR_RB_LOOK1 0  // main loop with a one-position lookahead instead of the pair ping-pong
 #endif
@@ -64,7 +73,9 @@ __device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-template <int D, int M, int V>
+// TT > 0: the tile holds TT cells (compile time: the B⁺ slot offsets (r·NG + kk·R)·T
+// become immediates of the shared loads); TT = 0: a.T (a layout whose tile was halved)
+template <int D, int M, int V, int TT>
 __global__ void __launch_bounds__(rb_threads(nmodes(M, D) - 1, V), 1) k_rowblk(KArgs a, PipeCfg pc) {
   constexpr int NM = nmodes(M, D), R = NM - 1, NV = D + 1, NCAP = NV * D;
   constexpr int NG = rb_ng(R, V), RB = rb_rb(R, V), NF = rb_nfull(R, V);
@@ -86,7 +97,7 @@ __global__ void __launch_bounds__(rb_threads(nmodes(M, D) - 1, V), 1) k_rowblk(K
   uint64_t* qfull = sempty + 2;     // [2] gather of Q_u[b] complete
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  const int T = a.T;
+  const int T = TT > 0 ? TT : a.T;
   const int MW = pc.ncw * 32, EW = pc.eww * 32, NB = MW + EW;  // main / epilogue threads
   const int64_t t0 = a.tile_begin + blockIdx.x;                 // this CTA's tiles: t0 + k·grid
   const int nk = t0 < a.tile_end ? int((a.tile_end - 1 - t0) / gridDim.x + 1) : 0;
@@ -353,6 +364,36 @@ __global__ void __launch_bounds__(rb_threads(nmodes(M, D) - 1, V), 1) k_rowblk(K
       };
 #endif
       int pp = 0;
+      constexpr bool kStatic = CWR_RB_STATIC < 0 ? R > 14 : CWR_RB_STATIC > 0;
+      if constexpr (kStatic) {
+        // whole stages while the successor pair exists: the first pair of a stage stays in
+        // it, the second opens the next stage — no per-pair stage / end tests
+        static_assert(PPS == 2, "static stage loop: 2 position pairs per stage");
+        auto pair_in = [&](int pp, const double (&q)[2][V], const double (&b)[2][RB], double (&qn)[2][V],
+                           double (&bn)[2][RB]) {
+          ldq2(ipn, qn);
+          ipn = ix2[(pp + 2) * T];
+          fma_pos(q[0], b[0]);
+          fma_pos(q[1], b[1]);
+          ldb(stage_ptr() + 2 * R * T, bn);
+        };
+        auto pair_out = [&](int pp, const double (&q)[2][V], const double (&b)[2][RB], double (&qn)[2][V],
+                            double (&bn)[2][RB]) {
+          ldq2(ipn, qn);
+          ipn = ix2[min(pp + 2, npr - 1) * T];
+          fma_pos(q[0], b[0]);
+          fma_pos(q[1], b[1]);
+          Ring nr = rg;
+          nr.next(S);
+          mbar_wait(&full[nr.st], nr.ph);
+          ldb((const double*)(stg + nr.st * pc.stage_bytes), bn);
+          release();
+        };
+        for (; pp + 2 < npr && pp + 1 < nfc; pp += 2) {
+          pair_in(pp, qa, ba, qb, bb);
+          pair_out(pp + 1, qb, bb, qa, ba);
+        }
+      }
       for (; pp + 1 < nfc; pp += 2) {
         pair(pp, qa, ba, qb, bb);
         pair(pp + 1, qb, bb, qa, ba);
@@ -472,19 +513,25 @@ __global__ void __launch_bounds__(rb_threads(nmodes(M, D) - 1, V), 1) k_rowblk(K
   cp_async_wait<0>();
 }
 
-// Instantiations per translation unit (rowblk_2d.cu, rowblk_3d.cu)
+// Instantiations per translation unit (rowblk_2d.cu, rowblk_3d.cu): full_tile = the
+// layout kept the full tile (rb_tfull), else the runtime-T instantiation
+template <int D, int M, int V>
+PipeFn rowblk_fn_t(bool full_tile) {
+  constexpr int TF = CWR_RB_TT ? rb_tfull(nmodes(M, D) - 1, V) : 0;
+  return full_tile ? k_rowblk<D, M, V, TF> : k_rowblk<D, M, V, 0>;
+}
 template <int D, int M>
-PipeFn rowblk_fn_v(int V) {
+PipeFn rowblk_fn_v(int V, bool full_tile) {
   switch (V) {
-    case 1: return k_rowblk<D, M, 1>;
-    case 2: return k_rowblk<D, M, 2>;
-    case 3: return k_rowblk<D, M, 3>;
-    case 4: return k_rowblk<D, M, 4>;
-    case 5: return k_rowblk<D, M, 5>;
-    case 6: return k_rowblk<D, M, 6>;
-    case 7: return k_rowblk<D, M, 7>;
-    case 8: return k_rowblk<D, M, 8>;
-    case 9: return k_rowblk<D, M, 9>;
+    case 1: return rowblk_fn_t<D, M, 1>(full_tile);
+    case 2: return rowblk_fn_t<D, M, 2>(full_tile);
+    case 3: return rowblk_fn_t<D, M, 3>(full_tile);
+    case 4: return rowblk_fn_t<D, M, 4>(full_tile);
+    case 5: return rowblk_fn_t<D, M, 5>(full_tile);
+    case 6: return rowblk_fn_t<D, M, 6>(full_tile);
+    case 7: return rowblk_fn_t<D, M, 7>(full_tile);
+    case 8: return rowblk_fn_t<D, M, 8>(full_tile);
+    case 9: return rowblk_fn_t<D, M, 9>(full_tile);
     default: return nullptr;
   }
 }

@@ -3,9 +3,9 @@
 
 namespace cwr {
 
-PipeFn rowblk_fn_2d(int M, int V) {
-  if (M == 3) return rowblk_fn_v<2, 3>(V);
-  if (M == 4) return rowblk_fn_v<2, 4>(V);
+PipeFn rowblk_fn_2d(int M, int V, bool full_tile) {
+  if (M == 3) return rowblk_fn_v<2, 3>(V, full_tile);
+  if (M == 4) return rowblk_fn_v<2, 4>(V, full_tile);
   return nullptr;
 }
 

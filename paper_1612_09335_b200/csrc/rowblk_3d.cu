@@ -3,9 +3,9 @@
 
 namespace cwr {
 
-PipeFn rowblk_fn_3d(int M, int V) {
-  if (M == 2) return rowblk_fn_v<3, 2>(V);
-  if (M == 3) return rowblk_fn_v<3, 3>(V);
+PipeFn rowblk_fn_3d(int M, int V, bool full_tile) {
+  if (M == 2) return rowblk_fn_v<3, 2>(V, full_tile);
+  if (M == 3) return rowblk_fn_v<3, 3>(V, full_tile);
   return nullptr;
 }
 

@@ -394,6 +394,30 @@ def test_many_tiles_per_cta_parity():
         assert np.array_equal(simple, full), (d, M, V, fam)
 
 
+def test_smaller_tile_parity():
+    """CWRECO_OPT_MAX_TILE: layouts with smaller tiles (the row-block kernel's runtime-T
+    instantiation, the one a layout whose tile had to be halved runs) give results
+    bitwise equal to the full-tile layout (compile-time T) and to k_simple, with many
+    tiles per CTA."""
+    for d, n, M, V, fam in [(3, 6, 3, 9, 1), (3, 6, 2, 5, 1), (2, 24, 3, 4, 1), (2, 24, 3, 4, 0)]:
+        nodes, cells, period = gen.box_mesh(d, n, True, 0.15, 29)
+        Q = np.random.default_rng(d * M + V).standard_normal((cells.shape[0], V)) + 1.0
+        ctx = P.setup_context(nodes, cells, period, M, V, device=0, family=fam)
+        Tfull = ctx.info()["tile_cells"]
+        Qp = torch.tensor(Q[ctx.permutation()], device="cuda")
+        full = ctx.reconstruct(Qp).cpu().numpy()
+        for cap in (Tfull // 2, 10):
+            ctx.set_option(P.OPT_MAX_TILE, cap)
+            ctx.precompute()
+            assert ctx.info()["tile_cells"] == cap, (d, M, V, fam, cap)
+            ctx.set_option(P.OPT_MAX_CTAS, 3)
+            got = ctx.reconstruct(Qp).cpu().numpy()
+            ctx.set_option(P.OPT_MAX_CTAS, 0)
+            assert np.array_equal(got, full), (d, M, V, fam, cap)
+        ctx.set_kernel("simple")
+        assert np.array_equal(ctx.reconstruct(Qp).cpu().numpy(), full)
+
+
 @pytest.mark.parametrize("family", ["0", "1"], ids=["cellvar", "rowblk"])
 @pytest.mark.parametrize("d,n,M,V,bc", [(2, 10, 3, 4, [1, 2, 2, 1]), (2, 9, 2, 4, [2, 2, 2, 2]),
                                         (3, 4, 2, 5, [1, 2, 1, 2, 2, 1]), (3, 4, 3, 5, [2, 0, 1, 1, 2, 2])],

@@ -15,6 +15,10 @@ efficiency = t_1 / (P · that).  The single-rank time t_1 is measured in the sam
 (--t1 skips it).
 
     python tools/rank_projection.py --config C4 --nranks 2 4 8 [--ranks 0 7]
+    python tools/rank_projection.py --config C5 --weak --nranks 2 4 8 --ranks 0
+
+--weak: the mesh grows with P as bench.py's weak ladder does (bench.workload_n: C5
+n = 100/126/159/200, ≈ 6 M cells per rank); efficiency = t_1 / that step.
 """
 import argparse
 import json
@@ -59,11 +63,14 @@ def main():
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--link-gbs", type=float, default=900.0)
     ap.add_argument("--t1", type=float, default=None, help="single-rank ms (skip measuring it)")
+    ap.add_argument("--weak", action="store_true", help="weak ladder: the mesh grows with P (bench.workload_n)")
     args = ap.parse_args()
+    import bench
     w = gen.make(args.config)
     d, M, V = w["d"], w["M"], w["V"]
     perm = None
     report = {"config": args.config, "n_cells": int(w["cells"].shape[0]), "link_gbs": args.link_gbs,
+              "scaling": "weak" if args.weak else "strong",
               "library": P.lib.cwreco_version().decode(), "ranks": {}}
     all_parts = [("all", P.PART_ALL), ("interior", P.PART_INTERIOR), ("boundary", P.PART_BOUNDARY)]
     if args.t1 is None:
@@ -83,6 +90,10 @@ def main():
     for Pn in args.nranks:
         ranks = args.ranks if args.ranks else list(range(Pn))
         rows = {}
+        if args.weak:
+            del w
+            w = gen.make(args.config, bench.workload_n(args.config, Pn))
+            perm = None
         for r in ranks:
             t0 = time.time()
             ctx = P.setup_context(w["nodes"], w["cells"], w["period"], M, V, device=0, rank=r, nranks=Pn)
@@ -112,10 +123,11 @@ def main():
             row["halo_bytes_in"], row["halo_bytes_out"], row["t_exchange_est_ms"] = recv_b, send_b, t_x
             row["t_overlapped_est_ms"] = max(row["t_all_ms"], row["t_interior_ms"] + t_x + row["t_boundary_ms"])
             worst = max(worst, row["t_overlapped_est_ms"])
-        report["ranks"][str(Pn)] = dict(per_rank=rows, step_est_ms=worst,
-                                        strong_eff_est=t1 / (Pn * worst) if worst > 0 else None,
+        eff = (t1 if args.weak else t1 / Pn) / worst if worst > 0 else None
+        report["ranks"][str(Pn)] = dict(per_rank=rows, step_est_ms=worst, n_cells=int(w["cells"].shape[0]),
+                                        **{("weak" if args.weak else "strong") + "_eff_est": eff},
                                         all_ranks_measured=full)
-        print(f"P={Pn}: projected step {worst:.3f} ms, strong efficiency {t1 / (Pn * worst):.3f}",
+        print(f"P={Pn}: projected step {worst:.3f} ms, {'weak' if args.weak else 'strong'} efficiency {eff:.3f}",
               file=sys.stderr, flush=True)
     print(json.dumps(report))
 

@@ -58,6 +58,12 @@ constexpr int RB_BAR_OFULL = 1, RB_BAR_OFREE = 2, RB_BAR_EW = 3;
 #ifndef CWR_RB_STATIC
 #define CWR_RB_STATIC -1
 #endif
+#ifndef CWR_RB_L2PF
+#define CWR_RB_L2PF 0  // producer: L2 prefetch this many position chunks ahead (0: none)
+#endif
+#ifndef CWR_RB_GCELL
+#define CWR_RB_GCELL 0  // union gather: one union cell per thread and step (else one element)
+#endif
 #ifndef CWR_RB_TT
 #define CWR_RB_TT 1  // instantiate the full tile size T as a compile-time constant
 #endif
@@ -152,10 +158,30 @@ __global__ void __launch_bounds__(rb_threads(nmodes(M, D) - 1, V), 1) k_rowblk(K
       };
       for (int k = 0; k < nk && k < 2; ++k) load_union(k);
       if (nk > 0) load_sector(0);
+#if CWR_RB_L2PF > 0
+      // L2 prefetch of the position chunks CWR_RB_L2PF chunks beyond the one being
+      // loaded into the ring: more bytes in flight than the ring's shared memory holds,
+      // so a stage's bulk copy finds its chunk in L2
+      int pfk = 0, pfc = 0;  // next chunk to prefetch (tile k of this CTA, chunk)
+      auto prefetch_to = [&](int k, int ch) {
+        const int64_t lim = int64_t(k) * a.NCH + ch + CWR_RB_L2PF;
+        while (pfk < nk && int64_t(pfk) * a.NCH + pfc <= lim) {
+          const uint32_t bytes = (uint32_t)(min(a.KC, a.G - pfc * a.KC) * a.kslice_bytes);
+          bulk_prefetch_l2(a.blocks + tile_of(pfk) * a.tile_bytes + a.u_bytes + pfc * a.chunk_bytes, bytes);
+          if (++pfc == a.NCH) {
+            pfc = 0;
+            ++pfk;
+          }
+        }
+      };
+#endif
       for (int k = 0; k < nk; ++k) {
         RB_TRACE(k, 9);
         const unsigned char* tb = a.blocks + tile_of(k) * a.tile_bytes;
         for (int ch = 0; ch < a.NCH; ++ch) {
+#if CWR_RB_L2PF > 0
+          prefetch_to(k, ch);
+#endif
           mbar_wait_sleep(&empty[rg.st], rg.ph ^ 1);
           const uint32_t bytes = (uint32_t)(min(a.KC, a.G - ch * a.KC) * a.kslice_bytes);
           mbar_expect_tx(&full[rg.st], bytes);
@@ -180,6 +206,18 @@ __global__ void __launch_bounds__(rb_threads(nmodes(M, D) - 1, V), 1) k_rowblk(K
     mbar_wait(&ufull[s], (k / 3) & 1);
     const int32_t* uid = (const int32_t*)(ubuf + s * pc.ubuf_bytes);
     double* dst = Qu + (size_t)(k & 1) * a.Umax * VP;
+#if CWR_RB_GCELL
+    if (!EXP(a, 1)) {
+      // one union cell per thread and step: its id once, then its V averages
+      for (int u = etid; u < a.Umax; u += EW) {
+        const int64_t j = uid[u];
+        const double* src = j < a.n_local ? a.Q + j * a.acs : a.Qbc + (j - a.n_local) * a.V;
+        const int64_t sv = j < a.n_local ? a.avs : 1;
+#pragma unroll
+        for (int vv = 0; vv < V; ++vv) cp_async8(dst + u * VP + vv, src + vv * sv);
+      }
+    }
+#else
     if (!EXP(a, 1)) {
       // element e = u·V + vv, e = etid, etid + EW, …: (u, vv) stepped without divisions
       int u = etid / V, vv = etid - (etid / V) * V;
@@ -194,6 +232,7 @@ __global__ void __launch_bounds__(rb_threads(nmodes(M, D) - 1, V), 1) k_rowblk(K
         }
       }
     }
+#endif
     cp_async_mbar_arrive_noinc(&qfull[k & 1]);
   };
 

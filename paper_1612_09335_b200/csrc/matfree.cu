@@ -37,6 +37,16 @@ namespace cwr {
     if (e_ != cudaSuccess) fail(CWRECO_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
   } while (0)
 
+#ifndef CWR_MF_V2
+#define CWR_MF_V2 1  // unrolled basis transform, rsqrt pivots, column back substitution
+#endif
+#ifndef CWR_MF_UNROLL
+#define CWR_MF_UNROLL 0  // basis transform fully unrolled (register pressure: spills at 4 CTAs/SM)
+#endif
+// resident 4-warp CTAs per SM the register allocation must allow (3-D M = 3 with many
+// variables: 3, i.e. 168 registers; otherwise 4, i.e. 128)
+__host__ __device__ constexpr int mf_minb(int D, int M, int V) { return D == 3 && M == 3 && V > 6 ? 3 : 4; }
+
 // Basis (monomial form) and quadrature tables of every supported (d, M), each in its
 // own slot of the constant bank, so contexts of different (d, M) on one device never
 // overwrite each other's tables (the tables depend only on (d, M)).
@@ -241,7 +251,7 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
 //     epilogue and store w.
 // fp64-ALU bound; HBM per cell ≈ geometry + stencil ids + Q + w.
 template <int D, int M, int V>
-__global__ void __launch_bounds__(128) k_matfree(MfArgs m, KArgs a) {
+__global__ void __launch_bounds__(128, mf_minb(D, M, V)) k_matfree(MfArgs m, KArgs a) {
   using S = MfShape<D, M, V>;
   constexpr int NM = S::NM, R = S::R, NV = S::NV, K = S::K, KP = S::KP, NC = S::NC, NCP = S::NCP, NB = S::NB,
                 XS = S::XS,
@@ -295,7 +305,11 @@ __global__ void __launch_bounds__(128) k_matfree(MfArgs m, KArgs a) {
     for (int v = 0; v < V; ++v) qi[v] = a.Q[i * a.acs + v * a.avs];
 
     // ---- 1. rows of X = [A | ΔQ]
+#if CWR_MF_UNROLL
+#pragma unroll 1  // one row at a time: the unrolled basis transform keeps one row's moments live
+#else
 #pragma unroll
+#endif
     for (int r = 0; r < KPL; ++r) {
       const int k = lane + 32 * r;
       if (k >= KP) continue;
@@ -305,9 +319,13 @@ __global__ void __launch_bounds__(128) k_matfree(MfArgs m, KArgs a) {
         for (int l = 0; l < NCP; ++l) xr[l] = 0.0;
         continue;
       }
-      const int32_t j = jc[r];
+      int32_t j = jc[0];
+      uint8_t jcode = cc[0];
+#pragma unroll
+      for (int rr = 1; rr < KPL; ++rr)  // selects, not a runtime-indexed register array
+        if (r == rr) j = jc[rr], jcode = cc[rr];
       double sh[D];
-      shift_vec<D>(cc[r], m.L, sh);
+      shift_vec<D>(jcode, m.L, sh);
       const double* Xj = m.X + int64_t(j) * NV * D;
       // vertices y_v of T_j in ξ_i coordinates, y_0 = J⁻¹(X_j0 + shift − X0),
       // y_v = y_0 + J⁻¹(X_jv − X_j0), accumulated into the power sums as they are formed
@@ -368,12 +386,24 @@ __global__ void __launch_bounds__(128) k_matfree(MfArgs m, KArgs a) {
       for (int n = 1; n <= M; ++n) {
         const int lo = D == 2 ? n * (n + 1) / 2 : n * (n + 1) * (n + 2) / 6;
         const int hi = D == 2 ? (n + 1) * (n + 2) / 2 : (n + 1) * (n + 2) * (n + 3) / 6;
+#if CWR_MF_UNROLL
+#pragma unroll  // compile-time offsets: the coefficients are constant-bank operands of the FMAs
+#else
 #pragma unroll 1
+#endif
         for (int l = lo; l < hi; ++l) {
+#if CWR_MF_V2
+          // four interleaved partial sums: the dependent chain is hi/4 FMAs, not hi
+          double s4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+          for (int e = 0; e < hi; ++e) s4[e & 3] = fma(mcoef[l * NM + e], mom[e], s4[e & 3]);
+          xr[l - 1] = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+#else
           double s2 = 0.0;
 #pragma unroll
           for (int e = 0; e < hi; ++e) s2 = fma(mcoef[l * NM + e], mom[e], s2);
           xr[l - 1] = s2;
+#endif
         }
       }
 #pragma unroll
@@ -476,7 +506,11 @@ __global__ void __launch_bounds__(128) k_matfree(MfArgs m, KArgs a) {
 #pragma unroll
     for (int c = 0; c < R; ++c) {
       const double dcc = __shfl_sync(0xffffffffu, g[c], c);
+#if CWR_MF_V2
+      const double inv = rsqrt(dcc);  // one op on the serial chain; NaN for a rank-deficient stencil
+#else
       const double inv = 1.0 / sqrt(dcc);  // NaN for a rank-deficient stencil (no silent result)
+#endif
       const double u = g[c] * inv;
       g[c] = u;
       if (lane == c) G[c * GS + NCP] = inv;  // 1/U[c][c] in the padding column
@@ -496,6 +530,19 @@ __global__ void __launch_bounds__(128) k_matfree(MfArgs m, KArgs a) {
 #pragma unroll
     for (int s2 = 0; s2 < NV; ++s2) valid[s2] = (vbits >> s2) & 1;
     if (lane < V) {
+#if CWR_MF_V2
+      // column-oriented: once p[c] is known it updates every row above it (independent
+      // FMAs), so the dependent chain is R steps long instead of R²/2
+      double t[R];
+#pragma unroll
+      for (int c = 0; c < R; ++c) t[c] = G[c * GS + R + lane];
+#pragma unroll
+      for (int c = R - 1; c >= 0; --c) {
+        acc[c] = t[c] * G[c * GS + NCP];
+#pragma unroll
+        for (int j = 0; j < c; ++j) t[j] = fma(-G[j * GS + c], acc[c], t[j]);
+      }
+#else
 #pragma unroll
       for (int c = R - 1; c >= 0; --c) {
         double t = G[c * GS + R + lane];
@@ -503,6 +550,7 @@ __global__ void __launch_bounds__(128) k_matfree(MfArgs m, KArgs a) {
         for (int mm = c + 1; mm < R; ++mm) t = fma(-G[c * GS + mm], acc[mm], t);
         acc[c] = t * G[c * GS + NCP];
       }
+#endif
 #pragma unroll
       for (int s2 = 0; s2 < NV; ++s2)
 #pragma unroll

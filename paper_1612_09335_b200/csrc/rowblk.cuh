@@ -61,9 +61,6 @@ constexpr int RB_BAR_OFULL = 1, RB_BAR_OFREE = 2, RB_BAR_EW = 3;
 #ifndef CWR_RB_L2PF
 #define CWR_RB_L2PF 0  // producer: L2 prefetch this many position chunks ahead (0: none)
 #endif
-#ifndef CWR_RB_GCELL
-#define CWR_RB_GCELL 0  // union gather: one union cell per thread and step (else one element)
-#endif
 #ifndef CWR_RB_TT
 #define CWR_RB_TT 1  // instantiate the full tile size T as a compile-time constant
 #endif
@@ -206,18 +203,6 @@ __global__ void __launch_bounds__(rb_threads(nmodes(M, D) - 1, V), 1) k_rowblk(K
     mbar_wait(&ufull[s], (k / 3) & 1);
     const int32_t* uid = (const int32_t*)(ubuf + s * pc.ubuf_bytes);
     double* dst = Qu + (size_t)(k & 1) * a.Umax * VP;
-#if CWR_RB_GCELL
-    if (!EXP(a, 1)) {
-      // one union cell per thread and step: its id once, then its V averages
-      for (int u = etid; u < a.Umax; u += EW) {
-        const int64_t j = uid[u];
-        const double* src = j < a.n_local ? a.Q + j * a.acs : a.Qbc + (j - a.n_local) * a.V;
-        const int64_t sv = j < a.n_local ? a.avs : 1;
-#pragma unroll
-        for (int vv = 0; vv < V; ++vv) cp_async8(dst + u * VP + vv, src + vv * sv);
-      }
-    }
-#else
     if (!EXP(a, 1)) {
       // element e = u·V + vv, e = etid, etid + EW, …: (u, vv) stepped without divisions
       int u = etid / V, vv = etid - (etid / V) * V;
@@ -232,7 +217,6 @@ __global__ void __launch_bounds__(rb_threads(nmodes(M, D) - 1, V), 1) k_rowblk(K
         }
       }
     }
-#endif
     cp_async_mbar_arrive_noinc(&qfull[k & 1]);
   };
 

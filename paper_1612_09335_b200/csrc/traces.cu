@@ -93,74 +93,22 @@ __global__ void __launch_bounds__(256) k_traces(const double* __restrict__ w, in
   }
 }
 
-// Round 2: one 1024-thread block per SM (the table Φ in shared memory once per SM, 32
-// warps in flight instead of 16), no output staging: the thread of unit (cell, face,
-// QB points) stores its QB·V contiguous outputs itself, and the units of consecutive
-// cells are consecutive threads, so a warp's stores cover one contiguous range.
-template <int NM, int V, int QB>
-__global__ void __launch_bounds__(1024) k_traces_wide(const double* __restrict__ w, int64_t ccs, int64_t cvs,
-                                                      const double* __restrict__ phi, int phi_n,
-                                                      const uint8_t* __restrict__ code, int nf, int nq, int cb,
-                                                      int64_t n_owned, double* __restrict__ out) {
-  extern __shared__ __align__(16) double tr_smem[];  // [phi_n] table
-  for (int k = threadIdx.x; k < phi_n; k += blockDim.x) tr_smem[k] = phi[k];
-  __syncthreads();
-  const int nb = nq / QB, units = nf * nb;
-  const int cl = threadIdx.x / units, fb = threadIdx.x - cl * units, f = fb / nb, q0 = (fb - f * nb) * QB;
-  if (cl >= cb) return;  // cb = cells per block step
-  for (int64_t i = int64_t(blockIdx.x) * cb + cl; i < n_owned; i += int64_t(gridDim.x) * cb) {
-    const double* p = tr_smem + (int(code[i * nf + f]) * nq + q0) * NM;
-    const double* wi = w + i * ccs;
-    double acc[V][QB];
-#pragma unroll
-    for (int v = 0; v < V; ++v)
-#pragma unroll
-      for (int b = 0; b < QB; ++b) acc[v][b] = 0.0;
-#pragma unroll 5
-    for (int l = 0; l < NM; ++l) {
-      double ph[QB], wv[V];
-#pragma unroll
-      for (int b = 0; b < QB; ++b) ph[b] = p[b * NM + l];
-#pragma unroll
-      for (int v = 0; v < V; ++v) wv[v] = __ldg(wi + v * cvs + l);
-#pragma unroll
-      for (int v = 0; v < V; ++v)
-#pragma unroll
-        for (int b = 0; b < QB; ++b) acc[v][b] = __fma_rn(wv[v], ph[b], acc[v][b]);
-    }
-    double* o = out + ((i * nf + f) * nq + q0) * V;
-#pragma unroll
-    for (int b = 0; b < QB; ++b)
-#pragma unroll
-      for (int v = 0; v < V; ++v) o[b * V + v] = acc[v][b];
-  }
-}
-
 using TrFn = void (*)(const double*, int64_t, int64_t, const double*, int, const uint8_t*, int, int, int, int64_t,
                       double*);
-#ifndef CWR_TR_WIDE
-#define CWR_TR_WIDE 1  // k_traces_wide (1024-thread blocks, direct stores) instead of k_traces
-#endif
 template <int NM, int QB>
 static TrFn tr_fn_v(int V) {
-#if CWR_TR_WIDE
-#define TRK k_traces_wide
-#else
-#define TRK k_traces
-#endif
   switch (V) {
-    case 1: return TRK<NM, 1, QB>;
-    case 2: return TRK<NM, 2, QB>;
-    case 3: return TRK<NM, 3, QB>;
-    case 4: return TRK<NM, 4, QB>;
-    case 5: return TRK<NM, 5, QB>;
-    case 6: return TRK<NM, 6, QB>;
-    case 7: return TRK<NM, 7, QB>;
-    case 8: return TRK<NM, 8, QB>;
-    case 9: return TRK<NM, 9, QB>;
+    case 1: return k_traces<NM, 1, QB>;
+    case 2: return k_traces<NM, 2, QB>;
+    case 3: return k_traces<NM, 3, QB>;
+    case 4: return k_traces<NM, 4, QB>;
+    case 5: return k_traces<NM, 5, QB>;
+    case 6: return k_traces<NM, 6, QB>;
+    case 7: return k_traces<NM, 7, QB>;
+    case 8: return k_traces<NM, 8, QB>;
+    case 9: return k_traces<NM, 9, QB>;
     default: return nullptr;
   }
-#undef TRK
 }
 // points per work unit (measured, tools/traces_bench.py with CWRECO_TRACE_QB, table in
 // shared memory): 3 for the 9-point faces of 3-D M = 2 (C3 1.08 ms), 2 for ℳ = 20 (C5:
@@ -279,20 +227,19 @@ void dev_face_traces(cwreco_ctx* c, const double* coeffs, int64_t ccs, int64_t c
   }
 #endif
   const int units = nv * (t->nq / qb);
-  const int threads = CWR_TR_WIDE ? 1024 : 256;
-  const int cb = std::max(1, threads / units);
+  const int cb = std::max(1, 256 / units);
   const int64_t groups = (c->n_owned + cb - 1) / cb;
   if (groups == 0) return;
   const int phi_n = t->ncc * t->nq * c->nm;
-  const size_t smem = (size_t((phi_n + 1) & ~1) + (CWR_TR_WIDE ? 0 : size_t(cb) * nv * t->nq * c->V)) * sizeof(double);
+  const size_t smem = (size_t((phi_n + 1) & ~1) + size_t(cb) * nv * t->nq * c->V) * sizeof(double);
   TrFn f = tr_fn(c->nm, c->V, qb);
   TCK(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 1, nsm = 148;
-  TCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)f, threads, smem));
+  TCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)f, 256, smem));
   TCK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
   const int64_t grid = std::min<int64_t>(groups, (int64_t)nsm * std::max(1, occ));
-  f<<<(unsigned)grid, threads, smem, (cudaStream_t)stream>>>(coeffs, ccs, cvs, t->phi, phi_n, t->code, nv, t->nq,
-                                                             cb, c->n_owned, traces);
+  f<<<(unsigned)grid, 256, smem, (cudaStream_t)stream>>>(coeffs, ccs, cvs, t->phi, phi_n, t->code, nv, t->nq, cb,
+                                                         c->n_owned, traces);
   TCK(cudaGetLastError());
 }
 

@@ -171,8 +171,14 @@ Layout make_layout(int d, int M, int V, int G, int max_smem, const std::function
 #ifndef CWR_RB_MAINREG20
 #define CWR_RB_MAINREG20 200  // main-warp registers for ℳ = 20 (0: no setmaxnreg)
 #endif
-CWR_HD constexpr int rb_main(int R, int V) { return (void)V, R > 14 ? CWR_RB_MAIN : 192; }
-CWR_HD constexpr int rb_ew(int R, int V) { return (void)V, R > 14 ? CWR_RB_EW : 5; }
+#ifndef CWR_RB_MAIN10
+#define CWR_RB_MAIN10 192  // ℳ = 10: main threads (T = CWR_RB_MAIN10 / NG cells)
+#endif
+#ifndef CWR_RB_EW10
+#define CWR_RB_EW10 5  // ℳ = 10: epilogue warps
+#endif
+CWR_HD constexpr int rb_main(int R, int V) { return (void)V, R > 14 ? CWR_RB_MAIN : CWR_RB_MAIN10; }
+CWR_HD constexpr int rb_ew(int R, int V) { return (void)V, R > 14 ? CWR_RB_EW : CWR_RB_EW10; }
 CWR_HD constexpr int rb_main_warps(int T, int NG) { return (T * NG + 31) / 32; }
 // the full row-block tile: main threads / row groups, even (T·R·8 a multiple of 16 bytes)
 CWR_HD constexpr int rb_tfull(int R, int V) { return (rb_main(R, V) / rb_ng(R, V)) & ~1; }

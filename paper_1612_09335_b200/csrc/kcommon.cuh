@@ -198,6 +198,13 @@ __device__ __forceinline__ void sector_apply(const double* sinv, const double (&
 }
 
 // ---------------------------------------------------------------- PTX helpers
+// fp64 tensor-core MMA, D = A·B + D with A 8×4 (row), B 4×8 (col): lane L holds
+// A[L/4][L%4], B[L%4][L/4] and D[L/4][2(L%4) + {0, 1}]
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

@@ -231,11 +231,6 @@ __device__ __forceinline__ void mono_moments(double (&mom)[NM], const double (&s
                                              const double (&T3)[D * D * D], std::integer_sequence<int, E...>) {
   ((mom[E] = mono_moment<D, M, E>(sv, S2, T3)), ...);
 }
-__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-               : "+d"(c0), "+d"(c1)
-               : "d"(a), "d"(b));
-}
 
 // One warp per cell (persistent grid):
 //  1. assembly: lane L builds rows k = L, L+32 of X = [A | ΔQ] (A[k][l−1] = average of

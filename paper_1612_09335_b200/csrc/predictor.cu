@@ -59,7 +59,22 @@ __host__ __device__ constexpr int pr_off(int D, int M) {
 }
 static __constant__ double c_pred[pr_off(4, 1)];
 
+#ifndef CWR_PRED_MMA
+#define CWR_PRED_MMA 1  // update phase as one CTA-wide GEMM on the fp64 tensor cores
+#endif
+// Tensor-core form of the update (CWR_PRED_MMA): per CTA and iteration
+//   U[k][n] = Σ_j A'[k][j] Ĝ[j][n],  j = b·𝓛 + l ∈ [0, d·𝓛),  n = cell·V + v ∈ [0, 32·V)
+// with A'[k][b·𝓛 + l] = A_b[k][l] the SAME for every cell: m8n8k4 DMMA tiles, rows k
+// padded to MT·8, j to KS·4 (zero), 4 column tiles per warp (32·V/8 tiles over V warps).
+// A' and C0 are stored per lane in fragment order ([k-step][m-tile][lane]) so a lane's
+// fragment is one coalesced load (L1-resident tables of ≤ 14 KB).
+__host__ __device__ constexpr int pr_mt(int D, int M) { return (pr_L(D, M) - pr_nk(D, M) + 7) / 8; }
+__host__ __device__ constexpr int pr_ks(int D, int M) { return (D * pr_L(D, M) + 3) / 4; }
+__host__ __device__ constexpr int pr_ks0(int D, int M) { return (pr_nk(D, M) + 3) / 4; }
+
 struct PredArgs {
+  const double* fa;    // A' fragments [KS][MT][32]
+  const double* fc;    // C0 fragments [KS0][MT][32]
   const double* w;     // coefficients: (c, v, m) at w[c·ccs + v·cvs + m]
   int64_t ccs, cvs;
   const double* jinv;  // [n_owned][d][d]  ∂ξ_b/∂x_a at [b·d + a]
@@ -112,6 +127,42 @@ __global__ void __launch_bounds__(256) k_predictor(PredArgs p) {
       for (int e = 0; e < NK * V; ++e) s = fmax(s, fabs(Q[it * L * V + e]));
       sc[it] = s;
     }
+#if CWR_PRED_MMA
+    constexpr int MT = pr_mt(D, M), KS = pr_ks(D, M), KS0 = pr_ks0(D, M), DL = D * L;
+    constexpr int NTW = CB / 8;  // column tiles per warp: 32·V columns / 8 / V warps
+    const int lane = tid & 31, warp = tid >> 5;
+    // this lane's B-fragment column n = (nt0 + t)·8 + lane/4 and its element offset
+    int nb[NTW];
+#pragma unroll
+    for (int t = 0; t < NTW; ++t) {
+      const int n = (warp * NTW + t) * 8 + (lane >> 2), cl = n / V;
+      nb[t] = cl * (D * L * V) + (n - cl * V);
+    }
+    // C0 q̂⁰ (fixed over the iterations) in accumulator layout: base = −C0·Q⁰
+    double basef[MT][NTW][2];
+    {
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int t = 0; t < NTW; ++t) basef[mt][t][0] = basef[mt][t][1] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < KS0; ++ks) {
+        const int j = ks * 4 + (lane & 3);
+        double fb[NTW];
+#pragma unroll
+        for (int t = 0; t < NTW; ++t) {  // Q⁰[cell][j][v] = Q[(cell·L + j)·V + v], n-offset as for Ĝ
+          const int n = (warp * NTW + t) * 8 + (lane >> 2), cl = n / V;
+          fb[t] = j < NK ? Q[(cl * L + j) * V + (n - cl * V)] : 0.0;
+        }
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          const double fa = __ldg(p.fc + (ks * MT + mt) * 32 + lane);
+#pragma unroll
+          for (int t = 0; t < NTW; ++t) dmma884(basef[mt][t][0], basef[mt][t][1], fa, fb[t]);
+        }
+      }
+    }
+#else
     // C0 q̂⁰ is fixed: kept in registers by the update threads (≤ 1 item per thread)
     const int ui = tid;
     const bool upd = ui < nc * V;
@@ -126,6 +177,7 @@ __global__ void __launch_bounds__(256) k_predictor(PredArgs p) {
         base[k] = -s;
       }
     }
+#endif
     for (int iter = 0; iter < p.maxit; ++iter) {
       __syncthreads();
       // ---- flux phase: (cell, node) → Ĝ_b = Σ_a Jinv[b][a] F_a(q̂)
@@ -167,6 +219,63 @@ __global__ void __launch_bounds__(256) k_predictor(PredArgs p) {
       }
       __syncthreads();
       // ---- update phase: (cell, variable) → the NU unknown rows
+#if CWR_PRED_MMA
+      {
+        double acc[MT][NTW][2];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+          for (int t = 0; t < NTW; ++t) acc[mt][t][0] = acc[mt][t][1] = 0.0;
+#pragma unroll 3
+        for (int ks = 0; ks < KS; ++ks) {
+          const int j = ks * 4 + (lane & 3);
+          double fb[NTW], fa[MT];
+#pragma unroll
+          for (int t = 0; t < NTW; ++t) fb[t] = j < DL ? G[nb[t] + j * V] : 0.0;
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) fa[mt] = __ldg(p.fa + (ks * MT + mt) * 32 + lane);
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+            for (int t = 0; t < NTW; ++t) dmma884(acc[mt][t][0], acc[mt][t][1], fa[mt], fb[t]);
+        }
+        // q̂¹ = −Δt·U − C0 q̂⁰ on the lane's elements (row k = mt·8 + lane/4, columns
+        // n = tile·8 + 2·(lane%4) + e); frozen cells keep their state
+        double dm[NTW][2];
+#pragma unroll
+        for (int t = 0; t < NTW; ++t) {
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int n = (warp * NTW + t) * 8 + 2 * (lane & 3) + e, cl = n / V, v = n - cl * V;
+            const bool live = cl < nc && !(flag[cl] & 1);
+            double mx = 0.0;
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+              const int k = mt * 8 + (lane >> 2);
+              if (live && k < NU) {
+                double* qk = Q + (cl * L + NK + k) * V + v;
+                const double nv = __fma_rn(-p.dt, acc[mt][t][e], basef[mt][t][e]);
+                mx = fmax(mx, fabs(nv - *qk));
+                *qk = nv;
+              }
+            }
+            dm[t][e] = mx;
+          }
+        }
+        // max over the rows k: lanes with the same lane%4 hold the same columns
+#pragma unroll
+        for (int t = 0; t < NTW; ++t)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            double x = dm[t][e];
+            x = fmax(x, __shfl_xor_sync(0xffffffffu, x, 4));
+            x = fmax(x, __shfl_xor_sync(0xffffffffu, x, 8));
+            x = fmax(x, __shfl_xor_sync(0xffffffffu, x, 16));
+            const int n = (warp * NTW + t) * 8 + 2 * (lane & 3) + e;
+            if ((lane >> 2) == 0 && n < nc * V) dl[n] = x;
+          }
+      }
+#else
       if (upd && !(flag[ucl] & 1)) {
         double acc[NU];
 #pragma unroll
@@ -190,6 +299,7 @@ __global__ void __launch_bounds__(256) k_predictor(PredArgs p) {
         }
         dl[ucl * V + uv] = dmax;
       }
+#endif
       __syncthreads();
       int active = 0;
       for (int cl = tid; cl < nc; cl += nth) {
@@ -242,6 +352,7 @@ static size_t pred_smem(int d, int M) {
 }
 
 struct PredState {
+  double* frag = nullptr;  // A' fragments, then C0 fragments (CWR_PRED_MMA)
   double* jinv = nullptr;
   double gamma = 1.4;
   int L = 0;
@@ -264,6 +375,30 @@ void dev_predictor_setup(cwreco_ctx* c, const PredictorHost& h, const std::vecto
   if (!s) c->pred = s = new PredState();
   cudaFree(s->jinv);
   s->jinv = nullptr;
+  // A'[k][b·L + l] = A_b[k][l] and C0[k][j] in DMMA A-fragment order [ks][mt][lane]:
+  // lane holds row mt·8 + lane/4, column ks·4 + lane%4 (zero outside the matrix)
+  {
+    const int d = c->d, L = h.L, nk = h.nk, nu = L - nk;
+    const int mt = (nu + 7) / 8, ks = (d * L + 3) / 4, ks0 = (nk + 3) / 4;
+    std::vector<double> fr(size_t(ks + ks0) * mt * 32, 0.0);
+    for (int a = 0; a < ks; ++a)
+      for (int m = 0; m < mt; ++m)
+        for (int ln = 0; ln < 32; ++ln) {
+          const int k = m * 8 + ln / 4, j = a * 4 + ln % 4;
+          if (k < nu && j < d * L) fr[(size_t(a) * mt + m) * 32 + ln] = h.A[(size_t(j / L) * nu + k) * L + j % L];
+        }
+    const size_t o0 = size_t(ks) * mt * 32;
+    for (int a = 0; a < ks0; ++a)
+      for (int m = 0; m < mt; ++m)
+        for (int ln = 0; ln < 32; ++ln) {
+          const int k = m * 8 + ln / 4, j = a * 4 + ln % 4;
+          if (k < nu && j < nk) fr[o0 + (size_t(a) * mt + m) * 32 + ln] = h.C0[size_t(k) * nk + j];
+        }
+    cudaFree(s->frag);
+    s->frag = nullptr;
+    PCK(cudaMalloc(&s->frag, fr.size() * sizeof(double)));
+    PCK(cudaMemcpy(s->frag, fr.data(), fr.size() * sizeof(double), cudaMemcpyHostToDevice));
+  }
   PCK(cudaMalloc(&s->jinv, std::max<size_t>(1, jinv.size()) * sizeof(double)));
   if (!jinv.empty()) PCK(cudaMemcpy(s->jinv, jinv.data(), jinv.size() * sizeof(double), cudaMemcpyHostToDevice));
   s->gamma = gamma;
@@ -275,6 +410,7 @@ void dev_predictor_destroy(cwreco_ctx* c) {
   if (!s) return;
   DeviceGuard dg(c->device);
   cudaFree(s->jinv);
+  cudaFree(s->frag);
   delete s;
   c->pred = nullptr;
 }
@@ -285,6 +421,8 @@ void dev_predict(cwreco_ctx* c, const double* w, int64_t ccs, int64_t cvs, doubl
   if (!s) fail(CWRECO_ESTATE, "predict: call cwreco_predictor_setup first");
   DeviceGuard dg(c->device);
   PredArgs a;
+  a.fa = s->frag;
+  a.fc = s->frag + size_t(pr_ks(c->d, c->M)) * pr_mt(c->d, c->M) * 32;
   a.w = w;
   a.ccs = ccs;
   a.cvs = cvs;

@@ -59,8 +59,11 @@ __host__ __device__ constexpr int pr_off(int D, int M) {
 }
 static __constant__ double c_pred[pr_off(4, 1)];
 
+// Update phase as one CTA-wide GEMM on the fp64 tensor cores: -1 = for 3-D M = 3 only
+// (C5 51.3 vs 67.2 ms; the smaller shapes pad NU to 8-row tiles and measured slower:
+// C3 3.10 vs 2.78, C2 3.39 vs 2.31 ms), 0 = never, 1 = always
 #ifndef CWR_PRED_MMA
-#define CWR_PRED_MMA 1  // update phase as one CTA-wide GEMM on the fp64 tensor cores
+#define CWR_PRED_MMA -1
 #endif
 // Tensor-core form of the update (CWR_PRED_MMA): per CTA and iteration
 //   U[k][n] = Σ_j A'[k][j] Ĝ[j][n],  j = b·𝓛 + l ∈ [0, d·𝓛),  n = cell·V + v ∈ [0, 32·V)
@@ -90,6 +93,7 @@ __global__ void __launch_bounds__(256) k_predictor(PredArgs p) {
   constexpr int V = D + 2, L = pr_L(D, M), NK = pr_nk(D, M), NU = L - NK;
   constexpr int CB = 32;  // cells per CTA
   constexpr int OA = pr_off(D, M), OC = OA + D * NU * L, OP = OC + NU * NK;
+  constexpr bool kMma = CWR_PRED_MMA < 0 ? (D == 3 && M == 3) : CWR_PRED_MMA > 0;
   extern __shared__ __align__(16) double psm[];
   double* Q = psm;                                   // [CB][L][V]
   double* G = Q + CB * L * V;                        // [CB][D][L][V]
@@ -127,57 +131,57 @@ __global__ void __launch_bounds__(256) k_predictor(PredArgs p) {
       for (int e = 0; e < NK * V; ++e) s = fmax(s, fabs(Q[it * L * V + e]));
       sc[it] = s;
     }
-#if CWR_PRED_MMA
     constexpr int MT = pr_mt(D, M), KS = pr_ks(D, M), KS0 = pr_ks0(D, M), DL = D * L;
     constexpr int NTW = CB / 8;  // column tiles per warp: 32·V columns / 8 / V warps
     const int lane = tid & 31, warp = tid >> 5;
-    // this lane's B-fragment column n = (nt0 + t)·8 + lane/4 and its element offset
     int nb[NTW];
-#pragma unroll
-    for (int t = 0; t < NTW; ++t) {
-      const int n = (warp * NTW + t) * 8 + (lane >> 2), cl = n / V;
-      nb[t] = cl * (D * L * V) + (n - cl * V);
-    }
-    // C0 q̂⁰ (fixed over the iterations) in accumulator layout: base = −C0·Q⁰
     double basef[MT][NTW][2];
-    {
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-        for (int t = 0; t < NTW; ++t) basef[mt][t][0] = basef[mt][t][1] = 0.0;
-#pragma unroll
-      for (int ks = 0; ks < KS0; ++ks) {
-        const int j = ks * 4 + (lane & 3);
-        double fb[NTW];
-#pragma unroll
-        for (int t = 0; t < NTW; ++t) {  // Q⁰[cell][j][v] = Q[(cell·L + j)·V + v], n-offset as for Ĝ
-          const int n = (warp * NTW + t) * 8 + (lane >> 2), cl = n / V;
-          fb[t] = j < NK ? Q[(cl * L + j) * V + (n - cl * V)] : 0.0;
-        }
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt) {
-          const double fa = __ldg(p.fc + (ks * MT + mt) * 32 + lane);
-#pragma unroll
-          for (int t = 0; t < NTW; ++t) dmma884(basef[mt][t][0], basef[mt][t][1], fa, fb[t]);
-        }
-      }
-    }
-#else
-    // C0 q̂⁰ is fixed: kept in registers by the update threads (≤ 1 item per thread)
+    // scalar form: C0 q̂⁰ is fixed: kept in registers by the update threads (≤ 1 item per thread)
     const int ui = tid;
     const bool upd = ui < nc * V;
     const int ucl = upd ? ui / V : 0, uv = upd ? ui - (ui / V) * V : 0;
     double base[NU];
-    if (upd) {
+    if constexpr (kMma) {
+      // this lane's B-fragment column n = (nt0 + t)·8 + lane/4 and its element offset
 #pragma unroll
-      for (int k = 0; k < NU; ++k) {
-        double s = 0.0;
+      for (int t = 0; t < NTW; ++t) {
+        const int n = (warp * NTW + t) * 8 + (lane >> 2), cl = n / V;
+        nb[t] = cl * (D * L * V) + (n - cl * V);
+      }
+      // C0 q̂⁰ (fixed over the iterations) in accumulator layout (q̂¹ = −Δt·U − basef)
+      {
 #pragma unroll
-        for (int j = 0; j < NK; ++j) s = __fma_rn(c_pred[OC + k * NK + j], Q[(ucl * L + j) * V + uv], s);
-        base[k] = -s;
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+          for (int t = 0; t < NTW; ++t) basef[mt][t][0] = basef[mt][t][1] = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < KS0; ++ks) {
+          const int j = ks * 4 + (lane & 3);
+          double fb[NTW];
+#pragma unroll
+          for (int t = 0; t < NTW; ++t) {  // Q⁰[cell][j][v] = Q[(cell·L + j)·V + v], n-offset as for Ĝ
+            const int n = (warp * NTW + t) * 8 + (lane >> 2), cl = n / V;
+            fb[t] = j < NK ? Q[(cl * L + j) * V + (n - cl * V)] : 0.0;
+          }
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) {
+            const double fa = __ldg(p.fc + (ks * MT + mt) * 32 + lane);
+#pragma unroll
+            for (int t = 0; t < NTW; ++t) dmma884(basef[mt][t][0], basef[mt][t][1], fa, fb[t]);
+          }
+        }
+      }
+    } else {
+      if (upd) {
+#pragma unroll
+        for (int k = 0; k < NU; ++k) {
+          double s = 0.0;
+#pragma unroll
+          for (int j = 0; j < NK; ++j) s = __fma_rn(c_pred[OC + k * NK + j], Q[(ucl * L + j) * V + uv], s);
+          base[k] = -s;
+        }
       }
     }
-#endif
     for (int iter = 0; iter < p.maxit; ++iter) {
       __syncthreads();
       // ---- flux phase: (cell, node) → Ĝ_b = Σ_a Jinv[b][a] F_a(q̂)
@@ -219,87 +223,87 @@ __global__ void __launch_bounds__(256) k_predictor(PredArgs p) {
       }
       __syncthreads();
       // ---- update phase: (cell, variable) → the NU unknown rows
-#if CWR_PRED_MMA
-      {
-        double acc[MT][NTW][2];
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-          for (int t = 0; t < NTW; ++t) acc[mt][t][0] = acc[mt][t][1] = 0.0;
-#pragma unroll 3
-        for (int ks = 0; ks < KS; ++ks) {
-          const int j = ks * 4 + (lane & 3);
-          double fb[NTW], fa[MT];
-#pragma unroll
-          for (int t = 0; t < NTW; ++t) fb[t] = j < DL ? G[nb[t] + j * V] : 0.0;
-#pragma unroll
-          for (int mt = 0; mt < MT; ++mt) fa[mt] = __ldg(p.fa + (ks * MT + mt) * 32 + lane);
+      if constexpr (kMma) {
+        {
+          double acc[MT][NTW][2];
 #pragma unroll
           for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-            for (int t = 0; t < NTW; ++t) dmma884(acc[mt][t][0], acc[mt][t][1], fa[mt], fb[t]);
-        }
-        // q̂¹ = −Δt·U − C0 q̂⁰ on the lane's elements (row k = mt·8 + lane/4, columns
-        // n = tile·8 + 2·(lane%4) + e); frozen cells keep their state
-        double dm[NTW][2];
+            for (int t = 0; t < NTW; ++t) acc[mt][t][0] = acc[mt][t][1] = 0.0;
+#pragma unroll 3
+          for (int ks = 0; ks < KS; ++ks) {
+            const int j = ks * 4 + (lane & 3);
+            double fb[NTW], fa[MT];
 #pragma unroll
-        for (int t = 0; t < NTW; ++t) {
+            for (int t = 0; t < NTW; ++t) fb[t] = j < DL ? G[nb[t] + j * V] : 0.0;
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int n = (warp * NTW + t) * 8 + 2 * (lane & 3) + e, cl = n / V, v = n - cl * V;
-            const bool live = cl < nc && !(flag[cl] & 1);
-            double mx = 0.0;
+            for (int mt = 0; mt < MT; ++mt) fa[mt] = __ldg(p.fa + (ks * MT + mt) * 32 + lane);
 #pragma unroll
-            for (int mt = 0; mt < MT; ++mt) {
-              const int k = mt * 8 + (lane >> 2);
-              if (live && k < NU) {
-                double* qk = Q + (cl * L + NK + k) * V + v;
-                const double nv = __fma_rn(-p.dt, acc[mt][t][e], basef[mt][t][e]);
-                mx = fmax(mx, fabs(nv - *qk));
-                *qk = nv;
+            for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+              for (int t = 0; t < NTW; ++t) dmma884(acc[mt][t][0], acc[mt][t][1], fa[mt], fb[t]);
+          }
+          // q̂¹ = −Δt·U − C0 q̂⁰ on the lane's elements (row k = mt·8 + lane/4, columns
+          // n = tile·8 + 2·(lane%4) + e); frozen cells keep their state
+          double dm[NTW][2];
+#pragma unroll
+          for (int t = 0; t < NTW; ++t) {
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int n = (warp * NTW + t) * 8 + 2 * (lane & 3) + e, cl = n / V, v = n - cl * V;
+              const bool live = cl < nc && !(flag[cl] & 1);
+              double mx = 0.0;
+#pragma unroll
+              for (int mt = 0; mt < MT; ++mt) {
+                const int k = mt * 8 + (lane >> 2);
+                if (live && k < NU) {
+                  double* qk = Q + (cl * L + NK + k) * V + v;
+                  const double nv = __fma_rn(-p.dt, acc[mt][t][e], -basef[mt][t][e]);
+                  mx = fmax(mx, fabs(nv - *qk));
+                  *qk = nv;
+                }
               }
+              dm[t][e] = mx;
             }
-            dm[t][e] = mx;
           }
+          // max over the rows k: lanes with the same lane%4 hold the same columns
+#pragma unroll
+          for (int t = 0; t < NTW; ++t)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              double x = dm[t][e];
+              x = fmax(x, __shfl_xor_sync(0xffffffffu, x, 4));
+              x = fmax(x, __shfl_xor_sync(0xffffffffu, x, 8));
+              x = fmax(x, __shfl_xor_sync(0xffffffffu, x, 16));
+              const int n = (warp * NTW + t) * 8 + 2 * (lane & 3) + e;
+              if ((lane >> 2) == 0 && n < nc * V) dl[n] = x;
+            }
         }
-        // max over the rows k: lanes with the same lane%4 hold the same columns
+      } else {
+        if (upd && !(flag[ucl] & 1)) {
+          double acc[NU];
 #pragma unroll
-        for (int t = 0; t < NTW; ++t)
+          for (int k = 0; k < NU; ++k) acc[k] = 0.0;
+          const double* Gc = G + (ucl * D * L) * V + uv;
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            double x = dm[t][e];
-            x = fmax(x, __shfl_xor_sync(0xffffffffu, x, 4));
-            x = fmax(x, __shfl_xor_sync(0xffffffffu, x, 8));
-            x = fmax(x, __shfl_xor_sync(0xffffffffu, x, 16));
-            const int n = (warp * NTW + t) * 8 + 2 * (lane & 3) + e;
-            if ((lane >> 2) == 0 && n < nc * V) dl[n] = x;
+          for (int b = 0; b < D; ++b)
+#pragma unroll
+            for (int l = 0; l < L; ++l) {
+              const double g = Gc[(b * L + l) * V];
+#pragma unroll
+              for (int k = 0; k < NU; ++k) acc[k] = __fma_rn(c_pred[OA + (b * NU + k) * L + l], g, acc[k]);
+            }
+          double dmax = 0.0;
+          double* qu = Q + (ucl * L + NK) * V + uv;
+#pragma unroll
+          for (int k = 0; k < NU; ++k) {
+            const double nv = __fma_rn(-p.dt, acc[k], base[k]);
+            dmax = fmax(dmax, fabs(nv - qu[k * V]));
+            qu[k * V] = nv;
           }
-      }
-#else
-      if (upd && !(flag[ucl] & 1)) {
-        double acc[NU];
-#pragma unroll
-        for (int k = 0; k < NU; ++k) acc[k] = 0.0;
-        const double* Gc = G + (ucl * D * L) * V + uv;
-#pragma unroll
-        for (int b = 0; b < D; ++b)
-#pragma unroll
-          for (int l = 0; l < L; ++l) {
-            const double g = Gc[(b * L + l) * V];
-#pragma unroll
-            for (int k = 0; k < NU; ++k) acc[k] = __fma_rn(c_pred[OA + (b * NU + k) * L + l], g, acc[k]);
-          }
-        double dmax = 0.0;
-        double* qu = Q + (ucl * L + NK) * V + uv;
-#pragma unroll
-        for (int k = 0; k < NU; ++k) {
-          const double nv = __fma_rn(-p.dt, acc[k], base[k]);
-          dmax = fmax(dmax, fabs(nv - qu[k * V]));
-          qu[k * V] = nv;
+          dl[ucl * V + uv] = dmax;
         }
-        dl[ucl * V + uv] = dmax;
       }
-#endif
       __syncthreads();
       int active = 0;
       for (int cl = tid; cl < nc; cl += nth) {

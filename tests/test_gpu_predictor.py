@@ -62,6 +62,10 @@ def test_predictor_parity(d, n, M):
     # deterministic, and dt = 0 gives w at every node (constant in τ)
     q2 = ctx.predict(w, dt).cpu().numpy()
     assert np.array_equal(q, q2)
+    # two CTAs walk every 32-cell group in turn (state carried across groups): same result
+    ctx.set_option(P.OPT_MAX_CTAS, 2)
+    assert np.array_equal(ctx.predict(w, dt).cpu().numpy(), q)
+    ctx.set_option(P.OPT_MAX_CTAS, 0)
     # Δt = 0: H drops out and q_h(ξ, τ) = w(ξ) — q̂_l = w at the node's spatial point
     q0 = ctx.predict(w, 0.0).cpu().numpy()
     want = np.einsum("lm,cvm->clv", S["Phi"], wc)

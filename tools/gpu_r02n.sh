@@ -4,6 +4,7 @@
 set -u
 mkdir -p gpurun_out
 bash tools/gpu_round.sh tests
+timeout 600 python -c "import __graft_entry__ as g; g.smoke(); print(\"smoke ok\")" > gpurun_out/smoke.log 2>&1; echo "smoke exit $?"; tail -2 gpurun_out/smoke.log
 bash tools/gpu_round.sh benchall
 timeout 900 python bench.py --config C5 --kernel matrixfree --steps 10 --warmup 3 --no-cpu-baseline \
     > gpurun_out/bench_mf_C5.json 2> gpurun_out/bench_mf_C5.err; echo "mf C5 $?"; cut -c1-300 gpurun_out/bench_mf_C5.json

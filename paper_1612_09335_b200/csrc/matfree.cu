@@ -40,6 +40,15 @@ namespace cwr {
 #ifndef CWR_MF_V2
 #define CWR_MF_V2 1  // unrolled basis transform, rsqrt pivots, column back substitution
 #endif
+#ifndef CWR_MF_TC
+#define CWR_MF_TC 1  // basis transform A = mom·Cᵀ on the fp64 tensor cores (else scalar FMAs)
+#endif
+#ifndef CWR_MF_CHOL_SMEM
+#define CWR_MF_CHOL_SMEM 1  // Cholesky rows broadcast through shared memory (else shuffles)
+#endif
+#ifndef CWR_MF_FAST_RSQ
+#define CWR_MF_FAST_RSQ 1  // rsqrt.approx + two Newton steps (else the library rsqrt)
+#endif
 #ifndef CWR_MF_UNROLL
 #define CWR_MF_UNROLL 0  // basis transform fully unrolled (register pressure: spills at 4 CTAs/SM)
 #endif
@@ -114,8 +123,10 @@ template <int D>
 __device__ __forceinline__ void shift_vec(uint8_t code, const double (&L)[3], double (&s)[D]) {
 #pragma unroll
   for (int a = 0; a < D; ++a) {
+    // branch-free: code 1 → +L, 2 → −L, 0 → 0 (mask the bits of L, flip its sign bit)
     const int c = (code >> (2 * a)) & 3;
-    s[a] = c == 1 ? L[a] : c == 2 ? -L[a] : 0.0;
+    const long long keep = (c == 1 || c == 2) ? -1LL : 0LL, sign = (long long)(c == 2) << 63;
+    s[a] = __longlong_as_double((__double_as_longlong(L[a]) & keep) ^ sign);
   }
 }
 
@@ -162,26 +173,73 @@ __host__ __device__ constexpr int mf_xs(int ncp) {
   return s;
 }
 
-// Per-warp shared scratch (doubles): X = [A | ΔQ] with KP rows of stride XS (the
+// Row stride of G / U: even (16-byte aligned rows: the Cholesky reads row pairs with
+// one 128-bit broadcast load) in the shared-memory Cholesky, else NCP + 1.
+__host__ __device__ constexpr int mf_gs(int ncp) { return CWR_MF_CHOL_SMEM ? ncp + 2 : ncp + 1; }
+// monomials of degree ≤ deg(ψ_l) (the basis transform's sum length for mode l)
+__host__ __device__ constexpr int mf_hi_of_mode(int D, int l) {
+  int n = 0;
+  while (nmodes(n, D) <= l) ++n;
+  return nmodes(n, D);
+}
+// k-steps (4 monomials each) the transform's 8-column tile nt needs: its columns are
+// modes 8nt+1 .. min(8nt+8, R), of degree ≤ that of the last one
+__host__ __device__ constexpr int mf_nk_tile(int D, int M, int nt) {
+  const int R = nmodes(M, D) - 1, l = 8 * nt + 8 < R ? 8 * nt + 8 : R;
+  return (mf_hi_of_mode(D, l) + 3) / 4;
+}
+
+// Per-warp shared scratch (doubles): X = [A | ΔQ] with KR rows of stride XS (the
 // Gram matrix and then the Cholesky factor reuse its first rows), then the sector
-// products [NV][D][V].
+// products [NV][D][V]; per CTA after the warps' scratch: the transform's B fragments.
 template <int D, int M, int V>
 struct MfShape {
   static constexpr int NM = nmodes(M, D), R = NM - 1, NV = D + 1, K = D * NM - 1;
-  static constexpr int KP = (K + 3) & ~3;            // rows padded to whole k-steps of 4
+  static constexpr int KP = (K + 3) & ~3;            // rows padded to whole k-steps of 4 (Gram)
+  static constexpr int KR = (K + 7) & ~7;            // rows padded to whole 8-row tiles (transform)
   static constexpr int NC = R + V;                   // columns of [A | ΔQ]
   static constexpr int NCP = (NC + 7) & ~7;          // padded to whole 8-column blocks
   static constexpr int NB = NCP / 8;                 // column blocks (DMMA tiles per side)
-  static constexpr int GS = NCP + 1;                 // row stride of G and U in the scratch
+  static constexpr int NK = (NM + 3) / 4;            // transform k-steps (monomials)
+  static constexpr int NT = (R + 7) / 8;             // transform column tiles
+  static constexpr int GS = mf_gs(NCP);              // row stride of G and U in the scratch
   static constexpr int XS = mf_xs(NCP);              // row stride of X (see mf_xs)
-  static constexpr int X_DBL = KP * XS > NCP * GS ? KP * XS : NCP * GS;  // X, then G / U
+  static constexpr int XR = CWR_MF_TC ? KR : KP;     // rows of X held
+  static constexpr int G_DBL = (CWR_MF_CHOL_SMEM ? 2 : 1) * NCP * GS;   // G / U (+ Uᵀ)
+  static constexpr int X_DBL = XR * XS > G_DBL ? XR * XS : G_DBL;         // X, then G / U
   static constexpr int PS_DBL = NV * D * V;
-  static constexpr int SCR = X_DBL + PS_DBL;
+  static constexpr int SCR = (X_DBL + PS_DBL + 1) & ~1;  // even: every warp's X 16-byte aligned
+  static constexpr int BF_DBL = CWR_MF_TC ? NT * NK * 32 : 0;
   static_assert(NC <= 32, "one lane per column of [G | AᵀΔQ]");
+  static_assert(4 * NK <= NCP, "the monomial moments fit in a row of X");
 };
 __host__ __device__ constexpr int mf_scr_doubles(int D, int M, int V) {
-  const int kp = (D * nmodes(M, D) - 1 + 3) & ~3, ncp = (nmodes(M, D) - 1 + V + 7) & ~7, xs = mf_xs(ncp);
-  return (kp * xs > ncp * (ncp + 1) ? kp * xs : ncp * (ncp + 1)) + (D + 1) * D * V;
+  const int k = D * nmodes(M, D) - 1, kp = (k + 3) & ~3, kr = (k + 7) & ~7, xr = CWR_MF_TC ? kr : kp;
+  const int ncp = (nmodes(M, D) - 1 + V + 7) & ~7, xs = mf_xs(ncp), gs = mf_gs(ncp);
+  const int g = (CWR_MF_CHOL_SMEM ? 2 : 1) * ncp * gs;
+  return ((xr * xs > g ? xr * xs : g) + (D + 1) * D * V + 1) & ~1;
+}
+__host__ __device__ constexpr int mf_bf_doubles(int D, int M) {
+  return CWR_MF_TC ? ((nmodes(M, D) - 1 + 7) / 8) * ((nmodes(M, D) + 3) / 4) * 32 : 0;
+}
+
+// 1/√x: the SFU approximation refined by two Newton steps (relative error at the
+// rounding level; NaN for x ≤ 0 as the library's rsqrt, so a rank-deficient stencil
+// still yields NaN, not a silent result)
+__device__ __forceinline__ double mf_rsqrt(double x) {
+#if CWR_MF_FAST_RSQ
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+#pragma unroll
+  for (int it = 0; it < 2; ++it) {
+    const double h = x * y;
+    const double r = fma(-h, y, 1.0);
+    y = fma(0.5 * y, r, y);
+  }
+  return y;
+#else
+  return rsqrt(x);
+#endif
 }
 
 // Moments of the monomials of degree ≤ 3 over a simplex with vertices y_0..y_D, in
@@ -248,9 +306,8 @@ __device__ __forceinline__ void mono_moments(double (&mom)[NM], const double (&s
 template <int D, int M, int V>
 __global__ void __launch_bounds__(128, mf_minb(D, M, V)) k_matfree(MfArgs m, KArgs a) {
   using S = MfShape<D, M, V>;
-  constexpr int NM = S::NM, R = S::R, NV = S::NV, K = S::K, KP = S::KP, NC = S::NC, NCP = S::NCP, NB = S::NB,
-                XS = S::XS,
-                GS = S::GS;
+  constexpr int NM = S::NM, R = S::R, NV = S::NV, K = S::K, KP = S::KP, KR = S::KR, NC = S::NC, NCP = S::NCP,
+                NB = S::NB, XS = S::XS, GS = S::GS;
   constexpr int KPL = (K + 31) / 32;  // rows of X per lane
 
   const int lane = threadIdx.x & 31;
@@ -258,6 +315,17 @@ __global__ void __launch_bounds__(128, mf_minb(D, M, V)) k_matfree(MfArgs m, KAr
   extern __shared__ __align__(16) double mf_smem[];
   double* X = mf_smem + (threadIdx.x >> 5) * S::SCR;  // [KP][XS], later G / U [NCP][GS]
   double* PSs = X + S::X_DBL;                          // [NV][D][V] sector products
+#if CWR_MF_TC
+  // B fragments of the basis transform, Cᵀ[k][n] = C[n+1][k] (lane L holds k = 4ks + L%4,
+  // n = 8nt + L/4), in fragment order after the warps' scratch: one conflict-free load each
+  double* Bs = mf_smem + (blockDim.x >> 5) * S::SCR;
+  for (int t = threadIdx.x; t < S::BF_DBL; t += blockDim.x) {
+    const int ln = t & 31, ks = (t >> 5) % S::NK, nt = (t >> 5) / S::NK;
+    const int kk = 4 * ks + (ln & 3), n = 8 * nt + (ln >> 2);
+    Bs[t] = (n < R && kk < NM) ? mcoef[(n + 1) * NM + kk] : 0.0;
+  }
+  __syncthreads();
+#endif
   const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
   // stencil ids and image codes of this lane's rows, loaded one cell ahead (the vertex
@@ -307,7 +375,7 @@ __global__ void __launch_bounds__(128, mf_minb(D, M, V)) k_matfree(MfArgs m, KAr
 #endif
     for (int r = 0; r < KPL; ++r) {
       const int k = lane + 32 * r;
-      if (k >= KP) continue;
+      if (k >= S::XR) continue;
       double* xr = X + k * XS;
       if (k >= K) {  // zero rows up to a whole k-step
 #pragma unroll
@@ -362,19 +430,23 @@ __global__ void __launch_bounds__(128, mf_minb(D, M, V)) k_matfree(MfArgs m, KAr
           for (int f = e; f < D; ++f) {
             const double pef = y[e] * y[f];
             S2[e][f] = v2 == 0 ? pef : S2[e][f] + pef;
-#pragma unroll
             if constexpr (M >= 3) {
 #pragma unroll
-              for (int g2 = f; g2 < D; ++g2) {
-                double& t3 = T3[(e * D + f) * D + g2];
-                t3 = v2 == 0 ? pef * y[g2] : fma(pef, y[g2], t3);
-              }
+              for (int g2 = f; g2 < D; ++g2)
+                T3[(e * D + f) * D + g2] = v2 == 0 ? pef * y[g2] : fma(pef, y[g2], T3[(e * D + f) * D + g2]);
             }
           }
         }
       }
       double mom[NM];
       mono_moments<D, M, NM>(mom, sv, S2, T3, std::make_integer_sequence<int, NM>{});
+#if CWR_MF_TC
+      // the row's monomial moments (zero-padded to whole k-steps); the transform to
+      // the basis runs on the tensor cores below
+#pragma unroll
+      for (int e = 0; e < 4 * S::NK; ++e) xr[e] = e < NM ? mom[e] : 0.0;
+    }
+#else
       // A[k][l−1] = Σ_e C[l][e]·mom[e] over the monomials of degree ≤ deg(ψ_l): rows in
       // blocks of one degree n (compile-time bounds), each block's row loop rolled
 #pragma unroll
@@ -406,6 +478,56 @@ __global__ void __launch_bounds__(128, mf_minb(D, M, V)) k_matfree(MfArgs m, KAr
 #pragma unroll
       for (int l = NC; l < NCP; ++l) xr[l] = 0.0;
     }
+#endif
+#if CWR_MF_TC
+    // ---- 1b. A = mom·Cᵀ on the fp64 tensor cores, one 8-row tile at a time, in place:
+    // A[k][l−1] = Σ_e C[l][e]·mom[k][e] (mode l uses the monomials of degree ≤ deg ψ_l,
+    // so column tile nt stops after mf_nk_tile k-steps)
+    {
+      double dq[KPL][V];
+#pragma unroll
+      for (int r = 0; r < KPL; ++r)
+#pragma unroll
+        for (int v = 0; v < V; ++v) dq[r][v] = lane + 32 * r < K ? a.Q[int64_t(jc[r]) * a.acs + v * a.avs] - qi[v] : 0.0;
+      __syncwarp();
+#pragma unroll 1
+      for (int t = 0; t < KR / 8; ++t) {
+        double* xt = X + (8 * t + (lane >> 2)) * XS;
+        double af[S::NK];
+#pragma unroll
+        for (int ks = 0; ks < S::NK; ++ks) af[ks] = xt[4 * ks + (lane & 3)];
+        double dd[S::NT][2];
+#pragma unroll
+        for (int nt = 0; nt < S::NT; ++nt) {
+          dd[nt][0] = dd[nt][1] = 0.0;
+#pragma unroll
+          for (int ks = 0; ks < mf_nk_tile(D, M, nt); ++ks)
+            dmma884(dd[nt][0], dd[nt][1], af[ks], Bs[(nt * S::NK + ks) * 32 + lane]);
+        }
+        __syncwarp();  // every lane's fragments of this tile are read before it is overwritten
+#pragma unroll
+        for (int nt = 0; nt < S::NT; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int col = 8 * nt + 2 * (lane & 3) + e;
+            if (col < R) xt[col] = dd[nt][e];
+          }
+      }
+      __syncwarp();
+      // ΔQ columns and their zero padding (rows ≥ K are zero already)
+#pragma unroll
+      for (int r = 0; r < KPL; ++r) {
+        const int k = lane + 32 * r;
+        if (k < K) {
+          double* xr = X + k * XS;
+#pragma unroll
+          for (int v = 0; v < V; ++v) xr[R + v] = dq[r][v];
+#pragma unroll
+          for (int l = NC; l < NCP; ++l) xr[l] = 0.0;
+        }
+      }
+    }
+#endif
 
     // ---- 4a. sectors: lane s < d+1 solves sector s for all variables
     bool vs = false;
@@ -477,6 +599,8 @@ __global__ void __launch_bounds__(128, mf_minb(D, M, V)) k_matfree(MfArgs m, KAr
     }
     __syncwarp();  // X is dead: G takes its place
     double* G = X;  // [NCP][GS]: G[r][c] for r < R (both triangles of AᵀA), c < NC
+    double* GT = X + NCP * GS;  // [NCP][GS]: Uᵀ (CWR_MF_CHOL_SMEM)
+    (void)GT;
     {
       const int gr = lane >> 2, gcol = 2 * (lane & 3);
 #pragma unroll
@@ -498,11 +622,41 @@ __global__ void __launch_bounds__(128, mf_minb(D, M, V)) k_matfree(MfArgs m, KAr
     double g[R];
 #pragma unroll
     for (int j = 0; j < R; ++j) g[j] = lane < NC ? G[j * GS + lane] : 0.0;
+#if CWR_MF_CHOL_SMEM
+    // row c of U goes straight to its final place in G (the g registers were loaded
+    // before), and the update reads it back as 128-bit broadcast loads of row pairs
+    __syncwarp();
+#pragma unroll
+    for (int c = 0; c < R; ++c) {
+      const double dcc = __shfl_sync(0xffffffffu, g[c], c);
+      const double inv = mf_rsqrt(dcc);  // NaN for a rank-deficient stencil (no silent result)
+      const double u = g[c] * inv;
+      g[c] = u;
+      if (lane < NC) G[c * GS + lane] = u;    // U[c][k] (k ≥ c), y[c] for k ≥ R
+      if (lane < R) GT[lane * GS + c] = u;    // Uᵀ: column k of U as a row (back substitution)
+      if (lane == c) G[c * GS + NCP] = inv;  // 1/U[c][c] in the padding column
+      __syncwarp();
+      const double* uc = G + c * GS;
+      int j = c + 1;
+      if (j & 1) {
+        if (j < R) g[j] = fma(-uc[j], u, g[j]);
+        ++j;
+      }
+#pragma unroll
+      for (; j + 1 < R; j += 2) {
+        const double2 p = *reinterpret_cast<const double2*>(uc + j);
+        g[j] = fma(-p.x, u, g[j]);
+        g[j + 1] = fma(-p.y, u, g[j + 1]);
+      }
+      if (j < R) g[j] = fma(-uc[j], u, g[j]);
+    }
+    __syncwarp();
+#else
 #pragma unroll
     for (int c = 0; c < R; ++c) {
       const double dcc = __shfl_sync(0xffffffffu, g[c], c);
 #if CWR_MF_V2
-      const double inv = rsqrt(dcc);  // one op on the serial chain; NaN for a rank-deficient stencil
+      const double inv = mf_rsqrt(dcc);  // one op on the serial chain; NaN for a rank-deficient stencil
 #else
       const double inv = 1.0 / sqrt(dcc);  // NaN for a rank-deficient stencil (no silent result)
 #endif
@@ -518,6 +672,7 @@ __global__ void __launch_bounds__(128, mf_minb(D, M, V)) k_matfree(MfArgs m, KAr
       for (int c = 0; c < R; ++c) G[c * GS + lane] = g[c];  // U[c][k] (k ≥ c), y[c] for k ≥ R
     }
     __syncwarp();
+#endif
 
     // ---- per variable (lane v): back substitution U p = y, gather, fused epilogue
     double acc[R], ps[NV][D];
@@ -534,8 +689,21 @@ __global__ void __launch_bounds__(128, mf_minb(D, M, V)) k_matfree(MfArgs m, KAr
 #pragma unroll
       for (int c = R - 1; c >= 0; --c) {
         acc[c] = t[c] * G[c * GS + NCP];
+#if CWR_MF_CHOL_SMEM
+        // U[j][c], j < c, is row c of Uᵀ: 128-bit broadcast loads of pairs
+        const double* ut = GT + c * GS;
+        int j = 0;
+#pragma unroll
+        for (; j + 1 < c; j += 2) {
+          const double2 p = *reinterpret_cast<const double2*>(ut + j);
+          t[j] = fma(-p.x, acc[c], t[j]);
+          t[j + 1] = fma(-p.y, acc[c], t[j + 1]);
+        }
+        if (j < c) t[j] = fma(-ut[j], acc[c], t[j]);
+#else
 #pragma unroll
         for (int j = 0; j < c; ++j) t[j] = fma(-G[j * GS + c], acc[c], t[j]);
+#endif
       }
 #else
 #pragma unroll
@@ -716,7 +884,8 @@ void dev_matfree_reconstruct(cwreco_ctx* c, const double* avgs, int64_t acs, int
   MCK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
   MfFn f = mf_fn(c->d, c->M, c->V);
   constexpr int kWarps = 4;  // warps (cells in flight) per CTA
-  const size_t smem = size_t(kWarps) * mf_scr_doubles(c->d, c->M, c->V) * sizeof(double);
+  const size_t smem =
+      (size_t(kWarps) * mf_scr_doubles(c->d, c->M, c->V) + mf_bf_doubles(c->d, c->M)) * sizeof(double);
   MCK(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 1;
   MCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)f, 32 * kWarps, smem));

@@ -19,8 +19,11 @@
 #include <string>
 #include <vector>
 
-#include "devguard.cuh"
-#include "internal.hpp"
+#include "kcommon.cuh"
+
+#ifndef CWR_TR_V2
+#define CWR_TR_V2 1  // staged-block kernel k_traces2 (else the register-tile kernel k_traces)
+#endif
 
 namespace cwr {
 
@@ -136,6 +139,190 @@ static TrFn tr_fn(int nm, int V, int qb) {
   return f;
 }
 
+// ---- k_traces2: a block of cb consecutive cells per step (persistent grid), the cells'
+// coefficients double-buffered in shared memory (one TMA bulk copy per step, the next
+// step's issued before this step's arithmetic), the basis table transposed to
+// Φ[code][l][q] so a thread's P consecutive points are 128-bit loads, every coefficient
+// pair a 128-bit broadcast load; a thread computes a P × V tile (points × variables)
+// of one face, the tiles land in shared memory in output order and the block's
+// contiguous output leaves in one bulk store that drains during the next step.
+template <int D, int M, int V>
+struct TrShape {
+  static constexpr int NM = nmodes(M, D), NF = D + 1, NQ = D == 2 ? M + 1 : (M + 1) * (M + 1);
+  static constexpr int P = NQ % 4 == 0 ? 4 : NQ % 3 == 0 ? 3 : NQ % 2 == 0 ? 2 : 1;  // points per thread
+  static constexpr int UN = NF * NQ / P;        // threads per cell
+  static constexpr int NMP = (NM + 1) & ~1;     // staged coefficient row (even: pair loads)
+  static constexpr int WC = V * NMP;            // staged doubles per cell
+  static constexpr int OUTC = NF * NQ * V;      // output doubles per cell
+};
+
+template <int D, int M, int V>
+__global__ void __launch_bounds__(512) k_traces2(const double* __restrict__ w, int64_t ccs, int64_t cvs,
+                                                 const double* __restrict__ phi, int ncc,
+                                                 const uint8_t* __restrict__ code, int cb, int64_t n_owned,
+                                                 double* __restrict__ out, int bulk_in, int bulk_out) {
+  using S = TrShape<D, M, V>;
+  constexpr int NM = S::NM, NF = S::NF, NQ = S::NQ, P = S::P, NMP = S::NMP, WC = S::WC, OUTC = S::OUTC;
+  extern __shared__ __align__(16) double tr2_smem[];
+  __shared__ __align__(8) uint64_t bar[2];
+  const int tid = threadIdx.x, bd = blockDim.x;
+  const int phn = (ncc * NM * NQ + 1) & ~1;
+  double* ph = tr2_smem;             // [ncc][NM][NQ]
+  double* wb0 = ph + phn;            // 2 × [cb][V][NMP]
+  double* ob = wb0 + 2 * cb * WC;    // [cb][NF][NQ][V]
+  for (int k = tid; k < ncc * NQ * NM; k += bd) {  // global table is [code][q][l]
+    const int cc = k / (NQ * NM), r = k - cc * (NQ * NM), q = r / NM, l = r - q * NM;
+    ph[(cc * NM + l) * NQ + q] = phi[k];
+  }
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const int64_t ngroups = (n_owned + cb - 1) / cb;
+  auto issue = [&](int64_t grp, int buf) {
+    const int64_t c0 = grp * cb;
+    const int ncell = (int)min((int64_t)cb, n_owned - c0);
+    double* wb = wb0 + buf * cb * WC;
+    if (bulk_in) {
+      if (tid == 0) {
+        const uint32_t bytes = uint32_t(ncell) * WC * 8;
+        mbar_expect_tx(&bar[buf], bytes);
+        bulk_g2s(wb, w + c0 * ccs, bytes, &bar[buf]);
+      }
+    } else {
+      for (int k = tid; k < ncell * V * NM; k += bd) {
+        const int cl = k / (V * NM), r = k - cl * (V * NM), v = r / NM, l = r - v * NM;
+        cp_async8(wb + cl * WC + v * NMP + l, w + (c0 + cl) * ccs + v * cvs + l);
+      }
+      cp_async_commit();
+    }
+  };
+  int j = 0;
+  if ((int64_t)blockIdx.x < ngroups) issue(blockIdx.x, 0);
+  for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x, ++j) {
+    const int buf = j & 1;
+    const bool more = grp + gridDim.x < ngroups;
+    if (more) issue(grp + gridDim.x, buf ^ 1);  // buffer buf^1 was released by the last step's barrier
+    if (bulk_in) {
+      mbar_wait(&bar[buf], (j >> 1) & 1);
+    } else {
+      if (more) cp_async_wait<1>();
+      else cp_async_wait<0>();
+      __syncthreads();
+    }
+    const int64_t c0 = grp * cb;
+    const int ncell = (int)min((int64_t)cb, n_owned - c0);
+    const double* wb = wb0 + buf * cb * WC;
+    double acc[P][V];
+    const int u = tid;
+    const bool act = u < ncell * S::UN;
+    int cl = 0, f = 0, q0 = 0;
+    if (act) {
+      cl = u / S::UN;
+      const int fu = u - cl * S::UN;
+      f = fu / (NQ / P);
+      q0 = (fu - f * (NQ / P)) * P;
+      const double* pp = ph + int(code[(c0 + cl) * NF + f]) * NM * NQ + q0;
+      const double* wc = wb + cl * WC;
+#pragma unroll
+      for (int p2 = 0; p2 < P; ++p2)
+#pragma unroll
+        for (int v = 0; v < V; ++v) acc[p2][v] = 0.0;
+#pragma unroll
+      for (int l = 0; l < NM; l += 2) {
+        const bool two = l + 1 < NM;
+        double w0[V], w1[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          const double2 t = *reinterpret_cast<const double2*>(wc + v * NMP + l);
+          w0[v] = t.x;
+          w1[v] = t.y;
+        }
+        double f0[P], f1[P];
+        if constexpr (P % 2 == 0) {
+#pragma unroll
+          for (int p2 = 0; p2 < P; p2 += 2) {
+            const double2 a0 = *reinterpret_cast<const double2*>(pp + l * NQ + p2);
+            f0[p2] = a0.x;
+            f0[p2 + 1] = a0.y;
+            if (two) {
+              const double2 a1 = *reinterpret_cast<const double2*>(pp + (l + 1) * NQ + p2);
+              f1[p2] = a1.x;
+              f1[p2 + 1] = a1.y;
+            }
+          }
+        } else {
+#pragma unroll
+          for (int p2 = 0; p2 < P; ++p2) {
+            f0[p2] = pp[l * NQ + p2];
+            if (two) f1[p2] = pp[(l + 1) * NQ + p2];
+          }
+        }
+#pragma unroll
+        for (int p2 = 0; p2 < P; ++p2)
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            acc[p2][v] = __fma_rn(w0[v], f0[p2], acc[p2][v]);
+            if (two) acc[p2][v] = __fma_rn(w1[v], f1[p2], acc[p2][v]);
+          }
+      }
+    }
+    if (bulk_out && tid == 0) bulk_wait_read();  // the last step's output has left ob
+    __syncthreads();
+    if (act) {
+      double* o = ob + ((cl * NF + f) * NQ + q0) * V;  // the tile's P·V outputs are contiguous
+      if constexpr ((P * V) % 2 == 0 && (NQ * V) % 2 == 0) {
+#pragma unroll
+        for (int k = 0; k < P * V; k += 2)
+          *reinterpret_cast<double2*>(o + k) = make_double2(acc[k / V][k % V], acc[(k + 1) / V][(k + 1) % V]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < P * V; ++k) o[k] = acc[k / V][k % V];
+      }
+    }
+    if (bulk_out) fence_proxy_async();  // generic-proxy writes of ob before the bulk store reads them
+    __syncthreads();
+    if (bulk_out) {
+      if (tid == 0) bulk_s2g(out + c0 * OUTC, ob, uint32_t(ncell) * OUTC * 8);
+    } else {
+      double* dst = out + c0 * OUTC;
+      for (int k = tid; k < ncell * OUTC; k += bd) dst[k] = ob[k];
+    }
+  }
+  if (bulk_out && tid == 0) bulk_wait_all();
+}
+
+using Tr2Fn = void (*)(const double*, int64_t, int64_t, const double*, int, const uint8_t*, int, int64_t, double*,
+                       int, int);
+template <int D, int M>
+static Tr2Fn tr2_fn_v(int V) {
+  switch (V) {
+    case 1: return k_traces2<D, M, 1>;
+    case 2: return k_traces2<D, M, 2>;
+    case 3: return k_traces2<D, M, 3>;
+    case 4: return k_traces2<D, M, 4>;
+    case 5: return k_traces2<D, M, 5>;
+    case 6: return k_traces2<D, M, 6>;
+    case 7: return k_traces2<D, M, 7>;
+    case 8: return k_traces2<D, M, 8>;
+    case 9: return k_traces2<D, M, 9>;
+    default: return nullptr;
+  }
+}
+static Tr2Fn tr2_fn(int d, int M, int V) {
+  Tr2Fn f = nullptr;
+  if (d == 2 && M == 1) f = tr2_fn_v<2, 1>(V);
+  if (d == 2 && M == 2) f = tr2_fn_v<2, 2>(V);
+  if (d == 2 && M == 3) f = tr2_fn_v<2, 3>(V);
+  if (d == 3 && M == 1) f = tr2_fn_v<3, 1>(V);
+  if (d == 3 && M == 2) f = tr2_fn_v<3, 2>(V);
+  if (d == 3 && M == 3) f = tr2_fn_v<3, 3>(V);
+  if (!f) fail(CWRECO_EUNSUPPORTED, "face traces: (d, M, nvars) not instantiated (M ≤ 3, nvars ≤ 9)");
+  return f;
+}
+
 void dev_traces_destroy(cwreco_ctx* c) {
   TraceState* t = (TraceState*)c->tr;
   if (!t) return;
@@ -219,6 +406,38 @@ void dev_face_traces(cwreco_ctx* c, const double* coeffs, int64_t ccs, int64_t c
   if (!c->tr) traces_prepare(c);
   TraceState* t = (TraceState*)c->tr;
   const int nv = c->d + 1;
+#if CWR_TR_V2
+  if (c->M <= 3) {
+    const int d = c->d, M = c->M, V = c->V, nm = c->nm, nq = t->nq;
+    const int P = nq % 4 == 0 ? 4 : nq % 3 == 0 ? 3 : nq % 2 == 0 ? 2 : 1, un = nv * nq / P;
+    const int nmp = (nm + 1) & ~1, wc = V * nmp, outc = nv * nq * V;
+    const int phn = (t->ncc * nm * nq + 1) & ~1;
+    int dev_smem = 0, nsm = 148;
+    TCK(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
+    TCK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
+    const int64_t budget = int64_t(dev_smem) - 64 - int64_t(phn) * 8;  // 64: the static mbarriers
+    int cb = std::min<int64_t>(512 / un, budget / (int64_t(2 * wc + outc) * 8));
+    if (cb < 1) fail(CWRECO_EUNSUPPORTED, "face traces: shape does not fit in shared memory");
+    const int64_t groups = (c->n_owned + cb - 1) / cb;
+    if (groups == 0) return;
+    const int threads = (cb * un + 31) & ~31;
+    const size_t smem = (size_t(phn) + size_t(cb) * (2 * wc + outc)) * sizeof(double);
+    // bulk copies need the dense layout (coefficients [cell][v][l] with an even ℳ) and
+    // 16-byte alignment; otherwise per-element cp.async in, thread-copied out
+    const int bulk_in = (cvs == nm && ccs == int64_t(V) * nm && nm % 2 == 0 && (uintptr_t(coeffs) & 15) == 0) ? 1 : 0;
+    const int bulk_out = (outc % 2 == 0 && (uintptr_t(traces) & 15) == 0) ? 1 : 0;
+    Tr2Fn f = tr2_fn(d, M, V);
+    TCK(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ = 1;
+    TCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)f, threads, smem));
+    int64_t grid = std::min<int64_t>(groups, (int64_t)nsm * std::max(1, occ));
+    if (c->max_ctas > 0) grid = std::min<int64_t>(grid, c->max_ctas);  // CWRECO_OPT_MAX_CTAS (tests)
+    f<<<(unsigned)grid, threads, smem, (cudaStream_t)stream>>>(coeffs, ccs, cvs, t->phi, t->ncc, t->code, cb,
+                                                               c->n_owned, traces, bulk_in, bulk_out);
+    TCK(cudaGetLastError());
+    return;
+  }
+#endif
   int qb = tr_qb(t->nq, c->nm);
 #ifdef CWRECO_EXPERIMENTS
   if (const char* e = std::getenv("CWRECO_TRACE_QB")) {  // tuning experiments only

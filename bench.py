@@ -472,7 +472,7 @@ def run_ours(args):
             "data": "synthetic",
             "config": {"workload": f"{args.config}: {WORKLOAD_TEXT[args.config]}", "n_cells_total": int(cells_total),
                        "n_cells_per_gpu": int(n_owned), "d": w["d"], "M": w["M"], "V": V, "box_n": n,
-                       "kernel": args.kernel, "l2": "flushed (512 MiB write) between timed steps",
+                       "kernel": "cwr::" + ksym, "kernel_mode": args.kernel, "l2": "flushed (512 MiB write) between timed steps",
                        "parallelism": f"cell partition x{world}" + (" + library NCCL halo, overlapped" if world > 1 else ""),
                        "setup_s": round(t_setup, 3), "library": version},
             "roofline": ({"bound": "alu", "achieved": mf_flops * n_owned / kern_s / 1e12, "peak": FP64_PEAK_TF,

@@ -9,15 +9,21 @@
 //   p̂_s = A_s⁻¹ ΔQ_s, A_s[m][l] = ψ_{l+1}(ξ_i(b_{j_m}))
 // then the same fused epilogue as the other kernels (P0, σ, ω, blend).
 //
-// One warp per cell (persistent grid): lane L holds the rows k = L, L+32 of A and
-// ΔQ (assembled by monomial quadrature exact for degree M, R19); Householder QR
-// with warp reductions (shuffle butterflies) applied to the V right-hand sides;
-// back substitution with the solution broadcast row by row; lanes 0..d solve the
-// sector systems; lanes 0..V−1 then gather their variable's coefficients and run
-// cweno_epilogue.  fp64-ALU bound (≈ 2·(n_e−1)·(ℳ−1)² FMAs per cell for the QR),
-// HBM traffic ≈ geometry + stencil ids + Q + w per cell.
-// Results agree with the oracle within the parity tolerance (not bitwise with the
-// matrix kernels: different QR order).
+// One warp per cell (persistent grid, 4-warp CTAs):
+//   1. lane L assembles rows k = L, L+32 of X = [mom | ΔQ] in shared memory: the
+//      stencil cell's vertices in the owner's reference frame, its monomial moments in
+//      closed form (Dirichlet formula, exact for polynomials: equal to the degree-M
+//      quadrature of R19 up to rounding);
+//   1b. the basis transform A = mom·Cᵀ (C: the modes' monomial coefficients) on the fp64
+//      tensor cores (mma.sync m8n8k4), one 8-row tile at a time, in place;
+//   2. Gram [AᵀA | AᵀΔQ] = XᵀX on the fp64 tensor cores, upper block tiles only;
+//   3. normal equations (R38): Cholesky AᵀA = UᵀU, lane k holding column k, the pivot
+//      rows broadcast through shared memory, the V right-hand sides forward-substituted
+//      in the same sweep; back substitution per variable (lane v) with Uᵀ rows;
+//   4. lanes 0..d solve the sector systems; lanes 0..V−1 run cweno_epilogue.
+// fp64-ALU bound, HBM traffic ≈ geometry + stencil ids + Q + w per cell.  Results agree
+// with the oracle within the parity tolerance (not bitwise with the matrix kernels:
+// a different solve).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -48,6 +54,9 @@ namespace cwr {
 #endif
 #ifndef CWR_MF_FAST_RSQ
 #define CWR_MF_FAST_RSQ 1  // rsqrt.approx + two Newton steps (else the library rsqrt)
+#endif
+#ifndef CWR_MF_PF
+#define CWR_MF_PF 0  // prefetch the next cell's stencil vertices / averages (1: L1, 2: L2)
 #endif
 #ifndef CWR_MF_UNROLL
 #define CWR_MF_UNROLL 0  // basis transform fully unrolled (register pressure: spills at 4 CTAs/SM)
@@ -526,6 +535,28 @@ __global__ void __launch_bounds__(128, mf_minb(D, M, V)) k_matfree(MfArgs m, KAr
           for (int l = NC; l < NCP; ++l) xr[l] = 0.0;
         }
       }
+    }
+#endif
+
+#if CWR_MF_PF
+    // the next cell's stencil vertices and averages (ids loaded at the top of this cell)
+    // towards the SM while the Gram / Cholesky phases run
+    if (i + nw < m.cell_end) {
+#pragma unroll
+      for (int r = 0; r < KPL; ++r)
+        if (lane + 32 * r < K) {
+          const double* xp = m.X + int64_t(jn[r]) * NV * D;
+          const double* qp = a.Q + int64_t(jn[r]) * a.acs;
+#if CWR_MF_PF == 1
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(xp));
+          if (D == 3) asm volatile("prefetch.global.L1 [%0];" ::"l"(xp + 8));
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(qp));
+#else
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(xp));
+          if (D == 3) asm volatile("prefetch.global.L2 [%0];" ::"l"(xp + 8));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(qp));
+#endif
+        }
     }
 #endif
 

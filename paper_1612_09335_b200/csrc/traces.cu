@@ -154,23 +154,38 @@ struct TrShape {
   static constexpr int NMP = (NM + 1) & ~1;     // staged coefficient row (even: pair loads)
   static constexpr int WC = V * NMP;            // staged doubles per cell
   static constexpr int OUTC = NF * NQ * V;      // output doubles per cell
+  static constexpr int TMAX = V > 6 ? 352 : 512;  // threads per CTA (P × V accumulators: 184 registers for V > 6)
 };
 
 template <int D, int M, int V>
-__global__ void __launch_bounds__(512) k_traces2(const double* __restrict__ w, int64_t ccs, int64_t cvs,
+__global__ void __launch_bounds__(TrShape<D, M, V>::TMAX) k_traces2(const double* __restrict__ w, int64_t ccs, int64_t cvs,
                                                  const double* __restrict__ phi, int ncc,
                                                  const uint8_t* __restrict__ code, int cb, int64_t n_owned,
-                                                 double* __restrict__ out, int bulk_in, int bulk_out) {
+                                                 double* __restrict__ out, int bulk_in, int bulk_out, int ng) {
   using S = TrShape<D, M, V>;
   constexpr int NM = S::NM, NF = S::NF, NQ = S::NQ, P = S::P, NMP = S::NMP, WC = S::WC, OUTC = S::OUTC;
+  // 16-point faces (3-D M = 3): a thread owns the point pairs t and t+4 of the row's 8
+  // and reads them in face-parity order, so the two faces of a quarter-warp touch
+  // disjoint banks on every 128-bit Φ load (4 threads of a face read 64 of a row's 128
+  // bytes; with q0 = 4t ownership both faces hit the same 16 banks: 2-way conflicts on
+  // the load that bounds this kernel); the output pieces land conflict-free as well
+#ifndef CWR_TR_SWZ
+#define CWR_TR_SWZ 1
+#endif
+  constexpr bool SWZ = CWR_TR_SWZ && NQ == 16 && P == 4;
   extern __shared__ __align__(16) double tr2_smem[];
-  __shared__ __align__(8) uint64_t bar[2];
-  const int tid = threadIdx.x, bd = blockDim.x;
+  __shared__ __align__(8) uint64_t bars[2][2];
+  // ng thread groups share the table Φ and walk their own blocks of cells with their own
+  // buffers, mbarriers and named barrier: one group's arithmetic overlaps the other's
+  // output staging and waits (the phases of a single group run one after the other)
+  const int bd = blockDim.x / ng, grp_id = threadIdx.x / bd, tid = threadIdx.x - grp_id * bd;
   const int phn = (ncc * NM * NQ + 1) & ~1;
-  double* ph = tr2_smem;             // [ncc][NM][NQ]
-  double* wb0 = ph + phn;            // 2 × [cb][V][NMP]
-  double* ob = wb0 + 2 * cb * WC;    // [cb][NF][NQ][V]
-  for (int k = tid; k < ncc * NQ * NM; k += bd) {  // global table is [code][q][l]
+  double* ph = tr2_smem;                                          // [ncc][NM][NQ]
+  double* wb0 = ph + phn + grp_id * ((cb * (2 * WC + OUTC) + 1) & ~1);  // 2 × [cb][V][NMP]
+  double* ob = wb0 + 2 * cb * WC;                                 // [cb][NF][NQ][V]
+  uint64_t* bar = bars[grp_id];
+  auto group_sync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + grp_id), "r"(bd) : "memory"); };
+  for (int k = threadIdx.x; k < ncc * NQ * NM; k += blockDim.x) {  // global table is [code][q][l]
     const int cc = k / (NQ * NM), r = k - cc * (NQ * NM), q = r / NM, l = r - q * NM;
     ph[(cc * NM + l) * NQ + q] = phi[k];
   }
@@ -181,6 +196,7 @@ __global__ void __launch_bounds__(512) k_traces2(const double* __restrict__ w, i
   }
   __syncthreads();
   const int64_t ngroups = (n_owned + cb - 1) / cb;
+  const int64_t first = (int64_t)blockIdx.x * ng + grp_id, step = (int64_t)gridDim.x * ng;
   auto issue = [&](int64_t grp, int buf) {
     const int64_t c0 = grp * cb;
     const int ncell = (int)min((int64_t)cb, n_owned - c0);
@@ -200,31 +216,40 @@ __global__ void __launch_bounds__(512) k_traces2(const double* __restrict__ w, i
     }
   };
   int j = 0;
-  if ((int64_t)blockIdx.x < ngroups) issue(blockIdx.x, 0);
-  for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x, ++j) {
+  if (first < ngroups) issue(first, 0);
+  // a thread keeps its (cell slot, face, point pairs) over the steps; its face's code byte
+  // comes from global memory (1 byte per face, streamed: a DRAM-latency load), fetched one
+  // step ahead so that no step waits for it
+  const int u = tid;
+  const int cl = u / S::UN, f = (u - cl * S::UN) / (NQ / P), t = u - cl * S::UN - f * (NQ / P), q0 = t * P;
+  int qo[(P + 1) / 2];  // row offset of the thread's k-th point pair
+#pragma unroll
+  for (int k = 0; k < (P + 1) / 2; ++k) qo[k] = SWZ ? 2 * (t + 4 * ((k + f) & 1)) : q0 + 2 * k;
+  auto load_code = [&](int64_t grp) -> int {
+    const int64_t c0 = grp * cb;
+    return (grp < ngroups && c0 + cl < n_owned && cl < cb) ? int(code[(c0 + cl) * NF + f]) : 0;
+  };
+  int fcode_next = load_code(first);
+  for (int64_t grp = first; grp < ngroups; grp += step, ++j) {
     const int buf = j & 1;
-    const bool more = grp + gridDim.x < ngroups;
-    if (more) issue(grp + gridDim.x, buf ^ 1);  // buffer buf^1 was released by the last step's barrier
+    const bool more = grp + step < ngroups;
+    if (more) issue(grp + step, buf ^ 1);  // buffer buf^1 was released by the last step's barrier
+    const int fcode = fcode_next;
+    fcode_next = load_code(grp + step);
+    const int64_t c0 = grp * cb;
+    const int ncell = (int)min((int64_t)cb, n_owned - c0);
+    const double* wb = wb0 + buf * cb * WC;
+    double acc[P][V];
+    const bool act = u < ncell * S::UN;
     if (bulk_in) {
       mbar_wait(&bar[buf], (j >> 1) & 1);
     } else {
       if (more) cp_async_wait<1>();
       else cp_async_wait<0>();
-      __syncthreads();
+      group_sync();
     }
-    const int64_t c0 = grp * cb;
-    const int ncell = (int)min((int64_t)cb, n_owned - c0);
-    const double* wb = wb0 + buf * cb * WC;
-    double acc[P][V];
-    const int u = tid;
-    const bool act = u < ncell * S::UN;
-    int cl = 0, f = 0, q0 = 0;
     if (act) {
-      cl = u / S::UN;
-      const int fu = u - cl * S::UN;
-      f = fu / (NQ / P);
-      q0 = (fu - f * (NQ / P)) * P;
-      const double* pp = ph + int(code[(c0 + cl) * NF + f]) * NM * NQ + q0;
+      const double* pp = ph + fcode * NM * NQ;
       const double* wc = wb + cl * WC;
 #pragma unroll
       for (int p2 = 0; p2 < P; ++p2)
@@ -244,11 +269,11 @@ __global__ void __launch_bounds__(512) k_traces2(const double* __restrict__ w, i
         if constexpr (P % 2 == 0) {
 #pragma unroll
           for (int p2 = 0; p2 < P; p2 += 2) {
-            const double2 a0 = *reinterpret_cast<const double2*>(pp + l * NQ + p2);
+            const double2 a0 = *reinterpret_cast<const double2*>(pp + l * NQ + qo[p2 / 2]);
             f0[p2] = a0.x;
             f0[p2 + 1] = a0.y;
             if (two) {
-              const double2 a1 = *reinterpret_cast<const double2*>(pp + (l + 1) * NQ + p2);
+              const double2 a1 = *reinterpret_cast<const double2*>(pp + (l + 1) * NQ + qo[p2 / 2]);
               f1[p2] = a1.x;
               f1[p2 + 1] = a1.y;
             }
@@ -256,8 +281,8 @@ __global__ void __launch_bounds__(512) k_traces2(const double* __restrict__ w, i
         } else {
 #pragma unroll
           for (int p2 = 0; p2 < P; ++p2) {
-            f0[p2] = pp[l * NQ + p2];
-            if (two) f1[p2] = pp[(l + 1) * NQ + p2];
+            f0[p2] = pp[l * NQ + q0 + p2];
+            if (two) f1[p2] = pp[(l + 1) * NQ + q0 + p2];
           }
         }
 #pragma unroll
@@ -270,10 +295,19 @@ __global__ void __launch_bounds__(512) k_traces2(const double* __restrict__ w, i
       }
     }
     if (bulk_out && tid == 0) bulk_wait_read();  // the last step's output has left ob
-    __syncthreads();
+    group_sync();
     if (act) {
       double* o = ob + ((cl * NF + f) * NQ + q0) * V;  // the tile's P·V outputs are contiguous
-      if constexpr ((P * V) % 2 == 0 && (NQ * V) % 2 == 0) {
+      if constexpr (SWZ) {
+#pragma unroll
+        for (int k = 0; k < P / 2; ++k) {  // two pieces of 2·V outputs (point pairs qo[k])
+          double* ok = ob + ((cl * NF + f) * NQ + qo[k]) * V;
+#pragma unroll
+          for (int e = 0; e < 2 * V; e += 2)
+            *reinterpret_cast<double2*>(ok + e) =
+                make_double2(acc[2 * k + e / V][e % V], acc[2 * k + (e + 1) / V][(e + 1) % V]);
+        }
+      } else if constexpr ((P * V) % 2 == 0 && (NQ * V) % 2 == 0) {
 #pragma unroll
         for (int k = 0; k < P * V; k += 2)
           *reinterpret_cast<double2*>(o + k) = make_double2(acc[k / V][k % V], acc[(k + 1) / V][(k + 1) % V]);
@@ -283,7 +317,7 @@ __global__ void __launch_bounds__(512) k_traces2(const double* __restrict__ w, i
       }
     }
     if (bulk_out) fence_proxy_async();  // generic-proxy writes of ob before the bulk store reads them
-    __syncthreads();
+    group_sync();
     if (bulk_out) {
       if (tid == 0) bulk_s2g(out + c0 * OUTC, ob, uint32_t(ncell) * OUTC * 8);
     } else {
@@ -295,7 +329,7 @@ __global__ void __launch_bounds__(512) k_traces2(const double* __restrict__ w, i
 }
 
 using Tr2Fn = void (*)(const double*, int64_t, int64_t, const double*, int, const uint8_t*, int, int64_t, double*,
-                       int, int);
+                       int, int, int);
 template <int D, int M>
 static Tr2Fn tr2_fn_v(int V) {
   switch (V) {
@@ -416,12 +450,24 @@ void dev_face_traces(cwreco_ctx* c, const double* coeffs, int64_t ccs, int64_t c
     TCK(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
     TCK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
     const int64_t budget = int64_t(dev_smem) - 64 - int64_t(phn) * 8;  // 64: the static mbarriers
-    int cb = std::min<int64_t>(512 / un, budget / (int64_t(2 * wc + outc) * 8));
+    // thread groups per CTA (see the kernel): two when each still has ≥ 2 warps of work;
+    // measured (profiles/r02q_traces_variants.log): C3 0.763 vs 0.778 ms with one group,
+    // C2 equal, but C5 4.88 vs 4.78 ms — ℳ = 20 stays on one group
+#ifndef CWR_TR_NG
+#define CWR_TR_NG (nm >= 20 ? 1 : 2)
+#endif
+    int ng = CWR_TR_NG;
+    int cb = 0;
+    for (; ng >= 1; --ng) {
+      cb = std::min<int64_t>((((V > 6 ? 352 : 512) / ng) & ~31) / un,  // whole warps per group within TMAX
+                             (budget - 16 * ng) / (int64_t(ng) * (2 * wc + outc) * 8));
+      if (ng == 1 || cb * un >= 64) break;
+    }
     if (cb < 1) fail(CWRECO_EUNSUPPORTED, "face traces: shape does not fit in shared memory");
     const int64_t groups = (c->n_owned + cb - 1) / cb;
     if (groups == 0) return;
-    const int threads = (cb * un + 31) & ~31;
-    const size_t smem = (size_t(phn) + size_t(cb) * (2 * wc + outc)) * sizeof(double);
+    const int threads = ng * ((cb * un + 31) & ~31);
+    const size_t smem = (size_t(phn) + size_t(ng) * ((size_t(cb) * (2 * wc + outc) + 1) & ~size_t(1))) * sizeof(double);
     // bulk copies need the dense layout (coefficients [cell][v][l] with an even ℳ) and
     // 16-byte alignment; otherwise per-element cp.async in, thread-copied out
     const int bulk_in = (cvs == nm && ccs == int64_t(V) * nm && nm % 2 == 0 && (uintptr_t(coeffs) & 15) == 0) ? 1 : 0;
@@ -430,10 +476,10 @@ void dev_face_traces(cwreco_ctx* c, const double* coeffs, int64_t ccs, int64_t c
     TCK(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 1;
     TCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)f, threads, smem));
-    int64_t grid = std::min<int64_t>(groups, (int64_t)nsm * std::max(1, occ));
+    int64_t grid = std::min<int64_t>((groups + ng - 1) / ng, (int64_t)nsm * std::max(1, occ));
     if (c->max_ctas > 0) grid = std::min<int64_t>(grid, c->max_ctas);  // CWRECO_OPT_MAX_CTAS (tests)
     f<<<(unsigned)grid, threads, smem, (cudaStream_t)stream>>>(coeffs, ccs, cvs, t->phi, t->ncc, t->code, cb,
-                                                               c->n_owned, traces, bulk_in, bulk_out);
+                                                               c->n_owned, traces, bulk_in, bulk_out, ng);
     TCK(cudaGetLastError());
     return;
   }

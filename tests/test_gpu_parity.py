@@ -289,8 +289,8 @@ def test_face_traces_parity(d, M, V, per):
     assert worst <= TOL, worst
 
 
-@pytest.mark.parametrize("d,M,V", [(2, 3, 4), (3, 2, 5), (3, 3, 5), (3, 3, 9)],
-                         ids=["2d-M3", "3d-M2", "3d-M3", "3d-M3-V9"])
+@pytest.mark.parametrize("d,M,V", [(2, 3, 4), (3, 2, 5), (3, 3, 5), (3, 3, 9), (3, 2, 9), (2, 1, 7)],
+                         ids=["2d-M3", "3d-M2", "3d-M3", "3d-M3-V9", "3d-M2-V9", "2d-M1-V7"])
 def test_face_traces_many_steps_and_strided(d, M, V):
     """The staged-block trace kernel with 2 CTAs walking every block of cells (double
     buffering of the coefficient blocks, output buffer reuse) equals the uncapped launch

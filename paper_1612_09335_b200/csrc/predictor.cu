@@ -71,6 +71,12 @@ static __constant__ double c_pred[pr_off(4, 1)];
 // padded to MT·8, j to KS·4 (zero), 4 column tiles per warp (32·V/8 tiles over V warps).
 // A' and C0 are stored per lane in fragment order ([k-step][m-tile][lane]) so a lane's
 // fragment is one coalesced load (L1-resident tables of ≤ 14 KB).
+// cells per CTA (the CTA always runs d+2 warps): CWR_PRED_CB3 for the tensor-core shape
+// 3-D M = 3 (5.6 KB of shared state per cell: 32 cells = one CTA per SM, 16 = two)
+#ifndef CWR_PRED_CB3
+#define CWR_PRED_CB3 32
+#endif
+__host__ __device__ constexpr int pr_cb(int D, int M) { return D == 3 && M == 3 ? CWR_PRED_CB3 : 32; }
 __host__ __device__ constexpr int pr_mt(int D, int M) { return (pr_L(D, M) - pr_nk(D, M) + 7) / 8; }
 __host__ __device__ constexpr int pr_ks(int D, int M) { return (D * pr_L(D, M) + 3) / 4; }
 __host__ __device__ constexpr int pr_ks0(int D, int M) { return (pr_nk(D, M) + 3) / 4; }
@@ -91,7 +97,7 @@ struct PredArgs {
 template <int D, int M>
 __global__ void __launch_bounds__(256) k_predictor(PredArgs p) {
   constexpr int V = D + 2, L = pr_L(D, M), NK = pr_nk(D, M), NU = L - NK;
-  constexpr int CB = 32;  // cells per CTA
+  constexpr int CB = pr_cb(D, M);  // cells per CTA
   constexpr int OA = pr_off(D, M), OC = OA + D * NU * L, OP = OC + NU * NK;
   constexpr bool kMma = CWR_PRED_MMA < 0 ? (D == 3 && M == 3) : CWR_PRED_MMA > 0;
   extern __shared__ __align__(16) double psm[];
@@ -351,7 +357,7 @@ static PredFn pred_fn(int d, int M) {
   fail(CWRECO_EUNSUPPORTED, "predictor: (d, M) not instantiated (M ≤ 3)");
 }
 static size_t pred_smem(int d, int M) {
-  const int L = pr_L(d, M), V = d + 2, CB = 32;
+  const int L = pr_L(d, M), V = d + 2, CB = pr_cb(d, M);
   return sizeof(double) * (size_t(CB) * L * V * (1 + d) + CB * d * d + CB * V + CB) + 2 * sizeof(int) * CB;
 }
 
@@ -442,9 +448,9 @@ void dev_predict(cwreco_ctx* c, const double* w, int64_t ccs, int64_t cvs, doubl
   PredFn f = pred_fn(c->d, c->M);
   int occ = 1, nsm = 148;
   const size_t smem = pred_smem(c->d, c->M);
-  PCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)f, 160, smem));
+  PCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)f, 32 * (c->d + 2), smem));
   PCK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
-  const int64_t blocks = (a.n + 31) / 32;
+  const int64_t blocks = (a.n + pr_cb(c->d, c->M) - 1) / pr_cb(c->d, c->M);
   int64_t grid = std::min<int64_t>(blocks, (int64_t)nsm * std::max(1, occ));
   if (c->max_ctas > 0) grid = std::min<int64_t>(grid, c->max_ctas);
   f<<<(unsigned)grid, 32 * (c->d + 2), smem, (cudaStream_t)stream>>>(a);

@@ -443,11 +443,16 @@ class Context:
 
     def predictor_nodes(self):
         """(nodes [𝓛][dim+1] (ξ, τ) in output order, number of known τ = 0 nodes)."""
-        n, k = ctypes.c_int(), ctypes.c_int()
-        _check(lib.cwreco_predictor_nodes(self._h, ctypes.byref(n), ctypes.byref(k), None))
-        nodes = np.empty((n.value, self.dim + 1))
-        _check(lib.cwreco_predictor_nodes(self._h, ctypes.byref(n), ctypes.byref(k), _ptr(nodes)))
-        return nodes, k.value
+        # the nodes depend only on (dim, M), fixed for the context; the library rebuilds its
+        # host matrices on every query, so predict() must not ask per call
+        cached = getattr(self, "_pred_nodes", None)
+        if cached is None:
+            n, k = ctypes.c_int(), ctypes.c_int()
+            _check(lib.cwreco_predictor_nodes(self._h, ctypes.byref(n), ctypes.byref(k), None))
+            nodes = np.empty((n.value, self.dim + 1))
+            _check(lib.cwreco_predictor_nodes(self._h, ctypes.byref(n), ctypes.byref(k), _ptr(nodes)))
+            cached = self._pred_nodes = (nodes, k.value)
+        return cached[0].copy(), cached[1]
 
     def predict(self, coeffs, dt, out=None, iters=None, stream=None):
         """cwreco_predict: coeffs CUDA [n_owned, V, ℳ] (mode axis contiguous) → out

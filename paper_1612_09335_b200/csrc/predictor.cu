@@ -68,15 +68,22 @@ static __constant__ double c_pred[pr_off(4, 1)];
 // Tensor-core form of the update (CWR_PRED_MMA): per CTA and iteration
 //   U[k][n] = Σ_j A'[k][j] Ĝ[j][n],  j = b·𝓛 + l ∈ [0, d·𝓛),  n = cell·V + v ∈ [0, 32·V)
 // with A'[k][b·𝓛 + l] = A_b[k][l] the SAME for every cell: m8n8k4 DMMA tiles, rows k
-// padded to MT·8, j to KS·4 (zero), 4 column tiles per warp (32·V/8 tiles over V warps).
+// padded to MT·8, j to KS·4 (zero), the 32·V/8 column tiles dealt to V·pr_wm warps.
 // A' and C0 are stored per lane in fragment order ([k-step][m-tile][lane]) so a lane's
 // fragment is one coalesced load (L1-resident tables of ≤ 14 KB).
-// cells per CTA (the CTA always runs d+2 warps): CWR_PRED_CB3 for the tensor-core shape
+// cells per CTA (the CTA runs (d+2)·pr_wm warps): CWR_PRED_CB3 for the tensor-core shape
 // 3-D M = 3 (5.6 KB of shared state per cell: 32 cells = one CTA per SM, 16 = two)
 #ifndef CWR_PRED_CB3
 #define CWR_PRED_CB3 32
 #endif
 __host__ __device__ constexpr int pr_cb(int D, int M) { return D == 3 && M == 3 ? CWR_PRED_CB3 : 32; }
+// warps per variable of the tensor-core shape (3-D M = 3): the CB·V/8 column tiles of the
+// update GEMM are dealt to (d+2)·pr_wm warps
+// (measured, profiles/r02w_predictor_wm_variants.log: C5 37.8 ms with 5 warps, 29.3 ms with 10)
+#ifndef CWR_PRED_WM3
+#define CWR_PRED_WM3 2
+#endif
+__host__ __device__ constexpr int pr_wm(int D, int M) { return D == 3 && M == 3 ? CWR_PRED_WM3 : 1; }
 __host__ __device__ constexpr int pr_mt(int D, int M) { return (pr_L(D, M) - pr_nk(D, M) + 7) / 8; }
 __host__ __device__ constexpr int pr_ks(int D, int M) { return (D * pr_L(D, M) + 3) / 4; }
 __host__ __device__ constexpr int pr_ks0(int D, int M) { return (pr_nk(D, M) + 3) / 4; }
@@ -95,7 +102,7 @@ struct PredArgs {
 };
 
 template <int D, int M>
-__global__ void __launch_bounds__(256) k_predictor(PredArgs p) {
+__global__ void __launch_bounds__(pr_wm(D, M) > 1 ? 32 * (D + 2) * pr_wm(D, M) : 256) k_predictor(PredArgs p) {
   constexpr int V = D + 2, L = pr_L(D, M), NK = pr_nk(D, M), NU = L - NK;
   constexpr int CB = pr_cb(D, M);  // cells per CTA
   constexpr int OA = pr_off(D, M), OC = OA + D * NU * L, OP = OC + NU * NK;
@@ -138,7 +145,7 @@ __global__ void __launch_bounds__(256) k_predictor(PredArgs p) {
       sc[it] = s;
     }
     constexpr int MT = pr_mt(D, M), KS = pr_ks(D, M), KS0 = pr_ks0(D, M), DL = D * L;
-    constexpr int NTW = CB / 8;  // column tiles per warp: 32·V columns / 8 / V warps
+    constexpr int NTW = CB / 8 / pr_wm(D, M);  // column tiles per warp: CB·V columns / 8 / (V·pr_wm warps)
     const int lane = tid & 31, warp = tid >> 5;
     int nb[NTW];
     double basef[MT][NTW][2];
@@ -448,12 +455,12 @@ void dev_predict(cwreco_ctx* c, const double* w, int64_t ccs, int64_t cvs, doubl
   PredFn f = pred_fn(c->d, c->M);
   int occ = 1, nsm = 148;
   const size_t smem = pred_smem(c->d, c->M);
-  PCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)f, 32 * (c->d + 2), smem));
+  PCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)f, 32 * (c->d + 2) * pr_wm(c->d, c->M), smem));
   PCK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
   const int64_t blocks = (a.n + pr_cb(c->d, c->M) - 1) / pr_cb(c->d, c->M);
   int64_t grid = std::min<int64_t>(blocks, (int64_t)nsm * std::max(1, occ));
   if (c->max_ctas > 0) grid = std::min<int64_t>(grid, c->max_ctas);
-  f<<<(unsigned)grid, 32 * (c->d + 2), smem, (cudaStream_t)stream>>>(a);
+  f<<<(unsigned)grid, 32 * (c->d + 2) * pr_wm(c->d, c->M), smem, (cudaStream_t)stream>>>(a);
   PCK(cudaGetLastError());
 }
 
